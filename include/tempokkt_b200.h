@@ -1,0 +1,158 @@
+/*
+ * tempokkt_b200.h -- C-ABI of the B200-native hot path of the
+ * multigrid-in-time KKT preconditioner (arXiv 2405.04808).
+ *
+ * Every entry point takes plain pointers and sizes (device pointers for
+ * vectors and stage data, a cudaStream_t passed as void*), returns an int
+ * status (TK_OK == 0) and never allocates on the hot path.  Each function
+ * names the reference interface it replaces (file:line inside
+ * /root/reference/pkg/src/tempokkt/).  INTEGRATION.md shows the ctypes
+ * binding the reference would add.
+ *
+ * Vector layout: exactly the reference's time-clustered ordering
+ * (kkt.py:6-16, KktLayout kkt.py:127-191):
+ *   block 0       (u_1, z_1, lam_1)                      size 2nu+nz
+ *   block i=1..N-1 (v_i, u_{i+1}, z_{i+1}, mu_i, lam_{i+1}) size 4nu+nz
+ *   block N       (v_N, mu_N)                             size 2nu
+ * so a device vector is bit-compatible with the reference's numpy vector.
+ */
+#ifndef TEMPOKKT_B200_H
+#define TEMPOKKT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TK_OK 0
+#define TK_ERR_ARG 1          /* bad sizes / null pointers  (errors.py:8 DimensionMismatch) */
+#define TK_ERR_CUDA 2         /* CUDA runtime error                                        */
+#define TK_ERR_UNSUPPORTED 3  /* structure not supported by the kernels                    */
+#define TK_ERR_NEWTON 4       /* forward Newton failed      (errors.py:40 NewtonDivergence) */
+
+#define TK_FAMILY_DENSE 0     /* small dense stage blocks (van der Pol): nu<=4, nz<=4       */
+#define TK_FAMILY_TRI 1       /* tridiagonal-in-space stage blocks (1D FE Burgers), nz==nu  */
+
+#define TK_MAX_DENSE 4
+
+/*
+ * One level of the operator ladder (replaces BlockTriKKT + DiagonalSolver,
+ * kkt.py:194-389, built per level by multigrid.py:358-410).
+ *
+ * Stage data are the reference's StageBlocks (kkt.py:53-80):
+ *   DENSE: K,C [N][nu][nu], B [N][nu][nz], row-major (same as numpy).
+ *   TRI:   K,C [N][3][nu] as (sub, diag, sup) diagonals; sub[0]=sup[nu-1]=0.
+ *          B is not stored: the family requires B_i = kappa * Qz (checked at
+ *          setup), which holds for the reference's Burgers (F_z = M,
+ *          w_control = alpha*M => kappa = 1/alpha).
+ * Weights (timedisc.py:194-206) are time-constant except the terminal stage:
+ *   Qm = q_u[i] = q_v[i] for i < N-1, Ql = q_u[N-1] = q_v[N-1], Qz = q_z[i].
+ *   DENSE: [nu][nu] / [nz][nz] plus their inverses (Qm_inv, Ql_inv, Qz_inv).
+ *   TRI:   [3][nu] diagonals; qz_cr = [3][nu] scalar cyclic-reduction
+ *          coefficients of Qz from tk_cr_scalar_factor().
+ */
+typedef struct tk_level {
+    int32_t family;
+    int32_t n_steps;
+    int32_t n_u;
+    int32_t n_z;
+    const double* K;
+    const double* C;
+    const double* B;
+    const double* Qm;
+    const double* Ql;
+    const double* Qz;
+    const double* Qm_inv;
+    const double* Ql_inv;
+    const double* Qz_inv;
+    double kappa;
+    const double* qz_cr;
+} tk_level;
+
+/* --- library ------------------------------------------------------------ */
+const char* tk_version(void);
+const char* tk_last_error(void);
+/* dim = N*(4nu+nz) (kkt.py:141). */
+int64_t tk_kkt_dim(int32_t n_steps, int32_t n_u, int32_t n_z);
+/* Bytes of dynamic shared memory the TRI kernels need for n_u (0 = unsupported). */
+int64_t tk_tri_smem_bytes(int32_t n_u);
+
+/* --- the operator (kkt.py) ---------------------------------------------- */
+/* y = A x                        replaces BlockTriKKT.apply        kkt.py:228 */
+int tk_kkt_apply(const tk_level* L, const double* x, double* y, void* stream);
+/* r = b - A x                    replaces `b - a.apply(x)`   smoothers.py:74, multigrid.py:456 */
+int tk_kkt_residual(const tk_level* L, const double* b, const double* x, double* r,
+                    void* stream);
+/* y = D x (no continuity couplings) replaces split_parts' D        kkt.py:400 and smoothers.py:142-151 */
+int tk_kkt_apply_diag(const tk_level* L, const double* x, double* y, void* stream);
+/* y = D^{-1} r  (all block rows in parallel) replaces DiagonalSolver.solve_all kkt.py:377 */
+int tk_diag_solve(const tk_level* L, const double* r, double* y, void* stream);
+
+/* --- smoothers (smoothers.py) --------------------------------------------- */
+/* One block-Jacobi sweep x_out = x_in + omega*D^{-1}(b - A x_in); x_in may be NULL
+ * (zero initial guess).  x_out must not alias x_in.  replaces jacobi_apply smoothers.py:61 */
+int tk_jacobi_sweep(const tk_level* L, const double* b, const double* x_in, double* x_out,
+                    double omega, void* stream);
+/* (D - L) delta = r, serial in time   replaces _forward_subst  smoothers.py:79 */
+int tk_forward_subst(const tk_level* L, const double* r, double* delta, void* stream);
+/* (D - U) delta = r, serial in time   replaces _backward_subst smoothers.py:95 */
+int tk_backward_subst(const tk_level* L, const double* r, double* delta, void* stream);
+
+/* --- transfers (multigrid.py:272-300) ------------------------------------- */
+/* xc = R xf  (injection for u,v,lam,mu; 2-interval average for z)    restrict_kkt multigrid.py:272 */
+int tk_restrict(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xf, double* xc,
+                void* stream);
+/* xf += P xc (linear interpolation / piecewise-constant copy)  prolong_kkt + `x + t.prolong_kkt(e)`
+ * multigrid.py:283 and :465 */
+int tk_prolong_add(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xc, double* xf,
+                   void* stream);
+/* rc = R (b - A x)  (work: fine-sized scratch)                 multigrid.py:456 */
+int tk_residual_restrict(const tk_level* L, const double* b, const double* x, double* rc,
+                         double* work, void* stream);
+
+/* --- Krylov vector kernels (krylov.py:77-191) ----------------------------- */
+/* Deterministic reductions: fixed grid, fixed order.  `out` is a device scalar.
+ * `work` is a device buffer of at least tk_reduce_work_len() doubles. */
+int64_t tk_reduce_work_len(void);
+int tk_dot(int64_t n, const double* x, const double* y, double* out, double* work, void* stream);
+int tk_nrm2(int64_t n, const double* x, double* out, double* work, void* stream);
+/* y += a*x;  y = a*x (scal into) ; x *= a */
+int tk_axpy(int64_t n, double a, const double* x, double* y, void* stream);
+int tk_scale_into(int64_t n, double a, const double* x, double* y, void* stream);
+/* y = b - y  (used for r = b - A x when A x is already in y) */
+int tk_rsub(int64_t n, const double* b, double* y, void* stream);
+/* x += V^T c: V is k rows of length n with leading dimension ld; c on device */
+int tk_gemv_t_add(int64_t n, int32_t k, const double* V, int64_t ld, const double* c,
+                  double* x, void* stream);
+
+/* --- setup: stage linearisation on the device (timedisc.py:133, kkt.py:100) - */
+/* van der Pol: K,C,B at (v_{i-1}, u_i, z_i), v_{-1} = u0.  n_controls in {1,2}. */
+int tk_stage_vanderpol(int32_t n_steps, double dt, double theta, double mu, int32_t n_controls,
+                       const double* u0, const double* u, const double* v, const double* z,
+                       double* K, double* C, double* B, void* stream);
+/* Burgers (problems.py:425): TRI diagonals of K, C at (v_{i-1}, u_i, z_i). */
+int tk_stage_burgers(int32_t n_steps, int32_t n_u, double dt, double theta, double nu,
+                     const double* u0, const double* u, const double* v, double* K, double* C,
+                     void* stream);
+
+/* --- setup: host routines (CPU) ------------------------------------------- */
+/* theta-method forward march with Newton (timedisc.py:152-191), host memory. */
+int tk_forward_vanderpol_host(int32_t n_steps, double dt, double theta, double mu,
+                              int32_t n_controls, const double* u0, const double* z,
+                              double newton_tol, double* states);
+int tk_forward_burgers_host(int32_t n_steps, int32_t n_u, double dt, double theta, double nu,
+                            const double* u0, const double* z, double newton_tol,
+                            double* states);
+/* Scalar cyclic-reduction coefficients of a symmetric tridiagonal matrix
+ * given as [3][n] (sub, diag, sup): out [3][n] = (inv_d, e_up, e_lo) at each
+ * node's elimination level.  Host memory. */
+int tk_cr_scalar_factor(int32_t n, const double* tri, double* out);
+/* Solve with those coefficients (host, for testing the layout). */
+int tk_cr_scalar_solve_host(int32_t n, const double* coef, const double* f, double* x);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TEMPOKKT_B200_H */

@@ -1,0 +1,200 @@
+// extern "C" entry points of libtempokkt_b200.so (include/tempokkt_b200.h).
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "tk_common.cuh"
+
+namespace tk {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return TK_OK;
+    set_error("%s: %s", where, cudaGetErrorString(e));
+    return TK_ERR_CUDA;
+}
+
+int check_launch(const char* where) { return cuda_status(cudaGetLastError(), where); }
+
+int dense_launch(const tk_level*, int, const double*, const double*, double*, double, cudaStream_t);
+int tri_launch(const tk_level*, int, const double*, const double*, double*, double, cudaStream_t);
+int64_t tri_smem_bytes(int n);
+int transfer_launch(int, int, int, int, const double*, double*, cudaStream_t);
+int64_t reduce_work_len();
+int dot_launch(int64_t, const double*, const double*, double*, double*, int, cudaStream_t);
+int vec_launch(int, int64_t, double, const double*, double*, cudaStream_t);
+int gemv_t_add_launch(int64_t, int, const double*, int64_t, const double*, double*, cudaStream_t);
+int stage_vdp_launch(int, double, double, double, int, const double*, const double*,
+                     const double*, const double*, double*, double*, double*, cudaStream_t);
+int stage_burgers_launch(int, int, double, double, double, const double*, const double*,
+                         const double*, double*, double*, cudaStream_t);
+
+static int check_level(const tk_level* L) {
+    if (!L) { set_error("null level"); return TK_ERR_ARG; }
+    if (L->n_steps < 1 || L->n_u < 1 || L->n_z < 1) {
+        set_error("bad level sizes N=%d nu=%d nz=%d", L->n_steps, L->n_u, L->n_z);
+        return TK_ERR_ARG;
+    }
+    if (!L->K || !L->C || !L->Qm || !L->Ql || !L->Qz) {
+        set_error("level is missing stage/weight data");
+        return TK_ERR_ARG;
+    }
+    if (L->family == TK_FAMILY_DENSE) {
+        if (!L->B || !L->Qm_inv || !L->Ql_inv || !L->Qz_inv) {
+            set_error("dense level is missing B or weight inverses");
+            return TK_ERR_ARG;
+        }
+    } else if (L->family == TK_FAMILY_TRI) {
+        if (!L->qz_cr) { set_error("tri level is missing qz_cr"); return TK_ERR_ARG; }
+    } else {
+        set_error("unknown family %d", L->family);
+        return TK_ERR_UNSUPPORTED;
+    }
+    return TK_OK;
+}
+
+static int level_op(const tk_level* L, int dense_op, int tri_op, const double* b,
+                    const double* x, double* y, double omega, void* stream) {
+    int rc = check_level(L);
+    if (rc) return rc;
+    cudaStream_t s = as_stream(stream);
+    if (L->family == TK_FAMILY_DENSE) return dense_launch(L, dense_op, b, x, y, omega, s);
+    return tri_launch(L, tri_op, b, x, y, omega, s);
+}
+
+}  // namespace tk
+
+using namespace tk;
+
+extern "C" {
+
+const char* tk_version(void) { return "tempokkt_b200 0.1 (sm_100a)"; }
+const char* tk_last_error(void) { return g_err; }
+
+int64_t tk_kkt_dim(int32_t n_steps, int32_t n_u, int32_t n_z) {
+    return (int64_t)n_steps * (4 * (int64_t)n_u + n_z);
+}
+
+int64_t tk_tri_smem_bytes(int32_t n_u) { return tri_smem_bytes(n_u); }
+
+int tk_kkt_apply(const tk_level* L, const double* x, double* y, void* stream) {
+    TK_CHECK_ARG(x && y, "tk_kkt_apply: null vector");
+    return level_op(L, 0, 0, nullptr, x, y, 1.0, stream);
+}
+
+int tk_kkt_apply_diag(const tk_level* L, const double* x, double* y, void* stream) {
+    TK_CHECK_ARG(x && y, "tk_kkt_apply_diag: null vector");
+    return level_op(L, 1, 1, nullptr, x, y, 1.0, stream);
+}
+
+int tk_kkt_residual(const tk_level* L, const double* b, const double* x, double* r,
+                    void* stream) {
+    TK_CHECK_ARG(b && x && r, "tk_kkt_residual: null vector");
+    return level_op(L, 2, 2, b, x, r, 1.0, stream);
+}
+
+int tk_diag_solve(const tk_level* L, const double* r, double* y, void* stream) {
+    TK_CHECK_ARG(r && y, "tk_diag_solve: null vector");
+    return level_op(L, 3, 3, r, nullptr, y, 1.0, stream);
+}
+
+int tk_jacobi_sweep(const tk_level* L, const double* b, const double* x_in, double* x_out,
+                    double omega, void* stream) {
+    TK_CHECK_ARG(b && x_out, "tk_jacobi_sweep: null vector");
+    TK_CHECK_ARG(x_in != x_out, "tk_jacobi_sweep: x_out must not alias x_in");
+    return level_op(L, 4, 4, b, x_in, x_out, omega, stream);
+}
+
+int tk_forward_subst(const tk_level* L, const double* r, double* delta, void* stream) {
+    TK_CHECK_ARG(r && delta && r != delta, "tk_forward_subst: bad vectors");
+    return level_op(L, 10, 10, r, nullptr, delta, 1.0, stream);
+}
+
+int tk_backward_subst(const tk_level* L, const double* r, double* delta, void* stream) {
+    TK_CHECK_ARG(r && delta && r != delta, "tk_backward_subst: bad vectors");
+    return level_op(L, 11, 11, r, nullptr, delta, 1.0, stream);
+}
+
+int tk_restrict(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xf, double* xc,
+                void* stream) {
+    TK_CHECK_ARG(xf && xc && n_fine >= 2 && n_fine % 2 == 0 && n_u >= 1 && n_z >= 1,
+                 "tk_restrict: bad arguments (n_fine must be even)");
+    return transfer_launch(1, n_fine, n_u, n_z, xf, xc, as_stream(stream));
+}
+
+int tk_prolong_add(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xc, double* xf,
+                   void* stream) {
+    TK_CHECK_ARG(xf && xc && n_fine >= 2 && n_fine % 2 == 0 && n_u >= 1 && n_z >= 1,
+                 "tk_prolong_add: bad arguments (n_fine must be even)");
+    return transfer_launch(0, n_fine, n_u, n_z, xc, xf, as_stream(stream));
+}
+
+int tk_residual_restrict(const tk_level* L, const double* b, const double* x, double* rc,
+                         double* work, void* stream) {
+    TK_CHECK_ARG(b && x && rc && work, "tk_residual_restrict: null vector");
+    int rcode = level_op(L, 2, 2, b, x, work, 1.0, stream);
+    if (rcode) return rcode;
+    return transfer_launch(1, L->n_steps, L->n_u, L->n_z, work, rc, as_stream(stream));
+}
+
+int64_t tk_reduce_work_len(void) { return reduce_work_len(); }
+
+int tk_dot(int64_t n, const double* x, const double* y, double* out, double* work,
+           void* stream) {
+    TK_CHECK_ARG(x && y && out && work && n >= 0, "tk_dot: bad arguments");
+    return dot_launch(n, x, y, out, work, 0, as_stream(stream));
+}
+
+int tk_nrm2(int64_t n, const double* x, double* out, double* work, void* stream) {
+    TK_CHECK_ARG(x && out && work && n >= 0, "tk_nrm2: bad arguments");
+    return dot_launch(n, x, x, out, work, 1, as_stream(stream));
+}
+
+int tk_axpy(int64_t n, double a, const double* x, double* y, void* stream) {
+    TK_CHECK_ARG(x && y, "tk_axpy: null vector");
+    return vec_launch(0, n, a, x, y, as_stream(stream));
+}
+
+int tk_scale_into(int64_t n, double a, const double* x, double* y, void* stream) {
+    TK_CHECK_ARG(x && y, "tk_scale_into: null vector");
+    return vec_launch(1, n, a, x, y, as_stream(stream));
+}
+
+int tk_rsub(int64_t n, const double* b, double* y, void* stream) {
+    TK_CHECK_ARG(b && y, "tk_rsub: null vector");
+    return vec_launch(2, n, 0.0, b, y, as_stream(stream));
+}
+
+int tk_gemv_t_add(int64_t n, int32_t k, const double* V, int64_t ld, const double* c, double* x,
+                  void* stream) {
+    TK_CHECK_ARG(V && c && x && k >= 0 && ld >= n, "tk_gemv_t_add: bad arguments");
+    if (k == 0) return TK_OK;
+    return gemv_t_add_launch(n, k, V, ld, c, x, as_stream(stream));
+}
+
+int tk_stage_vanderpol(int32_t n_steps, double dt, double theta, double mu, int32_t n_controls,
+                       const double* u0, const double* u, const double* v, const double* z,
+                       double* K, double* C, double* B, void* stream) {
+    TK_CHECK_ARG(n_steps >= 1 && (n_controls == 1 || n_controls == 2) && u0 && u && v && K && C &&
+                     B,
+                 "tk_stage_vanderpol: bad arguments");
+    return stage_vdp_launch(n_steps, dt, theta, mu, n_controls, u0, u, v, z, K, C, B,
+                            as_stream(stream));
+}
+
+int tk_stage_burgers(int32_t n_steps, int32_t n_u, double dt, double theta, double nu,
+                     const double* u0, const double* u, const double* v, double* K, double* C,
+                     void* stream) {
+    TK_CHECK_ARG(n_steps >= 1 && n_u >= 2 && u0 && u && v && K && C,
+                 "tk_stage_burgers: bad arguments");
+    return stage_burgers_launch(n_steps, n_u, dt, theta, nu, u0, u, v, K, C, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,415 @@
+// DENSE family: tiny per-interval KKT blocks (van der Pol: n_u = 2, n_z in {1,2}).
+//
+// One thread owns one block row of the Figure-3 operator (kkt.py:194-320);
+// the local KKT solve is done in registers by eliminating (v, mu) exactly,
+// then the control and the state through the constant weight inverses, and
+// solving the n_u x n_u SPD Schur system
+//     S = K Qu^{-1} K^T + B Qz^{-1} B^T
+// for the dynamics multiplier.  This is D_i^{-1} of DiagonalSolver
+// (kkt.py:338-389) without forming the (4nu+nz)^2 inverse: the HBM stream
+// per interval is the vectors plus K_i, C_i, B_i only.
+#include "tk_common.cuh"
+
+namespace tk {
+
+template <int NU, int NZ>
+struct DView {
+    Lay lay;
+    const double* __restrict__ K;
+    const double* __restrict__ C;
+    const double* __restrict__ B;
+    const double* __restrict__ Qm;
+    const double* __restrict__ Ql;
+    const double* __restrict__ Qz;
+    const double* __restrict__ Qm_inv;
+    const double* __restrict__ Ql_inv;
+    const double* __restrict__ Qz_inv;
+    DView(const tk_level* L)
+        : lay(L->n_steps, L->n_u, L->n_z), K(L->K), C(L->C), B(L->B), Qm(L->Qm), Ql(L->Ql),
+          Qz(L->Qz), Qm_inv(L->Qm_inv), Ql_inv(L->Ql_inv), Qz_inv(L->Qz_inv) {}
+};
+
+// y = A x, A row-major R x Cn
+template <int R, int Cn>
+__device__ __forceinline__ void mv(const double* __restrict__ A, const double* x, double* y) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < Cn; ++c) s += A[r * Cn + c] * x[c];
+        y[r] = s;
+    }
+}
+// y += A^T x, A row-major R x Cn (x length R, y length Cn)
+template <int R, int Cn>
+__device__ __forceinline__ void mtv_add(const double* __restrict__ A, const double* x, double* y) {
+#pragma unroll
+    for (int c = 0; c < Cn; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) s += A[r * Cn + c] * x[r];
+        y[c] += s;
+    }
+}
+template <int R, int Cn>
+__device__ __forceinline__ void mv_add(const double* __restrict__ A, const double* x, double* y) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < Cn; ++c) s += A[r * Cn + c] * x[c];
+        y[r] += s;
+    }
+}
+
+// Gaussian elimination with partial pivoting on a small dense system (in place).
+template <int N>
+__device__ __forceinline__ void small_solve(double (&A)[N][N], double (&b)[N]) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        int p = k;
+        double best = fabs(A[k][k]);
+#pragma unroll
+        for (int r = k + 1; r < N; ++r) {
+            double a = fabs(A[r][k]);
+            if (a > best) { best = a; p = r; }
+        }
+        if (p != k) {
+#pragma unroll
+            for (int c = 0; c < N; ++c) {
+                // unrolled swap with a runtime row index
+#pragma unroll
+                for (int r = k + 1; r < N; ++r)
+                    if (r == p) { double t = A[k][c]; A[k][c] = A[r][c]; A[r][c] = t; }
+            }
+#pragma unroll
+            for (int r = k + 1; r < N; ++r)
+                if (r == p) { double t = b[k]; b[k] = b[r]; b[r] = t; }
+        }
+        double inv = 1.0 / A[k][k];
+#pragma unroll
+        for (int r = k + 1; r < N; ++r) {
+            double l = A[r][k] * inv;
+#pragma unroll
+            for (int c = k + 1; c < N; ++c) A[r][c] -= l * A[k][c];
+            b[r] -= l * b[k];
+        }
+    }
+#pragma unroll
+    for (int k = N - 1; k >= 0; --k) {
+        double s = b[k];
+#pragma unroll
+        for (int c = k + 1; c < N; ++c) s -= A[k][c] * b[c];
+        b[k] = s / A[k][k];
+    }
+}
+
+template <int NU, int NZ>
+struct Seg {
+    double v[NU], u[NU], z[NZ], m[NU], l[NU];
+};
+
+template <int NU, int NZ>
+__device__ __forceinline__ void load_seg(const Lay& lay, int i, const double* x, Seg<NU, NZ>& s) {
+#pragma unroll
+    for (int e = 0; e < NU; ++e) { s.v[e] = 0.0; s.u[e] = 0.0; s.m[e] = 0.0; s.l[e] = 0.0; }
+#pragma unroll
+    for (int e = 0; e < NZ; ++e) s.z[e] = 0.0;
+    if (x == nullptr) return;
+    if (i >= 1) {
+        const double* pv = x + lay.off_v(i);
+        const double* pm = x + lay.off_mu(i);
+#pragma unroll
+        for (int e = 0; e < NU; ++e) { s.v[e] = pv[e]; s.m[e] = pm[e]; }
+    }
+    if (i < lay.N) {
+        const double* pu = x + lay.off_u(i);
+        const double* pz = x + lay.off_z(i);
+        const double* pl = x + lay.off_l(i);
+#pragma unroll
+        for (int e = 0; e < NU; ++e) { s.u[e] = pu[e]; s.l[e] = pl[e]; }
+#pragma unroll
+        for (int e = 0; e < NZ; ++e) s.z[e] = pz[e];
+    }
+}
+
+template <int NU, int NZ>
+__device__ __forceinline__ void store_seg(const Lay& lay, int i, double* y, const Seg<NU, NZ>& s) {
+    if (i >= 1) {
+        double* pv = y + lay.off_v(i);
+        double* pm = y + lay.off_mu(i);
+#pragma unroll
+        for (int e = 0; e < NU; ++e) { pv[e] = s.v[e]; pm[e] = s.m[e]; }
+    }
+    if (i < lay.N) {
+        double* pu = y + lay.off_u(i);
+        double* pz = y + lay.off_z(i);
+        double* pl = y + lay.off_l(i);
+#pragma unroll
+        for (int e = 0; e < NU; ++e) { pu[e] = s.u[e]; pl[e] = s.l[e]; }
+#pragma unroll
+        for (int e = 0; e < NZ; ++e) pz[e] = s.z[e];
+    }
+}
+
+// (A x)_i with optional continuity couplings: uprev = u_i (from block i-1)
+// feeding the mu rows, munext = mu_{i+1} (from block i+1) feeding the u rows.
+template <int NU, int NZ>
+__device__ __forceinline__ void apply_row(const DView<NU, NZ>& V, int i, const Seg<NU, NZ>& x,
+                                          const double* uprev, const double* munext,
+                                          Seg<NU, NZ>& y) {
+    const Lay& L = V.lay;
+    const bool has_vm = i >= 1, has_uzl = i < L.N;
+#pragma unroll
+    for (int e = 0; e < NU; ++e) { y.v[e] = 0.0; y.u[e] = 0.0; y.m[e] = 0.0; y.l[e] = 0.0; }
+#pragma unroll
+    for (int e = 0; e < NZ; ++e) y.z[e] = 0.0;
+    if (has_vm) {
+        const double* Qv = (i == L.N) ? V.Ql : V.Qm;  // q_v[i-1]
+        mv<NU, NU>(Qv, x.v, y.v);
+#pragma unroll
+        for (int e = 0; e < NU; ++e) {
+            y.v[e] -= x.m[e];
+            y.m[e] = -x.v[e] + (uprev ? uprev[e] : 0.0);
+        }
+    }
+    if (has_uzl) {
+        const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;  // q_u[i]
+        const double* K = V.K + (size_t)i * NU * NU;
+        const double* B = V.B + (size_t)i * NU * NZ;
+        mv<NU, NU>(Qu, x.u, y.u);
+        mtv_add<NU, NU>(K, x.l, y.u);
+        if (munext) {
+#pragma unroll
+            for (int e = 0; e < NU; ++e) y.u[e] += munext[e];
+        }
+        mv<NZ, NZ>(V.Qz, x.z, y.z);
+        mtv_add<NU, NZ>(B, x.l, y.z);
+        mv<NU, NU>(K, x.u, y.l);
+        mv_add<NU, NZ>(B, x.z, y.l);
+        if (has_vm) {
+            const double* C = V.C + (size_t)i * NU * NU;
+            mtv_add<NU, NU>(C, x.l, y.v);
+            mv_add<NU, NU>(C, x.v, y.l);
+        }
+    }
+}
+
+// d = D_i^{-1} r (local KKT solve of block row i).
+template <int NU, int NZ>
+__device__ __forceinline__ void solve_row(const DView<NU, NZ>& V, int i, const Seg<NU, NZ>& r,
+                                          Seg<NU, NZ>& d) {
+    const Lay& L = V.lay;
+    const bool has_vm = i >= 1, has_uzl = i < L.N;
+    double rl[NU];
+#pragma unroll
+    for (int e = 0; e < NU; ++e) rl[e] = r.l[e];
+    if (has_vm) {
+#pragma unroll
+        for (int e = 0; e < NU; ++e) d.v[e] = -r.m[e];  // mu-row: -v = r_mu
+    }
+    if (has_uzl) {
+        const double* Qu_inv = (i == L.N - 1) ? V.Ql_inv : V.Qm_inv;
+        const double* K = V.K + (size_t)i * NU * NU;
+        const double* B = V.B + (size_t)i * NU * NZ;
+        if (has_vm) {
+            const double* C = V.C + (size_t)i * NU * NU;
+            double cv[NU];
+            mv<NU, NU>(C, d.v, cv);
+#pragma unroll
+            for (int e = 0; e < NU; ++e) rl[e] -= cv[e];
+        }
+        // a = Qu^{-1} r_u, c = Qz^{-1} r_z
+        double a[NU], c[NZ];
+        mv<NU, NU>(Qu_inv, r.u, a);
+        mv<NZ, NZ>(V.Qz_inv, r.z, c);
+        // S = K Qu^-1 K^T + B Qz^-1 B^T ; t = K a + B c - rl
+        double KQ[NU][NU], BQ[NU][NZ];
+#pragma unroll
+        for (int p = 0; p < NU; ++p) {
+#pragma unroll
+            for (int q = 0; q < NU; ++q) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < NU; ++k) s += K[p * NU + k] * Qu_inv[k * NU + q];
+                KQ[p][q] = s;
+            }
+#pragma unroll
+            for (int q = 0; q < NZ; ++q) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < NZ; ++k) s += B[p * NZ + k] * V.Qz_inv[k * NZ + q];
+                BQ[p][q] = s;
+            }
+        }
+        double S[NU][NU], t[NU];
+#pragma unroll
+        for (int p = 0; p < NU; ++p) {
+#pragma unroll
+            for (int q = 0; q < NU; ++q) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < NU; ++k) s += KQ[p][k] * K[q * NU + k];
+#pragma unroll
+                for (int k = 0; k < NZ; ++k) s += BQ[p][k] * B[q * NZ + k];
+                S[p][q] = s;
+            }
+            double s = -rl[p];
+#pragma unroll
+            for (int k = 0; k < NU; ++k) s += K[p * NU + k] * a[k];
+#pragma unroll
+            for (int k = 0; k < NZ; ++k) s += B[p * NZ + k] * c[k];
+            t[p] = s;
+        }
+        small_solve<NU>(S, t);
+#pragma unroll
+        for (int e = 0; e < NU; ++e) d.l[e] = t[e];
+        // u = Qu^{-1}(r_u - K^T lam), z = Qz^{-1}(r_z - B^T lam)
+        double ku[NU], bz[NZ];
+#pragma unroll
+        for (int e = 0; e < NU; ++e) ku[e] = r.u[e];
+#pragma unroll
+        for (int e = 0; e < NZ; ++e) bz[e] = r.z[e];
+#pragma unroll
+        for (int q = 0; q < NU; ++q) {
+#pragma unroll
+            for (int p = 0; p < NU; ++p) ku[q] -= K[p * NU + q] * t[p];
+        }
+#pragma unroll
+        for (int q = 0; q < NZ; ++q) {
+#pragma unroll
+            for (int p = 0; p < NU; ++p) bz[q] -= B[p * NZ + q] * t[p];
+        }
+        mv<NU, NU>(Qu_inv, ku, d.u);
+        mv<NZ, NZ>(V.Qz_inv, bz, d.z);
+    }
+    if (has_vm) {
+        // v-row: Qv v - mu + C^T lam = r_v  =>  mu = Qv v + C^T lam - r_v
+        const double* Qv = (i == L.N) ? V.Ql : V.Qm;
+        mv<NU, NU>(Qv, d.v, d.m);
+        if (has_uzl) {
+            const double* C = V.C + (size_t)i * NU * NU;
+            mtv_add<NU, NU>(C, d.l, d.m);
+        }
+#pragma unroll
+        for (int e = 0; e < NU; ++e) d.m[e] -= r.v[e];
+    }
+}
+
+enum DenseMode { D_APPLY = 0, D_APPLY_DIAG = 1, D_RESIDUAL = 2, D_SOLVE = 3, D_JACOBI = 4 };
+
+template <int NU, int NZ, int MODE>
+__global__ void __launch_bounds__(128) dense_rows(DView<NU, NZ> V, const double* __restrict__ b,
+                                                  const double* __restrict__ x,
+                                                  double* __restrict__ y, double omega) {
+    const Lay& L = V.lay;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= L.N; i += gridDim.x * blockDim.x) {
+        Seg<NU, NZ> xs, ys;
+        const double* uprev = (i >= 1 && x) ? x + L.off_u(i - 1) : nullptr;
+        const double* munext = (i < L.N && x) ? x + L.off_mu(i + 1) : nullptr;
+        if (MODE == D_SOLVE) {
+            load_seg<NU, NZ>(L, i, b, xs);
+            solve_row<NU, NZ>(V, i, xs, ys);
+            store_seg<NU, NZ>(L, i, y, ys);
+            continue;
+        }
+        load_seg<NU, NZ>(L, i, x, xs);
+        apply_row<NU, NZ>(V, i, xs, MODE == D_APPLY_DIAG ? nullptr : uprev,
+                          MODE == D_APPLY_DIAG ? nullptr : munext, ys);
+        if (MODE == D_APPLY || MODE == D_APPLY_DIAG) {
+            store_seg<NU, NZ>(L, i, y, ys);
+            continue;
+        }
+        Seg<NU, NZ> bs;
+        load_seg<NU, NZ>(L, i, b, bs);
+#pragma unroll
+        for (int e = 0; e < NU; ++e) {
+            bs.v[e] -= ys.v[e]; bs.u[e] -= ys.u[e]; bs.m[e] -= ys.m[e]; bs.l[e] -= ys.l[e];
+        }
+#pragma unroll
+        for (int e = 0; e < NZ; ++e) bs.z[e] -= ys.z[e];
+        if (MODE == D_RESIDUAL) {
+            store_seg<NU, NZ>(L, i, y, bs);
+            continue;
+        }
+        // D_JACOBI: x_out = x + omega * D^{-1} (b - A x)
+        solve_row<NU, NZ>(V, i, bs, ys);
+#pragma unroll
+        for (int e = 0; e < NU; ++e) {
+            xs.v[e] += omega * ys.v[e]; xs.u[e] += omega * ys.u[e];
+            xs.m[e] += omega * ys.m[e]; xs.l[e] += omega * ys.l[e];
+        }
+#pragma unroll
+        for (int e = 0; e < NZ; ++e) xs.z[e] += omega * ys.z[e];
+        store_seg<NU, NZ>(L, i, y, xs);
+    }
+}
+
+// Serial block substitution (smoothers.py:79-109): one thread walks the time axis.
+template <int NU, int NZ, bool FORWARD>
+__global__ void dense_subst(DView<NU, NZ> V, const double* __restrict__ r, double* __restrict__ d) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    const Lay& L = V.lay;
+    for (int k = 0; k <= L.N; ++k) {
+        const int i = FORWARD ? k : L.N - k;
+        Seg<NU, NZ> rs, ds;
+        load_seg<NU, NZ>(L, i, r, rs);
+        if (FORWARD && i >= 1) {
+            const volatile double* up = d + L.off_u(i - 1);
+#pragma unroll
+            for (int e = 0; e < NU; ++e) rs.m[e] -= up[e];
+        }
+        if (!FORWARD && i < L.N) {
+            const volatile double* mn = d + L.off_mu(i + 1);
+#pragma unroll
+            for (int e = 0; e < NU; ++e) rs.u[e] -= mn[e];
+        }
+        solve_row<NU, NZ>(V, i, rs, ds);
+        store_seg<NU, NZ>(L, i, d, ds);
+    }
+}
+
+template <int NU, int NZ>
+static int dense_launch_t(const tk_level* Lv, int op, const double* b, const double* x, double* y,
+                          double omega, cudaStream_t s) {
+    DView<NU, NZ> V(Lv);
+    const int rows = Lv->n_steps + 1;
+    const int th = 128;
+    const int grid = grid_for(rows, th, 1 << 20);
+    switch (op) {
+        case D_APPLY: dense_rows<NU, NZ, D_APPLY><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
+        case D_APPLY_DIAG:
+            dense_rows<NU, NZ, D_APPLY_DIAG><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
+        case D_RESIDUAL: dense_rows<NU, NZ, D_RESIDUAL><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
+        case D_SOLVE: dense_rows<NU, NZ, D_SOLVE><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
+        case D_JACOBI: dense_rows<NU, NZ, D_JACOBI><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
+        case 10: dense_subst<NU, NZ, true><<<1, 1, 0, s>>>(V, b, y); break;
+        case 11: dense_subst<NU, NZ, false><<<1, 1, 0, s>>>(V, b, y); break;
+        default: set_error("dense: bad op %d", op); return TK_ERR_ARG;
+    }
+    return check_launch("dense_rows");
+}
+
+#define TK_DENSE_NZ(NU)                                                               \
+    switch (Lv->n_z) {                                                                \
+        case 1: return dense_launch_t<NU, 1>(Lv, op, b, x, y, omega, s);              \
+        case 2: return dense_launch_t<NU, 2>(Lv, op, b, x, y, omega, s);              \
+        case 3: return dense_launch_t<NU, 3>(Lv, op, b, x, y, omega, s);              \
+        case 4: return dense_launch_t<NU, 4>(Lv, op, b, x, y, omega, s);              \
+        default: break;                                                               \
+    }
+
+int dense_launch(const tk_level* Lv, int op, const double* b, const double* x, double* y,
+                 double omega, cudaStream_t s) {
+    switch (Lv->n_u) {
+        case 1: TK_DENSE_NZ(1); break;
+        case 2: TK_DENSE_NZ(2); break;
+        case 3: TK_DENSE_NZ(3); break;
+        case 4: TK_DENSE_NZ(4); break;
+        default: break;
+    }
+    set_error("dense family supports 1<=n_u,n_z<=4 (got n_u=%d n_z=%d)", Lv->n_u, Lv->n_z);
+    return TK_ERR_UNSUPPORTED;
+}
+
+}  // namespace tk

@@ -1,0 +1,88 @@
+"""Device plumbing: torch supplies HBM allocations, the current stream and
+host<->device copies; every computation goes through libtempokkt_b200.so."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import TempoKktError
+
+F64 = torch.float64
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise TempoKktError("a CUDA device is required (no CPU fallback for the hot path)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def empty(n, *shape) -> torch.Tensor:
+    dims = (n,) + shape if shape else (n,)
+    return torch.empty(dims, dtype=F64, device=device())
+
+
+def zeros(n, *shape) -> torch.Tensor:
+    dims = (n,) + shape if shape else (n,)
+    return torch.zeros(dims, dtype=F64, device=device())
+
+
+def is_host(x) -> bool:
+    return isinstance(x, np.ndarray) or (isinstance(x, torch.Tensor) and not x.is_cuda)
+
+
+def to_device(x) -> torch.Tensor:
+    """Contiguous float64 CUDA tensor view/copy of x (numpy or torch)."""
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda and x.dtype == F64 and x.is_contiguous():
+            return x
+        return x.to(device=device(), dtype=F64).contiguous()
+    arr = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    return torch.from_numpy(arr).to(device=device(), non_blocking=False)
+
+
+def to_host(x: torch.Tensor) -> np.ndarray:
+    return x.detach().cpu().numpy()
+
+
+# kernels launched per C-ABI call (for the bench's gpu_launches claim)
+KERNELS_PER_CALL = {"tk_residual_restrict": 2, "tk_dot": 2, "tk_nrm2": 2}
+
+
+class _Instrument:
+    """Optional launch counting / per-call CUDA-event timing (bench only)."""
+
+    def __init__(self):
+        self.counting = False
+        self.launches = 0
+        self.timed = None          # set of names to wrap with events, or None
+        self.records = []          # (name, args, start_event, end_event)
+
+
+INSTR = _Instrument()
+
+
+def call(name: str, *args) -> None:
+    lib = _lib.load()
+    ins = INSTR
+    if ins.timed is not None and name in ins.timed:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rc = getattr(lib, name)(*args)
+        e1.record()
+        ins.records.append((name, args, e0, e1))
+    else:
+        rc = getattr(lib, name)(*args)
+    _lib.check(rc, name)
+    if ins.counting:
+        ins.launches += KERNELS_PER_CALL.get(name, 1)
+
+
+def P(t) -> int:
+    return None if t is None else t.data_ptr()

@@ -1,0 +1,355 @@
+"""The virtual-variable augmented (KKT) operator on the device.
+
+Mirrors the reference module kkt.py: ``StageBlocks`` (:53-80),
+``build_stage_blocks`` (:100-124), ``KktLayout`` (:127-191),
+``BlockTriKKT`` (:194-276), ``assemble_kkt`` (:279-320),
+``DiagonalSolver`` (:338-389).  Vectors are float64 CUDA tensors in the
+reference's exact time-clustered ordering; numpy inputs are accepted and
+answered with numpy (host<->device copies around the device computation).
+
+Stage data live in HBM in one of two structure families chosen at
+assembly (include/tempokkt_b200.h):
+
+* DENSE -- n_u, n_z <= 4 (van der Pol): K, C, B as [N, nu, nu|nz];
+* TRI   -- tridiagonal-in-space blocks with n_z == n_u and B = kappa*Qz
+  (P1 Burgers): K, C as [N, 3, nu] diagonals.
+
+Anything else raises :class:`UnsupportedStructure` -- there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as dev
+from .errors import DimensionMismatch, UnsupportedStructure
+from .timedisc import ProblemSpec, stage_jacobians, stage_weights
+
+FAMILY_DENSE = _lib.FAMILY_DENSE
+FAMILY_TRI = _lib.FAMILY_TRI
+MAX_DENSE = 4
+
+
+class KktLayout:
+    """Index map of the time-clustered ordering (kkt.py:127-191)."""
+
+    def __init__(self, n_steps: int, n_u: int, n_z: int):
+        self.n_steps, self.n_u, self.n_z = n_steps, n_u, n_z
+        self.first_size = 2 * n_u + n_z
+        self.interior_size = 4 * n_u + n_z
+        self.last_size = 2 * n_u
+        self.dim = n_steps * (4 * n_u + n_z)
+        n, nu, nz = n_steps, n_u, n_z
+        starts = np.empty(n + 1, dtype=np.intp)
+        starts[0] = 0
+        starts[1:] = self.first_size + np.arange(n) * self.interior_size
+        self.block_starts = starts
+        t = np.arange(1, n + 1)
+        seg = lambda off, w: off[:, None] + np.arange(w)[None, :]
+        self._rows = {
+            "u": seg(np.where(t == 1, 0, starts[t - 1] + nu), nu),
+            "v": seg(starts[t], nu),
+            "z": seg(np.where(t == 1, nu, starts[t - 1] + 2 * nu), nz),
+            "lam": seg(np.where(t == 1, nu + nz, starts[t - 1] + 3 * nu + nz), nu),
+            "mu": seg(np.where(t == n, starts[t] + nu, starts[t] + 2 * nu + nz), nu),
+        }
+
+    def rows(self, kind: str) -> np.ndarray:
+        return self._rows[kind]
+
+    def offset(self, kind: str, t: int) -> int:
+        return int(self._rows[kind][t - 1, 0])
+
+    def block_size(self, i: int) -> int:
+        if i == 0:
+            return self.first_size
+        if i == self.n_steps:
+            return self.last_size
+        return self.interior_size
+
+    def pack(self, u, v, z, lam, mu) -> np.ndarray:
+        out = np.empty(self.dim)
+        for k, a in (("u", u), ("v", v), ("z", z), ("lam", lam), ("mu", mu)):
+            out[self._rows[k]] = a
+        return out
+
+    def unpack(self, x: np.ndarray):
+        x = np.asarray(x)
+        if x.shape != (self.dim,):
+            raise DimensionMismatch(f"vector shape {x.shape} != ({self.dim},)")
+        return tuple(x[self._rows[k]] for k in ("u", "v", "z", "lam", "mu"))
+
+
+def _tri_diags(a: np.ndarray) -> np.ndarray:
+    """[3, n] (sub, diag, sup) of a tridiagonal matrix; sub[0] = sup[-1] = 0."""
+    n = a.shape[0]
+    out = np.zeros((3, n))
+    out[1] = np.diag(a)
+    out[0, 1:] = np.diag(a, -1)
+    out[2, :-1] = np.diag(a, 1)
+    return out
+
+
+def _is_tridiagonal(a: np.ndarray) -> bool:
+    return not (np.triu(a, 2).any() or np.tril(a, -2).any())
+
+
+@dataclass
+class StageBlocks:
+    """Per-stage linearisation data resident in HBM (kkt.py:53-80).
+
+    ``K``, ``C`` (and ``B`` for DENSE) are per-stage device tensors;
+    the weights are time-constant apart from the terminal stage
+    (``Qm`` for stages < N-1, ``Ql`` for stage N-1; ``Qz`` all stages).
+    """
+
+    family: int
+    n_steps: int
+    n_u: int
+    n_z: int
+    K: torch.Tensor
+    C: torch.Tensor
+    B: Optional[torch.Tensor]
+    Qm: torch.Tensor
+    Ql: torch.Tensor
+    Qz: torch.Tensor
+    Qm_inv: Optional[torch.Tensor] = None
+    Ql_inv: Optional[torch.Tensor] = None
+    Qz_inv: Optional[torch.Tensor] = None
+    kappa: float = 0.0
+    qz_cr: Optional[torch.Tensor] = None
+    host_weights: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def dim(self) -> int:
+        return self.n_steps * (4 * self.n_u + self.n_z)
+
+
+def _weights(family, q_mid, q_last, q_z, kappa):
+    """Upload the constant weights in the family's storage format."""
+    hw = dict(q_mid=q_mid, q_last=q_last, q_z=q_z)
+    if family == FAMILY_DENSE:
+        return dict(Qm=dev.to_device(q_mid), Ql=dev.to_device(q_last), Qz=dev.to_device(q_z),
+                    Qm_inv=dev.to_device(np.linalg.inv(q_mid)),
+                    Ql_inv=dev.to_device(np.linalg.inv(q_last)),
+                    Qz_inv=dev.to_device(np.linalg.inv(q_z)), kappa=0.0, qz_cr=None,
+                    host_weights=hw)
+    qz3 = np.ascontiguousarray(_tri_diags(q_z))
+    cr = np.empty_like(qz3)
+    _lib.check(_lib.load().tk_cr_scalar_factor(q_z.shape[0], qz3.ctypes.data, cr.ctypes.data),
+               "tk_cr_scalar_factor")
+    return dict(Qm=dev.to_device(_tri_diags(q_mid)), Ql=dev.to_device(_tri_diags(q_last)),
+                Qz=dev.to_device(qz3), kappa=float(kappa), qz_cr=dev.to_device(cr),
+                host_weights=hw)
+
+
+def _problem_weights(p: ProblemSpec, dt: float, n: int):
+    q_mid, _, q_z = stage_weights(p, dt, 0, max(n, 2))
+    q_last, _, _ = stage_weights(p, dt, n - 1, n)
+    return np.ascontiguousarray(q_mid), np.ascontiguousarray(q_last), np.ascontiguousarray(q_z)
+
+
+def _choose_family(n_u, n_z, q_mid, q_z, kappa_ok):
+    if n_u <= MAX_DENSE and n_z <= MAX_DENSE:
+        return FAMILY_DENSE
+    if n_z == n_u and _is_tridiagonal(q_mid) and _is_tridiagonal(q_z) and kappa_ok:
+        return FAMILY_TRI
+    raise UnsupportedStructure(
+        f"stage blocks with n_u={n_u}, n_z={n_z} are neither small dense (<= {MAX_DENSE}) "
+        "nor tridiagonal with B = kappa*Qz")
+
+
+def build_stage_blocks(p: ProblemSpec, dt: float, u_seq, v_seq, z_seq) -> StageBlocks:
+    """Linearise every stage at (u, v, z) with spacing dt (kkt.py:100-124).
+
+    Built-in problems (``p.native``) are linearised on the device by
+    tk_stage_vanderpol / tk_stage_burgers; other specs go through their
+    Python callables once (setup) and are uploaded.
+    """
+    n = int(np.shape(u_seq)[0])
+    nu, nz = p.n_u, p.n_z
+    q_mid, q_last, q_z = _problem_weights(p, dt, n)
+    nat = p.native
+    if nat is not None and nat["kind"] == "vanderpol":
+        u = dev.to_device(u_seq)
+        v = dev.to_device(v_seq)
+        z = dev.to_device(z_seq)
+        u0 = dev.to_device(p.u0)
+        K = dev.empty(n, nu, nu)
+        Cm = dev.empty(n, nu, nu)
+        B = dev.empty(n, nu, nz)
+        dev.call("tk_stage_vanderpol", n, dt, p.theta, nat["mu"], nz, dev.P(u0), dev.P(u),
+                 dev.P(v), dev.P(z), dev.P(K), dev.P(Cm), dev.P(B), dev.stream())
+        w = _weights(FAMILY_DENSE, q_mid, q_last, q_z, 0.0)
+        return StageBlocks(FAMILY_DENSE, n, nu, nz, K, Cm, B, **w)
+    if nat is not None and nat["kind"] == "burgers":
+        # F_z = M and w_control = alpha*M  =>  B = dt*M = kappa*Qz, kappa = 1/alpha
+        kappa = float(p.mass[0, 0] / p.w_control[0, 0])
+        u = dev.to_device(u_seq)
+        v = dev.to_device(v_seq)
+        u0 = dev.to_device(p.u0)
+        K = dev.empty(n, 3, nu)
+        Cm = dev.empty(n, 3, nu)
+        dev.call("tk_stage_burgers", n, nu, dt, p.theta, nat["nu"], dev.P(u0), dev.P(u),
+                 dev.P(v), dev.P(K), dev.P(Cm), dev.stream())
+        w = _weights(FAMILY_TRI, q_mid, q_last, q_z, kappa)
+        return StageBlocks(FAMILY_TRI, n, nu, nz, K, Cm, None, **w)
+    # generic ProblemSpec: evaluate the callables once on the host
+    u_seq, v_seq, z_seq = (np.asarray(a, dtype=np.float64) for a in (u_seq, v_seq, z_seq))
+    k = np.empty((n, nu, nu)); c = np.empty((n, nu, nu)); b = np.empty((n, nu, nz))
+    v_prev = np.asarray(p.u0, dtype=np.float64)
+    for i in range(n):
+        k[i], c[i], b[i] = stage_jacobians(p, v_prev, u_seq[i], z_seq[i], dt)
+        v_prev = v_seq[i]
+    qu = np.empty((n, nu, nu)); qz = np.empty((n, nz, nz))
+    for i in range(n):
+        qu[i], _, qz[i] = stage_weights(p, dt, i, n)
+    return stage_blocks_from_arrays(k, c, b, qu, qu, qz)
+
+
+def stage_blocks_from_arrays(k, c, b, q_u, q_v, q_z) -> StageBlocks:
+    """Upload reference-layout StageBlocks arrays (kkt.py:63-68) after
+    checking the time structure of the weights and choosing the family."""
+    k, c, b, q_u, q_v, q_z = (np.ascontiguousarray(a, dtype=np.float64)
+                              for a in (k, c, b, q_u, q_v, q_z))
+    n, nu, nz = k.shape[0], k.shape[1], b.shape[2]
+    if not np.array_equal(q_u, q_v):
+        raise UnsupportedStructure("q_u and q_v must be equal (timedisc.py:206)")
+    if n > 1 and not (q_u[:-1] == q_u[0]).all():
+        raise UnsupportedStructure("q_u must be time-constant before the last stage")
+    if not (q_z == q_z[0]).all():
+        raise UnsupportedStructure("q_z must be time-constant")
+    q_mid, q_last, qz = q_u[0], q_u[-1], q_z[0]
+    kappa, kappa_ok = 0.0, False
+    if nz == nu and qz[0, 0] != 0.0:
+        kappa = float(b[0, 0, 0] / qz[0, 0])
+        kappa_ok = bool(np.allclose(b, kappa * qz[None], rtol=0.0,
+                                    atol=1e-13 * max(np.abs(b).max(), 1e-300)))
+    fam = _choose_family(nu, nz, q_mid, qz, kappa_ok)
+    if fam == FAMILY_DENSE:
+        w = _weights(fam, q_mid, q_last, qz, 0.0)
+        return StageBlocks(fam, n, nu, nz, dev.to_device(k), dev.to_device(c),
+                           dev.to_device(b), **w)
+    if not all(_is_tridiagonal(a) for a in (k[i] for i in range(n))) or \
+            not all(_is_tridiagonal(a) for a in (c[i] for i in range(n))):
+        raise UnsupportedStructure("K_i / C_i are not tridiagonal")
+    kd = np.stack([_tri_diags(k[i]) for i in range(n)])
+    cd = np.stack([_tri_diags(c[i]) for i in range(n)])
+    w = _weights(fam, q_mid, q_last, qz, kappa)
+    return StageBlocks(fam, n, nu, nz, dev.to_device(kd), dev.to_device(cd), None, **w)
+
+
+class BlockTriKKT:
+    """Symmetric block-tridiagonal augmented operator on the device
+    (kkt.py:194-276).  ``apply``/``residual``/``apply_diag`` launch the
+    CUDA kernels; numpy in -> numpy out."""
+
+    def __init__(self, stage: StageBlocks):
+        self.stage = stage
+        self.n_steps, self.n_u, self.n_z = stage.n_steps, stage.n_u, stage.n_z
+        self._layout = None
+        s = stage
+        self.level = _lib.TkLevel(
+            family=s.family, n_steps=s.n_steps, n_u=s.n_u, n_z=s.n_z,
+            K=dev.P(s.K), C=dev.P(s.C), B=dev.P(s.B), Qm=dev.P(s.Qm), Ql=dev.P(s.Ql),
+            Qz=dev.P(s.Qz), Qm_inv=dev.P(s.Qm_inv), Ql_inv=dev.P(s.Ql_inv),
+            Qz_inv=dev.P(s.Qz_inv), kappa=s.kappa, qz_cr=dev.P(s.qz_cr))
+        self.lref = C.byref(self.level)
+
+    @property
+    def dim(self) -> int:
+        return self.stage.dim
+
+    @property
+    def family(self) -> int:
+        return self.stage.family
+
+    @property
+    def layout(self) -> KktLayout:
+        if self._layout is None:
+            self._layout = KktLayout(self.n_steps, self.n_u, self.n_z)
+        return self._layout
+
+    def _chk(self, x):
+        if x.shape != (self.dim,):
+            raise DimensionMismatch(f"vector shape {tuple(x.shape)} != ({self.dim},)")
+
+    def apply(self, x, out=None):
+        """y = A x (kkt.py:228)."""
+        host = dev.is_host(x)
+        x = dev.to_device(x)
+        self._chk(x)
+        y = dev.empty(self.dim) if out is None else out
+        dev.call("tk_kkt_apply", self.lref, dev.P(x), dev.P(y), dev.stream())
+        return dev.to_host(y) if host else y
+
+    def residual(self, b, x, out=None):
+        """r = b - A x."""
+        host = dev.is_host(b)
+        b, x = dev.to_device(b), dev.to_device(x)
+        self._chk(b); self._chk(x)
+        r = dev.empty(self.dim) if out is None else out
+        dev.call("tk_kkt_residual", self.lref, dev.P(b), dev.P(x), dev.P(r), dev.stream())
+        return dev.to_host(r) if host else r
+
+    def apply_diag(self, x, out=None):
+        """y = D x (block diagonal part, kkt.py:400-410)."""
+        host = dev.is_host(x)
+        x = dev.to_device(x)
+        self._chk(x)
+        y = dev.empty(self.dim) if out is None else out
+        dev.call("tk_kkt_apply_diag", self.lref, dev.P(x), dev.P(y), dev.stream())
+        return dev.to_host(y) if host else y
+
+    def as_operator(self):
+        from .krylov import LinearOperator
+        return LinearOperator(dim=self.dim, apply=self.apply)
+
+    def materialize(self) -> np.ndarray:
+        """Dense matrix by applying A to the unit vectors (small N only)."""
+        if self.dim > 6000:
+            raise ValueError("materialize is meant for small desk instances")
+        eye = torch.eye(self.dim, dtype=dev.F64, device=dev.device())
+        cols = [self.apply(eye[j].contiguous()) for j in range(self.dim)]
+        return dev.to_host(torch.stack(cols, dim=1))
+
+
+def assemble_kkt(s: StageBlocks, nu: Optional[int] = None,
+                 nz: Optional[int] = None) -> BlockTriKKT:
+    """kkt.py:279-320 -- the operator is matrix-free over the stage data."""
+    if (nu is not None and nu != s.n_u) or (nz is not None and nz != s.n_z):
+        raise DimensionMismatch("stage blocks do not match the stated dimensions")
+    return BlockTriKKT(s)
+
+
+class DiagonalSolver:
+    """D^{-1} over all block rows (kkt.py:338-389), one exact local KKT solve
+    per time interval on the device (no explicit inverses are formed)."""
+
+    def __init__(self, a: BlockTriKKT):
+        self.a = a
+        self.layout = a.layout if a.dim <= 1 << 22 else None
+        self.n_steps = a.n_steps
+
+    def solve_all(self, r, out=None):
+        host = dev.is_host(r)
+        r = dev.to_device(r)
+        self.a._chk(r)
+        y = dev.empty(self.a.dim) if out is None else out
+        dev.call("tk_diag_solve", self.a.lref, dev.P(r), dev.P(y), dev.stream())
+        return dev.to_host(y) if host else y
+
+    def solve_block(self, i: int, r_block):
+        """Solve one diagonal block (convenience; embeds it in a full vector)."""
+        lay = self.a.layout
+        s, w = lay.block_starts[i], lay.block_size(i)
+        full = np.zeros(self.a.dim)
+        full[s:s + w] = np.asarray(dev.to_host(r_block) if isinstance(r_block, torch.Tensor)
+                                   else r_block)
+        return dev.to_host(self.solve_all(dev.to_device(full)))[s:s + w]

@@ -1,0 +1,236 @@
+"""Right-preconditioned (F)GMRES with device-resident Krylov bases
+(reference krylov.py:77-210).
+
+Same algorithm, stopping rules and reports as the reference -- modified
+Gram-Schmidt Arnoldi, Givens rotations, restarts, happy-breakdown test --
+so iteration counts and residual histories match it.  The basis V (and Z
+for FGMRES) live in HBM; every vector operation is a libtempokkt_b200.so
+kernel (deterministic reductions) and only the Hessenberg scalars come back
+to the host.  numpy right-hand sides are accepted (the solution is returned
+as numpy).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as dev
+from .errors import Breakdown, DimensionMismatch, NonFiniteValue
+
+BREAKDOWN_TOL = 1e-14
+
+
+@dataclass
+class LinearOperator:
+    dim: int
+    apply: Callable
+
+    def __call__(self, x):
+        return self.apply(x)
+
+
+@dataclass
+class Preconditioner:
+    apply: Callable
+    is_flexible: bool = False
+
+    def __call__(self, r):
+        return self.apply(r)
+
+
+@dataclass
+class SolveReport:
+    iterations: int
+    residual_history: list = field(default_factory=list)
+    converged: bool = False
+    final_relative_residual: float = float("nan")
+
+
+class VecOps:
+    """Thin wrapper over the BLAS-1 kernels with a reusable scalar buffer."""
+
+    def __init__(self):
+        lib = _lib.load()
+        self.work = dev.empty(int(lib.tk_reduce_work_len()))
+        self.scal = dev.empty(8)
+
+    def dot_dev(self, x, y, slot=0):
+        dev.call("tk_dot", x.numel(), dev.P(x), dev.P(y), self.scal[slot:].data_ptr(),
+                 dev.P(self.work), dev.stream())
+        return self.scal[slot]
+
+    def dot(self, x, y) -> float:
+        return float(self.dot_dev(x, y).item())
+
+    def nrm2(self, x) -> float:
+        dev.call("tk_nrm2", x.numel(), dev.P(x), self.scal.data_ptr(), dev.P(self.work),
+                 dev.stream())
+        return float(self.scal[0].item())
+
+    def axpy(self, a, x, y):
+        dev.call("tk_axpy", x.numel(), float(a), dev.P(x), dev.P(y), dev.stream())
+
+    def scale_into(self, a, x, y):
+        dev.call("tk_scale_into", x.numel(), float(a), dev.P(x), dev.P(y), dev.stream())
+
+    def gemv_t_add(self, V, c, x):
+        """x += V[:k]^T c (V rows contiguous)."""
+        k = int(c.numel())
+        if k == 0:
+            return
+        cd = dev.to_device(c)
+        dev.call("tk_gemv_t_add", x.numel(), k, dev.P(V), V.stride(0), dev.P(cd), dev.P(x),
+                 dev.stream())
+
+
+_OPS = None
+
+
+def vec_ops() -> VecOps:
+    global _OPS
+    if _OPS is None:
+        _OPS = VecOps()
+    return _OPS
+
+
+def _as_prec(prec):
+    if prec is None or isinstance(prec, Preconditioner):
+        return prec
+    return Preconditioner(apply=prec)
+
+
+def _residual(op, b, x):
+    """r = b - op(x) with the rsub kernel (op(x) is a fresh tensor)."""
+    y = dev.to_device(op(x))
+    dev.call("tk_rsub", y.numel(), dev.P(b), dev.P(y), dev.stream())
+    return y
+
+
+def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
+    if not (0.0 < rel_tol < 1.0):
+        raise ValueError(f"rel_tol must lie in (0,1), got {rel_tol}")
+    n = op.dim
+    host = dev.is_host(b)
+    b = dev.to_device(b)
+    if b.shape != (n,):
+        raise DimensionMismatch(f"rhs shape {tuple(b.shape)} != operator dim {n}")
+    ops = vec_ops()
+    prec = _as_prec(prec)
+    if restart is None:
+        restart = max_iters
+    if restart < 1:
+        raise ValueError("restart must be >= 1")
+    if x0 is None:
+        x = dev.zeros(n)
+        r = b.clone()                      # b - A*0, bitwise
+    else:
+        x = dev.to_device(x0).clone()
+        if x.shape != (n,):
+            raise DimensionMismatch(f"x0 shape {tuple(x.shape)} != operator dim {n}")
+        r = _residual(op, b, x)
+    beta0 = ops.nrm2(r)
+    if not math.isfinite(beta0):
+        raise NonFiniteValue("non-finite initial residual")
+    history = [beta0]
+    if beta0 == 0.0:
+        rep = SolveReport(0, history, True, 0.0)
+        return (dev.to_host(x) if host else x), rep
+    target = rel_tol * beta0
+    total = 0
+    beta = beta0
+    while True:
+        if beta <= target:
+            break
+        m = min(restart, max_iters - total)
+        if m <= 0:
+            break
+        V = torch.empty((m + 1, n), dtype=dev.F64, device=b.device)
+        Z = torch.empty((m, n), dtype=dev.F64, device=b.device) \
+            if (flexible and prec is not None) else None
+        H = np.zeros((m + 1, m)); cs = np.zeros(m); sn = np.zeros(m)
+        g = np.zeros(m + 1)
+        g[0] = beta
+        ops.scale_into(1.0 / beta, r, V[0])
+        jd = 0
+        broke = False
+        for j in range(m):
+            if prec is None:
+                zj = V[j]
+            else:
+                zj = prec(V[j])
+                if Z is not None:
+                    Z[j].copy_(zj)
+                    zj = Z[j]
+            w = op(zj)
+            for i in range(j + 1):
+                hij = ops.dot(V[i], w)
+                H[i, j] = hij
+                ops.axpy(-hij, V[i], w)
+            hj1 = ops.nrm2(w)
+            H[j + 1, j] = hj1
+            if not math.isfinite(hj1) or not np.isfinite(H[:j + 1, j]).all():
+                raise NonFiniteValue("non-finite Hessenberg entry in Arnoldi")
+            for i in range(j):
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            den = float(np.hypot(H[j, j], H[j + 1, j]))
+            if den == 0.0:
+                raise Breakdown("zero diagonal in Givens elimination")
+            cs[j] = H[j, j] / den
+            sn[j] = H[j + 1, j] / den
+            H[j, j] = den
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            total += 1
+            jd = j + 1
+            est = abs(g[j + 1])
+            history.append(est)
+            if hj1 <= BREAKDOWN_TOL * beta0:
+                broke = True
+                break
+            if est <= target or total >= max_iters:
+                break
+            ops.scale_into(1.0 / hj1, w, V[j + 1])
+        if jd > 0:
+            y = np.zeros(jd)
+            for i in range(jd - 1, -1, -1):
+                y[i] = (g[i] - H[i, i + 1:jd] @ y[i + 1:jd]) / H[i, i]
+            yt = torch.from_numpy(y)
+            if Z is not None:
+                ops.gemv_t_add(Z, yt, x)
+            else:
+                vy = dev.zeros(n)
+                ops.gemv_t_add(V, yt, vy)
+                ops.axpy(1.0, vy if prec is None else dev.to_device(prec(vy)), x)
+        del V, Z
+        r = _residual(op, b, x)
+        true_norm = ops.nrm2(r)
+        beta = true_norm
+        if broke and true_norm > max(target, 10 * BREAKDOWN_TOL * beta0):
+            raise Breakdown("zero Arnoldi norm with nonzero residual")
+        if true_norm <= target or total >= max_iters or broke:
+            break
+    if not bool(torch.isfinite(x).all()):
+        raise NonFiniteValue("non-finite solution vector")
+    final_rel = ops.nrm2(_residual(op, b, x)) / beta0
+    report = SolveReport(iterations=total, residual_history=history,
+                         converged=final_rel <= rel_tol, final_relative_residual=final_rel)
+    return (dev.to_host(x) if host else x), report
+
+
+def gmres(op, prec, b, x0=None, rel_tol=1e-10, max_iters=401, restart=None):
+    """Restarted right-preconditioned GMRES (krylov.py:194-201)."""
+    return _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible=False)
+
+
+def fgmres(op, prec, b, x0=None, rel_tol=1e-10, max_iters=401, restart=None):
+    """Flexible GMRES (krylov.py:204-210)."""
+    return _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible=True)

@@ -36,3 +36,31 @@ def oracle_problem(g):
 @pytest.fixture(params=CASES)
 def golden_case(request):
     return request.param, load_golden(request.param)
+
+
+def product_problem(g):
+    """The product-side ProblemSpec + TimeGrid for a golden case."""
+    import paper_2405_04808_b200 as P
+    n, T = int(g["n"]), float(g["t_final"])
+    grid = P.TimeGrid(T, n)
+    if "n_controls" in g:
+        cfg = P.VanDerPolConfig(mu=float(g["mu"]), alpha=float(g["alpha"]),
+                                u_init=tuple(g["u0"]), n_controls=int(g["n_controls"]))
+        return P.build_vanderpol(cfg, grid, theta=float(g["theta"]), with_targets=False), grid
+    cfg = P.BurgersConfig(nu=float(g["nu"]), alpha=float(g["alpha"]), n_elems=int(g["n_u"]) + 1,
+                          theta=float(g["theta"]), u0_kind=str(g["u0_kind"]))
+    return P.build_burgers(cfg, grid), grid
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def have_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False

@@ -1,0 +1,76 @@
+"""CPU tests of the C-ABI boundary: the library loads, exports every symbol
+declared in include/tempokkt_b200.h, and its host routines (forward march,
+scalar cyclic-reduction factor) agree with the reference's golden vectors."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden, product_problem, rel, CASES
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "tempokkt_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(tk_\w+)\s*\(", src, re.M)))
+
+
+def test_library_exports_header():
+    from paper_2405_04808_b200 import _lib
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.EXPORTED)
+    assert lib.tk_version().startswith(b"tempokkt_b200")
+    assert lib.tk_kkt_dim(7, 2, 1) == 7 * 9
+
+
+def test_null_args_rejected_without_gpu():
+    from paper_2405_04808_b200 import _lib
+    lib = _lib.load()
+    assert lib.tk_kkt_apply(None, None, None, None) == _lib.TK_ERR_ARG
+    assert lib.tk_restrict(3, 2, 1, None, None, None) == _lib.TK_ERR_ARG
+    assert b"n_fine" in lib.tk_last_error() or lib.tk_last_error()
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_host_forward_march_matches_reference(name):
+    import paper_2405_04808_b200 as P
+    g = load_golden(name)
+    p, grid = product_problem(g)
+    z = g["z"] if name.startswith("cfg") else np.zeros((grid.n_steps, p.n_z))
+    tr = P.forward_solve(p, z, grid)
+    assert rel(tr.states, g["fwd_states"]) < 1e-14
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 31, 64, 100, 513])
+def test_cr_scalar_factor(n):
+    from paper_2405_04808_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(n)
+    d = 4.0 + rng.random(n)
+    e = rng.random(n)
+    e[-1] = 0.0
+    a = np.diag(d) + np.diag(e[:-1], 1) + np.diag(e[:-1], -1)
+    tri = np.zeros((3, n)); tri[1] = d; tri[2, :-1] = e[:-1]; tri[0, 1:] = e[:-1]
+    coef = np.empty((3, n))
+    assert lib.tk_cr_scalar_factor(n, tri.ctypes.data, coef.ctypes.data) == 0
+    f = rng.standard_normal(n)
+    x = np.empty(n)
+    assert lib.tk_cr_scalar_solve_host(n, coef.ctypes.data, f.ctypes.data, x.ctypes.data) == 0
+    assert np.abs(a @ x - f).max() < 1e-13
+
+
+def test_configs_match_baseline_shapes():
+    from paper_2405_04808_b200 import configs
+    s = configs.build_setup(0)
+    assert (s.grid.n_steps, s.n_u, s.n_z, s.levels) == (512, 2, 1, 3)
+    g = load_golden("cfg0_vdp")
+    assert rel(s.u, g["fwd_states"]) < 1e-14
+    assert np.array_equal(s.rhs(), np.random.default_rng(0).standard_normal(512 * 9))
+    s1 = configs.build_setup(1, nt=64, nx=16)
+    g1 = load_golden("cfg1_burgers")
+    assert rel(s1.u, g1["fwd_states"]) < 1e-14
