@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 multigrid-in-time KKT preconditioner.
+
+Metric (BASELINE.json): V-cycle time-step.DoF/s -- per V-cycle application,
+the number of time steps times the KKT unknowns per step (4 N_u + N_z),
+divided by the application time -- plus the full MG-preconditioned FGMRES
+solve time.  One "step" = one V-cycle application of the rediscretised
+hierarchy (pre-smooth, residual-restrict, recursion, SGS-GMRES coarse solve,
+prolong-correct, post-smooth) to one right-hand side resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  See DESIGN.md for the contract details.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU reference
+def oracle_sample(index: int):
+    """Bounded sample of configs[index] for the CPU reference (the oracle
+    restatement of tempokkt, dense per-block inverses as the reference)."""
+    from oracle import tk_oracle as O
+    from paper_2405_04808_b200 import configs
+    p = dict(configs.CONFIGS[index])
+    if p["problem"] == "vanderpol":
+        nt, levels = 4096, min(p["levels"], 8)
+        prob = O.vanderpol(mu=p["mu"], alpha=p["alpha"], n_controls=p["n_controls"],
+                           u0=p["u0"], theta=p["theta"])
+        nz = p["n_controls"]
+        xs = None
+    else:
+        nt, levels = 8, 3
+        prob = O.burgers(n_u=p["nx"], nu=p["nu"], alpha=p["alpha"], theta=p["theta"],
+                         u0_kind=p["u0_kind"])
+        nz = p["nx"]
+        xs = np.arange(1, p["nx"] + 1) / (p["nx"] + 1.0)
+    from paper_2405_04808_b200.timedisc import TimeGrid
+    dt_full = p["t_final"] / p["nt"]
+    grid = TimeGrid(dt_full * nt, nt)       # same dt as the full workload, fewer steps
+    pp = dict(p, nt=nt, t_final=grid.t_final)
+    z = configs._controls(pp, grid, nz, xs)
+    states = O.forward_solve(prob, z, nt, grid.dt)
+    h = O.build_hierarchy(prob, states, states, z, nt, grid.dt, levels, sweeps=1,
+                          cycle_kind="v", coarse_tol=1e-2)
+    b = np.random.default_rng(p["seed"]).standard_normal(h.levels[0].kkt.dim)
+    desc = f"configs[{index}] shape at nt={nt} (same dt, n_u, n_z), {levels}-level V(1,1)"
+    return h, b, nt * (4 * prob.n_u + prob.n_z), desc
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = max((d.get("num_threads") or 1) for d in threadpool_info())
+        return int(n)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def time_oracle(index: int, steps: int, warmup: int, budget_s: float = 20.0):
+    from oracle import tk_oracle as O
+    h, b, unknowns, desc = oracle_sample(index)
+    for _ in range(warmup):
+        O.cycle(h, 0, b)
+    t0 = time.perf_counter()
+    done = 0
+    while done < steps:
+        O.cycle(h, 0, b)
+        done += 1
+        if time.perf_counter() - t0 > budget_s and done >= 1:
+            break
+    dt = (time.perf_counter() - t0) / done
+    return unknowns / dt, desc + f", {done} timed V-cycles", done
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    torch.cuda.set_device(local_rank)
+    import paper_2405_04808_b200 as P
+    from paper_2405_04808_b200 import configs, device as dev, roofline
+    from paper_2405_04808_b200.krylov import vec_ops
+
+    if world > 1:
+        from paper_2405_04808_b200 import slabs
+        return slabs.bench_rank(args, rank, world, local_rank)
+
+    setup = configs.build_setup(args.config)
+    S = setup.solver
+    h = P.build_hierarchy(setup.problem, setup.u, setup.v, setup.z, setup.grid, setup.levels,
+                          sweeps=S["sweeps"], omega=S["omega"], cycle_kind=S["cycle"],
+                          coarse_tol=S["coarse_tol"], coarse_max_iters=S["coarse_max_iters"])
+    r_host = setup.rhs()
+    r_dev = dev.to_device(r_host)
+    prec = P.mg_preconditioner(h)
+    stream = torch.cuda.current_stream()
+    unknowns = setup.grid.n_steps * setup.dof_per_step
+
+    for _ in range(max(args.warmup, 1)):
+        prec(r_dev)
+    torch.cuda.synchronize()
+
+    # per-kernel breakdown from one untimed profiled step (events around every call)
+    names = {"tk_jacobi_sweep", "tk_residual_restrict", "tk_prolong_add", "tk_forward_subst",
+             "tk_backward_subst", "tk_kkt_apply", "tk_kkt_apply_diag", "tk_kkt_residual",
+             "tk_dot", "tk_nrm2", "tk_axpy", "tk_scale_into", "tk_rsub", "tk_gemv_t_add"}
+    dev.INSTR.timed, dev.INSTR.records = names, []
+    prec(r_dev)
+    torch.cuda.synchronize()
+    per = {}
+    for nm, a, e0, e1 in dev.INSTR.records:
+        ms = e0.elapsed_time(e1)
+        d = per.setdefault(nm, {"calls": 0, "ms": 0.0, "bytes": 0})
+        d["calls"] += 1
+        d["ms"] += ms
+        d["bytes"] += roofline.algorithmic_bytes(nm, a)
+    dev.INSTR.timed, dev.INSTR.records = None, []
+    dominant = max(per, key=lambda k: per[k]["ms"])
+
+    # timed region: K V-cycles, CUDA events on the launching stream; the
+    # dominant kernel's launches are bracketed by events for the roofline
+    clk = ClockSampler(local_rank)
+    clk.start()
+    time.sleep(0.3)
+    dev.INSTR.timed, dev.INSTR.records = {dominant, "tk_jacobi_sweep"}, []
+    dev.INSTR.counting, dev.INSTR.launches = True, 0
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        prec(r_dev)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    total_ms = e0.elapsed_time(e1)
+    launches = dev.INSTR.launches
+    recs = dev.INSTR.records
+    dev.INSTR.timed, dev.INSTR.records, dev.INSTR.counting = None, [], False
+    clocks = clk.stop()
+    ms_step = total_ms / args.steps
+    value = unknowns / (ms_step * 1e-3)
+
+    def kernel_stats(nm, fine_only=False):
+        rs = [(a, s.elapsed_time(t)) for n_, a, s, t in recs if n_ == nm]
+        if fine_only and nm == "tk_jacobi_sweep":
+            top = max(roofline.dim_of(a[0]._obj) for a, _ in rs)
+            rs = [(a, ms) for a, ms in rs if roofline.dim_of(a[0]._obj) == top]
+        byts = sum(roofline.algorithmic_bytes(nm, a) for a, _ in rs)
+        ms = sum(m for _, m in rs)
+        return byts / len(rs), ms / len(rs), len(rs)
+
+    peaks, peak_kind = load_peaks()
+    hbm = float(peaks["hbm_gbs"])
+    b_dom, ms_dom, n_dom = kernel_stats(dominant)
+    ach = b_dom / (ms_dom * 1e-3) / 1e9
+    b_j, ms_j, n_j = kernel_stats("tk_jacobi_sweep", fine_only=True)
+    ach_j = b_j / (ms_j * 1e-3) / 1e9
+
+    # e2e through the public preconditioner with pinned host buffers
+    r_pin = torch.from_numpy(r_host).pin_memory()
+    out_pin = torch.empty(r_host.shape[0], dtype=torch.float64).pin_memory()
+    e2e_steps = max(2, min(args.steps, 5))
+    for _ in range(1):
+        r_dev.copy_(r_pin, non_blocking=True)
+        out_pin.copy_(prec(r_dev), non_blocking=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        r_dev.copy_(r_pin, non_blocking=True)
+        out_pin.copy_(prec(r_dev), non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+
+    solve = None
+    if args.solve_config >= 0:
+        ss = configs.build_setup(args.solve_config)
+        S2 = ss.solver
+        h2 = P.build_hierarchy(ss.problem, ss.u, ss.v, ss.z, ss.grid, ss.levels,
+                               sweeps=S2["sweeps"], cycle_kind=S2["cycle"],
+                               coarse_tol=S2["coarse_tol"])
+        b2 = dev.to_device(ss.rhs())
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x2, rep = P.fgmres(h2.levels[0].kkt.as_operator(), P.mg_preconditioner(h2), b2,
+                           rel_tol=S2["rel_tol"], max_iters=S2["max_iters"])
+        torch.cuda.synchronize()
+        solve = {"config": f"configs[{args.solve_config}] {ss.describe()}",
+                 "seconds": round(time.perf_counter() - t0, 4), "outer": "fgmres",
+                 "iterations": rep.iterations, "final_rel_residual": rep.final_relative_residual,
+                 "coarse_iters_avg": h2.stats.average}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        v_cpu, desc, n_cpu = time_oracle(args.config, steps=3, warmup=1)
+        cpu = {"value": v_cpu, "unit": "time-step*DoF/s", "cores": cpu_threads(),
+               "kind": "port", "sample": desc}
+
+    line = {
+        "metric": "V-cycle time-step*DoF/s (fp64) + full MG-FGMRES solve time",
+        "value": value, "unit": "time-step*DoF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: forward-march linearisation + N(0,1) rhs (seeded)",
+        "config": {"workload": f"configs[{args.config}] {setup.describe()}",
+                   "n_steps": setup.grid.n_steps, "n_u": setup.n_u, "n_z": setup.n_z,
+                   "levels": setup.levels, "cycle": "V(1,1) block-Jacobi, coarse SGS-GMRES 1e-2",
+                   "kkt_dim": setup.dim, "parallelism": f"time-slabs x{world}",
+                   "l2": "inputs larger than L2" if setup.dim * 8 > 126e6 else
+                         "inputs smaller than L2 (no flush)"},
+        "e2e": {"value": unknowns / (e2e_ms * 1e-3), "unit": "time-step*DoF/s",
+                "h2d_bytes_per_step": int(r_host.nbytes), "d2h_bytes_per_step": int(r_host.nbytes),
+                "ms_per_step": e2e_ms, "api": "mg_preconditioner(h)(r) with pinned host r"},
+        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": ach,
+                     "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                     "peak_kind": peak_kind, "launches_timed": n_dom,
+                     "bytes_per_launch": b_dom, "ms_per_launch": ms_dom,
+                     "fine_jacobi": {"achieved": ach_j, "frac": ach_j / hbm,
+                                     "bytes_per_launch": b_j, "ms_per_launch": ms_j}},
+        "kernels": {k: {"calls": v["calls"], "ms": round(v["ms"], 4),
+                        "share": round(v["ms"] / sum(x["ms"] for x in per.values()), 4),
+                        "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}
+                    for k, v in sorted(per.items(), key=lambda kv: -kv[1]["ms"])},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+        "solve": solve,
+    }
+    return line
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    v, desc, n = time_oracle(args.config, steps=max(args.steps, 1), warmup=args.warmup,
+                             budget_s=60.0)
+    cores = cpu_threads()
+    return {"impl": "reference",
+            "metric": "V-cycle time-step*DoF/s (fp64) + full MG-FGMRES solve time",
+            "value": v, "unit": "time-step*DoF/s", "n_gpus": world, "steps": n,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"configs[{args.config}] (bounded CPU sample)"},
+            "cpu_baseline": {"value": v, "unit": "time-step*DoF/s", "cores": cores,
+                             "kind": "port", "sample": desc},
+            "e2e": {"value": v, "unit": "time-step*DoF/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--solve-config", type=int, default=1)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local_rank)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

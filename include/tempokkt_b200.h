@@ -68,6 +68,13 @@ typedef struct tk_level {
     const double* Qz_inv;
     double kappa;
     const double* qz_cr;
+    /* Optional Gauss-Seidel acceleration data (see tk_subst_factor):
+     * fac     precomputed local-solve factors   (tk_subst_factor_len doubles)
+     * scratch coupling-chain buffer             (tk_subst_scratch_len doubles)
+     * When both are set, tk_forward_subst / tk_backward_subst run as
+     * parallel solve -> serial n_u-vector chain -> parallel solve. */
+    double* fac;
+    double* scratch;
 } tk_level;
 
 /* --- library ------------------------------------------------------------ */
@@ -98,6 +105,13 @@ int tk_jacobi_sweep(const tk_level* L, const double* b, const double* x_in, doub
 int tk_forward_subst(const tk_level* L, const double* r, double* delta, void* stream);
 /* (D - U) delta = r, serial in time   replaces _backward_subst smoothers.py:95 */
 int tk_backward_subst(const tk_level* L, const double* r, double* delta, void* stream);
+/* Sizes (in doubles) of L->fac and L->scratch, and the one-off factorisation
+ * filling L->fac (TRI: per-interval cyclic-reduction factors of the (u,lam)
+ * system + C_i; DENSE: the n_u x n_u chain matrices P_u D_i^{-1} E_mu and
+ * P_mu D_i^{-1} E_u).  Built once per level (kkt.py:338 DiagonalSolver). */
+int64_t tk_subst_factor_len(const tk_level* L);
+int64_t tk_subst_scratch_len(const tk_level* L);
+int tk_subst_factor(const tk_level* L, void* stream);
 
 /* --- transfers (multigrid.py:272-300) ------------------------------------- */
 /* xc = R xf  (injection for u,v,lam,mu; 2-interval average for z)    restrict_kkt multigrid.py:272 */

@@ -36,6 +36,7 @@ class TkLevel(C.Structure):
         ("Qm", _p), ("Ql", _p), ("Qz", _p),
         ("Qm_inv", _p), ("Ql_inv", _p), ("Qz_inv", _p),
         ("kappa", _d), ("qz_cr", _p),
+        ("fac", _p), ("scratch", _p),
     ]
 
 
@@ -51,6 +52,9 @@ _SIGS = {
     "tk_jacobi_sweep": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _d, _p]),
     "tk_forward_subst": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
     "tk_backward_subst": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
+    "tk_subst_factor_len": (_i64, [C.POINTER(TkLevel)]),
+    "tk_subst_scratch_len": (_i64, [C.POINTER(TkLevel)]),
+    "tk_subst_factor": (C.c_int, [C.POINTER(TkLevel), _p]),
     "tk_restrict": (C.c_int, [_i32, _i32, _i32, _p, _p, _p]),
     "tk_prolong_add": (C.c_int, [_i32, _i32, _i32, _p, _p, _p]),
     "tk_residual_restrict": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p, _p]),

@@ -26,6 +26,10 @@ int check_launch(const char* where) { return cuda_status(cudaGetLastError(), whe
 int dense_launch(const tk_level*, int, const double*, const double*, double*, double, cudaStream_t);
 int tri_launch(const tk_level*, int, const double*, const double*, double*, double, cudaStream_t);
 int64_t tri_smem_bytes(int n);
+int64_t tri_fac_len(const tk_level*);
+int64_t tri_scratch_len(const tk_level*);
+int64_t dense_fac_len(const tk_level*);
+int64_t dense_scratch_len(const tk_level*);
 int transfer_launch(int, int, int, int, const double*, double*, cudaStream_t);
 int64_t reduce_work_len();
 int dot_launch(int64_t, const double*, const double*, double*, double*, int, cudaStream_t);
@@ -120,6 +124,20 @@ int tk_forward_subst(const tk_level* L, const double* r, double* delta, void* st
 int tk_backward_subst(const tk_level* L, const double* r, double* delta, void* stream) {
     TK_CHECK_ARG(r && delta && r != delta, "tk_backward_subst: bad vectors");
     return level_op(L, 11, 11, r, nullptr, delta, 1.0, stream);
+}
+
+int64_t tk_subst_factor_len(const tk_level* L) {
+    if (check_level(L)) return -1;
+    return L->family == TK_FAMILY_DENSE ? dense_fac_len(L) : tri_fac_len(L);
+}
+
+int64_t tk_subst_scratch_len(const tk_level* L) {
+    if (check_level(L)) return -1;
+    return L->family == TK_FAMILY_DENSE ? dense_scratch_len(L) : tri_scratch_len(L);
+}
+
+int tk_subst_factor(const tk_level* L, void* stream) {
+    return level_op(L, 12, 12, nullptr, nullptr, nullptr, 1.0, stream);
 }
 
 int tk_restrict(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xf, double* xc,

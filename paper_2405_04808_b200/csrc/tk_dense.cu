@@ -369,6 +369,178 @@ __global__ void dense_subst(DView<NU, NZ> V, const double* __restrict__ r, doubl
     }
 }
 
+// ---------------------------------------------------------------------------
+// Gauss-Seidel substitution as parallel solve -> chain -> parallel solve.
+// Forward: u_i = a_i^u - G_i u_{i-1} with G_i = P_u D_i^{-1} E_mu; backward:
+// mu_i = a_i^mu - H_i mu_{i+1} with H_i = P_mu D_i^{-1} E_u (nu x nu, built
+// once by dense_factor).  The affine chain is evaluated by one CTA as a
+// chunked parallel scan of map compositions.
+// ---------------------------------------------------------------------------
+template <int NU, int NZ>
+__global__ void dense_factor(DView<NU, NZ> V, double* __restrict__ fac) {
+    const Lay& L = V.lay;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= L.N; i += gridDim.x * blockDim.x) {
+        double* G = fac + (size_t)i * 2 * NU * NU;
+        double* H = G + NU * NU;
+        for (int e = 0; e < 2 * NU * NU; ++e) G[e] = 0.0;
+        if (i == 0 || i == L.N) continue;
+#pragma unroll
+        for (int k = 0; k < NU; ++k) {
+            Seg<NU, NZ> r, d;
+            load_seg<NU, NZ>(L, i, nullptr, r);
+            r.m[k] = 1.0;
+            solve_row<NU, NZ>(V, i, r, d);
+#pragma unroll
+            for (int e = 0; e < NU; ++e) G[e * NU + k] = d.u[e];
+            load_seg<NU, NZ>(L, i, nullptr, r);
+            r.u[k] = 1.0;
+            solve_row<NU, NZ>(V, i, r, d);
+#pragma unroll
+            for (int e = 0; e < NU; ++e) H[e * NU + k] = d.m[e];
+        }
+    }
+}
+
+template <int NU>
+struct Aff {  // x -> P x + p
+    double P[NU][NU];
+    double p[NU];
+};
+
+template <int NU>
+__device__ __forceinline__ void aff_compose(const Aff<NU>& second, const Aff<NU>& first,
+                                            Aff<NU>& out) {
+#pragma unroll
+    for (int r = 0; r < NU; ++r) {
+        double s = second.p[r];
+#pragma unroll
+        for (int c = 0; c < NU; ++c) {
+            double t = 0.0;
+#pragma unroll
+            for (int k = 0; k < NU; ++k) t += second.P[r][k] * first.P[k][c];
+            out.P[r][c] = t;
+            s += second.P[r][c] * first.p[c];
+        }
+        out.p[r] = s;
+    }
+}
+
+template <int NU>
+struct ScanT { static constexpr int value = NU <= 2 ? 256 : 64; };
+
+template <int NU, bool FWD>
+__global__ void __launch_bounds__(ScanT<NU>::value) dense_chain(Lay L, const double* __restrict__ a,
+                                                            const double* __restrict__ fac,
+                                                            double* __restrict__ chain) {
+    constexpr int kScanThreads = ScanT<NU>::value;
+    __shared__ Aff<NU> maps[2][kScanThreads];
+    const int N = L.N, tid = threadIdx.x;
+    const int M = N - 1;
+    const int c = (M + kScanThreads - 1) / kScanThreads;
+    const int lo = tid * c, hi = min(M, lo + c);
+    auto blk = [&](int k) { return FWD ? 1 + k : N - 1 - k; };
+    auto aseg = [&](int i) { return a + (FWD ? L.off_u(i) : L.off_mu(i)); };
+    auto mat = [&](int i) { return fac + (size_t)i * 2 * NU * NU + (FWD ? 0 : NU * NU); };
+    double x0[NU];
+    {
+        const double* s0 = aseg(FWD ? 0 : N);
+#pragma unroll
+        for (int e = 0; e < NU; ++e) x0[e] = s0[e];
+        if (tid == 0) {
+#pragma unroll
+            for (int e = 0; e < NU; ++e) chain[(size_t)(FWD ? 0 : N) * NU + e] = x0[e];
+        }
+    }
+    Aff<NU> F;
+#pragma unroll
+    for (int r = 0; r < NU; ++r) {
+        F.p[r] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NU; ++q) F.P[r][q] = (r == q) ? 1.0 : 0.0;
+    }
+    for (int k = lo; k < hi; ++k) {   // F <- (x -> a - G x) o F
+        const int i = blk(k);
+        const double* G = mat(i);
+        const double* ai = aseg(i);
+        Aff<NU> S, T;
+#pragma unroll
+        for (int r = 0; r < NU; ++r) {
+            S.p[r] = ai[r];
+#pragma unroll
+            for (int q = 0; q < NU; ++q) S.P[r][q] = -G[r * NU + q];
+        }
+        aff_compose<NU>(S, F, T);
+        F = T;
+    }
+    maps[0][tid] = F;
+    __syncthreads();
+    int src = 0;
+    for (int d = 1; d < kScanThreads; d <<= 1) {   // inclusive Hillis-Steele scan
+        if (tid >= d) aff_compose<NU>(maps[src][tid], maps[src][tid - d], maps[src ^ 1][tid]);
+        else maps[src ^ 1][tid] = maps[src][tid];
+        src ^= 1;
+        __syncthreads();
+    }
+    double x[NU];
+    if (tid == 0) {
+#pragma unroll
+        for (int e = 0; e < NU; ++e) x[e] = x0[e];
+    } else {
+        const Aff<NU>& S = maps[src][tid - 1];
+#pragma unroll
+        for (int r = 0; r < NU; ++r) {
+            double s = S.p[r];
+#pragma unroll
+            for (int q = 0; q < NU; ++q) s += S.P[r][q] * x0[q];
+            x[r] = s;
+        }
+    }
+    for (int k = lo; k < hi; ++k) {
+        const int i = blk(k);
+        const double* G = mat(i);
+        const double* ai = aseg(i);
+        double y[NU];
+#pragma unroll
+        for (int r = 0; r < NU; ++r) {
+            double s = ai[r];
+#pragma unroll
+            for (int q = 0; q < NU; ++q) s -= G[r * NU + q] * x[q];
+            y[r] = s;
+        }
+#pragma unroll
+        for (int r = 0; r < NU; ++r) {
+            x[r] = y[r];
+            chain[(size_t)i * NU + r] = y[r];
+        }
+    }
+}
+
+template <int NU, int NZ, bool FWD>
+__global__ void __launch_bounds__(128) dense_rows_cpl(DView<NU, NZ> V, const double* __restrict__ r,
+                                                      const double* __restrict__ chain,
+                                                      double* __restrict__ y) {
+    const Lay& L = V.lay;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= L.N; i += gridDim.x * blockDim.x) {
+        Seg<NU, NZ> rs, ds;
+        load_seg<NU, NZ>(L, i, r, rs);
+        if (FWD && i >= 1) {
+#pragma unroll
+            for (int e = 0; e < NU; ++e) rs.m[e] -= chain[(size_t)(i - 1) * NU + e];
+        }
+        if (!FWD && i < L.N) {
+#pragma unroll
+            for (int e = 0; e < NU; ++e) rs.u[e] -= chain[(size_t)(i + 1) * NU + e];
+        }
+        solve_row<NU, NZ>(V, i, rs, ds);
+        store_seg<NU, NZ>(L, i, y, ds);
+    }
+}
+
+int64_t dense_fac_len(const tk_level* Lv) {
+    return (int64_t)(Lv->n_steps + 1) * 2 * Lv->n_u * Lv->n_u;
+}
+int64_t dense_scratch_len(const tk_level* Lv) { return (int64_t)(Lv->n_steps + 1) * Lv->n_u; }
+
 template <int NU, int NZ>
 static int dense_launch_t(const tk_level* Lv, int op, const double* b, const double* x, double* y,
                           double omega, cudaStream_t s) {
@@ -383,8 +555,28 @@ static int dense_launch_t(const tk_level* Lv, int op, const double* b, const dou
         case D_RESIDUAL: dense_rows<NU, NZ, D_RESIDUAL><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
         case D_SOLVE: dense_rows<NU, NZ, D_SOLVE><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
         case D_JACOBI: dense_rows<NU, NZ, D_JACOBI><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
-        case 10: dense_subst<NU, NZ, true><<<1, 1, 0, s>>>(V, b, y); break;
-        case 11: dense_subst<NU, NZ, false><<<1, 1, 0, s>>>(V, b, y); break;
+        case 10:
+        case 11: {
+            const bool fwd = op == 10;
+            if (!Lv->fac || !Lv->scratch) {
+                if (fwd) dense_subst<NU, NZ, true><<<1, 1, 0, s>>>(V, b, y);
+                else dense_subst<NU, NZ, false><<<1, 1, 0, s>>>(V, b, y);
+                break;
+            }
+            dense_rows<NU, NZ, D_SOLVE><<<grid, th, 0, s>>>(V, b, nullptr, y, 1.0);
+            if (fwd) {
+                dense_chain<NU, true><<<1, ScanT<NU>::value, 0, s>>>(V.lay, y, Lv->fac, Lv->scratch);
+                dense_rows_cpl<NU, NZ, true><<<grid, th, 0, s>>>(V, b, Lv->scratch, y);
+            } else {
+                dense_chain<NU, false><<<1, ScanT<NU>::value, 0, s>>>(V.lay, y, Lv->fac, Lv->scratch);
+                dense_rows_cpl<NU, NZ, false><<<grid, th, 0, s>>>(V, b, Lv->scratch, y);
+            }
+            break;
+        }
+        case 12:
+            if (!Lv->fac) { set_error("tk_subst_factor: level has no fac buffer"); return TK_ERR_ARG; }
+            dense_factor<NU, NZ><<<grid, th, 0, s>>>(V, Lv->fac);
+            break;
         default: set_error("dense: bad op %d", op); return TK_ERR_ARG;
     }
     return check_launch("dense_rows");

@@ -11,10 +11,15 @@
 //   z   = w - k lam,   mu = Qv v + C^T lam - r_v
 // using B = k Qz (k = kappa; Burgers: F_z = M, w_control = alpha M, k = 1/alpha).
 // The (u,lam) system is symmetric quasi-definite, so cyclic reduction needs
-// no pivoting.  All reductions run in shared memory (16 doubles per node).
+// no pivoting.  All reductions run in shared memory; node j lives at the
+// padded index PI(j) = j + j/16, which keeps every stride-2^l reduction
+// level free of (or at most 2-way) bank conflicts.
 #include "tk_common.cuh"
 
 namespace tk {
+
+__host__ __device__ __forceinline__ int PI(int j) { return j + (j >> 4); }
+__host__ __device__ __forceinline__ int padded(int n) { return n + (n >> 4) + 1; }
 
 struct TView {
     Lay lay;
@@ -31,7 +36,7 @@ struct TView {
           Qz(L->Qz), cr(L->qz_cr), kappa(L->kappa) {}
 };
 
-// (A x)_j for a tridiagonal A stored [3][n] = (sub, diag, sup)
+// (A x)_j for a tridiagonal A stored [3][n] = (sub, diag, sup); x in global memory
 __device__ __forceinline__ double tmv(const double* A, int n, const double* x, int j) {
     double s = A[n + j] * x[j];
     if (j > 0) s += A[j] * x[j - 1];
@@ -45,130 +50,230 @@ __device__ __forceinline__ double tmtv(const double* A, int n, const double* x, 
     if (j < n - 1) s += A[j + 1] * x[j + 1];
     return s;
 }
+// same with x in padded shared memory
+__device__ __forceinline__ double tmv_s(const double* A, int n, const double* xs, int j) {
+    double s = A[n + j] * xs[PI(j)];
+    if (j > 0) s += A[j] * xs[PI(j - 1)];
+    if (j < n - 1) s += A[2 * n + j] * xs[PI(j + 1)];
+    return s;
+}
+__device__ __forceinline__ double tmtv_s(const double* A, int n, const double* xs, int j) {
+    double s = A[n + j] * xs[PI(j)];
+    if (j > 0) s += A[2 * n + j - 1] * xs[PI(j - 1)];
+    if (j < n - 1) s += A[j + 1] * xs[PI(j + 1)];
+    return s;
+}
 
 static constexpr int kTriArrays = 16;
 
 struct TriSm {
     double *Da, *Db, *Dc, *E0, *E1, *E2, *E3, *L0, *L1, *L2, *L3, *f0, *f1, *fw, *sv, *srv;
     __device__ TriSm(double* sm, int n) {
+        const int np = padded(n);
         double* p = sm;
-        Da = p; p += n; Db = p; p += n; Dc = p; p += n;
-        E0 = p; p += n; E1 = p; p += n; E2 = p; p += n; E3 = p; p += n;
-        L0 = p; p += n; L1 = p; p += n; L2 = p; p += n; L3 = p; p += n;
-        f0 = p; p += n; f1 = p; p += n; fw = p; p += n; sv = p; p += n; srv = p;
+        Da = p; p += np; Db = p; p += np; Dc = p; p += np;
+        E0 = p; p += np; E1 = p; p += np; E2 = p; p += np; E3 = p; p += np;
+        L0 = p; p += np; L1 = p; p += np; L2 = p; p += np; L3 = p; p += np;
+        f0 = p; p += np; f1 = p; p += np; fw = p; p += np; sv = p; p += np; srv = p;
+    }
+};
+
+// nodes eliminated at CR level lev (j = s-1 + 2s*m < n) and kept (j = 2s-1 + 2s*m < n)
+__host__ __device__ __forceinline__ int lvl_count(int n, int lev) {
+    const int s = 1 << lev;
+    return n >= s ? ((n - s) >> (lev + 1)) + 1 : 0;
+}
+__host__ __device__ __forceinline__ int kept_count(int n, int lev) { return n >> (lev + 1); }
+
+template <bool RHS>
+struct CrSolve {
+    // phase 1 at level lev for eliminated index m: invert D_p, snapshot lower coupling
+    static __device__ __forceinline__ void elim(TriSm& S, int n, int lev, int m) {
+        const int s = 1 << lev;
+        const int p = s - 1 + 2 * s * m;
+        const int P = PI(p);
+        const double a = S.Da[P], b = S.Db[P], c = S.Dc[P];
+        const double idet = 1.0 / (a * c - b * b);
+        S.Da[P] = c * idet;
+        S.Db[P] = -b * idet;
+        S.Dc[P] = a * idet;
+        if (p - s >= 0) {
+            const int Q = PI(p - s);
+            S.L0[P] = S.E0[Q]; S.L1[P] = S.E1[Q]; S.L2[P] = S.E2[Q]; S.L3[P] = S.E3[Q];
+        } else {
+            S.L0[P] = 0.0; S.L1[P] = 0.0; S.L2[P] = 0.0; S.L3[P] = 0.0;
+        }
+    }
+    // phase 2 at level lev for kept index m: Schur update of D_j, E_j, f_j
+    static __device__ __forceinline__ void keep(TriSm& S, int n, int lev, int m,
+                                                const double* cinv, const double* cup,
+                                                const double* clo) {
+        const int s = 1 << lev;
+        const int j = 2 * s - 1 + 2 * s * m;
+        const int p = j - s, q = j + s;
+        const int J = PI(j), P = PI(p);
+        double da = S.Da[J], db = S.Db[J], dc = S.Dc[J];
+        double g0 = 0.0, g1 = 0.0, w = 0.0;
+        if (RHS) { g0 = S.f0[J]; g1 = S.f1[J]; w = S.fw[J] - cup[p] * cinv[p] * S.fw[P]; }
+        {   // lower neighbour p: coupling A = E_p (row p, col j)
+            const double e0 = S.E0[P], e1 = S.E1[P], e2 = S.E2[P], e3 = S.E3[P];
+            const double pa = S.Da[P], pb = S.Db[P], pc = S.Dc[P];
+            const double t00 = e0 * pa + e2 * pb, t01 = e0 * pb + e2 * pc;
+            const double t10 = e1 * pa + e3 * pb, t11 = e1 * pb + e3 * pc;
+            da -= t00 * e0 + t01 * e2;
+            db -= t00 * e1 + t01 * e3;
+            dc -= t10 * e1 + t11 * e3;
+            if (RHS) {
+                const double h0 = S.f0[P], h1 = S.f1[P];
+                g0 -= t00 * h0 + t01 * h1;
+                g1 -= t10 * h0 + t11 * h1;
+            }
+        }
+        double n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0;
+        if (q < n) {  // upper neighbour q: coupling A = E_j (row j, col q)
+            const int Qi = PI(q);
+            const double e0 = S.E0[J], e1 = S.E1[J], e2 = S.E2[J], e3 = S.E3[J];
+            const double qa = S.Da[Qi], qb = S.Db[Qi], qc = S.Dc[Qi];
+            const double t00 = e0 * qa + e1 * qb, t01 = e0 * qb + e1 * qc;
+            const double t10 = e2 * qa + e3 * qb, t11 = e2 * qb + e3 * qc;
+            da -= t00 * e0 + t01 * e1;
+            db -= t00 * e2 + t01 * e3;
+            dc -= t10 * e2 + t11 * e3;
+            if (RHS) {
+                const double h0 = S.f0[Qi], h1 = S.f1[Qi];
+                g0 -= t00 * h0 + t01 * h1;
+                g1 -= t10 * h0 + t11 * h1;
+                w -= clo[q] * cinv[q] * S.fw[Qi];
+            }
+            if (q + s < n) {
+                const double k0 = S.E0[Qi], k1 = S.E1[Qi], k2 = S.E2[Qi], k3 = S.E3[Qi];
+                n0 = -(t00 * k0 + t01 * k2);
+                n1 = -(t00 * k1 + t01 * k3);
+                n2 = -(t10 * k0 + t11 * k2);
+                n3 = -(t10 * k1 + t11 * k3);
+            }
+        }
+        S.Da[J] = da; S.Db[J] = db; S.Dc[J] = dc;
+        S.E0[J] = n0; S.E1[J] = n1; S.E2[J] = n2; S.E3[J] = n3;
+        if (RHS) { S.f0[J] = g0; S.f1[J] = g1; S.fw[J] = w; }
+    }
+    static __device__ __forceinline__ void root(TriSm& S, int n, int top, const double* cinv) {
+        const int r = (1 << top) - 1, R = PI(r);
+        const double a = S.Da[R], b = S.Db[R], c = S.Dc[R];
+        const double idet = 1.0 / (a * c - b * b);
+        S.Da[R] = c * idet; S.Db[R] = -b * idet; S.Dc[R] = a * idet;
+        if (RHS) {
+            const double g0 = S.f0[R], g1 = S.f1[R];
+            S.f0[R] = (c * g0 - b * g1) * idet;
+            S.f1[R] = (a * g1 - b * g0) * idet;
+            S.fw[R] = cinv[r] * S.fw[R];
+        } else {
+            S.E0[R] = 0.0; S.E1[R] = 0.0; S.E2[R] = 0.0; S.E3[R] = 0.0;
+            S.L0[R] = 0.0; S.L1[R] = 0.0; S.L2[R] = 0.0; S.L3[R] = 0.0;
+        }
+    }
+    // back substitution at level lev for eliminated index m
+    static __device__ __forceinline__ void back(TriSm& S, int n, int lev, int m,
+                                                const double* cinv, const double* cup,
+                                                const double* clo) {
+        const int s = 1 << lev;
+        const int p = s - 1 + 2 * s * m;
+        const int P = PI(p);
+        double g0 = S.f0[P], g1 = S.f1[P], w = S.fw[P];
+        if (p - s >= 0) {
+            const int Q = PI(p - s);
+            const double xa = S.f0[Q], xb = S.f1[Q];
+            g0 -= S.L0[P] * xa + S.L2[P] * xb;
+            g1 -= S.L1[P] * xa + S.L3[P] * xb;
+            w -= clo[p] * S.fw[Q];
+        }
+        if (p + s < n) {
+            const int Q = PI(p + s);
+            const double xa = S.f0[Q], xb = S.f1[Q];
+            g0 -= S.E0[P] * xa + S.E1[P] * xb;
+            g1 -= S.E2[P] * xa + S.E3[P] * xb;
+            w -= cup[p] * S.fw[Q];
+        }
+        const double pa = S.Da[P], pb = S.Db[P], pc = S.Dc[P];
+        S.f0[P] = pa * g0 + pb * g1;
+        S.f1[P] = pb * g0 + pc * g1;
+        S.fw[P] = cinv[p] * w;
     }
 };
 
 // Block cyclic reduction of the symmetric quasi-definite 2x2-block tridiagonal
 // system held in S (D sym (a,b,c), E upper coupling, f rhs), jointly with the
 // scalar reduction of Qz w = fw using precomputed coefficients cr = [3][n]
-// (inv_d, e_up, e_lo per node at its elimination level).  Solution overwrites f.
+// (inv_d, e_up, e_lo per node at its elimination level).  With RHS=false only
+// the factorisation is performed.  Solutions overwrite f0/f1/fw.  Levels with
+// more than 32 eliminated nodes run CTA-wide (two barriers per level); the
+// deeper levels, the root and their back-substitution run in warp 0 with
+// __syncwarp only.
+template <bool RHS>
 __device__ void cr_solve(int n, TriSm& S, const double* __restrict__ cr) {
+    using K = CrSolve<RHS>;
     const int tid = threadIdx.x, nth = blockDim.x;
     const double* cinv = cr;
     const double* cup = cr + n;
     const double* clo = cr + 2 * n;
     const int top = 31 - __clz(n);
-    for (int lev = 0; lev < top; ++lev) {
-        const int s = 1 << lev;
-        for (int m = tid;; m += nth) {
-            const int p = s - 1 + 2 * s * m;
-            if (p >= n) break;
-            const double a = S.Da[p], b = S.Db[p], c = S.Dc[p];
-            const double idet = 1.0 / (a * c - b * b);
-            S.Da[p] = c * idet;
-            S.Db[p] = -b * idet;
-            S.Dc[p] = a * idet;
-            if (p - s >= 0) {
-                S.L0[p] = S.E0[p - s]; S.L1[p] = S.E1[p - s];
-                S.L2[p] = S.E2[p - s]; S.L3[p] = S.E3[p - s];
-            } else {
-                S.L0[p] = 0.0; S.L1[p] = 0.0; S.L2[p] = 0.0; S.L3[p] = 0.0;
-            }
-        }
+    int lev = 0;
+    for (; lev < top; ++lev) {
+        const int ce = lvl_count(n, lev);
+        if (ce <= 32) break;
+        for (int m = tid; m < ce; m += nth) K::elim(S, n, lev, m);
         __syncthreads();
-        for (int m = tid;; m += nth) {
-            const int j = 2 * s - 1 + 2 * s * m;
-            if (j >= n) break;
-            const int p = j - s, q = j + s;
-            double da = S.Da[j], db = S.Db[j], dc = S.Dc[j];
-            double g0 = S.f0[j], g1 = S.f1[j];
-            {   // lower neighbour p: coupling A = E_p (row p, col j)
-                const double e0 = S.E0[p], e1 = S.E1[p], e2 = S.E2[p], e3 = S.E3[p];
-                const double pa = S.Da[p], pb = S.Db[p], pc = S.Dc[p];
-                const double t00 = e0 * pa + e2 * pb, t01 = e0 * pb + e2 * pc;
-                const double t10 = e1 * pa + e3 * pb, t11 = e1 * pb + e3 * pc;
-                da -= t00 * e0 + t01 * e2;
-                db -= t00 * e1 + t01 * e3;
-                dc -= t10 * e1 + t11 * e3;
-                const double h0 = S.f0[p], h1 = S.f1[p];
-                g0 -= t00 * h0 + t01 * h1;
-                g1 -= t10 * h0 + t11 * h1;
-            }
-            double w = S.fw[j] - cup[p] * cinv[p] * S.fw[p];
-            double n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0;
-            if (q < n) {  // upper neighbour q: coupling A = E_j (row j, col q)
-                const double e0 = S.E0[j], e1 = S.E1[j], e2 = S.E2[j], e3 = S.E3[j];
-                const double qa = S.Da[q], qb = S.Db[q], qc = S.Dc[q];
-                const double t00 = e0 * qa + e1 * qb, t01 = e0 * qb + e1 * qc;
-                const double t10 = e2 * qa + e3 * qb, t11 = e2 * qb + e3 * qc;
-                da -= t00 * e0 + t01 * e1;
-                db -= t00 * e2 + t01 * e3;
-                dc -= t10 * e2 + t11 * e3;
-                const double h0 = S.f0[q], h1 = S.f1[q];
-                g0 -= t00 * h0 + t01 * h1;
-                g1 -= t10 * h0 + t11 * h1;
-                if (q + s < n) {
-                    const double k0 = S.E0[q], k1 = S.E1[q], k2 = S.E2[q], k3 = S.E3[q];
-                    n0 = -(t00 * k0 + t01 * k2);
-                    n1 = -(t00 * k1 + t01 * k3);
-                    n2 = -(t10 * k0 + t11 * k2);
-                    n3 = -(t10 * k1 + t11 * k3);
-                }
-                w -= clo[q] * cinv[q] * S.fw[q];
-            }
-            S.Da[j] = da; S.Db[j] = db; S.Dc[j] = dc;
-            S.f0[j] = g0; S.f1[j] = g1;
-            S.E0[j] = n0; S.E1[j] = n1; S.E2[j] = n2; S.E3[j] = n3;
-            S.fw[j] = w;
-        }
+        const int ck = kept_count(n, lev);
+        for (int m = tid; m < ck; m += nth) K::keep(S, n, lev, m, cinv, cup, clo);
         __syncthreads();
     }
-    if (tid == 0) {
-        const int r = (1 << top) - 1;
-        const double a = S.Da[r], b = S.Db[r], c = S.Dc[r];
-        const double idet = 1.0 / (a * c - b * b);
-        const double g0 = S.f0[r], g1 = S.f1[r];
-        S.Da[r] = c * idet; S.Db[r] = -b * idet; S.Dc[r] = a * idet;
-        S.f0[r] = (c * g0 - b * g1) * idet;
-        S.f1[r] = (a * g1 - b * g0) * idet;
-        S.fw[r] = cinv[r] * S.fw[r];
+    const int lw = lev;
+    if (tid < 32) {
+        for (int l = lw; l < top; ++l) {
+            if (tid < lvl_count(n, l)) K::elim(S, n, l, tid);
+            __syncwarp();
+            if (tid < kept_count(n, l)) K::keep(S, n, l, tid, cinv, cup, clo);
+            __syncwarp();
+        }
+        if (tid == 0) K::root(S, n, top, cinv);
+        __syncwarp();
+        if (RHS) {
+            for (int l = top - 1; l >= lw; --l) {
+                if (tid < lvl_count(n, l)) K::back(S, n, l, tid, cinv, cup, clo);
+                __syncwarp();
+            }
+        }
     }
     __syncthreads();
-    for (int lev = top - 1; lev >= 0; --lev) {
-        const int s = 1 << lev;
-        for (int m = tid;; m += nth) {
-            const int p = s - 1 + 2 * s * m;
-            if (p >= n) break;
-            double g0 = S.f0[p], g1 = S.f1[p], w = S.fw[p];
-            if (p - s >= 0) {
-                const double xa = S.f0[p - s], xb = S.f1[p - s];
-                g0 -= S.L0[p] * xa + S.L2[p] * xb;
-                g1 -= S.L1[p] * xa + S.L3[p] * xb;
-                w -= clo[p] * S.fw[p - s];
-            }
-            if (p + s < n) {
-                const double xa = S.f0[p + s], xb = S.f1[p + s];
-                g0 -= S.E0[p] * xa + S.E1[p] * xb;
-                g1 -= S.E2[p] * xa + S.E3[p] * xb;
-                w -= cup[p] * S.fw[p + s];
-            }
-            const double pa = S.Da[p], pb = S.Db[p], pc = S.Dc[p];
-            S.f0[p] = pa * g0 + pb * g1;
-            S.f1[p] = pb * g0 + pc * g1;
-            S.fw[p] = cinv[p] * w;
-        }
+    if (!RHS) return;
+    for (lev = lw - 1; lev >= 0; --lev) {
+        const int ce = lvl_count(n, lev);
+        for (int m = tid; m < ce; m += nth) K::back(S, n, lev, m, cinv, cup, clo);
         __syncthreads();
+    }
+}
+
+// Load D/E of the (u,lam) system of interval i into shared memory.
+__device__ __forceinline__ void tri_init_de(const TView& V, int i, TriSm& S) {
+    const Lay& L = V.lay;
+    const int n = V.n;
+    const double k2 = V.kappa * V.kappa;
+    const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;
+    const double* K = V.K + (size_t)i * 3 * n;
+    const double* Qz = V.Qz;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const int J = PI(j);
+        S.Da[J] = Qu[n + j];
+        S.Db[J] = K[n + j];
+        S.Dc[J] = -k2 * Qz[n + j];
+        if (j < n - 1) {
+            S.E0[J] = Qu[2 * n + j];
+            S.E1[J] = K[j + 1];
+            S.E2[J] = K[2 * n + j];
+            S.E3[J] = -k2 * Qz[2 * n + j];
+        } else {
+            S.E0[J] = 0.0; S.E1[J] = 0.0; S.E2[J] = 0.0; S.E3[J] = 0.0;
+        }
     }
 }
 
@@ -185,7 +290,7 @@ __device__ void tri_block(const TView& V, int i, const double* b, const double* 
     const int tid = threadIdx.x, nth = blockDim.x;
     const bool has_vm = i >= 1, has_uzl = i < L.N;
     TriSm S(sm, n);
-    const double kap = V.kappa, k2 = kap * kap;
+    const double kap = V.kappa;
     const double* Qv = (i == L.N) ? V.Ql : V.Qm;
     const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;
     const double* Qz = V.Qz;
@@ -195,6 +300,7 @@ __device__ void tri_block(const TView& V, int i, const double* b, const double* 
                   ol = L.off_l(i);
 
     for (int j = tid; j < n; j += nth) {
+        const int J = PI(j);
         double rv = 0.0, ru = 0.0, rz = 0.0, rm = 0.0, rl = 0.0;
         if (has_vm) { rv = b[ov + j]; rm = b[om + j]; }
         if (has_uzl) { ru = b[ou + j]; rz = b[oz + j]; rl = b[ol + j]; }
@@ -215,47 +321,38 @@ __device__ void tri_block(const TView& V, int i, const double* b, const double* 
         }
         if (has_vm && uprev) rm -= uprev[j];
         if (has_uzl && munext) ru -= munext[j];
-        if (has_vm) { S.sv[j] = -rm; S.srv[j] = rv; }
-        if (has_uzl) { S.f0[j] = ru; S.f1[j] = rl - kap * rz; S.fw[j] = rz; }
+        if (has_vm) { S.sv[J] = -rm; S.srv[J] = rv; }
+        if (has_uzl) { S.f0[J] = ru; S.f1[J] = rl - kap * rz; S.fw[J] = rz; }
     }
     __syncthreads();
     if (!has_uzl) {  // last block (v_N, mu_N): mu = Qv v - r_v
         for (int j = tid; j < n; j += nth) {
-            double dv = S.sv[j];
-            double dm = tmv(Qv, n, S.sv, j) - S.srv[j];
-            double bv = xupd ? xupd[ov + j] : 0.0, bm = xupd ? xupd[om + j] : 0.0;
+            const double dv = S.sv[PI(j)];
+            const double dm = tmv_s(Qv, n, S.sv, j) - S.srv[PI(j)];
+            const double bv = xupd ? xupd[ov + j] : 0.0, bm = xupd ? xupd[om + j] : 0.0;
             out[ov + j] = bv + omega * dv;
             out[om + j] = bm + omega * dm;
         }
         __syncthreads();
         return;
     }
-    for (int j = tid; j < n; j += nth) {
-        if (C) S.f1[j] -= tmv(C, n, S.sv, j);
-        S.Da[j] = Qu[n + j];
-        S.Db[j] = K[n + j];
-        S.Dc[j] = -k2 * Qz[n + j];
-        if (j < n - 1) {
-            S.E0[j] = Qu[2 * n + j];
-            S.E1[j] = K[j + 1];
-            S.E2[j] = K[2 * n + j];
-            S.E3[j] = -k2 * Qz[2 * n + j];
-        } else {
-            S.E0[j] = 0.0; S.E1[j] = 0.0; S.E2[j] = 0.0; S.E3[j] = 0.0;
-        }
+    if (C) {
+        for (int j = tid; j < n; j += nth) S.f1[PI(j)] -= tmv_s(C, n, S.sv, j);
     }
+    tri_init_de(V, i, S);
     __syncthreads();
-    cr_solve(n, S, V.cr);
+    cr_solve<true>(n, S, V.cr);
     for (int j = tid; j < n; j += nth) {
-        const double du = S.f0[j], dl = S.f1[j];
-        const double dz = S.fw[j] - kap * dl;
+        const int J = PI(j);
+        const double du = S.f0[J], dl = S.f1[J];
+        const double dz = S.fw[J] - kap * dl;
         out[ou + j] = (xupd ? xupd[ou + j] : 0.0) + omega * du;
         out[oz + j] = (xupd ? xupd[oz + j] : 0.0) + omega * dz;
         out[ol + j] = (xupd ? xupd[ol + j] : 0.0) + omega * dl;
         if (has_vm) {
-            const double dv = S.sv[j];
-            double dm = tmv(Qv, n, S.sv, j) - S.srv[j];
-            if (C) dm += tmtv(C, n, S.f1, j);
+            const double dv = S.sv[J];
+            double dm = tmv_s(Qv, n, S.sv, j) - S.srv[J];
+            if (C) dm += tmtv_s(C, n, S.f1, j);
             out[ov + j] = (xupd ? xupd[ov + j] : 0.0) + omega * dv;
             out[om + j] = (xupd ? xupd[om + j] : 0.0) + omega * dm;
         }
@@ -287,6 +384,299 @@ __global__ void tri_subst(TView V, const double* __restrict__ r, double* d) {
         tri_block(V, i, r, nullptr, uprev, munext, d, 1.0, nullptr, sm);
     }
 }
+
+// ---------------------------------------------------------------------------
+// Gauss-Seidel substitution as  parallel solve -> serial chain -> parallel solve.
+// Forward (D-L)d = r:  d_i = D_i^{-1}(r_i - E_mu u_{i-1}), u_i = P_u d_i.  With
+// a_i = D_i^{-1} r_i (parallel), the chain is  u_i = a_i^u + y_i, where y_i is
+// the u-part of the (u,lam) solve with rhs (0, -C_i u_{i-1}).  Backward:
+// mu_i = a_i^mu + C_i^T lam_i with lam_i from the rhs (-mu_{i+1}, 0).  The
+// chain solves reuse per-interval cyclic-reduction factors precomputed once
+// (fac record [14][n]: P(3) M1(4) M2(4) C(3)), staged by cp.async double
+// buffering so only the CR recurrences sit on the serial critical path.
+// ---------------------------------------------------------------------------
+static constexpr int kFacRows = 14;
+
+// Level order of the factor rows: node j = s-1 + 2s*m (s = 2^l) is eliminated
+// at level l = ctz(j+1) with index m = (j+1) >> (l+1); level l occupies
+// [lvl_off(l), lvl_off(l+1)).  Every CR level then reads a contiguous run.
+__device__ __forceinline__ int lvl_pos(int n, int j) {
+    const int lev = __ffs(j + 1) - 1;
+    int off = 0;
+    for (int l = 0; l < lev; ++l) off += lvl_count(n, l);
+    return off + ((j + 1) >> (lev + 1));
+}
+
+// One CTA per interval i in [0, N): factor record of the (u,lam) system.
+__global__ void tri_factor_kernel(TView V, double* __restrict__ fac) {
+    extern __shared__ double sm[];
+    const Lay& L = V.lay;
+    const int n = V.n;
+    TriSm S(sm, n);
+    for (int i = blockIdx.x; i < L.N; i += gridDim.x) {
+        tri_init_de(V, i, S);
+        __syncthreads();
+        cr_solve<false>(n, S, V.cr);
+        double* out = fac + (size_t)i * kFacRows * n;
+        const double* C = (i >= 1) ? V.C + (size_t)i * 3 * n : nullptr;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            const int J = PI(j);
+            const int o = lvl_pos(n, j);
+            const double pa = S.Da[J], pb = S.Db[J], pc = S.Dc[J];
+            const double e0 = S.E0[J], e1 = S.E1[J], e2 = S.E2[J], e3 = S.E3[J];
+            const double l0 = S.L0[J], l1 = S.L1[J], l2 = S.L2[J], l3 = S.L3[J];
+            out[0 * n + o] = pa; out[1 * n + o] = pb; out[2 * n + o] = pc;
+            out[3 * n + o] = e0 * pa + e2 * pb;  out[4 * n + o] = e0 * pb + e2 * pc;
+            out[5 * n + o] = e1 * pa + e3 * pb;  out[6 * n + o] = e1 * pb + e3 * pc;
+            out[7 * n + o] = l0 * pa + l1 * pb;  out[8 * n + o] = l0 * pb + l1 * pc;
+            out[9 * n + o] = l2 * pa + l3 * pb;  out[10 * n + o] = l2 * pb + l3 * pc;
+            out[11 * n + j] = C ? C[j] : 0.0;
+            out[12 * n + j] = C ? C[n + j] : 0.0;
+            out[13 * n + j] = C ? C[2 * n + j] : 0.0;
+        }
+        __syncthreads();
+    }
+}
+
+// rhs-only block cyclic reduction with a level-ordered factor record fb
+// ([14][n], rows 0..10 = P, M1, M2 in level order; shared or global memory).
+// f0/f1 are padded shared arrays in natural node order.
+struct CrRhsRows {
+    const double *Pa, *Pb, *Pc, *A0, *A1, *A2, *A3, *B0, *B1, *B2, *B3;
+    __device__ CrRhsRows(const double* fb, int n)
+        : Pa(fb), Pb(fb + n), Pc(fb + 2 * n), A0(fb + 3 * n), A1(fb + 4 * n), A2(fb + 5 * n),
+          A3(fb + 6 * n), B0(fb + 7 * n), B1(fb + 8 * n), B2(fb + 9 * n), B3(fb + 10 * n) {}
+};
+
+// forward rhs reduction of level lev for kept-node index m (level-ordered factors at off)
+__device__ __forceinline__ void cr_rhs_down(const CrRhsRows& F, int n, int lev, int off, int m,
+                                            double* f0, double* f1) {
+    const int s = 1 << lev;
+    const int j = 2 * s - 1 + 2 * s * m;
+    const int p = j - s, q = j + s;
+    const int J = PI(j), P = PI(p), Pf = off + m;
+    const double h0 = f0[P], h1 = f1[P];
+    double g0 = f0[J] - (F.A0[Pf] * h0 + F.A1[Pf] * h1);
+    double g1 = f1[J] - (F.A2[Pf] * h0 + F.A3[Pf] * h1);
+    if (q < n) {
+        const int Q = PI(q), Qf = Pf + 1;
+        const double k0 = f0[Q], k1 = f1[Q];
+        g0 -= F.B0[Qf] * k0 + F.B1[Qf] * k1;
+        g1 -= F.B2[Qf] * k0 + F.B3[Qf] * k1;
+    }
+    f0[J] = g0;
+    f1[J] = g1;
+}
+
+// back substitution of eliminated-node index m at level lev
+__device__ __forceinline__ void cr_rhs_up(const CrRhsRows& F, int n, int lev, int off, int m,
+                                          double* f0, double* f1) {
+    const int s = 1 << lev;
+    const int p = s - 1 + 2 * s * m;
+    const int P = PI(p), Pf = off + m;
+    const double g0 = f0[P], g1 = f1[P];
+    double x0 = F.Pa[Pf] * g0 + F.Pb[Pf] * g1;
+    double x1 = F.Pb[Pf] * g0 + F.Pc[Pf] * g1;
+    if (p - s >= 0) {  // - M2_p^T x_{p-s}
+        const int Q = PI(p - s);
+        const double a = f0[Q], b = f1[Q];
+        x0 -= F.B0[Pf] * a + F.B2[Pf] * b;
+        x1 -= F.B1[Pf] * a + F.B3[Pf] * b;
+    }
+    if (p + s < n) {   // - M1_p^T x_{p+s}
+        const int Q = PI(p + s);
+        const double a = f0[Q], b = f1[Q];
+        x0 -= F.A0[Pf] * a + F.A2[Pf] * b;
+        x1 -= F.A1[Pf] * a + F.A3[Pf] * b;
+    }
+    f0[P] = x0;
+    f1[P] = x1;
+}
+
+// rhs-only block cyclic reduction.  Levels with more than 32 active nodes
+// run CTA-wide (one barrier per level); the remaining levels, the root and
+// their back-substitution run inside warp 0 with __syncwarp only.
+__device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0, double* f1) {
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const CrRhsRows F(fb, n);
+    const int top = 31 - __clz(n);
+    int off = 0, lev = 0;
+    for (; lev < top; ++lev) {            // CTA-wide levels
+        const int cnt = lvl_count(n, lev);  // eliminated nodes at this level (>= kept)
+        if (cnt <= 32) break;
+        const int ck = kept_count(n, lev);
+        for (int m = tid; m < ck; m += nth) cr_rhs_down(F, n, lev, off, m, f0, f1);
+        off += cnt;
+        __syncthreads();
+    }
+    const int lw = lev;
+    if (tid < 32) {                       // warp-level tail
+        int o = off;
+        for (int l = lw; l < top; ++l) {
+            if (tid < kept_count(n, l)) cr_rhs_down(F, n, l, o, tid, f0, f1);
+            o += lvl_count(n, l);
+            __syncwarp();
+        }
+        if (tid == 0) {
+            const int r = (1 << top) - 1, R = PI(r);
+            const double g0 = f0[R], g1 = f1[R];
+            f0[R] = F.Pa[o] * g0 + F.Pb[o] * g1;
+            f1[R] = F.Pb[o] * g0 + F.Pc[o] * g1;
+        }
+        __syncwarp();
+        for (int l = top - 1; l >= lw; --l) {
+            const int ce = lvl_count(n, l);
+            o -= ce;
+            if (tid < ce) cr_rhs_up(F, n, l, o, tid, f0, f1);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (lev = lw - 1; lev >= 0; --lev) {  // CTA-wide back-substitution
+        const int ce = lvl_count(n, lev);
+        off -= ce;
+        for (int m = tid; m < ce; m += nth) cr_rhs_up(F, n, lev, off, m, f0, f1);
+        __syncthreads();
+    }
+}
+
+// --- TMA bulk copies + mbarrier (sm_90+; SASS UBLKCP / SYNCS) -------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_g2s(void* dst, const void* src, unsigned bytes,
+                                        uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+
+// Serial coupling chain (one CTA).  FWD: chain[i] = u_i, BWD: chain[i] = mu_i.
+// `a` = D^{-1} r from pass 1.  STAGED: the next interval's factor record
+// (14n doubles) and a-segment (n doubles) are TMA bulk-copied into the other
+// half of a double buffer while the current interval's recurrences run.
+template <bool FWD, bool STAGED>
+__global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
+                                 const double* __restrict__ fac, double* __restrict__ chain) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(8) uint64_t bars[2];
+    const Lay& L = V.lay;
+    const int n = V.n, N = L.N, np = padded(n);
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int rec = kFacRows * n;
+    const int brec = rec + n;
+    double* buf0 = sm;
+    double* buf1 = STAGED ? sm + brec : sm;
+    double* f0 = STAGED ? sm + 2 * brec : sm;
+    double* f1 = f0 + np;
+    double* dv = f1 + np;
+    const int K = N - 1;  // chain steps after the seed
+    auto blk = [&](int k) { return FWD ? 1 + k : N - 1 - k; };
+    auto aseg = [&](int i) { return a + (FWD ? L.off_u(i) : L.off_mu(i)); };
+    {   // seed: u_0 = a_0^u (FWD) / mu_N = a_N^mu (BWD)
+        const int i0 = FWD ? 0 : N;
+        const double* s0 = aseg(i0);
+        for (int j = tid; j < n; j += nth) {
+            dv[PI(j)] = s0[j];
+            chain[(size_t)i0 * n + j] = s0[j];
+        }
+    }
+    if (STAGED && tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto prefetch = [&](int k) {   // thread 0 only
+        double* b = (k & 1) ? buf1 : buf0;
+        uint64_t* bar = &bars[k & 1];
+        const int i = blk(k);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_tx(bar, (unsigned)(brec * sizeof(double)));
+        tma_g2s(b, fac + (size_t)i * rec, (unsigned)(rec * sizeof(double)), bar);
+        tma_g2s(b + rec, aseg(i), (unsigned)(n * sizeof(double)), bar);
+    };
+    if (STAGED && K > 0 && tid == 0) prefetch(0);
+    for (int k = 0; k < K; ++k) {
+        const int i = blk(k);
+        const double* fb;
+        const double* ai;
+        if (STAGED) {
+            if (tid == 0 && k + 1 < K) prefetch(k + 1);
+            mbar_wait(&bars[k & 1], (unsigned)((k >> 1) & 1));
+            fb = (k & 1) ? buf1 : buf0;
+            ai = fb + rec;
+        } else {
+            fb = fac + (size_t)i * rec;
+            ai = aseg(i);
+        }
+        const double *Cs = fb + 11 * n, *Cd = fb + 12 * n, *Cp = fb + 13 * n;
+        for (int j = tid; j < n; j += nth) {
+            const int J = PI(j);
+            if (FWD) {  // rhs (0, -C u_{i-1})
+                double cv = Cd[j] * dv[J];
+                if (j > 0) cv += Cs[j] * dv[PI(j - 1)];
+                if (j < n - 1) cv += Cp[j] * dv[PI(j + 1)];
+                f0[J] = 0.0;
+                f1[J] = -cv;
+            } else {    // rhs (-mu_{i+1}, 0)
+                f0[J] = -dv[J];
+                f1[J] = 0.0;
+            }
+        }
+        __syncthreads();
+        cr_rhs(n, fb, f0, f1);
+        for (int j = tid; j < n; j += nth) {
+            const int J = PI(j);
+            double val;
+            if (FWD) {
+                val = ai[j] + f0[J];
+            } else {    // + (C^T lam)_j
+                double ct = Cd[j] * f1[J];
+                if (j > 0) ct += Cp[j - 1] * f1[PI(j - 1)];
+                if (j < n - 1) ct += Cs[j + 1] * f1[PI(j + 1)];
+                val = ai[j] + ct;
+            }
+            dv[J] = val;
+            chain[(size_t)i * n + j] = val;
+        }
+        __syncthreads();
+    }
+}
+
+// Pass 3: parallel solves with the chain as the continuity coupling.
+template <bool FWD>
+__global__ void tri_rows_cpl(TView V, const double* __restrict__ r,
+                             const double* __restrict__ chain, double* __restrict__ y) {
+    extern __shared__ double sm[];
+    const Lay& L = V.lay;
+    const int n = V.n;
+    for (int i = blockIdx.x; i <= L.N; i += gridDim.x) {
+        const double* uprev = (FWD && i >= 1) ? chain + (size_t)(i - 1) * n : nullptr;
+        const double* munext = (!FWD && i < L.N) ? chain + (size_t)(i + 1) * n : nullptr;
+        tri_block(V, i, r, nullptr, uprev, munext, y, 1.0, nullptr, sm);
+    }
+}
+
+int64_t tri_fac_len(const tk_level* Lv) { return (int64_t)Lv->n_steps * kFacRows * Lv->n_u; }
+int64_t tri_scratch_len(const tk_level* Lv) { return (int64_t)(Lv->n_steps + 1) * Lv->n_u; }
 
 enum TriApply { T_APPLY = 0, T_APPLY_DIAG = 1, T_RESIDUAL = 2 };
 
@@ -335,14 +725,21 @@ __global__ void tri_apply(TView V, const double* __restrict__ b, const double* _
 }
 
 int64_t tri_smem_bytes(int n) {
-    if (n < 2 || n > 1792) return 0;
-    return (int64_t)kTriArrays * n * (int64_t)sizeof(double);
+    if (n < 2 || n > 1664) return 0;
+    return (int64_t)kTriArrays * padded(n) * (int64_t)sizeof(double);
 }
 
 static int tri_threads(int n) {
     int t = (n / 2 + 31) / 32 * 32;
     if (t < 32) t = 32;
     if (t > 512) t = 512;
+    return t;
+}
+
+static int tri_chain_threads(int n) {
+    int t = (n / 4 + 31) / 32 * 32;
+    if (t < 32) t = 32;
+    if (t > 128) t = 128;
     return t;
 }
 
@@ -365,19 +762,40 @@ int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, dou
     }
     const int64_t smem = tri_smem_bytes(n);
     if (smem == 0) {
-        set_error("tri family kernels support 2 <= n_u <= 1792 (got %d)", n);
+        set_error("tri family kernels support 2 <= n_u <= 1664 (got %d)", n);
         return TK_ERR_UNSUPPORTED;
     }
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(tri_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(tri_subst<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024);
-        cudaFuncSetAttribute(tri_subst<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024);
+        const int mx = 227 * 1024;
+        cudaFuncSetAttribute(tri_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_rows, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        cudaFuncSetAttribute(tri_rows_cpl<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        cudaFuncSetAttribute(tri_rows_cpl<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        cudaFuncSetAttribute(tri_subst<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_subst<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_rows_cpl<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_rows_cpl<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        // the chain kernels also hold two static mbarriers
+        const int mxc = mx - 1024;
+        cudaFuncSetAttribute(tri_chain_kernel<true, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
+        cudaFuncSetAttribute(tri_chain_kernel<false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
+        cudaFuncSetAttribute(tri_chain_kernel<true, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
+        cudaFuncSetAttribute(tri_chain_kernel<false, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_status(e, "tri: cudaFuncSetAttribute");
         attr_done = true;
     }
     const int th = tri_threads(n);
+    const bool fast = Lv->fac != nullptr && Lv->scratch != nullptr;
     switch (op) {
         case 3:  // diag solve
             tri_rows<<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
@@ -385,8 +803,45 @@ int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, dou
         case 4:  // jacobi
             tri_rows<<<rows, th, smem, s>>>(V, b, x, y, omega);
             break;
-        case 10: tri_subst<true><<<1, th, smem, s>>>(V, b, y); break;
-        case 11: tri_subst<false><<<1, th, smem, s>>>(V, b, y); break;
+        case 10:
+        case 11: {
+            const bool fwd = op == 10;
+            if (!fast) {
+                if (fwd) tri_subst<true><<<1, th, smem, s>>>(V, b, y);
+                else tri_subst<false><<<1, th, smem, s>>>(V, b, y);
+                break;
+            }
+            // pass 1: a = D^{-1} r into y
+            tri_rows<<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
+            // pass 2: serial chain on the coupling vector
+            const int cth = tri_chain_threads(n);
+            const int np = padded(n);
+            const int64_t staged = (int64_t)(2 * (kFacRows + 1) * n + 3 * np) * 8;
+            const int64_t direct = (int64_t)(3 * np) * 8;
+            // TMA bulk copies need 16-byte aligned sources and sizes: n even and
+            // even segment offsets (always true for the Burgers layout, nz == nu)
+            const bool aligned = (n % 2 == 0) && (Lv->n_z % 2 == 0);
+            double* fac = Lv->fac;
+            double* chn = Lv->scratch;
+            if (aligned && staged <= 227 * 1024 - 1024) {
+                if (fwd) tri_chain_kernel<true, true><<<1, cth, staged, s>>>(V, y, fac, chn);
+                else tri_chain_kernel<false, true><<<1, cth, staged, s>>>(V, y, fac, chn);
+            } else {
+                if (fwd) tri_chain_kernel<true, false><<<1, cth, direct, s>>>(V, y, fac, chn);
+                else tri_chain_kernel<false, false><<<1, cth, direct, s>>>(V, y, fac, chn);
+            }
+            // pass 3: parallel solves with the chain coupling
+            if (fwd) tri_rows_cpl<true><<<rows, th, smem, s>>>(V, b, chn, y);
+            else tri_rows_cpl<false><<<rows, th, smem, s>>>(V, b, chn, y);
+            break;
+        }
+        case 12:  // factor
+            if (!Lv->fac) {
+                set_error("tk_subst_factor: level has no fac buffer");
+                return TK_ERR_ARG;
+            }
+            tri_factor_kernel<<<Lv->n_steps, th, smem, s>>>(V, Lv->fac);
+            break;
         default: set_error("tri: bad op %d", op); return TK_ERR_ARG;
     }
     return check_launch("tri_rows");

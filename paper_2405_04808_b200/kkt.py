@@ -20,6 +20,7 @@ Anything else raises :class:`UnsupportedStructure` -- there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -261,6 +262,24 @@ class BlockTriKKT:
             Qz=dev.P(s.Qz), Qm_inv=dev.P(s.Qm_inv), Ql_inv=dev.P(s.Ql_inv),
             Qz_inv=dev.P(s.Qz_inv), kappa=s.kappa, qz_cr=dev.P(s.qz_cr))
         self.lref = C.byref(self.level)
+        self._fac = None
+        self._scratch = None
+
+    def ensure_subst(self) -> None:
+        """Precompute the Gauss-Seidel chain factors once (tk_subst_factor);
+        afterwards tk_forward_subst / tk_backward_subst run as parallel solve
+        -> serial coupling chain -> parallel solve.  ``TK_SERIAL_SUBST=1``
+        keeps the plain serial kernels (used by tests to cross-check)."""
+        if self._fac is not None or os.environ.get("TK_SERIAL_SUBST") == "1":
+            return
+        lib = _lib.load()
+        nf = int(lib.tk_subst_factor_len(self.lref))
+        ns = int(lib.tk_subst_scratch_len(self.lref))
+        self._fac = dev.empty(nf)
+        self._scratch = dev.empty(ns)
+        self.level.fac = self._fac.data_ptr()
+        self.level.scratch = self._scratch.data_ptr()
+        dev.call("tk_subst_factor", self.lref, dev.stream())
 
     @property
     def dim(self) -> int:

@@ -48,6 +48,7 @@ def jacobi_apply(a: BlockTriKKT, dfac, b, x, sweeps: int = 1, omega: float = 1.0
 
 def forward_subst(a: BlockTriKKT, r, out=None):
     """Solve (D - L) delta = r (smoothers.py:79-92)."""
+    a.ensure_subst()
     d = dev.empty(a.dim) if out is None else out
     dev.call("tk_forward_subst", a.lref, dev.P(r), dev.P(d), dev.stream())
     return d
@@ -55,6 +56,7 @@ def forward_subst(a: BlockTriKKT, r, out=None):
 
 def backward_subst(a: BlockTriKKT, r, out=None):
     """Solve (D - U) delta = r (smoothers.py:95-109)."""
+    a.ensure_subst()
     d = dev.empty(a.dim) if out is None else out
     dev.call("tk_backward_subst", a.lref, dev.P(r), dev.P(d), dev.stream())
     return d
