@@ -361,7 +361,7 @@ __device__ void tri_block(const TView& V, int i, const double* b, const double* 
 }
 
 // Parallel over block rows: jacobi (x may be null) or plain D^{-1} b.
-__global__ void tri_rows(TView V, const double* __restrict__ b, const double* __restrict__ x,
+__global__ void __launch_bounds__(256, 3) tri_rows(TView V, const double* __restrict__ b, const double* __restrict__ x,
                          double* __restrict__ y, double omega) {
     extern __shared__ double sm[];
     const Lay& L = V.lay;
@@ -663,7 +663,7 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
 
 // Pass 3: parallel solves with the chain as the continuity coupling.
 template <bool FWD>
-__global__ void tri_rows_cpl(TView V, const double* __restrict__ r,
+__global__ void __launch_bounds__(256, 3) tri_rows_cpl(TView V, const double* __restrict__ r,
                              const double* __restrict__ chain, double* __restrict__ y) {
     extern __shared__ double sm[];
     const Lay& L = V.lay;
@@ -732,14 +732,20 @@ int64_t tri_smem_bytes(int n) {
 static int tri_threads(int n) {
     int t = (n / 2 + 31) / 32 * 32;
     if (t < 32) t = 32;
-    if (t > 512) t = 512;
+    if (t > 256) t = 256;
     return t;
 }
 
 static int tri_chain_threads(int n) {
-    int t = (n / 4 + 31) / 32 * 32;
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = getenv("TK_CHAIN_THREADS");
+        forced = e ? atoi(e) : 0;
+    }
+    if (forced >= 32) return forced;
+    int t = (n / 2 + 31) / 32 * 32;
     if (t < 32) t = 32;
-    if (t > 128) t = 128;
+    if (t > 256) t = 256;
     return t;
 }
 
