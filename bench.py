@@ -281,7 +281,7 @@ def run_ours(args, rank, world, local_rank):
         "metric": "V-cycle time-step*DoF/s (fp64) + full MG-FGMRES solve time",
         "value": value, "unit": "time-step*DoF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: forward-march linearisation + N(0,1) rhs (seeded)",
         "config": {"workload": f"configs[{args.config}] {setup.describe()}",
                    "n_steps": setup.grid.n_steps, "n_u": setup.n_u, "n_z": setup.n_z,
@@ -319,7 +319,7 @@ def run_reference(args, rank, world):
     return {"impl": "reference",
             "metric": "V-cycle time-step*DoF/s (fp64) + full MG-FGMRES solve time",
             "value": v, "unit": "time-step*DoF/s", "n_gpus": world, "steps": n,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"configs[{args.config}] (bounded CPU sample)"},
             "cpu_baseline": {"value": v, "unit": "time-step*DoF/s", "cores": cores,

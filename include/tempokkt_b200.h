@@ -75,6 +75,19 @@ typedef struct tk_level {
      * parallel solve -> serial n_u-vector chain -> parallel solve. */
     double* fac;
     double* scratch;
+    /* Time slab (multi-GPU sharding).  The level handles global block rows
+     * [row0, row1) (row1 == 0 means n_steps+1, i.e. the whole level); every
+     * vector argument is then the LOCAL slice starting at the global offset of
+     * row0, and K, C, B hold stages [row0, min(row1, n_steps)).  The continuity
+     * couplings across the slab edges come from two n_u halo buffers:
+     *   halo_u  = u-segment of global row row0-1   (required if row0 > 0)
+     *   halo_mu = mu-segment of global row row1    (required if row1 <= n_steps)
+     * refreshed by the caller's neighbour exchange before each call.  The
+     * serial-in-time substitutions require the whole level (no slab). */
+    int32_t row0;
+    int32_t row1;
+    const double* halo_u;
+    const double* halo_mu;
 } tk_level;
 
 /* --- library ------------------------------------------------------------ */
@@ -121,7 +134,19 @@ int tk_restrict(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xf, doub
  * multigrid.py:283 and :465 */
 int tk_prolong_add(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xc, double* xf,
                    void* stream);
-/* rc = R (b - A x)  (work: fine-sized scratch)                 multigrid.py:456 */
+/* Slab versions for the time-sharded hierarchy: [row0, row1) are FINE block
+ * rows (row0 even; row1 even or n_fine+1), the coarse slice covers coarse rows
+ * [row0/2, row1/2) (or through n_fine/2 for the last slab).  Restriction is
+ * slab-local; prolongation needs the previous slab's last coarse (u, lam)
+ * segments (halo_prev_ul, 2 n_u) and the next slab's first coarse (v, mu)
+ * segments (halo_next_vm, 2 n_u).  tk_restrict / tk_prolong_add are the
+ * whole-level special case. */
+int tk_restrict_slab(int32_t n_fine, int32_t n_u, int32_t n_z, int32_t row0, int32_t row1,
+                     const double* xf, double* xc, void* stream);
+int tk_prolong_add_slab(int32_t n_fine, int32_t n_u, int32_t n_z, int32_t row0, int32_t row1,
+                        const double* xc, const double* halo_prev_ul,
+                        const double* halo_next_vm, double* xf, void* stream);
+/* rc = R (b - A x)  (work: fine-sized scratch; honours the level's slab)  multigrid.py:456 */
 int tk_residual_restrict(const tk_level* L, const double* b, const double* x, double* rc,
                          double* work, void* stream);
 

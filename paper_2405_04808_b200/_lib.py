@@ -37,6 +37,7 @@ class TkLevel(C.Structure):
         ("Qm_inv", _p), ("Ql_inv", _p), ("Qz_inv", _p),
         ("kappa", _d), ("qz_cr", _p),
         ("fac", _p), ("scratch", _p),
+        ("row0", _i32), ("row1", _i32), ("halo_u", _p), ("halo_mu", _p),
     ]
 
 
@@ -57,6 +58,8 @@ _SIGS = {
     "tk_subst_factor": (C.c_int, [C.POINTER(TkLevel), _p]),
     "tk_restrict": (C.c_int, [_i32, _i32, _i32, _p, _p, _p]),
     "tk_prolong_add": (C.c_int, [_i32, _i32, _i32, _p, _p, _p]),
+    "tk_restrict_slab": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _p, _p, _p]),
+    "tk_prolong_add_slab": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p]),
     "tk_residual_restrict": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p, _p]),
     "tk_reduce_work_len": (_i64, []),
     "tk_dot": (C.c_int, [_i64, _p, _p, _p, _p, _p]),

@@ -30,7 +30,8 @@ int64_t tri_fac_len(const tk_level*);
 int64_t tri_scratch_len(const tk_level*);
 int64_t dense_fac_len(const tk_level*);
 int64_t dense_scratch_len(const tk_level*);
-int transfer_launch(int, int, int, int, const double*, double*, cudaStream_t);
+int transfer_launch(int, int, int, int, int, int, const double*, const double*, const double*,
+                    double*, cudaStream_t);
 int64_t reduce_work_len();
 int dot_launch(int64_t, const double*, const double*, double*, double*, int, cudaStream_t);
 int vec_launch(int, int64_t, double, const double*, double*, cudaStream_t);
@@ -49,6 +50,17 @@ static int check_level(const tk_level* L) {
     if (!L->K || !L->C || !L->Qm || !L->Ql || !L->Qz) {
         set_error("level is missing stage/weight data");
         return TK_ERR_ARG;
+    }
+    {
+        const int r1 = L->row1 > 0 ? L->row1 : L->n_steps + 1;
+        if (L->row0 < 0 || L->row0 >= r1 || r1 > L->n_steps + 1) {
+            set_error("bad time slab [%d, %d) for N=%d", L->row0, L->row1, L->n_steps);
+            return TK_ERR_ARG;
+        }
+        if ((L->row0 > 0 && !L->halo_u) || (r1 <= L->n_steps && !L->halo_mu)) {
+            set_error("time slab [%d, %d) needs its halo buffers", L->row0, r1);
+            return TK_ERR_ARG;
+        }
     }
     if (L->family == TK_FAMILY_DENSE) {
         if (!L->B || !L->Qm_inv || !L->Ql_inv || !L->Qz_inv) {
@@ -144,14 +156,33 @@ int tk_restrict(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xf, doub
                 void* stream) {
     TK_CHECK_ARG(xf && xc && n_fine >= 2 && n_fine % 2 == 0 && n_u >= 1 && n_z >= 1,
                  "tk_restrict: bad arguments (n_fine must be even)");
-    return transfer_launch(1, n_fine, n_u, n_z, xf, xc, as_stream(stream));
+    return transfer_launch(1, n_fine, n_u, n_z, 0, 0, xf, nullptr, nullptr, xc,
+                           as_stream(stream));
 }
 
 int tk_prolong_add(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xc, double* xf,
                    void* stream) {
     TK_CHECK_ARG(xf && xc && n_fine >= 2 && n_fine % 2 == 0 && n_u >= 1 && n_z >= 1,
                  "tk_prolong_add: bad arguments (n_fine must be even)");
-    return transfer_launch(0, n_fine, n_u, n_z, xc, xf, as_stream(stream));
+    return transfer_launch(0, n_fine, n_u, n_z, 0, 0, xc, nullptr, nullptr, xf,
+                           as_stream(stream));
+}
+
+int tk_restrict_slab(int32_t n_fine, int32_t n_u, int32_t n_z, int32_t row0, int32_t row1,
+                     const double* xf, double* xc, void* stream) {
+    TK_CHECK_ARG(xf && xc && n_fine >= 2 && n_fine % 2 == 0 && n_u >= 1 && n_z >= 1,
+                 "tk_restrict_slab: bad arguments (n_fine must be even)");
+    return transfer_launch(1, n_fine, n_u, n_z, row0, row1, xf, nullptr, nullptr, xc,
+                           as_stream(stream));
+}
+
+int tk_prolong_add_slab(int32_t n_fine, int32_t n_u, int32_t n_z, int32_t row0, int32_t row1,
+                        const double* xc, const double* halo_prev_ul,
+                        const double* halo_next_vm, double* xf, void* stream) {
+    TK_CHECK_ARG(xf && xc && n_fine >= 2 && n_fine % 2 == 0 && n_u >= 1 && n_z >= 1,
+                 "tk_prolong_add_slab: bad arguments (n_fine must be even)");
+    return transfer_launch(0, n_fine, n_u, n_z, row0, row1, xc, halo_prev_ul, halo_next_vm, xf,
+                           as_stream(stream));
 }
 
 int tk_residual_restrict(const tk_level* L, const double* b, const double* x, double* rc,
@@ -159,7 +190,8 @@ int tk_residual_restrict(const tk_level* L, const double* b, const double* x, do
     TK_CHECK_ARG(b && x && rc && work, "tk_residual_restrict: null vector");
     int rcode = level_op(L, 2, 2, b, x, work, 1.0, stream);
     if (rcode) return rcode;
-    return transfer_launch(1, L->n_steps, L->n_u, L->n_z, work, rc, as_stream(stream));
+    return transfer_launch(1, L->n_steps, L->n_u, L->n_z, L->row0, L->row1, work, nullptr,
+                           nullptr, rc, as_stream(stream));
 }
 
 int64_t tk_reduce_work_len(void) { return reduce_work_len(); }

@@ -54,6 +54,29 @@ struct Lay {
     __host__ __device__ int64_t t_mu(int t) const { return off_mu(t); }
 };
 
+// Time slab of a level: global block rows [r0, r1); local vectors start at the
+// global offset `base` of row r0; stage arrays start at stage r0; hu / hm are
+// the halo u-segment of row r0-1 and mu-segment of row r1.
+struct Slab {
+    int r0, r1;
+    int64_t base;
+    const double* hu;
+    const double* hm;
+    __host__ Slab(const tk_level* L, const Lay& lay)
+        : r0(L->row0), r1(L->row1 > 0 ? L->row1 : L->n_steps + 1), base(lay.start(L->row0)),
+          hu(L->halo_u), hm(L->halo_mu) {}
+    __host__ __device__ bool whole(int N) const { return r0 == 0 && r1 == N + 1; }
+    // coupling sources of row i for a local vector x (nullptr when absent)
+    __host__ __device__ const double* uprev(const Lay& L, const double* x, int i) const {
+        if (i < 1) return nullptr;
+        return (i - 1 >= r0) ? x + (L.off_u(i - 1) - base) : hu;
+    }
+    __host__ __device__ const double* munext(const Lay& L, const double* x, int i) const {
+        if (i >= L.N) return nullptr;
+        return (i + 1 < r1) ? x + (L.off_mu(i + 1) - base) : hm;
+    }
+};
+
 inline int grid_for(int64_t n, int threads, int cap = 148 * 16) {
     int64_t g = (n + threads - 1) / threads;
     if (g > cap) g = cap;

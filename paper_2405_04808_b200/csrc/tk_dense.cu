@@ -24,9 +24,15 @@ struct DView {
     const double* __restrict__ Qm_inv;
     const double* __restrict__ Ql_inv;
     const double* __restrict__ Qz_inv;
+    Slab sl;
     DView(const tk_level* L)
         : lay(L->n_steps, L->n_u, L->n_z), K(L->K), C(L->C), B(L->B), Qm(L->Qm), Ql(L->Ql),
-          Qz(L->Qz), Qm_inv(L->Qm_inv), Ql_inv(L->Ql_inv), Qz_inv(L->Qz_inv) {}
+          Qz(L->Qz), Qm_inv(L->Qm_inv), Ql_inv(L->Ql_inv), Qz_inv(L->Qz_inv),
+          sl(L, Lay(L->n_steps, L->n_u, L->n_z)) {}
+    // stage data of global block row i (stage arrays start at the slab's first row)
+    __device__ const double* Ki(int i) const { return K + (size_t)(i - sl.r0) * NU * NU; }
+    __device__ const double* Ci(int i) const { return C + (size_t)(i - sl.r0) * NU * NU; }
+    __device__ const double* Bi(int i) const { return B + (size_t)(i - sl.r0) * NU * NZ; }
 };
 
 // y = A x, A row-major R x Cn
@@ -110,22 +116,23 @@ struct Seg {
 };
 
 template <int NU, int NZ>
-__device__ __forceinline__ void load_seg(const Lay& lay, int i, const double* x, Seg<NU, NZ>& s) {
+__device__ __forceinline__ void load_seg(const Lay& lay, int i, const double* x, Seg<NU, NZ>& s,
+                                         int64_t base = 0) {
 #pragma unroll
     for (int e = 0; e < NU; ++e) { s.v[e] = 0.0; s.u[e] = 0.0; s.m[e] = 0.0; s.l[e] = 0.0; }
 #pragma unroll
     for (int e = 0; e < NZ; ++e) s.z[e] = 0.0;
     if (x == nullptr) return;
     if (i >= 1) {
-        const double* pv = x + lay.off_v(i);
-        const double* pm = x + lay.off_mu(i);
+        const double* pv = x + (lay.off_v(i) - base);
+        const double* pm = x + (lay.off_mu(i) - base);
 #pragma unroll
         for (int e = 0; e < NU; ++e) { s.v[e] = pv[e]; s.m[e] = pm[e]; }
     }
     if (i < lay.N) {
-        const double* pu = x + lay.off_u(i);
-        const double* pz = x + lay.off_z(i);
-        const double* pl = x + lay.off_l(i);
+        const double* pu = x + (lay.off_u(i) - base);
+        const double* pz = x + (lay.off_z(i) - base);
+        const double* pl = x + (lay.off_l(i) - base);
 #pragma unroll
         for (int e = 0; e < NU; ++e) { s.u[e] = pu[e]; s.l[e] = pl[e]; }
 #pragma unroll
@@ -134,17 +141,18 @@ __device__ __forceinline__ void load_seg(const Lay& lay, int i, const double* x,
 }
 
 template <int NU, int NZ>
-__device__ __forceinline__ void store_seg(const Lay& lay, int i, double* y, const Seg<NU, NZ>& s) {
+__device__ __forceinline__ void store_seg(const Lay& lay, int i, double* y, const Seg<NU, NZ>& s,
+                                          int64_t base = 0) {
     if (i >= 1) {
-        double* pv = y + lay.off_v(i);
-        double* pm = y + lay.off_mu(i);
+        double* pv = y + (lay.off_v(i) - base);
+        double* pm = y + (lay.off_mu(i) - base);
 #pragma unroll
         for (int e = 0; e < NU; ++e) { pv[e] = s.v[e]; pm[e] = s.m[e]; }
     }
     if (i < lay.N) {
-        double* pu = y + lay.off_u(i);
-        double* pz = y + lay.off_z(i);
-        double* pl = y + lay.off_l(i);
+        double* pu = y + (lay.off_u(i) - base);
+        double* pz = y + (lay.off_z(i) - base);
+        double* pl = y + (lay.off_l(i) - base);
 #pragma unroll
         for (int e = 0; e < NU; ++e) { pu[e] = s.u[e]; pl[e] = s.l[e]; }
 #pragma unroll
@@ -175,8 +183,8 @@ __device__ __forceinline__ void apply_row(const DView<NU, NZ>& V, int i, const S
     }
     if (has_uzl) {
         const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;  // q_u[i]
-        const double* K = V.K + (size_t)i * NU * NU;
-        const double* B = V.B + (size_t)i * NU * NZ;
+        const double* K = V.Ki(i);
+        const double* B = V.Bi(i);
         mv<NU, NU>(Qu, x.u, y.u);
         mtv_add<NU, NU>(K, x.l, y.u);
         if (munext) {
@@ -188,7 +196,7 @@ __device__ __forceinline__ void apply_row(const DView<NU, NZ>& V, int i, const S
         mv<NU, NU>(K, x.u, y.l);
         mv_add<NU, NZ>(B, x.z, y.l);
         if (has_vm) {
-            const double* C = V.C + (size_t)i * NU * NU;
+            const double* C = V.Ci(i);
             mtv_add<NU, NU>(C, x.l, y.v);
             mv_add<NU, NU>(C, x.v, y.l);
         }
@@ -210,10 +218,10 @@ __device__ __forceinline__ void solve_row(const DView<NU, NZ>& V, int i, const S
     }
     if (has_uzl) {
         const double* Qu_inv = (i == L.N - 1) ? V.Ql_inv : V.Qm_inv;
-        const double* K = V.K + (size_t)i * NU * NU;
-        const double* B = V.B + (size_t)i * NU * NZ;
+        const double* K = V.Ki(i);
+        const double* B = V.Bi(i);
         if (has_vm) {
-            const double* C = V.C + (size_t)i * NU * NU;
+            const double* C = V.Ci(i);
             double cv[NU];
             mv<NU, NU>(C, d.v, cv);
 #pragma unroll
@@ -288,7 +296,7 @@ __device__ __forceinline__ void solve_row(const DView<NU, NZ>& V, int i, const S
         const double* Qv = (i == L.N) ? V.Ql : V.Qm;
         mv<NU, NU>(Qv, d.v, d.m);
         if (has_uzl) {
-            const double* C = V.C + (size_t)i * NU * NU;
+            const double* C = V.Ci(i);
             mtv_add<NU, NU>(C, d.l, d.m);
         }
 #pragma unroll
@@ -303,25 +311,28 @@ __global__ void __launch_bounds__(128) dense_rows(DView<NU, NZ> V, const double*
                                                   const double* __restrict__ x,
                                                   double* __restrict__ y, double omega) {
     const Lay& L = V.lay;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= L.N; i += gridDim.x * blockDim.x) {
+    const Slab& S = V.sl;
+    const int64_t bs0 = S.base;
+    for (int i = S.r0 + blockIdx.x * blockDim.x + threadIdx.x; i < S.r1;
+         i += gridDim.x * blockDim.x) {
         Seg<NU, NZ> xs, ys;
-        const double* uprev = (i >= 1 && x) ? x + L.off_u(i - 1) : nullptr;
-        const double* munext = (i < L.N && x) ? x + L.off_mu(i + 1) : nullptr;
+        const double* uprev = x ? S.uprev(L, x, i) : nullptr;
+        const double* munext = x ? S.munext(L, x, i) : nullptr;
         if (MODE == D_SOLVE) {
-            load_seg<NU, NZ>(L, i, b, xs);
+            load_seg<NU, NZ>(L, i, b, xs, bs0);
             solve_row<NU, NZ>(V, i, xs, ys);
-            store_seg<NU, NZ>(L, i, y, ys);
+            store_seg<NU, NZ>(L, i, y, ys, bs0);
             continue;
         }
-        load_seg<NU, NZ>(L, i, x, xs);
+        load_seg<NU, NZ>(L, i, x, xs, bs0);
         apply_row<NU, NZ>(V, i, xs, MODE == D_APPLY_DIAG ? nullptr : uprev,
                           MODE == D_APPLY_DIAG ? nullptr : munext, ys);
         if (MODE == D_APPLY || MODE == D_APPLY_DIAG) {
-            store_seg<NU, NZ>(L, i, y, ys);
+            store_seg<NU, NZ>(L, i, y, ys, bs0);
             continue;
         }
         Seg<NU, NZ> bs;
-        load_seg<NU, NZ>(L, i, b, bs);
+        load_seg<NU, NZ>(L, i, b, bs, bs0);
 #pragma unroll
         for (int e = 0; e < NU; ++e) {
             bs.v[e] -= ys.v[e]; bs.u[e] -= ys.u[e]; bs.m[e] -= ys.m[e]; bs.l[e] -= ys.l[e];
@@ -329,7 +340,7 @@ __global__ void __launch_bounds__(128) dense_rows(DView<NU, NZ> V, const double*
 #pragma unroll
         for (int e = 0; e < NZ; ++e) bs.z[e] -= ys.z[e];
         if (MODE == D_RESIDUAL) {
-            store_seg<NU, NZ>(L, i, y, bs);
+            store_seg<NU, NZ>(L, i, y, bs, bs0);
             continue;
         }
         // D_JACOBI: x_out = x + omega * D^{-1} (b - A x)
@@ -341,7 +352,7 @@ __global__ void __launch_bounds__(128) dense_rows(DView<NU, NZ> V, const double*
         }
 #pragma unroll
         for (int e = 0; e < NZ; ++e) xs.z[e] += omega * ys.z[e];
-        store_seg<NU, NZ>(L, i, y, xs);
+        store_seg<NU, NZ>(L, i, y, xs, bs0);
     }
 }
 
@@ -545,9 +556,13 @@ template <int NU, int NZ>
 static int dense_launch_t(const tk_level* Lv, int op, const double* b, const double* x, double* y,
                           double omega, cudaStream_t s) {
     DView<NU, NZ> V(Lv);
-    const int rows = Lv->n_steps + 1;
+    const int rows = V.sl.r1 - V.sl.r0;
     const int th = 128;
     const int grid = grid_for(rows, th, 1 << 20);
+    if (op >= 10 && !V.sl.whole(Lv->n_steps)) {
+        set_error("block Gauss-Seidel substitution needs the whole level (no time slab)");
+        return TK_ERR_ARG;
+    }
     switch (op) {
         case D_APPLY: dense_rows<NU, NZ, D_APPLY><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
         case D_APPLY_DIAG:

@@ -1,79 +1,143 @@
 // Time-level transfers on the reference layout (multigrid.py:263-300):
 // states/multipliers (u, v, lam, mu) use injection down / linear interpolation
 // up; piecewise-constant controls use 2-interval averages down / copies up.
-// One thread per (time index, slot); a slot enumerates the 4nu+nz variables
-// of one time index: [u | v | z | mu | lam].
+//
+// Both kernels run over a time slab of FINE block rows [r0, r1) (the whole
+// level is the slab [0, N+1)).  One thread per element of the output slice:
+// the element's global offset gives (block row, variable kind, component,
+// time index), from which the source elements are located.  Restriction is
+// slab-local; prolongation reads two halo segments: the previous slab's last
+// coarse (u, lam) and the next slab's first coarse (v, mu).
 #include "tk_common.cuh"
 
 namespace tk {
 
-__device__ __forceinline__ int64_t slot_off(const Lay& L, int t, int slot, bool& is_z) {
+enum Kind { KU = 0, KV = 1, KZ = 2, KM = 3, KL = 4 };
+
+// Decode a global offset g of layout L into (kind, component, time index t).
+__device__ __forceinline__ void decode(const Lay& L, int64_t g, int& kind, int& c, int& t) {
     const int nu = L.nu, nz = L.nz;
-    is_z = false;
-    if (slot < nu) return L.t_u(t) + slot;
-    slot -= nu;
-    if (slot < nu) return L.t_v(t) + slot;
-    slot -= nu;
-    if (slot < nz) { is_z = true; return L.t_z(t) + slot; }
-    slot -= nz;
-    if (slot < nu) return L.t_mu(t) + slot;
-    slot -= nu;
-    return L.t_l(t) + slot;
+    if (g < L.F) {                               // block 0: u1 z1 lam1
+        const int o = (int)g;
+        t = 1;
+        if (o < nu) { kind = KU; c = o; }
+        else if (o < nu + nz) { kind = KZ; c = o - nu; }
+        else { kind = KL; c = o - nu - nz; }
+        return;
+    }
+    const int64_t q = g - L.F;
+    int i = (int)(q / L.m) + 1;
+    int o = (int)(q - (int64_t)(i - 1) * L.m);
+    if (i >= L.N) {                              // last block: v_N mu_N
+        i = L.N;
+        o = (int)(g - L.start(L.N));
+        t = L.N;
+        if (o < nu) { kind = KV; c = o; } else { kind = KM; c = o - nu; }
+        return;
+    }
+    // interior block i: v_i u_{i+1} z_{i+1} mu_i lam_{i+1}
+    if (o < nu) { kind = KV; c = o; t = i; }
+    else if (o < 2 * nu) { kind = KU; c = o - nu; t = i + 1; }
+    else if (o < 2 * nu + nz) { kind = KZ; c = o - 2 * nu; t = i + 1; }
+    else if (o < 3 * nu + nz) { kind = KM; c = o - 2 * nu - nz; t = i; }
+    else { kind = KL; c = o - 3 * nu - nz; t = i + 1; }
 }
 
-__global__ void restrict_kernel(Lay Lf, Lay Lc, const double* __restrict__ xf,
-                                double* __restrict__ xc) {
-    const int64_t m = Lc.m;
-    const int64_t total = (int64_t)Lc.N * m;
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+__device__ __forceinline__ int64_t kind_off(const Lay& L, int kind, int t) {
+    switch (kind) {
+        case KU: return L.t_u(t);
+        case KV: return L.t_v(t);
+        case KZ: return L.t_z(t);
+        case KM: return L.t_mu(t);
+        default: return L.t_l(t);
+    }
+}
+
+// coarse slice [cbase, cbase + clen) of layout Lc; element (kind, c, t) with halos
+__device__ __forceinline__ double coarse_val(const Lay& Lc, const double* xc, int64_t cbase,
+                                             int64_t clen, const double* hprev,
+                                             const double* hnext, int kind, int c, int t) {
+    const int64_t g = kind_off(Lc, kind, t) + c;
+    const int64_t l = g - cbase;
+    if (l >= 0 && l < clen) return xc[l];
+    if (l < 0) return hprev[(kind == KU ? 0 : Lc.nu) + c];   // previous slab: (u, lam)
+    return hnext[(kind == KV ? 0 : Lc.nu) + c];                // next slab: (v, mu)
+}
+
+__global__ void restrict_kernel(Lay Lf, Lay Lc, int64_t fbase, int64_t cbase, int64_t clen,
+                                const double* __restrict__ xf, double* __restrict__ xc) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < clen;
          k += (int64_t)gridDim.x * blockDim.x) {
-        const int t = (int)(k / m) + 1;
-        const int slot = (int)(k % m);
-        bool is_z;
-        const int64_t oc = slot_off(Lc, t, slot, is_z);
-        if (is_z) {
-            const int64_t a = slot_off(Lf, 2 * t - 1, slot, is_z);
-            const int64_t b = slot_off(Lf, 2 * t, slot, is_z);
-            xc[oc] = 0.5 * (xf[a] + xf[b]);
+        int kind, c, t;
+        decode(Lc, cbase + k, kind, c, t);
+        if (kind == KZ) {
+            const double a = xf[kind_off(Lf, KZ, 2 * t - 1) + c - fbase];
+            const double b = xf[kind_off(Lf, KZ, 2 * t) + c - fbase];
+            xc[k] = 0.5 * (a + b);
         } else {
-            xc[oc] = xf[slot_off(Lf, 2 * t, slot, is_z)];
+            xc[k] = xf[kind_off(Lf, kind, 2 * t) + c - fbase];
         }
     }
 }
 
-__global__ void prolong_add_kernel(Lay Lf, Lay Lc, const double* __restrict__ xc,
-                                   double* __restrict__ xf) {
-    const int64_t m = Lf.m;
-    const int64_t total = (int64_t)Lf.N * m;
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+__global__ void prolong_add_kernel(Lay Lf, Lay Lc, int64_t fbase, int64_t flen, int64_t cbase,
+                                   int64_t clen, const double* __restrict__ xc,
+                                   const double* __restrict__ hprev,
+                                   const double* __restrict__ hnext, double* __restrict__ xf) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < flen;
          k += (int64_t)gridDim.x * blockDim.x) {
-        const int t = (int)(k / m) + 1;
-        const int slot = (int)(k % m);
-        bool is_z;
-        const int64_t of = slot_off(Lf, t, slot, is_z);
+        int kind, c, t;
+        decode(Lf, fbase + k, kind, c, t);
         double val;
-        if (is_z) {
-            val = xc[slot_off(Lc, (t + 1) / 2, slot, is_z)];
+        if (kind == KZ) {
+            val = coarse_val(Lc, xc, cbase, clen, hprev, hnext, KZ, c, (t + 1) / 2);
         } else if ((t & 1) == 0) {
-            val = xc[slot_off(Lc, t / 2, slot, is_z)];
+            val = coarse_val(Lc, xc, cbase, clen, hprev, hnext, kind, c, t / 2);
         } else if (t == 1) {
-            val = xc[slot_off(Lc, 1, slot, is_z)];
+            val = coarse_val(Lc, xc, cbase, clen, hprev, hnext, kind, c, 1);
         } else {
             const int j = (t - 1) / 2;
-            val = 0.5 * (xc[slot_off(Lc, j, slot, is_z)] + xc[slot_off(Lc, j + 1, slot, is_z)]);
+            val = 0.5 * (coarse_val(Lc, xc, cbase, clen, hprev, hnext, kind, c, j) +
+                         coarse_val(Lc, xc, cbase, clen, hprev, hnext, kind, c, j + 1));
         }
-        xf[of] = xf[of] + val;
+        xf[k] = xf[k] + val;
     }
 }
 
-int transfer_launch(int restrict_op, int n_fine, int nu, int nz, const double* in, double* out,
-                    cudaStream_t s) {
+// fine rows [r0, r1) -> coarse rows [r0/2, r1/2) (through N/2 for the last slab)
+static void slab_geom(const Lay& Lf, const Lay& Lc, int r0, int r1, int64_t& fbase,
+                      int64_t& flen, int64_t& cbase, int64_t& clen) {
+    const int c0 = r0 / 2;
+    const int c1 = (r1 == Lf.N + 1) ? Lc.N + 1 : r1 / 2;
+    fbase = Lf.start(r0);
+    flen = (r1 == Lf.N + 1 ? Lf.dim() : Lf.start(r1)) - fbase;
+    cbase = Lc.start(c0);
+    clen = (c1 == Lc.N + 1 ? Lc.dim() : Lc.start(c1)) - cbase;
+}
+
+int transfer_launch(int restrict_op, int n_fine, int nu, int nz, int r0, int r1, const double* in,
+                    const double* hprev, const double* hnext, double* out, cudaStream_t s) {
     Lay Lf(n_fine, nu, nz), Lc(n_fine / 2, nu, nz);
+    if (r1 <= 0) r1 = n_fine + 1;
+    if (r0 < 0 || r0 >= r1 || r1 > n_fine + 1 || (r0 & 1) || ((r1 & 1) && r1 != n_fine + 1)) {
+        set_error("transfer: bad fine slab [%d, %d) for N=%d (edges must be even)", r0, r1,
+                  n_fine);
+        return TK_ERR_ARG;
+    }
+    int64_t fbase, flen, cbase, clen;
+    slab_geom(Lf, Lc, r0, r1, fbase, flen, cbase, clen);
+    const bool need_prev = r0 > 0, need_next = r1 <= n_fine;
     const int th = 256;
     if (restrict_op) {
-        restrict_kernel<<<grid_for(Lc.dim(), th, 148 * 32), th, 0, s>>>(Lf, Lc, in, out);
+        restrict_kernel<<<grid_for(clen, th, 148 * 32), th, 0, s>>>(Lf, Lc, fbase, cbase, clen,
+                                                                    in, out);
     } else {
-        prolong_add_kernel<<<grid_for(Lf.dim(), th, 148 * 32), th, 0, s>>>(Lf, Lc, in, out);
+        if ((need_prev && !hprev) || (need_next && !hnext)) {
+            set_error("prolong_add: slab [%d, %d) needs its coarse halo segments", r0, r1);
+            return TK_ERR_ARG;
+        }
+        prolong_add_kernel<<<grid_for(flen, th, 148 * 32), th, 0, s>>>(
+            Lf, Lc, fbase, flen, cbase, clen, in, hprev, hnext, out);
     }
     return check_launch("transfer");
 }

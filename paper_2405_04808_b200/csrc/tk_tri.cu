@@ -31,9 +31,13 @@ struct TView {
     const double* Qz;
     const double* cr;
     double kappa;
+    Slab sl;
     TView(const tk_level* L)
         : lay(L->n_steps, L->n_u, L->n_z), n(L->n_u), K(L->K), C(L->C), Qm(L->Qm), Ql(L->Ql),
-          Qz(L->Qz), cr(L->qz_cr), kappa(L->kappa) {}
+          Qz(L->Qz), cr(L->qz_cr), kappa(L->kappa), sl(L, Lay(L->n_steps, L->n_u, L->n_z)) {}
+    // stage diagonals of global block row i (stage arrays start at the slab's first row)
+    __device__ const double* Ki(int i) const { return K + (size_t)(i - sl.r0) * 3 * n; }
+    __device__ const double* Ci(int i) const { return C + (size_t)(i - sl.r0) * 3 * n; }
 };
 
 // (A x)_j for a tridiagonal A stored [3][n] = (sub, diag, sup); x in global memory
@@ -259,7 +263,7 @@ __device__ __forceinline__ void tri_init_de(const TView& V, int i, TriSm& S) {
     const int n = V.n;
     const double k2 = V.kappa * V.kappa;
     const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;
-    const double* K = V.K + (size_t)i * 3 * n;
+    const double* K = V.Ki(i);
     const double* Qz = V.Qz;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
         const int J = PI(j);
@@ -294,10 +298,11 @@ __device__ void tri_block(const TView& V, int i, const double* b, const double* 
     const double* Qv = (i == L.N) ? V.Ql : V.Qm;
     const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;
     const double* Qz = V.Qz;
-    const double* K = has_uzl ? V.K + (size_t)i * 3 * n : nullptr;
-    const double* C = (has_uzl && has_vm) ? V.C + (size_t)i * 3 * n : nullptr;
-    const int64_t ov = L.off_v(i), ou = L.off_u(i), oz = L.off_z(i), om = L.off_mu(i),
-                  ol = L.off_l(i);
+    const double* K = has_uzl ? V.Ki(i) : nullptr;
+    const double* C = (has_uzl && has_vm) ? V.Ci(i) : nullptr;
+    const int64_t bs = V.sl.base;
+    const int64_t ov = L.off_v(i) - bs, ou = L.off_u(i) - bs, oz = L.off_z(i) - bs,
+                  om = L.off_mu(i) - bs, ol = L.off_l(i) - bs;
 
     for (int j = tid; j < n; j += nth) {
         const int J = PI(j);
@@ -365,9 +370,9 @@ __global__ void __launch_bounds__(256, 3) tri_rows(TView V, const double* __rest
                          double* __restrict__ y, double omega) {
     extern __shared__ double sm[];
     const Lay& L = V.lay;
-    for (int i = blockIdx.x; i <= L.N; i += gridDim.x) {
-        const double* uprev = (x && i >= 1) ? x + L.off_u(i - 1) : nullptr;
-        const double* munext = (x && i < L.N) ? x + L.off_mu(i + 1) : nullptr;
+    for (int i = V.sl.r0 + blockIdx.x; i < V.sl.r1; i += gridDim.x) {
+        const double* uprev = x ? V.sl.uprev(L, x, i) : nullptr;
+        const double* munext = x ? V.sl.munext(L, x, i) : nullptr;
         tri_block(V, i, b, x, uprev, munext, y, omega, x, sm);
     }
 }
@@ -687,16 +692,17 @@ __global__ void tri_apply(TView V, const double* __restrict__ b, const double* _
     const Lay& L = V.lay;
     const int n = V.n;
     const double kap = V.kappa;
-    for (int i = blockIdx.x; i <= L.N; i += gridDim.x) {
+    const int64_t bs = V.sl.base;
+    for (int i = V.sl.r0 + blockIdx.x; i < V.sl.r1; i += gridDim.x) {
         const bool has_vm = i >= 1, has_uzl = i < L.N;
         const double* Qv = (i == L.N) ? V.Ql : V.Qm;
         const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;
-        const double* K = has_uzl ? V.K + (size_t)i * 3 * n : nullptr;
-        const double* C = (has_uzl && has_vm) ? V.C + (size_t)i * 3 * n : nullptr;
-        const int64_t ov = L.off_v(i), ou = L.off_u(i), oz = L.off_z(i), om = L.off_mu(i),
-                      ol = L.off_l(i);
-        const double* uprev = (MODE != T_APPLY_DIAG && has_vm) ? x + L.off_u(i - 1) : nullptr;
-        const double* munext = (MODE != T_APPLY_DIAG && has_uzl) ? x + L.off_mu(i + 1) : nullptr;
+        const double* K = has_uzl ? V.Ki(i) : nullptr;
+        const double* C = (has_uzl && has_vm) ? V.Ci(i) : nullptr;
+        const int64_t ov = L.off_v(i) - bs, ou = L.off_u(i) - bs, oz = L.off_z(i) - bs,
+                      om = L.off_mu(i) - bs, ol = L.off_l(i) - bs;
+        const double* uprev = (MODE != T_APPLY_DIAG) ? V.sl.uprev(L, x, i) : nullptr;
+        const double* munext = (MODE != T_APPLY_DIAG) ? V.sl.munext(L, x, i) : nullptr;
         for (int j = threadIdx.x; j < n; j += blockDim.x) {
             if (has_vm) {
                 double av = tmv(Qv, n, x + ov, j) - x[om + j];
@@ -757,7 +763,11 @@ int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, dou
         set_error("tri family needs n_z == n_u (got %d, %d)", Lv->n_u, Lv->n_z);
         return TK_ERR_UNSUPPORTED;
     }
-    const int rows = Lv->n_steps + 1;
+    const int rows = V.sl.r1 - V.sl.r0;
+    if (op >= 10 && !V.sl.whole(Lv->n_steps)) {
+        set_error("block Gauss-Seidel substitution needs the whole level (no time slab)");
+        return TK_ERR_ARG;
+    }
     if (op == T_APPLY || op == T_APPLY_DIAG || op == T_RESIDUAL) {
         const int th = n >= 256 ? 256 : 128;
         const int grid = rows < (1 << 30) ? rows : (1 << 30);

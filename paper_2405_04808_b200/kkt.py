@@ -126,10 +126,36 @@ class StageBlocks:
     kappa: float = 0.0
     qz_cr: Optional[torch.Tensor] = None
     host_weights: dict = field(default_factory=dict, repr=False)
+    # time slab: global block rows [row0, row1) of a level with n_global steps
+    # (row1 == 0: the whole level); K/C/B then hold stages [row0, min(row1, N)).
+    n_global: int = 0
+    row0: int = 0
+    row1: int = 0
+
+    def __post_init__(self):
+        if self.n_global == 0:
+            self.n_global = self.n_steps
+
+    @property
+    def rows(self):
+        return self.row0, (self.row1 if self.row1 > 0 else self.n_global + 1)
 
     @property
     def dim(self) -> int:
-        return self.n_steps * (4 * self.n_u + self.n_z)
+        r0, r1 = self.rows
+        return slab_span(self.n_global, self.n_u, self.n_z, r0, r1)[1]
+
+
+def row_start(n: int, nu: int, nz: int, i: int) -> int:
+    """Global offset of block row i (kkt.py:144-147)."""
+    return 0 if i == 0 else (2 * nu + nz) + (i - 1) * (4 * nu + nz)
+
+
+def slab_span(n: int, nu: int, nz: int, r0: int, r1: int):
+    """(offset, length) of block rows [r0, r1) in the global vector."""
+    a = row_start(n, nu, nz, r0)
+    b = n * (4 * nu + nz) if r1 >= n + 1 else row_start(n, nu, nz, r1)
+    return a, b - a
 
 
 def _weights(family, q_mid, q_last, q_z, kappa):
@@ -166,41 +192,51 @@ def _choose_family(n_u, n_z, q_mid, q_z, kappa_ok):
         "nor tridiagonal with B = kappa*Qz")
 
 
-def build_stage_blocks(p: ProblemSpec, dt: float, u_seq, v_seq, z_seq) -> StageBlocks:
+def build_stage_blocks(p: ProblemSpec, dt: float, u_seq, v_seq, z_seq,
+                       rows=None) -> StageBlocks:
     """Linearise every stage at (u, v, z) with spacing dt (kkt.py:100-124).
 
     Built-in problems (``p.native``) are linearised on the device by
     tk_stage_vanderpol / tk_stage_burgers; other specs go through their
-    Python callables once (setup) and are uploaded.
+    Python callables once (setup) and are uploaded.  ``rows=(r0, r1)``
+    builds only the stages of the time slab of block rows [r0, r1).
     """
     n = int(np.shape(u_seq)[0])
     nu, nz = p.n_u, p.n_z
     q_mid, q_last, q_z = _problem_weights(p, dt, n)
     nat = p.native
-    if nat is not None and nat["kind"] == "vanderpol":
-        u = dev.to_device(u_seq)
-        v = dev.to_device(v_seq)
-        z = dev.to_device(z_seq)
-        u0 = dev.to_device(p.u0)
-        K = dev.empty(n, nu, nu)
-        Cm = dev.empty(n, nu, nu)
-        B = dev.empty(n, nu, nz)
-        dev.call("tk_stage_vanderpol", n, dt, p.theta, nat["mu"], nz, dev.P(u0), dev.P(u),
-                 dev.P(v), dev.P(z), dev.P(K), dev.P(Cm), dev.P(B), dev.stream())
-        w = _weights(FAMILY_DENSE, q_mid, q_last, q_z, 0.0)
-        return StageBlocks(FAMILY_DENSE, n, nu, nz, K, Cm, B, **w)
-    if nat is not None and nat["kind"] == "burgers":
-        # F_z = M and w_control = alpha*M  =>  B = dt*M = kappa*Qz, kappa = 1/alpha
+    r0, r1 = (0, n + 1) if rows is None else (int(rows[0]), int(rows[1]))
+    slab = dict(n_global=n, row0=r0, row1=0 if rows is None else r1)
+    s0, s1 = r0, min(r1, n)           # stages of the slab
+    ns = max(s1 - s0, 0)
+    if nat is not None and nat["kind"] in ("vanderpol", "burgers"):
+        u = dev.to_device(np.asarray(u_seq)[s0:s1] if not isinstance(u_seq, torch.Tensor)
+                          else u_seq[s0:s1])
+        v = dev.to_device(np.asarray(v_seq)[s0:s1] if not isinstance(v_seq, torch.Tensor)
+                          else v_seq[s0:s1])
+        first = p.u0 if s0 == 0 else (v_seq[s0 - 1])
+        u0 = dev.to_device(first)
+        if nat["kind"] == "vanderpol":
+            z = dev.to_device(np.asarray(z_seq)[s0:s1] if not isinstance(z_seq, torch.Tensor)
+                              else z_seq[s0:s1])
+            K = dev.empty(max(ns, 1), nu, nu)
+            Cm = dev.empty(max(ns, 1), nu, nu)
+            B = dev.empty(max(ns, 1), nu, nz)
+            if ns:
+                dev.call("tk_stage_vanderpol", ns, dt, p.theta, nat["mu"], nz, dev.P(u0),
+                         dev.P(u), dev.P(v), dev.P(z), dev.P(K), dev.P(Cm), dev.P(B),
+                         dev.stream())
+            w = _weights(FAMILY_DENSE, q_mid, q_last, q_z, 0.0)
+            return StageBlocks(FAMILY_DENSE, ns, nu, nz, K, Cm, B, **w, **slab)
+        # Burgers: F_z = M and w_control = alpha*M  =>  B = dt*M = kappa*Qz, kappa = 1/alpha
         kappa = float(p.mass[0, 0] / p.w_control[0, 0])
-        u = dev.to_device(u_seq)
-        v = dev.to_device(v_seq)
-        u0 = dev.to_device(p.u0)
-        K = dev.empty(n, 3, nu)
-        Cm = dev.empty(n, 3, nu)
-        dev.call("tk_stage_burgers", n, nu, dt, p.theta, nat["nu"], dev.P(u0), dev.P(u),
-                 dev.P(v), dev.P(K), dev.P(Cm), dev.stream())
+        K = dev.empty(max(ns, 1), 3, nu)
+        Cm = dev.empty(max(ns, 1), 3, nu)
+        if ns:
+            dev.call("tk_stage_burgers", ns, nu, dt, p.theta, nat["nu"], dev.P(u0), dev.P(u),
+                     dev.P(v), dev.P(K), dev.P(Cm), dev.stream())
         w = _weights(FAMILY_TRI, q_mid, q_last, q_z, kappa)
-        return StageBlocks(FAMILY_TRI, n, nu, nz, K, Cm, None, **w)
+        return StageBlocks(FAMILY_TRI, ns, nu, nz, K, Cm, None, **w, **slab)
     # generic ProblemSpec: evaluate the callables once on the host
     u_seq, v_seq, z_seq = (np.asarray(a, dtype=np.float64) for a in (u_seq, v_seq, z_seq))
     k = np.empty((n, nu, nu)); c = np.empty((n, nu, nu)); b = np.empty((n, nu, nz))
@@ -211,7 +247,15 @@ def build_stage_blocks(p: ProblemSpec, dt: float, u_seq, v_seq, z_seq) -> StageB
     qu = np.empty((n, nu, nu)); qz = np.empty((n, nz, nz))
     for i in range(n):
         qu[i], _, qz[i] = stage_weights(p, dt, i, n)
-    return stage_blocks_from_arrays(k, c, b, qu, qu, qz)
+    st = stage_blocks_from_arrays(k, c, b, qu, qu, qz)
+    if rows is None:
+        return st
+    st.K = st.K[s0:max(s1, s0 + 1)].contiguous()
+    st.C = st.C[s0:max(s1, s0 + 1)].contiguous()
+    if st.B is not None:
+        st.B = st.B[s0:max(s1, s0 + 1)].contiguous()
+    st.n_steps, st.n_global, st.row0, st.row1 = ns, n, r0, r1
+    return st
 
 
 def stage_blocks_from_arrays(k, c, b, q_u, q_v, q_z) -> StageBlocks:
@@ -253,17 +297,37 @@ class BlockTriKKT:
 
     def __init__(self, stage: StageBlocks):
         self.stage = stage
-        self.n_steps, self.n_u, self.n_z = stage.n_steps, stage.n_u, stage.n_z
+        self.n_steps, self.n_u, self.n_z = stage.n_global, stage.n_u, stage.n_z
+        self.row0, self.row1 = stage.rows
+        self.is_slab = not (self.row0 == 0 and self.row1 == self.n_steps + 1)
         self._layout = None
         s = stage
+        # halo buffers of a time slab (refreshed by the neighbour exchange)
+        self.halo_u = dev.zeros(s.n_u) if self.row0 > 0 else None
+        self.halo_mu = dev.zeros(s.n_u) if self.row1 <= self.n_steps else None
         self.level = _lib.TkLevel(
-            family=s.family, n_steps=s.n_steps, n_u=s.n_u, n_z=s.n_z,
+            family=s.family, n_steps=s.n_global, n_u=s.n_u, n_z=s.n_z,
             K=dev.P(s.K), C=dev.P(s.C), B=dev.P(s.B), Qm=dev.P(s.Qm), Ql=dev.P(s.Ql),
             Qz=dev.P(s.Qz), Qm_inv=dev.P(s.Qm_inv), Ql_inv=dev.P(s.Ql_inv),
-            Qz_inv=dev.P(s.Qz_inv), kappa=s.kappa, qz_cr=dev.P(s.qz_cr))
+            Qz_inv=dev.P(s.Qz_inv), kappa=s.kappa, qz_cr=dev.P(s.qz_cr),
+            row0=self.row0, row1=0 if not self.is_slab else self.row1,
+            halo_u=dev.P(self.halo_u), halo_mu=dev.P(self.halo_mu))
         self.lref = C.byref(self.level)
         self._fac = None
         self._scratch = None
+
+    # --- slab geometry (local offsets of the boundary segments) -------------
+    def seg_offset(self, kind: str, row: int) -> int:
+        """Local offset of segment `kind` of global block row `row`."""
+        nu, nz, N = self.n_u, self.n_z, self.n_steps
+        start = row_start(N, nu, nz, row) - row_start(N, nu, nz, self.row0)
+        if row == 0:
+            off = {"u": 0, "z": nu, "lam": nu + nz}[kind]
+        elif row == N:
+            off = {"v": 0, "mu": nu}[kind]
+        else:
+            off = {"v": 0, "u": nu, "z": 2 * nu, "mu": 2 * nu + nz, "lam": 3 * nu + nz}[kind]
+        return start + off
 
     def ensure_subst(self) -> None:
         """Precompute the Gauss-Seidel chain factors once (tk_subst_factor);

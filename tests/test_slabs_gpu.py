@@ -1,0 +1,102 @@
+"""Time-slab sharding on one GPU: R virtual ranks (threads) drive the slab
+kernels with halo exchanges; the distributed V-cycle, operator and dots must
+reproduce the single-slab path (row-local kernels => bitwise for the cycle)."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, product_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(name):
+    g = load_golden(name)
+    p, grid = product_problem(g)
+    return g, p, grid
+
+
+@pytest.mark.parametrize("name,R,levels", [("cfg1_burgers", 2, 4), ("cfg1_burgers", 4, 4),
+                                           ("cfg0_vdp", 2, 3), ("cfg0_vdp", 4, 3),
+                                           ("burgers_ref", 2, 3)])
+def test_virtual_ranks_match_single(name, R, levels):
+    import torch
+
+    import paper_2405_04808_b200 as P
+    from paper_2405_04808_b200 import slabs
+    g, p, grid = _setup(name)
+    u, v, z, b = g["u"], g["v"], g["z"], g["b"]
+    h = P.build_hierarchy(p, u, v, z, grid, levels, sweeps=int(g["sweeps"]), coarse_tol=1e-2)
+    ref = P.cycle(h, 0, b)
+    ref_ax = P.assemble_kkt(P.build_stage_blocks(p, grid.dt, u, v, z)).apply(g["x"])
+
+    comms = slabs.ThreadComm.group(R)
+
+    def body(c):
+        sh = slabs.SlabHierarchy(p, u, v, z, grid, levels, c, sweeps=int(g["sweeps"]),
+                                 coarse_tol=1e-2)
+        off, ln = sh.local_span()
+        bl = torch.from_numpy(np.ascontiguousarray(b[off:off + ln])).cuda()
+        xl = torch.from_numpy(np.ascontiguousarray(g["x"][off:off + ln])).cuda()
+        out = sh.vcycle(bl)
+        ax = sh.apply(xl)
+        d = sh.dot(xl, bl)
+        torch.cuda.synchronize()
+        return off, out.cpu().numpy(), ax.cpu().numpy(), d
+
+    res = slabs.run_threads(comms, body)
+    got = np.concatenate([r[1] for r in sorted(res, key=lambda t: t[0])])
+    ax = np.concatenate([r[2] for r in sorted(res, key=lambda t: t[0])])
+    assert got.shape == ref.shape
+    assert np.array_equal(got, ref), np.abs(got - ref).max()
+    assert np.array_equal(ax, ref_ax)
+    d = res[0][3]
+    assert abs(d - float(np.dot(g["x"], b))) <= 1e-12 * abs(np.dot(np.abs(g["x"]), np.abs(b)))
+
+
+def test_slab_transfers_and_halo_checks():
+    import torch
+
+    from paper_2405_04808_b200 import _lib, slabs
+    from paper_2405_04808_b200 import device as dev
+    lib = _lib.load()
+    N, nu, nz = 16, 2, 1
+    m = 4 * nu + nz
+    rng = np.random.default_rng(0)
+    xf = rng.standard_normal(N * m)
+    xc = rng.standard_normal((N // 2) * m)
+    # whole-level restrict / prolong
+    full_r = dev.empty((N // 2) * m)
+    dev.call("tk_restrict", N, nu, nz, dev.P(dev.to_device(xf)), dev.P(full_r), dev.stream())
+    full_p = dev.to_device(xf).clone()
+    dev.call("tk_prolong_add", N, nu, nz, dev.P(dev.to_device(xc)), dev.P(full_p), dev.stream())
+    for r0, r1 in ((0, 8), (8, 17), (4, 12)):
+        fo, fl = slabs.slab_span(N, nu, nz, r0, r1)
+        c0, c1 = r0 // 2, (N // 2 + 1) if r1 == N + 1 else r1 // 2
+        co, cl = slabs.slab_span(N // 2, nu, nz, c0, c1)
+        rc = dev.empty(cl)
+        dev.call("tk_restrict_slab", N, nu, nz, r0, r1, dev.P(dev.to_device(xf[fo:fo + fl])),
+                 dev.P(rc), dev.stream())
+        assert np.array_equal(dev.to_host(rc), dev.to_host(full_r)[co:co + cl])
+        # prolong with halos taken from the global coarse vector
+        hp = np.zeros(2 * nu)
+        hn = np.zeros(2 * nu)
+        if r0 > 0:
+            o_u = slabs.row_start(N // 2, nu, nz, c0 - 1) + (0 if c0 - 1 == 0 else nu)
+            o_l = slabs.row_start(N // 2, nu, nz, c0 - 1) + (nu + nz if c0 - 1 == 0
+                                                              else 3 * nu + nz)
+            hp = np.concatenate([xc[o_u:o_u + nu], xc[o_l:o_l + nu]])
+        if r1 <= N:
+            base = slabs.row_start(N // 2, nu, nz, c1)
+            o_v = base
+            o_m = base + (nu if c1 == N // 2 else 2 * nu + nz)
+            hn = np.concatenate([xc[o_v:o_v + nu], xc[o_m:o_m + nu]])
+        xl = dev.to_device(xf[fo:fo + fl]).clone()
+        xcl, hpd, hnd = (dev.to_device(a) for a in (xc[co:co + cl], hp, hn))  # keep alive
+        dev.call("tk_prolong_add_slab", N, nu, nz, r0, r1, dev.P(xcl), dev.P(hpd), dev.P(hnd),
+                 dev.P(xl), dev.stream())
+        assert np.array_equal(dev.to_host(xl), dev.to_host(full_p)[fo:fo + fl])
+    # odd slab edges are rejected
+    bad = dev.empty(8)
+    assert lib.tk_restrict_slab(N, nu, nz, 1, 8, dev.P(bad), dev.P(bad), None) == _lib.TK_ERR_ARG
+    torch.cuda.synchronize()
