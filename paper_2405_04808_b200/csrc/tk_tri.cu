@@ -14,12 +14,22 @@
 // no pivoting.  All reductions run in shared memory; node j lives at the
 // padded index PI(j) = j + j/16, which keeps every stride-2^l reduction
 // level free of (or at most 2-way) bank conflicts.
+//
+// Every kernel is templated on NT, the number of spatial nodes when it is a
+// compile-time constant (64..2048 are dispatched; NT = 0 is the generic
+// runtime-n build): shared-memory row offsets then fold into immediates and
+// the cyclic-reduction level loops unroll.
 #include "tk_common.cuh"
 
 namespace tk {
 
-__host__ __device__ __forceinline__ int PI(int j) { return j + (j >> 4); }
-__host__ __device__ __forceinline__ int padded(int n) { return n + (n >> 4) + 1; }
+__host__ __device__ __forceinline__ constexpr int PI(int j) { return j + (j >> 4); }
+__host__ __device__ __forceinline__ constexpr int padded(int n) { return n + (n >> 4) + 1; }
+__host__ __device__ __forceinline__ constexpr int ilog2(int n) {
+    return n <= 1 ? 0 : 1 + ilog2(n >> 1);
+}
+
+static constexpr int kMaxLev = 12;   // n <= 4096
 
 struct TView {
     Lay lay;
@@ -36,9 +46,12 @@ struct TView {
         : lay(L->n_steps, L->n_u, L->n_z), n(L->n_u), K(L->K), C(L->C), Qm(L->Qm), Ql(L->Ql),
           Qz(L->Qz), cr(L->qz_cr), kappa(L->kappa), sl(L, Lay(L->n_steps, L->n_u, L->n_z)) {}
     // stage diagonals of global block row i (stage arrays start at the slab's first row)
-    __device__ const double* Ki(int i) const { return K + (size_t)(i - sl.r0) * 3 * n; }
-    __device__ const double* Ci(int i) const { return C + (size_t)(i - sl.r0) * 3 * n; }
+    __device__ const double* Ki(int i, int n_) const { return K + (size_t)(i - sl.r0) * 3 * n_; }
+    __device__ const double* Ci(int i, int n_) const { return C + (size_t)(i - sl.r0) * 3 * n_; }
 };
+
+template <int NT>
+__device__ __forceinline__ int dimn(const TView& V) { return NT > 0 ? NT : V.n; }
 
 // (A x)_j for a tridiagonal A stored [3][n] = (sub, diag, sup); x in global memory
 __device__ __forceinline__ double tmv(const double* A, int n, const double* x, int j) {
@@ -70,65 +83,88 @@ __device__ __forceinline__ double tmtv_s(const double* A, int n, const double* x
 
 static constexpr int kTriArrays = 16;
 
+// 16 padded node arrays; all addressed from one base with constant row offsets
+// when n is a compile-time constant.
 struct TriSm {
-    double *Da, *Db, *Dc, *E0, *E1, *E2, *E3, *L0, *L1, *L2, *L3, *f0, *f1, *fw, *sv, *srv;
-    __device__ TriSm(double* sm, int n) {
-        const int np = padded(n);
-        double* p = sm;
-        Da = p; p += np; Db = p; p += np; Dc = p; p += np;
-        E0 = p; p += np; E1 = p; p += np; E2 = p; p += np; E3 = p; p += np;
-        L0 = p; p += np; L1 = p; p += np; L2 = p; p += np; L3 = p; p += np;
-        f0 = p; p += np; f1 = p; p += np; fw = p; p += np; sv = p; p += np; srv = p;
-    }
+    double* b;
+    int np;
+    __device__ TriSm(double* sm, int n) : b(sm), np(padded(n)) {}
+    __device__ double* Da() const { return b; }
+    __device__ double* Db() const { return b + np; }
+    __device__ double* Dc() const { return b + 2 * np; }
+    __device__ double* E0() const { return b + 3 * np; }
+    __device__ double* E1() const { return b + 4 * np; }
+    __device__ double* E2() const { return b + 5 * np; }
+    __device__ double* E3() const { return b + 6 * np; }
+    __device__ double* L0() const { return b + 7 * np; }
+    __device__ double* L1() const { return b + 8 * np; }
+    __device__ double* L2() const { return b + 9 * np; }
+    __device__ double* L3() const { return b + 10 * np; }
+    __device__ double* f0() const { return b + 11 * np; }
+    __device__ double* f1() const { return b + 12 * np; }
+    __device__ double* fw() const { return b + 13 * np; }
+    __device__ double* sv() const { return b + 14 * np; }
+    __device__ double* srv() const { return b + 15 * np; }
 };
 
 // nodes eliminated at CR level lev (j = s-1 + 2s*m < n) and kept (j = 2s-1 + 2s*m < n)
-__host__ __device__ __forceinline__ int lvl_count(int n, int lev) {
-    const int s = 1 << lev;
-    return n >= s ? ((n - s) >> (lev + 1)) + 1 : 0;
+__host__ __device__ __forceinline__ constexpr int lvl_count(int n, int lev) {
+    return n >= (1 << lev) ? ((n - (1 << lev)) >> (lev + 1)) + 1 : 0;
 }
-__host__ __device__ __forceinline__ int kept_count(int n, int lev) { return n >> (lev + 1); }
+__host__ __device__ __forceinline__ constexpr int kept_count(int n, int lev) {
+    return n >> (lev + 1);
+}
+// number of leading levels with more than 32 eliminated nodes (run CTA-wide)
+__host__ __device__ __forceinline__ constexpr int cta_levels(int n) {
+    int l = 0;
+    while (l < ilog2(n) && lvl_count(n, l) > 32) ++l;
+    return l;
+}
 
 template <bool RHS>
 struct CrSolve {
     // phase 1 at level lev for eliminated index m: invert D_p, snapshot lower coupling
-    static __device__ __forceinline__ void elim(TriSm& S, int n, int lev, int m) {
+    static __device__ __forceinline__ void elim(const TriSm& S, int n, int lev, int m) {
         const int s = 1 << lev;
         const int p = s - 1 + 2 * s * m;
         const int P = PI(p);
-        const double a = S.Da[P], b = S.Db[P], c = S.Dc[P];
+        const double a = S.Da()[P], b = S.Db()[P], c = S.Dc()[P];
         const double idet = 1.0 / (a * c - b * b);
-        S.Da[P] = c * idet;
-        S.Db[P] = -b * idet;
-        S.Dc[P] = a * idet;
+        S.Da()[P] = c * idet;
+        S.Db()[P] = -b * idet;
+        S.Dc()[P] = a * idet;
         if (p - s >= 0) {
             const int Q = PI(p - s);
-            S.L0[P] = S.E0[Q]; S.L1[P] = S.E1[Q]; S.L2[P] = S.E2[Q]; S.L3[P] = S.E3[Q];
+            S.L0()[P] = S.E0()[Q]; S.L1()[P] = S.E1()[Q];
+            S.L2()[P] = S.E2()[Q]; S.L3()[P] = S.E3()[Q];
         } else {
-            S.L0[P] = 0.0; S.L1[P] = 0.0; S.L2[P] = 0.0; S.L3[P] = 0.0;
+            S.L0()[P] = 0.0; S.L1()[P] = 0.0; S.L2()[P] = 0.0; S.L3()[P] = 0.0;
         }
     }
     // phase 2 at level lev for kept index m: Schur update of D_j, E_j, f_j
-    static __device__ __forceinline__ void keep(TriSm& S, int n, int lev, int m,
+    static __device__ __forceinline__ void keep(const TriSm& S, int n, int lev, int m,
                                                 const double* cinv, const double* cup,
                                                 const double* clo) {
         const int s = 1 << lev;
         const int j = 2 * s - 1 + 2 * s * m;
         const int p = j - s, q = j + s;
         const int J = PI(j), P = PI(p);
-        double da = S.Da[J], db = S.Db[J], dc = S.Dc[J];
+        double da = S.Da()[J], db = S.Db()[J], dc = S.Dc()[J];
         double g0 = 0.0, g1 = 0.0, w = 0.0;
-        if (RHS) { g0 = S.f0[J]; g1 = S.f1[J]; w = S.fw[J] - cup[p] * cinv[p] * S.fw[P]; }
+        if (RHS) {
+            g0 = S.f0()[J]; g1 = S.f1()[J];
+            w = S.fw()[J] - cup[p] * cinv[p] * S.fw()[P];
+        }
         {   // lower neighbour p: coupling A = E_p (row p, col j)
-            const double e0 = S.E0[P], e1 = S.E1[P], e2 = S.E2[P], e3 = S.E3[P];
-            const double pa = S.Da[P], pb = S.Db[P], pc = S.Dc[P];
+            const double e0 = S.E0()[P], e1 = S.E1()[P], e2 = S.E2()[P], e3 = S.E3()[P];
+            const double pa = S.Da()[P], pb = S.Db()[P], pc = S.Dc()[P];
             const double t00 = e0 * pa + e2 * pb, t01 = e0 * pb + e2 * pc;
             const double t10 = e1 * pa + e3 * pb, t11 = e1 * pb + e3 * pc;
             da -= t00 * e0 + t01 * e2;
             db -= t00 * e1 + t01 * e3;
             dc -= t10 * e1 + t11 * e3;
             if (RHS) {
-                const double h0 = S.f0[P], h1 = S.f1[P];
+                const double h0 = S.f0()[P], h1 = S.f1()[P];
                 g0 -= t00 * h0 + t01 * h1;
                 g1 -= t10 * h0 + t11 * h1;
             }
@@ -136,72 +172,72 @@ struct CrSolve {
         double n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0;
         if (q < n) {  // upper neighbour q: coupling A = E_j (row j, col q)
             const int Qi = PI(q);
-            const double e0 = S.E0[J], e1 = S.E1[J], e2 = S.E2[J], e3 = S.E3[J];
-            const double qa = S.Da[Qi], qb = S.Db[Qi], qc = S.Dc[Qi];
+            const double e0 = S.E0()[J], e1 = S.E1()[J], e2 = S.E2()[J], e3 = S.E3()[J];
+            const double qa = S.Da()[Qi], qb = S.Db()[Qi], qc = S.Dc()[Qi];
             const double t00 = e0 * qa + e1 * qb, t01 = e0 * qb + e1 * qc;
             const double t10 = e2 * qa + e3 * qb, t11 = e2 * qb + e3 * qc;
             da -= t00 * e0 + t01 * e1;
             db -= t00 * e2 + t01 * e3;
             dc -= t10 * e2 + t11 * e3;
             if (RHS) {
-                const double h0 = S.f0[Qi], h1 = S.f1[Qi];
+                const double h0 = S.f0()[Qi], h1 = S.f1()[Qi];
                 g0 -= t00 * h0 + t01 * h1;
                 g1 -= t10 * h0 + t11 * h1;
-                w -= clo[q] * cinv[q] * S.fw[Qi];
+                w -= clo[q] * cinv[q] * S.fw()[Qi];
             }
             if (q + s < n) {
-                const double k0 = S.E0[Qi], k1 = S.E1[Qi], k2 = S.E2[Qi], k3 = S.E3[Qi];
+                const double k0 = S.E0()[Qi], k1 = S.E1()[Qi], k2 = S.E2()[Qi], k3 = S.E3()[Qi];
                 n0 = -(t00 * k0 + t01 * k2);
                 n1 = -(t00 * k1 + t01 * k3);
                 n2 = -(t10 * k0 + t11 * k2);
                 n3 = -(t10 * k1 + t11 * k3);
             }
         }
-        S.Da[J] = da; S.Db[J] = db; S.Dc[J] = dc;
-        S.E0[J] = n0; S.E1[J] = n1; S.E2[J] = n2; S.E3[J] = n3;
-        if (RHS) { S.f0[J] = g0; S.f1[J] = g1; S.fw[J] = w; }
+        S.Da()[J] = da; S.Db()[J] = db; S.Dc()[J] = dc;
+        S.E0()[J] = n0; S.E1()[J] = n1; S.E2()[J] = n2; S.E3()[J] = n3;
+        if (RHS) { S.f0()[J] = g0; S.f1()[J] = g1; S.fw()[J] = w; }
     }
-    static __device__ __forceinline__ void root(TriSm& S, int n, int top, const double* cinv) {
-        const int r = (1 << top) - 1, R = PI(r);
-        const double a = S.Da[R], b = S.Db[R], c = S.Dc[R];
+    static __device__ __forceinline__ void root(const TriSm& S, int n, const double* cinv) {
+        const int r = (1 << ilog2(n)) - 1, R = PI(r);
+        const double a = S.Da()[R], b = S.Db()[R], c = S.Dc()[R];
         const double idet = 1.0 / (a * c - b * b);
-        S.Da[R] = c * idet; S.Db[R] = -b * idet; S.Dc[R] = a * idet;
+        S.Da()[R] = c * idet; S.Db()[R] = -b * idet; S.Dc()[R] = a * idet;
         if (RHS) {
-            const double g0 = S.f0[R], g1 = S.f1[R];
-            S.f0[R] = (c * g0 - b * g1) * idet;
-            S.f1[R] = (a * g1 - b * g0) * idet;
-            S.fw[R] = cinv[r] * S.fw[R];
+            const double g0 = S.f0()[R], g1 = S.f1()[R];
+            S.f0()[R] = (c * g0 - b * g1) * idet;
+            S.f1()[R] = (a * g1 - b * g0) * idet;
+            S.fw()[R] = cinv[r] * S.fw()[R];
         } else {
-            S.E0[R] = 0.0; S.E1[R] = 0.0; S.E2[R] = 0.0; S.E3[R] = 0.0;
-            S.L0[R] = 0.0; S.L1[R] = 0.0; S.L2[R] = 0.0; S.L3[R] = 0.0;
+            S.E0()[R] = 0.0; S.E1()[R] = 0.0; S.E2()[R] = 0.0; S.E3()[R] = 0.0;
+            S.L0()[R] = 0.0; S.L1()[R] = 0.0; S.L2()[R] = 0.0; S.L3()[R] = 0.0;
         }
     }
     // back substitution at level lev for eliminated index m
-    static __device__ __forceinline__ void back(TriSm& S, int n, int lev, int m,
+    static __device__ __forceinline__ void back(const TriSm& S, int n, int lev, int m,
                                                 const double* cinv, const double* cup,
                                                 const double* clo) {
         const int s = 1 << lev;
         const int p = s - 1 + 2 * s * m;
         const int P = PI(p);
-        double g0 = S.f0[P], g1 = S.f1[P], w = S.fw[P];
+        double g0 = S.f0()[P], g1 = S.f1()[P], w = S.fw()[P];
         if (p - s >= 0) {
             const int Q = PI(p - s);
-            const double xa = S.f0[Q], xb = S.f1[Q];
-            g0 -= S.L0[P] * xa + S.L2[P] * xb;
-            g1 -= S.L1[P] * xa + S.L3[P] * xb;
-            w -= clo[p] * S.fw[Q];
+            const double xa = S.f0()[Q], xb = S.f1()[Q];
+            g0 -= S.L0()[P] * xa + S.L2()[P] * xb;
+            g1 -= S.L1()[P] * xa + S.L3()[P] * xb;
+            w -= clo[p] * S.fw()[Q];
         }
         if (p + s < n) {
             const int Q = PI(p + s);
-            const double xa = S.f0[Q], xb = S.f1[Q];
-            g0 -= S.E0[P] * xa + S.E1[P] * xb;
-            g1 -= S.E2[P] * xa + S.E3[P] * xb;
-            w -= cup[p] * S.fw[Q];
+            const double xa = S.f0()[Q], xb = S.f1()[Q];
+            g0 -= S.E0()[P] * xa + S.E1()[P] * xb;
+            g1 -= S.E2()[P] * xa + S.E3()[P] * xb;
+            w -= cup[p] * S.fw()[Q];
         }
-        const double pa = S.Da[P], pb = S.Db[P], pc = S.Dc[P];
-        S.f0[P] = pa * g0 + pb * g1;
-        S.f1[P] = pb * g0 + pc * g1;
-        S.fw[P] = cinv[p] * w;
+        const double pa = S.Da()[P], pb = S.Db()[P], pc = S.Dc()[P];
+        S.f0()[P] = pa * g0 + pb * g1;
+        S.f1()[P] = pb * g0 + pc * g1;
+        S.fw()[P] = cinv[p] * w;
     }
 };
 
@@ -214,35 +250,40 @@ struct CrSolve {
 // deeper levels, the root and their back-substitution run in warp 0 with
 // __syncwarp only.
 template <bool RHS>
-__device__ void cr_solve(int n, TriSm& S, const double* __restrict__ cr) {
+__device__ __forceinline__ void cr_solve(int n, const TriSm& S, const double* __restrict__ cr) {
     using K = CrSolve<RHS>;
     const int tid = threadIdx.x, nth = blockDim.x;
     const double* cinv = cr;
     const double* cup = cr + n;
     const double* clo = cr + 2 * n;
-    const int top = 31 - __clz(n);
-    int lev = 0;
-    for (; lev < top; ++lev) {
+    const int top = ilog2(n);
+    const int lw = cta_levels(n);
+#pragma unroll
+    for (int lev = 0; lev < kMaxLev; ++lev) {
+        if (lev >= lw) break;
         const int ce = lvl_count(n, lev);
-        if (ce <= 32) break;
         for (int m = tid; m < ce; m += nth) K::elim(S, n, lev, m);
         __syncthreads();
         const int ck = kept_count(n, lev);
         for (int m = tid; m < ck; m += nth) K::keep(S, n, lev, m, cinv, cup, clo);
         __syncthreads();
     }
-    const int lw = lev;
     if (tid < 32) {
-        for (int l = lw; l < top; ++l) {
+#pragma unroll
+        for (int l = 0; l < kMaxLev; ++l) {
+            if (l < lw) continue;
+            if (l >= top) break;
             if (tid < lvl_count(n, l)) K::elim(S, n, l, tid);
             __syncwarp();
             if (tid < kept_count(n, l)) K::keep(S, n, l, tid, cinv, cup, clo);
             __syncwarp();
         }
-        if (tid == 0) K::root(S, n, top, cinv);
+        if (tid == 0) K::root(S, n, cinv);
         __syncwarp();
         if (RHS) {
-            for (int l = top - 1; l >= lw; --l) {
+#pragma unroll
+            for (int l = kMaxLev - 1; l >= 0; --l) {
+                if (l >= top || l < lw) continue;
                 if (tid < lvl_count(n, l)) K::back(S, n, l, tid, cinv, cup, clo);
                 __syncwarp();
             }
@@ -250,7 +291,9 @@ __device__ void cr_solve(int n, TriSm& S, const double* __restrict__ cr) {
     }
     __syncthreads();
     if (!RHS) return;
-    for (lev = lw - 1; lev >= 0; --lev) {
+#pragma unroll
+    for (int lev = kMaxLev - 1; lev >= 0; --lev) {
+        if (lev >= lw) continue;
         const int ce = lvl_count(n, lev);
         for (int m = tid; m < ce; m += nth) K::back(S, n, lev, m, cinv, cup, clo);
         __syncthreads();
@@ -258,25 +301,24 @@ __device__ void cr_solve(int n, TriSm& S, const double* __restrict__ cr) {
 }
 
 // Load D/E of the (u,lam) system of interval i into shared memory.
-__device__ __forceinline__ void tri_init_de(const TView& V, int i, TriSm& S) {
+__device__ __forceinline__ void tri_init_de(const TView& V, int n, int i, const TriSm& S) {
     const Lay& L = V.lay;
-    const int n = V.n;
     const double k2 = V.kappa * V.kappa;
     const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;
-    const double* K = V.Ki(i);
+    const double* K = V.Ki(i, n);
     const double* Qz = V.Qz;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
         const int J = PI(j);
-        S.Da[J] = Qu[n + j];
-        S.Db[J] = K[n + j];
-        S.Dc[J] = -k2 * Qz[n + j];
+        S.Da()[J] = Qu[n + j];
+        S.Db()[J] = K[n + j];
+        S.Dc()[J] = -k2 * Qz[n + j];
         if (j < n - 1) {
-            S.E0[J] = Qu[2 * n + j];
-            S.E1[J] = K[j + 1];
-            S.E2[J] = K[2 * n + j];
-            S.E3[J] = -k2 * Qz[2 * n + j];
+            S.E0()[J] = Qu[2 * n + j];
+            S.E1()[J] = K[j + 1];
+            S.E2()[J] = K[2 * n + j];
+            S.E3()[J] = -k2 * Qz[2 * n + j];
         } else {
-            S.E0[J] = 0.0; S.E1[J] = 0.0; S.E2[J] = 0.0; S.E3[J] = 0.0;
+            S.E0()[J] = 0.0; S.E1()[J] = 0.0; S.E2()[J] = 0.0; S.E3()[J] = 0.0;
         }
     }
 }
@@ -286,20 +328,21 @@ __device__ __forceinline__ void tri_init_de(const TView& V, int i, TriSm& S) {
 //   out = (xupd ? xupd : 0) + omega * D^{-1} r
 // Pointers that may be written by the same kernel (serial substitution) are
 // read through plain loads (no __restrict__/.nc).
-__device__ void tri_block(const TView& V, int i, const double* b, const double* x,
-                          const double* uprev, const double* munext, double* out, double omega,
-                          const double* xupd, double* sm) {
+template <int NT>
+__device__ __forceinline__ void tri_block(const TView& V, int i, const double* b, const double* x,
+                                          const double* uprev, const double* munext, double* out,
+                                          double omega, const double* xupd, double* sm) {
     const Lay& L = V.lay;
-    const int n = V.n;
+    const int n = dimn<NT>(V);
     const int tid = threadIdx.x, nth = blockDim.x;
     const bool has_vm = i >= 1, has_uzl = i < L.N;
-    TriSm S(sm, n);
+    const TriSm S(sm, n);
     const double kap = V.kappa;
     const double* Qv = (i == L.N) ? V.Ql : V.Qm;
     const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;
     const double* Qz = V.Qz;
-    const double* K = has_uzl ? V.Ki(i) : nullptr;
-    const double* C = (has_uzl && has_vm) ? V.Ci(i) : nullptr;
+    const double* K = has_uzl ? V.Ki(i, n) : nullptr;
+    const double* C = (has_uzl && has_vm) ? V.Ci(i, n) : nullptr;
     const int64_t bs = V.sl.base;
     const int64_t ov = L.off_v(i) - bs, ou = L.off_u(i) - bs, oz = L.off_z(i) - bs,
                   om = L.off_mu(i) - bs, ol = L.off_l(i) - bs;
@@ -326,14 +369,14 @@ __device__ void tri_block(const TView& V, int i, const double* b, const double* 
         }
         if (has_vm && uprev) rm -= uprev[j];
         if (has_uzl && munext) ru -= munext[j];
-        if (has_vm) { S.sv[J] = -rm; S.srv[J] = rv; }
-        if (has_uzl) { S.f0[J] = ru; S.f1[J] = rl - kap * rz; S.fw[J] = rz; }
+        if (has_vm) { S.sv()[J] = -rm; S.srv()[J] = rv; }
+        if (has_uzl) { S.f0()[J] = ru; S.f1()[J] = rl - kap * rz; S.fw()[J] = rz; }
     }
     __syncthreads();
     if (!has_uzl) {  // last block (v_N, mu_N): mu = Qv v - r_v
         for (int j = tid; j < n; j += nth) {
-            const double dv = S.sv[PI(j)];
-            const double dm = tmv_s(Qv, n, S.sv, j) - S.srv[PI(j)];
+            const double dv = S.sv()[PI(j)];
+            const double dm = tmv_s(Qv, n, S.sv(), j) - S.srv()[PI(j)];
             const double bv = xupd ? xupd[ov + j] : 0.0, bm = xupd ? xupd[om + j] : 0.0;
             out[ov + j] = bv + omega * dv;
             out[om + j] = bm + omega * dm;
@@ -342,22 +385,22 @@ __device__ void tri_block(const TView& V, int i, const double* b, const double* 
         return;
     }
     if (C) {
-        for (int j = tid; j < n; j += nth) S.f1[PI(j)] -= tmv_s(C, n, S.sv, j);
+        for (int j = tid; j < n; j += nth) S.f1()[PI(j)] -= tmv_s(C, n, S.sv(), j);
     }
-    tri_init_de(V, i, S);
+    tri_init_de(V, n, i, S);
     __syncthreads();
     cr_solve<true>(n, S, V.cr);
     for (int j = tid; j < n; j += nth) {
         const int J = PI(j);
-        const double du = S.f0[J], dl = S.f1[J];
-        const double dz = S.fw[J] - kap * dl;
+        const double du = S.f0()[J], dl = S.f1()[J];
+        const double dz = S.fw()[J] - kap * dl;
         out[ou + j] = (xupd ? xupd[ou + j] : 0.0) + omega * du;
         out[oz + j] = (xupd ? xupd[oz + j] : 0.0) + omega * dz;
         out[ol + j] = (xupd ? xupd[ol + j] : 0.0) + omega * dl;
         if (has_vm) {
-            const double dv = S.sv[J];
-            double dm = tmv_s(Qv, n, S.sv, j) - S.srv[J];
-            if (C) dm += tmtv_s(C, n, S.f1, j);
+            const double dv = S.sv()[J];
+            double dm = tmv_s(Qv, n, S.sv(), j) - S.srv()[J];
+            if (C) dm += tmtv_s(C, n, S.f1(), j);
             out[ov + j] = (xupd ? xupd[ov + j] : 0.0) + omega * dv;
             out[om + j] = (xupd ? xupd[om + j] : 0.0) + omega * dm;
         }
@@ -366,27 +409,29 @@ __device__ void tri_block(const TView& V, int i, const double* b, const double* 
 }
 
 // Parallel over block rows: jacobi (x may be null) or plain D^{-1} b.
-__global__ void __launch_bounds__(256, 3) tri_rows(TView V, const double* __restrict__ b, const double* __restrict__ x,
-                         double* __restrict__ y, double omega) {
-    extern __shared__ double sm[];
+template <int NT>
+__global__ void __launch_bounds__(256, 3) tri_rows(TView V, const double* __restrict__ b,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ y, double omega) {
+    extern __shared__ __align__(16) double sm[];
     const Lay& L = V.lay;
     for (int i = V.sl.r0 + blockIdx.x; i < V.sl.r1; i += gridDim.x) {
         const double* uprev = x ? V.sl.uprev(L, x, i) : nullptr;
         const double* munext = x ? V.sl.munext(L, x, i) : nullptr;
-        tri_block(V, i, b, x, uprev, munext, y, omega, x, sm);
+        tri_block<NT>(V, i, b, x, uprev, munext, y, omega, x, sm);
     }
 }
 
 // Serial substitution over the time axis (smoothers.py:79-109), one CTA.
-template <bool FORWARD>
+template <bool FORWARD, int NT>
 __global__ void tri_subst(TView V, const double* __restrict__ r, double* d) {
-    extern __shared__ double sm[];
+    extern __shared__ __align__(16) double sm[];
     const Lay& L = V.lay;
     for (int k = 0; k <= L.N; ++k) {
         const int i = FORWARD ? k : L.N - k;
         const double* uprev = (FORWARD && i >= 1) ? d + L.off_u(i - 1) : nullptr;
         const double* munext = (!FORWARD && i < L.N) ? d + L.off_mu(i + 1) : nullptr;
-        tri_block(V, i, r, nullptr, uprev, munext, d, 1.0, nullptr, sm);
+        tri_block<NT>(V, i, r, nullptr, uprev, munext, d, 1.0, nullptr, sm);
     }
 }
 
@@ -397,8 +442,9 @@ __global__ void tri_subst(TView V, const double* __restrict__ r, double* d) {
 // the u-part of the (u,lam) solve with rhs (0, -C_i u_{i-1}).  Backward:
 // mu_i = a_i^mu + C_i^T lam_i with lam_i from the rhs (-mu_{i+1}, 0).  The
 // chain solves reuse per-interval cyclic-reduction factors precomputed once
-// (fac record [14][n]: P(3) M1(4) M2(4) C(3)), staged by cp.async double
-// buffering so only the CR recurrences sit on the serial critical path.
+// (fac record [14][n]: P(3) M1(4) M2(4) in CR level order, then C(3)),
+// TMA bulk-staged in a double buffer so only the recurrences of the current
+// interval sit on the serial critical path.
 // ---------------------------------------------------------------------------
 static constexpr int kFacRows = 14;
 
@@ -413,23 +459,24 @@ __device__ __forceinline__ int lvl_pos(int n, int j) {
 }
 
 // One CTA per interval i in [0, N): factor record of the (u,lam) system.
+template <int NT>
 __global__ void tri_factor_kernel(TView V, double* __restrict__ fac) {
-    extern __shared__ double sm[];
+    extern __shared__ __align__(16) double sm[];
     const Lay& L = V.lay;
-    const int n = V.n;
-    TriSm S(sm, n);
+    const int n = dimn<NT>(V);
+    const TriSm S(sm, n);
     for (int i = blockIdx.x; i < L.N; i += gridDim.x) {
-        tri_init_de(V, i, S);
+        tri_init_de(V, n, i, S);
         __syncthreads();
         cr_solve<false>(n, S, V.cr);
         double* out = fac + (size_t)i * kFacRows * n;
-        const double* C = (i >= 1) ? V.C + (size_t)i * 3 * n : nullptr;
+        const double* C = (i >= 1) ? V.Ci(i, n) : nullptr;
         for (int j = threadIdx.x; j < n; j += blockDim.x) {
             const int J = PI(j);
             const int o = lvl_pos(n, j);
-            const double pa = S.Da[J], pb = S.Db[J], pc = S.Dc[J];
-            const double e0 = S.E0[J], e1 = S.E1[J], e2 = S.E2[J], e3 = S.E3[J];
-            const double l0 = S.L0[J], l1 = S.L1[J], l2 = S.L2[J], l3 = S.L3[J];
+            const double pa = S.Da()[J], pb = S.Db()[J], pc = S.Dc()[J];
+            const double e0 = S.E0()[J], e1 = S.E1()[J], e2 = S.E2()[J], e3 = S.E3()[J];
+            const double l0 = S.L0()[J], l1 = S.L1()[J], l2 = S.L2()[J], l3 = S.L3()[J];
             out[0 * n + o] = pa; out[1 * n + o] = pb; out[2 * n + o] = pc;
             out[3 * n + o] = e0 * pa + e2 * pb;  out[4 * n + o] = e0 * pb + e2 * pc;
             out[5 * n + o] = e1 * pa + e3 * pb;  out[6 * n + o] = e1 * pb + e3 * pc;
@@ -443,56 +490,50 @@ __global__ void tri_factor_kernel(TView V, double* __restrict__ fac) {
     }
 }
 
-// rhs-only block cyclic reduction with a level-ordered factor record fb
-// ([14][n], rows 0..10 = P, M1, M2 in level order; shared or global memory).
-// f0/f1 are padded shared arrays in natural node order.
-struct CrRhsRows {
-    const double *Pa, *Pb, *Pc, *A0, *A1, *A2, *A3, *B0, *B1, *B2, *B3;
-    __device__ CrRhsRows(const double* fb, int n)
-        : Pa(fb), Pb(fb + n), Pc(fb + 2 * n), A0(fb + 3 * n), A1(fb + 4 * n), A2(fb + 5 * n),
-          A3(fb + 6 * n), B0(fb + 7 * n), B1(fb + 8 * n), B2(fb + 9 * n), B3(fb + 10 * n) {}
-};
-
-// forward rhs reduction of level lev for kept-node index m (level-ordered factors at off)
-__device__ __forceinline__ void cr_rhs_down(const CrRhsRows& F, int n, int lev, int off, int m,
-                                            double* f0, double* f1) {
+// forward rhs reduction of level lev for kept-node index m (level-ordered
+// factors at off; record rows of length n at fb; f1 = f0 + np)
+__device__ __forceinline__ void cr_rhs_down(const double* fb, int n, int np, int lev, int off,
+                                            int m, double* f0) {
+    double* f1 = f0 + np;
     const int s = 1 << lev;
     const int j = 2 * s - 1 + 2 * s * m;
     const int p = j - s, q = j + s;
     const int J = PI(j), P = PI(p), Pf = off + m;
     const double h0 = f0[P], h1 = f1[P];
-    double g0 = f0[J] - (F.A0[Pf] * h0 + F.A1[Pf] * h1);
-    double g1 = f1[J] - (F.A2[Pf] * h0 + F.A3[Pf] * h1);
+    double g0 = f0[J] - (fb[3 * n + Pf] * h0 + fb[4 * n + Pf] * h1);
+    double g1 = f1[J] - (fb[5 * n + Pf] * h0 + fb[6 * n + Pf] * h1);
     if (q < n) {
         const int Q = PI(q), Qf = Pf + 1;
         const double k0 = f0[Q], k1 = f1[Q];
-        g0 -= F.B0[Qf] * k0 + F.B1[Qf] * k1;
-        g1 -= F.B2[Qf] * k0 + F.B3[Qf] * k1;
+        g0 -= fb[7 * n + Qf] * k0 + fb[8 * n + Qf] * k1;
+        g1 -= fb[9 * n + Qf] * k0 + fb[10 * n + Qf] * k1;
     }
     f0[J] = g0;
     f1[J] = g1;
 }
 
 // back substitution of eliminated-node index m at level lev
-__device__ __forceinline__ void cr_rhs_up(const CrRhsRows& F, int n, int lev, int off, int m,
-                                          double* f0, double* f1) {
+__device__ __forceinline__ void cr_rhs_up(const double* fb, int n, int np, int lev, int off,
+                                          int m, double* f0) {
+    double* f1 = f0 + np;
     const int s = 1 << lev;
     const int p = s - 1 + 2 * s * m;
     const int P = PI(p), Pf = off + m;
     const double g0 = f0[P], g1 = f1[P];
-    double x0 = F.Pa[Pf] * g0 + F.Pb[Pf] * g1;
-    double x1 = F.Pb[Pf] * g0 + F.Pc[Pf] * g1;
+    const double pa = fb[Pf], pb = fb[n + Pf], pc = fb[2 * n + Pf];
+    double x0 = pa * g0 + pb * g1;
+    double x1 = pb * g0 + pc * g1;
     if (p - s >= 0) {  // - M2_p^T x_{p-s}
         const int Q = PI(p - s);
         const double a = f0[Q], b = f1[Q];
-        x0 -= F.B0[Pf] * a + F.B2[Pf] * b;
-        x1 -= F.B1[Pf] * a + F.B3[Pf] * b;
+        x0 -= fb[7 * n + Pf] * a + fb[9 * n + Pf] * b;
+        x1 -= fb[8 * n + Pf] * a + fb[10 * n + Pf] * b;
     }
     if (p + s < n) {   // - M1_p^T x_{p+s}
         const int Q = PI(p + s);
         const double a = f0[Q], b = f1[Q];
-        x0 -= F.A0[Pf] * a + F.A2[Pf] * b;
-        x1 -= F.A1[Pf] * a + F.A3[Pf] * b;
+        x0 -= fb[3 * n + Pf] * a + fb[5 * n + Pf] * b;
+        x1 -= fb[4 * n + Pf] * a + fb[6 * n + Pf] * b;
     }
     f0[P] = x0;
     f1[P] = x1;
@@ -501,46 +542,54 @@ __device__ __forceinline__ void cr_rhs_up(const CrRhsRows& F, int n, int lev, in
 // rhs-only block cyclic reduction.  Levels with more than 32 active nodes
 // run CTA-wide (one barrier per level); the remaining levels, the root and
 // their back-substitution run inside warp 0 with __syncwarp only.
-__device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0, double* f1) {
+__device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0) {
     const int tid = threadIdx.x, nth = blockDim.x;
-    const CrRhsRows F(fb, n);
-    const int top = 31 - __clz(n);
-    int off = 0, lev = 0;
-    for (; lev < top; ++lev) {            // CTA-wide levels
-        const int cnt = lvl_count(n, lev);  // eliminated nodes at this level (>= kept)
-        if (cnt <= 32) break;
+    const int np = padded(n);
+    const int top = ilog2(n);
+    const int lw = cta_levels(n);
+    int off = 0;
+#pragma unroll
+    for (int lev = 0; lev < kMaxLev; ++lev) {   // CTA-wide levels
+        if (lev >= lw) break;
         const int ck = kept_count(n, lev);
-        for (int m = tid; m < ck; m += nth) cr_rhs_down(F, n, lev, off, m, f0, f1);
-        off += cnt;
+        for (int m = tid; m < ck; m += nth) cr_rhs_down(fb, n, np, lev, off, m, f0);
+        off += lvl_count(n, lev);
         __syncthreads();
     }
-    const int lw = lev;
     if (tid < 32) {                       // warp-level tail
         int o = off;
-        for (int l = lw; l < top; ++l) {
-            if (tid < kept_count(n, l)) cr_rhs_down(F, n, l, o, tid, f0, f1);
+#pragma unroll
+        for (int l = 0; l < kMaxLev; ++l) {
+            if (l < lw) continue;
+            if (l >= top) break;
+            if (tid < kept_count(n, l)) cr_rhs_down(fb, n, np, l, o, tid, f0);
             o += lvl_count(n, l);
             __syncwarp();
         }
         if (tid == 0) {
             const int r = (1 << top) - 1, R = PI(r);
+            double* f1 = f0 + np;
             const double g0 = f0[R], g1 = f1[R];
-            f0[R] = F.Pa[o] * g0 + F.Pb[o] * g1;
-            f1[R] = F.Pb[o] * g0 + F.Pc[o] * g1;
+            f0[R] = fb[o] * g0 + fb[n + o] * g1;
+            f1[R] = fb[n + o] * g0 + fb[2 * n + o] * g1;
         }
         __syncwarp();
-        for (int l = top - 1; l >= lw; --l) {
+#pragma unroll
+        for (int l = kMaxLev - 1; l >= 0; --l) {
+            if (l >= top || l < lw) continue;
             const int ce = lvl_count(n, l);
             o -= ce;
-            if (tid < ce) cr_rhs_up(F, n, l, o, tid, f0, f1);
+            if (tid < ce) cr_rhs_up(fb, n, np, l, o, tid, f0);
             __syncwarp();
         }
     }
     __syncthreads();
-    for (lev = lw - 1; lev >= 0; --lev) {  // CTA-wide back-substitution
+#pragma unroll
+    for (int lev = kMaxLev - 1; lev >= 0; --lev) {  // CTA-wide back-substitution
+        if (lev >= lw) continue;
         const int ce = lvl_count(n, lev);
         off -= ce;
-        for (int m = tid; m < ce; m += nth) cr_rhs_up(F, n, lev, off, m, f0, f1);
+        for (int m = tid; m < ce; m += nth) cr_rhs_up(fb, n, np, lev, off, m, f0);
         __syncthreads();
     }
 }
@@ -577,13 +626,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // `a` = D^{-1} r from pass 1.  STAGED: the next interval's factor record
 // (14n doubles) and a-segment (n doubles) are TMA bulk-copied into the other
 // half of a double buffer while the current interval's recurrences run.
-template <bool FWD, bool STAGED>
+template <bool FWD, bool STAGED, int NT>
 __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
                                  const double* __restrict__ fac, double* __restrict__ chain) {
     extern __shared__ __align__(16) double sm[];
     __shared__ __align__(8) uint64_t bars[2];
     const Lay& L = V.lay;
-    const int n = V.n, N = L.N, np = padded(n);
+    const int n = dimn<NT>(V), N = L.N, np = padded(n);
     const int tid = threadIdx.x, nth = blockDim.x;
     const int rec = kFacRows * n;
     const int brec = rec + n;
@@ -647,7 +696,7 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
             }
         }
         __syncthreads();
-        cr_rhs(n, fb, f0, f1);
+        cr_rhs(n, fb, f0);
         for (int j = tid; j < n; j += nth) {
             const int J = PI(j);
             double val;
@@ -667,16 +716,17 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
 }
 
 // Pass 3: parallel solves with the chain as the continuity coupling.
-template <bool FWD>
+template <bool FWD, int NT>
 __global__ void __launch_bounds__(256, 3) tri_rows_cpl(TView V, const double* __restrict__ r,
-                             const double* __restrict__ chain, double* __restrict__ y) {
-    extern __shared__ double sm[];
+                                                       const double* __restrict__ chain,
+                                                       double* __restrict__ y) {
+    extern __shared__ __align__(16) double sm[];
     const Lay& L = V.lay;
-    const int n = V.n;
+    const int n = dimn<NT>(V);
     for (int i = blockIdx.x; i <= L.N; i += gridDim.x) {
         const double* uprev = (FWD && i >= 1) ? chain + (size_t)(i - 1) * n : nullptr;
         const double* munext = (!FWD && i < L.N) ? chain + (size_t)(i + 1) * n : nullptr;
-        tri_block(V, i, r, nullptr, uprev, munext, y, 1.0, nullptr, sm);
+        tri_block<NT>(V, i, r, nullptr, uprev, munext, y, 1.0, nullptr, sm);
     }
 }
 
@@ -697,8 +747,8 @@ __global__ void tri_apply(TView V, const double* __restrict__ b, const double* _
         const bool has_vm = i >= 1, has_uzl = i < L.N;
         const double* Qv = (i == L.N) ? V.Ql : V.Qm;
         const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;
-        const double* K = has_uzl ? V.Ki(i) : nullptr;
-        const double* C = (has_uzl && has_vm) ? V.Ci(i) : nullptr;
+        const double* K = has_uzl ? V.Ki(i, n) : nullptr;
+        const double* C = (has_uzl && has_vm) ? V.Ci(i, n) : nullptr;
         const int64_t ov = L.off_v(i) - bs, ou = L.off_u(i) - bs, oz = L.off_z(i) - bs,
                       om = L.off_mu(i) - bs, ol = L.off_l(i) - bs;
         const double* uprev = (MODE != T_APPLY_DIAG) ? V.sl.uprev(L, x, i) : nullptr;
@@ -755,56 +805,43 @@ static int tri_chain_threads(int n) {
     return t;
 }
 
-int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, double* y,
-               double omega, cudaStream_t s) {
+template <int NT>
+static int tri_launch_t(const tk_level* Lv, int op, const double* b, const double* x, double* y,
+                        double omega, cudaStream_t s) {
     TView V(Lv);
     const int n = Lv->n_u;
-    if (Lv->n_z != Lv->n_u) {
-        set_error("tri family needs n_z == n_u (got %d, %d)", Lv->n_u, Lv->n_z);
-        return TK_ERR_UNSUPPORTED;
-    }
     const int rows = V.sl.r1 - V.sl.r0;
-    if (op >= 10 && !V.sl.whole(Lv->n_steps)) {
-        set_error("block Gauss-Seidel substitution needs the whole level (no time slab)");
-        return TK_ERR_ARG;
-    }
-    if (op == T_APPLY || op == T_APPLY_DIAG || op == T_RESIDUAL) {
-        const int th = n >= 256 ? 256 : 128;
-        const int grid = rows < (1 << 30) ? rows : (1 << 30);
-        if (op == T_APPLY) tri_apply<T_APPLY><<<grid, th, 0, s>>>(V, b, x, y);
-        else if (op == T_APPLY_DIAG) tri_apply<T_APPLY_DIAG><<<grid, th, 0, s>>>(V, b, x, y);
-        else tri_apply<T_RESIDUAL><<<grid, th, 0, s>>>(V, b, x, y);
-        return check_launch("tri_apply");
-    }
     const int64_t smem = tri_smem_bytes(n);
-    if (smem == 0) {
-        set_error("tri family kernels support 2 <= n_u <= 1664 (got %d)", n);
-        return TK_ERR_UNSUPPORTED;
-    }
     static bool attr_done = false;
     if (!attr_done) {
         const int mx = 227 * 1024;
-        cudaFuncSetAttribute(tri_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(tri_rows, cudaFuncAttributePreferredSharedMemoryCarveout,
+        cudaFuncSetAttribute(tri_rows<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_rows<NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
-        cudaFuncSetAttribute(tri_rows_cpl<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        cudaFuncSetAttribute(tri_subst<true, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_subst<false, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             mx);
+        cudaFuncSetAttribute(tri_factor_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             mx);
+        cudaFuncSetAttribute(tri_rows_cpl<true, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             mx);
+        cudaFuncSetAttribute(tri_rows_cpl<false, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             mx);
+        cudaFuncSetAttribute(tri_rows_cpl<true, NT>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
-        cudaFuncSetAttribute(tri_rows_cpl<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        cudaFuncSetAttribute(tri_rows_cpl<false, NT>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
-        cudaFuncSetAttribute(tri_subst<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(tri_subst<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(tri_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(tri_rows_cpl<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(tri_rows_cpl<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         // the chain kernels also hold two static mbarriers
         const int mxc = mx - 1024;
-        cudaFuncSetAttribute(tri_chain_kernel<true, true>,
+        cudaFuncSetAttribute(tri_chain_kernel<true, true, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
-        cudaFuncSetAttribute(tri_chain_kernel<false, true>,
+        cudaFuncSetAttribute(tri_chain_kernel<false, true, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
-        cudaFuncSetAttribute(tri_chain_kernel<true, false>,
+        cudaFuncSetAttribute(tri_chain_kernel<true, false, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
-        cudaFuncSetAttribute(tri_chain_kernel<false, false>,
+        cudaFuncSetAttribute(tri_chain_kernel<false, false, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_status(e, "tri: cudaFuncSetAttribute");
@@ -814,21 +851,21 @@ int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, dou
     const bool fast = Lv->fac != nullptr && Lv->scratch != nullptr;
     switch (op) {
         case 3:  // diag solve
-            tri_rows<<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
+            tri_rows<NT><<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
             break;
         case 4:  // jacobi
-            tri_rows<<<rows, th, smem, s>>>(V, b, x, y, omega);
+            tri_rows<NT><<<rows, th, smem, s>>>(V, b, x, y, omega);
             break;
         case 10:
         case 11: {
             const bool fwd = op == 10;
             if (!fast) {
-                if (fwd) tri_subst<true><<<1, th, smem, s>>>(V, b, y);
-                else tri_subst<false><<<1, th, smem, s>>>(V, b, y);
+                if (fwd) tri_subst<true, NT><<<1, th, smem, s>>>(V, b, y);
+                else tri_subst<false, NT><<<1, th, smem, s>>>(V, b, y);
                 break;
             }
             // pass 1: a = D^{-1} r into y
-            tri_rows<<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
+            tri_rows<NT><<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
             // pass 2: serial chain on the coupling vector
             const int cth = tri_chain_threads(n);
             const int np = padded(n);
@@ -840,15 +877,15 @@ int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, dou
             double* fac = Lv->fac;
             double* chn = Lv->scratch;
             if (aligned && staged <= 227 * 1024 - 1024) {
-                if (fwd) tri_chain_kernel<true, true><<<1, cth, staged, s>>>(V, y, fac, chn);
-                else tri_chain_kernel<false, true><<<1, cth, staged, s>>>(V, y, fac, chn);
+                if (fwd) tri_chain_kernel<true, true, NT><<<1, cth, staged, s>>>(V, y, fac, chn);
+                else tri_chain_kernel<false, true, NT><<<1, cth, staged, s>>>(V, y, fac, chn);
             } else {
-                if (fwd) tri_chain_kernel<true, false><<<1, cth, direct, s>>>(V, y, fac, chn);
-                else tri_chain_kernel<false, false><<<1, cth, direct, s>>>(V, y, fac, chn);
+                if (fwd) tri_chain_kernel<true, false, NT><<<1, cth, direct, s>>>(V, y, fac, chn);
+                else tri_chain_kernel<false, false, NT><<<1, cth, direct, s>>>(V, y, fac, chn);
             }
             // pass 3: parallel solves with the chain coupling
-            if (fwd) tri_rows_cpl<true><<<rows, th, smem, s>>>(V, b, chn, y);
-            else tri_rows_cpl<false><<<rows, th, smem, s>>>(V, b, chn, y);
+            if (fwd) tri_rows_cpl<true, NT><<<rows, th, smem, s>>>(V, b, chn, y);
+            else tri_rows_cpl<false, NT><<<rows, th, smem, s>>>(V, b, chn, y);
             break;
         }
         case 12:  // factor
@@ -856,11 +893,46 @@ int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, dou
                 set_error("tk_subst_factor: level has no fac buffer");
                 return TK_ERR_ARG;
             }
-            tri_factor_kernel<<<Lv->n_steps, th, smem, s>>>(V, Lv->fac);
+            tri_factor_kernel<NT><<<Lv->n_steps, th, smem, s>>>(V, Lv->fac);
             break;
         default: set_error("tri: bad op %d", op); return TK_ERR_ARG;
     }
     return check_launch("tri_rows");
+}
+
+int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, double* y,
+               double omega, cudaStream_t s) {
+    TView V(Lv);
+    const int n = Lv->n_u;
+    if (Lv->n_z != Lv->n_u) {
+        set_error("tri family needs n_z == n_u (got %d, %d)", Lv->n_u, Lv->n_z);
+        return TK_ERR_UNSUPPORTED;
+    }
+    if (op >= 10 && !V.sl.whole(Lv->n_steps)) {
+        set_error("block Gauss-Seidel substitution needs the whole level (no time slab)");
+        return TK_ERR_ARG;
+    }
+    const int rows = V.sl.r1 - V.sl.r0;
+    if (op == T_APPLY || op == T_APPLY_DIAG || op == T_RESIDUAL) {
+        const int th = n >= 256 ? 256 : 128;
+        const int grid = rows < (1 << 30) ? rows : (1 << 30);
+        if (op == T_APPLY) tri_apply<T_APPLY><<<grid, th, 0, s>>>(V, b, x, y);
+        else if (op == T_APPLY_DIAG) tri_apply<T_APPLY_DIAG><<<grid, th, 0, s>>>(V, b, x, y);
+        else tri_apply<T_RESIDUAL><<<grid, th, 0, s>>>(V, b, x, y);
+        return check_launch("tri_apply");
+    }
+    if (tri_smem_bytes(n) == 0) {
+        set_error("tri family kernels support 2 <= n_u <= 1664 (got %d)", n);
+        return TK_ERR_UNSUPPORTED;
+    }
+    switch (n) {
+        case 64: return tri_launch_t<64>(Lv, op, b, x, y, omega, s);
+        case 128: return tri_launch_t<128>(Lv, op, b, x, y, omega, s);
+        case 256: return tri_launch_t<256>(Lv, op, b, x, y, omega, s);
+        case 512: return tri_launch_t<512>(Lv, op, b, x, y, omega, s);
+        case 1024: return tri_launch_t<1024>(Lv, op, b, x, y, omega, s);
+        default: return tri_launch_t<0>(Lv, op, b, x, y, omega, s);
+    }
 }
 
 }  // namespace tk
