@@ -12,7 +12,7 @@ import os
 from .errors import NativeLibraryError, TempoKktError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtempokkt_b200.so")
+LIB_PATH = os.environ.get("TK_LIB_PATH", os.path.join(_PKG, "libtempokkt_b200.so"))
 
 TK_OK = 0
 TK_ERR_ARG = 1

@@ -17,12 +17,13 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libtempokkt_b200.so")
+BUILD = os.environ.get("TK_BUILD_DIR", os.path.join(PKG, "_build"))
+LIB = os.environ.get("TK_LIB_OUT", os.path.join(PKG, "libtempokkt_b200.so"))
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC] + \
+    os.environ.get("TK_EXTRA_FLAGS", "").split()
 
 
 def sources():

@@ -448,6 +448,20 @@ __global__ void tri_subst(TView V, const double* __restrict__ r, double* d) {
 // ---------------------------------------------------------------------------
 static constexpr int kFacRows = 14;
 
+// Cut level c of the chain's cyclic reduction: levels below c run as usual;
+// the reduced system on the A = n >> c <= 32 active nodes left at level c is
+// solved with its precomputed dense inverse W (2A x 2A, stored transposed).
+__host__ __device__ __forceinline__ constexpr int cut_level(int n) {
+    int c = 0;
+    while ((n >> c) > 32) ++c;
+    return c;
+}
+__host__ __device__ __forceinline__ constexpr int cut_nodes(int n) { return n >> cut_level(n); }
+// doubles per interval record: P, M1, M2 (levels < c, level order), C, W^T
+__host__ __device__ __forceinline__ constexpr int fac_record(int n) {
+    return kFacRows * n + 4 * cut_nodes(n) * cut_nodes(n);
+}
+
 // Level order of the factor rows: node j = s-1 + 2s*m (s = 2^l) is eliminated
 // at level l = ctz(j+1) with index m = (j+1) >> (l+1); level l occupies
 // [lvl_off(l), lvl_off(l+1)).  Every CR level then reads a contiguous run.
@@ -459,36 +473,106 @@ __device__ __forceinline__ int lvl_pos(int n, int j) {
 }
 
 // One CTA per interval i in [0, N): factor record of the (u,lam) system.
+// Extra dynamic smem after the 16 node arrays: the 2A x 4A augmented matrix
+// of the reduced system and a pivot column (Gauss-Jordan, no pivoting needed:
+// the reduced system is symmetric quasi-definite).
 template <int NT>
 __global__ void tri_factor_kernel(TView V, double* __restrict__ fac) {
     extern __shared__ __align__(16) double sm[];
     const Lay& L = V.lay;
     const int n = dimn<NT>(V);
+    const int tid = threadIdx.x, nth = blockDim.x;
     const TriSm S(sm, n);
+    const int c = cut_level(n), A = cut_nodes(n), M = 2 * A, M2 = 2 * M;
+    double* G = sm + kTriArrays * padded(n);     // [M][2M]
+    double* fcol = G + M * M2;                   // [M]
+    using K = CrSolve<false>;
+    const double* cinv = V.cr;
     for (int i = blockIdx.x; i < L.N; i += gridDim.x) {
         tri_init_de(V, n, i, S);
         __syncthreads();
-        cr_solve<false>(n, S, V.cr);
-        double* out = fac + (size_t)i * kFacRows * n;
-        const double* C = (i >= 1) ? V.Ci(i, n) : nullptr;
-        for (int j = threadIdx.x; j < n; j += blockDim.x) {
-            const int J = PI(j);
-            const int o = lvl_pos(n, j);
-            const double pa = S.Da()[J], pb = S.Db()[J], pc = S.Dc()[J];
-            const double e0 = S.E0()[J], e1 = S.E1()[J], e2 = S.E2()[J], e3 = S.E3()[J];
-            const double l0 = S.L0()[J], l1 = S.L1()[J], l2 = S.L2()[J], l3 = S.L3()[J];
-            out[0 * n + o] = pa; out[1 * n + o] = pb; out[2 * n + o] = pc;
-            out[3 * n + o] = e0 * pa + e2 * pb;  out[4 * n + o] = e0 * pb + e2 * pc;
-            out[5 * n + o] = e1 * pa + e3 * pb;  out[6 * n + o] = e1 * pb + e3 * pc;
-            out[7 * n + o] = l0 * pa + l1 * pb;  out[8 * n + o] = l0 * pb + l1 * pc;
-            out[9 * n + o] = l2 * pa + l3 * pb;  out[10 * n + o] = l2 * pb + l3 * pc;
-            out[11 * n + j] = C ? C[j] : 0.0;
-            out[12 * n + j] = C ? C[n + j] : 0.0;
-            out[13 * n + j] = C ? C[2 * n + j] : 0.0;
+        for (int lev = 0; lev < c; ++lev) {      // partial factorisation: levels < c
+            const int ce = lvl_count(n, lev);
+            for (int m = tid; m < ce; m += nth) K::elim(S, n, lev, m);
+            __syncthreads();
+            const int ck = kept_count(n, lev);
+            for (int m = tid; m < ck; m += nth) K::keep(S, n, lev, m, cinv, cinv, cinv);
+            __syncthreads();
+        }
+        // reduced system on the active nodes j_m = (m+1) 2^c - 1
+        for (int e = tid; e < M * M2; e += nth) G[e] = 0.0;
+        __syncthreads();
+        for (int m = tid; m < A; m += nth) {
+            const int J = PI(((m + 1) << c) - 1);
+            const int r = 2 * m;
+            G[r * M2 + r] = S.Da()[J];
+            G[r * M2 + r + 1] = S.Db()[J];
+            G[(r + 1) * M2 + r] = S.Db()[J];
+            G[(r + 1) * M2 + r + 1] = S.Dc()[J];
+            G[r * M2 + M + r] = 1.0;
+            G[(r + 1) * M2 + M + r + 1] = 1.0;
+            if (m + 1 < A) {
+                const double e0 = S.E0()[J], e1 = S.E1()[J], e2 = S.E2()[J], e3 = S.E3()[J];
+                G[r * M2 + r + 2] = e0; G[r * M2 + r + 3] = e1;
+                G[(r + 1) * M2 + r + 2] = e2; G[(r + 1) * M2 + r + 3] = e3;
+                G[(r + 2) * M2 + r] = e0; G[(r + 3) * M2 + r] = e1;
+                G[(r + 2) * M2 + r + 1] = e2; G[(r + 3) * M2 + r + 1] = e3;
+            }
+        }
+        __syncthreads();
+        for (int k = 0; k < M; ++k) {            // Gauss-Jordan
+            const double piv = G[k * M2 + k];
+            for (int r = tid; r < M; r += nth) fcol[r] = (r == k) ? 0.0 : G[r * M2 + k] / piv;
+            __syncthreads();
+            for (int e = tid; e < M * M2; e += nth) {
+                const int r = e / M2, col = e - r * M2;
+                if (r != k) G[e] -= fcol[r] * G[k * M2 + col];
+            }
+            __syncthreads();
+            for (int col = tid; col < M2; col += nth) G[k * M2 + col] /= piv;
+            __syncthreads();
+        }
+        double* out = fac + (size_t)i * fac_record(n);
+        const double* Cm = (i >= 1) ? V.Ci(i, n) : nullptr;
+        for (int j = tid; j < n; j += nth) {
+            const int lev = __ffs(j + 1) - 1;
+            if (lev < c) {
+                const int J = PI(j);
+                const int o = lvl_pos(n, j);
+                const double pa = S.Da()[J], pb = S.Db()[J], pc = S.Dc()[J];
+                const double e0 = S.E0()[J], e1 = S.E1()[J], e2 = S.E2()[J], e3 = S.E3()[J];
+                const double l0 = S.L0()[J], l1 = S.L1()[J], l2 = S.L2()[J], l3 = S.L3()[J];
+                out[0 * n + o] = pa; out[1 * n + o] = pb; out[2 * n + o] = pc;
+                out[3 * n + o] = e0 * pa + e2 * pb;  out[4 * n + o] = e0 * pb + e2 * pc;
+                out[5 * n + o] = e1 * pa + e3 * pb;  out[6 * n + o] = e1 * pb + e3 * pc;
+                out[7 * n + o] = l0 * pa + l1 * pb;  out[8 * n + o] = l0 * pb + l1 * pc;
+                out[9 * n + o] = l2 * pa + l3 * pb;  out[10 * n + o] = l2 * pb + l3 * pc;
+            }
+            out[11 * n + j] = Cm ? Cm[j] : 0.0;
+            out[12 * n + j] = Cm ? Cm[n + j] : 0.0;
+            out[13 * n + j] = Cm ? Cm[2 * n + j] : 0.0;
+        }
+        double* W = out + kFacRows * n;           // W^T: W[col][row]
+        for (int e = tid; e < M * M; e += nth) {
+            const int r = e / M, col = e - r * M;
+            W[col * M + r] = G[r * M2 + M + col];
         }
         __syncthreads();
     }
 }
+
+#ifdef TK_PROF
+// phase timestamps of one chain step (debug builds only: -DTK_PROF)
+__device__ long long g_tk_prof[16];
+#define TKP(slot, cond)                                                  \
+    do {                                                                 \
+        if ((cond) && threadIdx.x == 0) g_tk_prof[slot] = clock64();     \
+    } while (0)
+#else
+#define TKP(slot, cond) \
+    do {                \
+    } while (0)
+#endif
 
 // forward rhs reduction of level lev for kept-node index m (level-ordered
 // factors at off; record rows of length n at fb; f1 = f0 + np)
@@ -500,16 +584,12 @@ __device__ __forceinline__ void cr_rhs_down(const double* fb, int n, int np, int
     const int p = j - s, q = j + s;
     const int J = PI(j), P = PI(p), Pf = off + m;
     const double h0 = f0[P], h1 = f1[P];
-    double g0 = f0[J] - (fb[3 * n + Pf] * h0 + fb[4 * n + Pf] * h1);
-    double g1 = f1[J] - (fb[5 * n + Pf] * h0 + fb[6 * n + Pf] * h1);
-    if (q < n) {
-        const int Q = PI(q), Qf = Pf + 1;
-        const double k0 = f0[Q], k1 = f1[Q];
-        g0 -= fb[7 * n + Qf] * k0 + fb[8 * n + Qf] * k1;
-        g1 -= fb[9 * n + Qf] * k0 + fb[10 * n + Qf] * k1;
-    }
-    f0[J] = g0;
-    f1[J] = g1;
+    const double k0 = (q < n) ? f0[PI(q)] : 0.0, k1 = (q < n) ? f1[PI(q)] : 0.0;
+    const int Qf = (q < n) ? Pf + 1 : Pf;
+    const double t0 = fb[7 * n + Qf] * k0 + fb[8 * n + Qf] * k1;
+    const double t1 = fb[9 * n + Qf] * k0 + fb[10 * n + Qf] * k1;
+    f0[J] = fma(-fb[3 * n + Pf], h0, fma(-fb[4 * n + Pf], h1, f0[J])) - t0;
+    f1[J] = fma(-fb[5 * n + Pf], h0, fma(-fb[6 * n + Pf], h1, f1[J])) - t1;
 }
 
 // back substitution of eliminated-node index m at level lev
@@ -539,14 +619,15 @@ __device__ __forceinline__ void cr_rhs_up(const double* fb, int n, int np, int l
     f1[P] = x1;
 }
 
-// rhs-only block cyclic reduction.  Levels with more than 32 active nodes
-// run CTA-wide (one barrier per level); the remaining levels, the root and
-// their back-substitution run inside warp 0 with __syncwarp only.
-__device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0) {
+// rhs-only solve with a factor record: cyclic-reduction levels below the cut
+// (CTA-wide while more than 32 nodes are eliminated, then in warp 0), the
+// reduced system by the dense inverse W, and the back-substitution.
+__device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0, bool prof = false) {
     const int tid = threadIdx.x, nth = blockDim.x;
     const int np = padded(n);
-    const int top = ilog2(n);
-    const int lw = cta_levels(n);
+    const int c = cut_level(n), A = cut_nodes(n), M = 2 * A;
+    const int lw = cta_levels(n) < c ? cta_levels(n) : c;
+    double* f1 = f0 + np;
     int off = 0;
 #pragma unroll
     for (int lev = 0; lev < kMaxLev; ++lev) {   // CTA-wide levels
@@ -556,34 +637,67 @@ __device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0) {
         off += lvl_count(n, lev);
         __syncthreads();
     }
-    if (tid < 32) {                       // warp-level tail
-        int o = off;
+    TKP(2, prof);
+    if (lw < c) {
+        if (tid < 32) {                   // warp-level levels below the cut
+            int o = off;
 #pragma unroll
-        for (int l = 0; l < kMaxLev; ++l) {
-            if (l < lw) continue;
-            if (l >= top) break;
-            if (tid < kept_count(n, l)) cr_rhs_down(fb, n, np, l, o, tid, f0);
-            o += lvl_count(n, l);
-            __syncwarp();
+            for (int l = 0; l < kMaxLev; ++l) {
+                if (l < lw) continue;
+                if (l >= c) break;
+                if (tid < kept_count(n, l)) cr_rhs_down(fb, n, np, l, o, tid, f0);
+                o += lvl_count(n, l);
+                __syncwarp();
+            }
         }
-        if (tid == 0) {
-            const int r = (1 << top) - 1, R = PI(r);
-            double* f1 = f0 + np;
-            const double g0 = f0[R], g1 = f1[R];
-            f0[R] = fb[o] * g0 + fb[n + o] * g1;
-            f1[R] = fb[n + o] * g0 + fb[2 * n + o] * g1;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int l = kMaxLev - 1; l >= 0; --l) {
-            if (l >= top || l < lw) continue;
-            const int ce = lvl_count(n, l);
-            o -= ce;
-            if (tid < ce) cr_rhs_up(fb, n, np, l, o, tid, f0);
-            __syncwarp();
-        }
+        __syncthreads();
     }
-    __syncthreads();
+    // dense solve of the reduced system: x = W g on the A active nodes
+    {
+        const double* Wt = fb + kFacRows * n;
+        double x = 0.0;
+        if (tid < M) {
+            double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+            int col = 0;
+            for (; col + 4 <= M; col += 4) {
+                const int J0 = PI(((col >> 1) + 1 << c) - 1);
+                const int J1 = PI((((col + 2) >> 1) + 1 << c) - 1);
+                acc0 = fma(Wt[col * M + tid], f0[J0], acc0);
+                acc1 = fma(Wt[(col + 1) * M + tid], f1[J0], acc1);
+                acc2 = fma(Wt[(col + 2) * M + tid], f0[J1], acc2);
+                acc3 = fma(Wt[(col + 3) * M + tid], f1[J1], acc3);
+            }
+            for (; col < M; col += 2) {
+                const int J0 = PI(((col >> 1) + 1 << c) - 1);
+                acc0 = fma(Wt[col * M + tid], f0[J0], acc0);
+                acc1 = fma(Wt[(col + 1) * M + tid], f1[J0], acc1);
+            }
+            x = (acc0 + acc1) + (acc2 + acc3);
+        }
+        __syncthreads();
+        if (tid < M) {
+            const int J = PI(((tid >> 1) + 1 << c) - 1);
+            (tid & 1 ? f1 : f0)[J] = x;
+        }
+        __syncthreads();
+    }
+    TKP(3, prof);
+    if (lw < c) {
+        if (tid < 32) {                   // warp-level back-substitution
+            int o = off;
+            for (int l = lw; l < c; ++l) o += lvl_count(n, l);
+#pragma unroll
+            for (int l = kMaxLev - 1; l >= 0; --l) {
+                if (l >= c || l < lw) continue;
+                const int ce = lvl_count(n, l);
+                o -= ce;
+                if (tid < ce) cr_rhs_up(fb, n, np, l, o, tid, f0);
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+    }
+    TKP(4, prof);
 #pragma unroll
     for (int lev = kMaxLev - 1; lev >= 0; --lev) {  // CTA-wide back-substitution
         if (lev >= lw) continue;
@@ -592,6 +706,7 @@ __device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0) {
         for (int m = tid; m < ce; m += nth) cr_rhs_up(fb, n, np, lev, off, m, f0);
         __syncthreads();
     }
+    TKP(5, prof);
 }
 
 // --- TMA bulk copies + mbarrier (sm_90+; SASS UBLKCP / SYNCS) -------------
@@ -623,9 +738,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 }
 
 // Serial coupling chain (one CTA).  FWD: chain[i] = u_i, BWD: chain[i] = mu_i.
-// `a` = D^{-1} r from pass 1.  STAGED: the next interval's factor record
-// (14n doubles) and a-segment (n doubles) are TMA bulk-copied into the other
-// half of a double buffer while the current interval's recurrences run.
+// `a` = D^{-1} r from pass 1.  STAGED: the next interval's record and
+// a-segment are TMA bulk-copied into the other half of a double buffer while
+// the current interval is solved.  The output of step k and the right-hand
+// side of step k+1 are formed in one pass (two ping-pong rhs buffers).
 template <bool FWD, bool STAGED, int NT>
 __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
                                  const double* __restrict__ fac, double* __restrict__ chain) {
@@ -634,31 +750,31 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
     const Lay& L = V.lay;
     const int n = dimn<NT>(V), N = L.N, np = padded(n);
     const int tid = threadIdx.x, nth = blockDim.x;
-    const int rec = kFacRows * n;
+    const int rec = fac_record(n);
     const int brec = rec + n;
     double* buf0 = sm;
     double* buf1 = STAGED ? sm + brec : sm;
-    double* f0 = STAGED ? sm + 2 * brec : sm;
-    double* f1 = f0 + np;
-    double* dv = f1 + np;
+    double* fbase = STAGED ? sm + 2 * brec : sm;
+    double* fr[2] = {fbase, fbase + 2 * np};
     const int K = N - 1;  // chain steps after the seed
     auto blk = [&](int k) { return FWD ? 1 + k : N - 1 - k; };
     auto aseg = [&](int i) { return a + (FWD ? L.off_u(i) : L.off_mu(i)); };
-    {   // seed: u_0 = a_0^u (FWD) / mu_N = a_N^mu (BWD)
-        const int i0 = FWD ? 0 : N;
-        const double* s0 = aseg(i0);
-        for (int j = tid; j < n; j += nth) {
-            dv[PI(j)] = s0[j];
-            chain[(size_t)i0 * n + j] = s0[j];
-        }
-    }
-    if (STAGED && tid == 0) {
+    auto record = [&](int k) -> const double* {
+        return STAGED ? ((k & 1) ? buf1 : buf0) : fac + (size_t)blk(k) * rec;
+    };
+    auto aval = [&](int k) -> const double* { return STAGED ? record(k) + rec : aseg(blk(k)); };
+    const int i0 = FWD ? 0 : N;
+    const double* s0 = aseg(i0);
+    for (int j = tid; j < n; j += nth) chain[(size_t)i0 * n + j] = s0[j];
+    if (K <= 0) return;
+    const int pt = nth - 1;        // the thread issuing the TMA prefetches
+    if (STAGED && tid == pt) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    auto prefetch = [&](int k) {   // thread 0 only
+    auto prefetch = [&](int k) {
         double* b = (k & 1) ? buf1 : buf0;
         uint64_t* bar = &bars[k & 1];
         const int i = blk(k);
@@ -667,51 +783,73 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
         tma_g2s(b, fac + (size_t)i * rec, (unsigned)(rec * sizeof(double)), bar);
         tma_g2s(b + rec, aseg(i), (unsigned)(n * sizeof(double)), bar);
     };
-    if (STAGED && K > 0 && tid == 0) prefetch(0);
-    for (int k = 0; k < K; ++k) {
-        const int i = blk(k);
-        const double* fb;
-        const double* ai;
-        if (STAGED) {
-            if (tid == 0 && k + 1 < K) prefetch(k + 1);
-            mbar_wait(&bars[k & 1], (unsigned)((k >> 1) & 1));
-            fb = (k & 1) ? buf1 : buf0;
-            ai = fb + rec;
-        } else {
-            fb = fac + (size_t)i * rec;
-            ai = aseg(i);
-        }
+    if (STAGED && tid == pt) prefetch(0);
+    if (STAGED) mbar_wait(&bars[0], 0u);
+    {   // right-hand side of step 0 from the seed
+        const double* fb = record(0);
         const double *Cs = fb + 11 * n, *Cd = fb + 12 * n, *Cp = fb + 13 * n;
+        double* f0 = fr[0];
+        double* f1 = f0 + np;
         for (int j = tid; j < n; j += nth) {
             const int J = PI(j);
-            if (FWD) {  // rhs (0, -C u_{i-1})
-                double cv = Cd[j] * dv[J];
-                if (j > 0) cv += Cs[j] * dv[PI(j - 1)];
-                if (j < n - 1) cv += Cp[j] * dv[PI(j + 1)];
+            if (FWD) {
+                double cv = Cd[j] * s0[j];
+                if (j > 0) cv += Cs[j] * s0[j - 1];
+                if (j < n - 1) cv += Cp[j] * s0[j + 1];
                 f0[J] = 0.0;
                 f1[J] = -cv;
-            } else {    // rhs (-mu_{i+1}, 0)
-                f0[J] = -dv[J];
+            } else {
+                f0[J] = -s0[j];
                 f1[J] = 0.0;
             }
         }
-        __syncthreads();
-        cr_rhs(n, fb, f0);
+    }
+    __syncthreads();
+    for (int k = 0; k < K; ++k) {
+        const int i = blk(k);
+        const bool prof = (k == K / 2);
+        TKP(0, prof);
+        if (STAGED && tid == pt && k + 1 < K) prefetch(k + 1);
+        const double* fb = record(k);
+        const double* ai = aval(k);
+        double* f0 = fr[k & 1];
+        double* f1 = f0 + np;
+        TKP(1, prof);
+        cr_rhs(n, fb, f0, prof);
+        const bool more = k + 1 < K;
+        if (STAGED && more) mbar_wait(&bars[(k + 1) & 1], (unsigned)(((k + 1) >> 1) & 1));
+        const double* fbn = more ? record(k + 1) : fb;
+        double* g0 = fr[(k + 1) & 1];
+        double* g1 = g0 + np;
+        const double *Cs = fb + 11 * n, *Cd = fb + 12 * n, *Cp = fb + 13 * n;
+        const double *Ns = fbn + 11 * n, *Nd = fbn + 12 * n, *Np = fbn + 13 * n;
         for (int j = tid; j < n; j += nth) {
             const int J = PI(j);
-            double val;
-            if (FWD) {
-                val = ai[j] + f0[J];
-            } else {    // + (C^T lam)_j
+            if (FWD) {   // u_i = a + u-part; next rhs (0, -C_{i+1} u_i)
+                const double val = ai[j] + f0[J];
+                chain[(size_t)i * n + j] = val;
+                if (more) {
+                    double cv = Nd[j] * val;
+                    if (j > 0) cv += Ns[j] * (ai[j - 1] + f0[PI(j - 1)]);
+                    if (j < n - 1) cv += Np[j] * (ai[j + 1] + f0[PI(j + 1)]);
+                    g0[J] = 0.0;
+                    g1[J] = -cv;
+                }
+            } else {     // mu_i = a + C^T lam; next rhs (-mu_i, 0)
                 double ct = Cd[j] * f1[J];
                 if (j > 0) ct += Cp[j - 1] * f1[PI(j - 1)];
                 if (j < n - 1) ct += Cs[j + 1] * f1[PI(j + 1)];
-                val = ai[j] + ct;
+                const double val = ai[j] + ct;
+                chain[(size_t)i * n + j] = val;
+                if (more) {
+                    g0[J] = -val;
+                    g1[J] = 0.0;
+                }
             }
-            dv[J] = val;
-            chain[(size_t)i * n + j] = val;
         }
+        (void)Ns; (void)Nd; (void)Np;
         __syncthreads();
+        TKP(6, prof);
     }
 }
 
@@ -730,7 +868,13 @@ __global__ void __launch_bounds__(256, 3) tri_rows_cpl(TView V, const double* __
     }
 }
 
-int64_t tri_fac_len(const tk_level* Lv) { return (int64_t)Lv->n_steps * kFacRows * Lv->n_u; }
+#ifdef TK_PROF
+extern "C" int tk_debug_prof(long long* out16) {
+    return cudaMemcpyFromSymbol(out16, g_tk_prof, sizeof(long long) * 16) == cudaSuccess ? 0 : 2;
+}
+#endif
+
+int64_t tri_fac_len(const tk_level* Lv) { return (int64_t)Lv->n_steps * fac_record(Lv->n_u); }
 int64_t tri_scratch_len(const tk_level* Lv) { return (int64_t)(Lv->n_steps + 1) * Lv->n_u; }
 
 enum TriApply { T_APPLY = 0, T_APPLY_DIAG = 1, T_RESIDUAL = 2 };
@@ -869,8 +1013,8 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             // pass 2: serial chain on the coupling vector
             const int cth = tri_chain_threads(n);
             const int np = padded(n);
-            const int64_t staged = (int64_t)(2 * (kFacRows + 1) * n + 3 * np) * 8;
-            const int64_t direct = (int64_t)(3 * np) * 8;
+            const int64_t staged = (int64_t)(2 * (fac_record(n) + n) + 4 * np) * 8;
+            const int64_t direct = (int64_t)(4 * np) * 8;
             // TMA bulk copies need 16-byte aligned sources and sizes: n even and
             // even segment offsets (always true for the Burgers layout, nz == nu)
             const bool aligned = (n % 2 == 0) && (Lv->n_z % 2 == 0);
@@ -893,7 +1037,16 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                 set_error("tk_subst_factor: level has no fac buffer");
                 return TK_ERR_ARG;
             }
-            tri_factor_kernel<NT><<<Lv->n_steps, th, smem, s>>>(V, Lv->fac);
+            {
+                const int M = 2 * cut_nodes(n);
+                const int64_t fsm = smem + (int64_t)(M * 2 * M + M) * 8;
+                if (fsm > 227 * 1024) {
+                    set_error("tk_subst_factor: n_u=%d needs %lld bytes of shared memory", n,
+                              (long long)fsm);
+                    return TK_ERR_UNSUPPORTED;
+                }
+                tri_factor_kernel<NT><<<Lv->n_steps, th, fsm, s>>>(V, Lv->fac);
+            }
             break;
         default: set_error("tri: bad op %d", op); return TK_ERR_ARG;
     }
