@@ -622,7 +622,8 @@ __device__ __forceinline__ void cr_rhs_up(const double* fb, int n, int np, int l
 // rhs-only solve with a factor record: cyclic-reduction levels below the cut
 // (CTA-wide while more than 32 nodes are eliminated, then in warp 0), the
 // reduced system by the dense inverse W, and the back-substitution.
-__device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0, bool prof = false) {
+__device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0, double* part,
+                                       bool prof = false) {
     const int tid = threadIdx.x, nth = blockDim.x;
     const int np = padded(n);
     const int c = cut_level(n), A = cut_nodes(n), M = 2 * A;
@@ -652,30 +653,29 @@ __device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0, bool
         }
         __syncthreads();
     }
-    // dense solve of the reduced system: x = W g on the A active nodes
+    // dense solve of the reduced system: x = W g on the A active nodes.  Row r
+    // is split over G = nth / M thread groups (column chunks); partial sums
+    // meet in the shared scratch `part` ([blockDim.x] doubles).
     {
         const double* Wt = fb + kFacRows * n;
-        double x = 0.0;
-        if (tid < M) {
-            double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-            int col = 0;
-            for (; col + 4 <= M; col += 4) {
-                const int J0 = PI(((col >> 1) + 1 << c) - 1);
-                const int J1 = PI((((col + 2) >> 1) + 1 << c) - 1);
-                acc0 = fma(Wt[col * M + tid], f0[J0], acc0);
-                acc1 = fma(Wt[(col + 1) * M + tid], f1[J0], acc1);
-                acc2 = fma(Wt[(col + 2) * M + tid], f0[J1], acc2);
-                acc3 = fma(Wt[(col + 3) * M + tid], f1[J1], acc3);
+        const int G = (nth / M) > 0 ? nth / M : 1;
+        const int r = tid % M, grp = tid / M;
+        double acc0 = 0.0, acc1 = 0.0;
+        if (grp < G && tid < G * M) {
+            const int nodes = A;           // columns come in (u, lam) pairs per node
+            const int per = (nodes + G - 1) / G;
+            const int m0 = grp * per, m1 = min(nodes, m0 + per);
+            for (int m = m0; m < m1; ++m) {
+                const int J = PI(((m + 1) << c) - 1);
+                acc0 = fma(Wt[(2 * m) * M + r], f0[J], acc0);
+                acc1 = fma(Wt[(2 * m + 1) * M + r], f1[J], acc1);
             }
-            for (; col < M; col += 2) {
-                const int J0 = PI(((col >> 1) + 1 << c) - 1);
-                acc0 = fma(Wt[col * M + tid], f0[J0], acc0);
-                acc1 = fma(Wt[(col + 1) * M + tid], f1[J0], acc1);
-            }
-            x = (acc0 + acc1) + (acc2 + acc3);
+            part[tid] = acc0 + acc1;
         }
         __syncthreads();
         if (tid < M) {
+            double x = 0.0;
+            for (int g = 0; g < G; ++g) x += part[g * M + tid];
             const int J = PI(((tid >> 1) + 1 << c) - 1);
             (tid & 1 ? f1 : f0)[J] = x;
         }
@@ -815,7 +815,7 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
         double* f0 = fr[k & 1];
         double* f1 = f0 + np;
         TKP(1, prof);
-        cr_rhs(n, fb, f0, prof);
+        cr_rhs(n, fb, f0, fbase + 4 * np, prof);
         const bool more = k + 1 < K;
         if (STAGED && more) mbar_wait(&bars[(k + 1) & 1], (unsigned)(((k + 1) >> 1) & 1));
         const double* fbn = more ? record(k + 1) : fb;
@@ -1013,8 +1013,8 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             // pass 2: serial chain on the coupling vector
             const int cth = tri_chain_threads(n);
             const int np = padded(n);
-            const int64_t staged = (int64_t)(2 * (fac_record(n) + n) + 4 * np) * 8;
-            const int64_t direct = (int64_t)(4 * np) * 8;
+            const int64_t staged = (int64_t)(2 * (fac_record(n) + n) + 4 * np + 256) * 8;
+            const int64_t direct = (int64_t)(4 * np + 256) * 8;
             // TMA bulk copies need 16-byte aligned sources and sizes: n even and
             // even segment offsets (always true for the Burgers layout, nz == nu)
             const bool aligned = (n % 2 == 0) && (Lv->n_z % 2 == 0);
