@@ -32,6 +32,41 @@ sys.path.insert(0, ROOT)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 
 
+# ncu-measured DRAM traffic per C-ABI call: which CUDA kernels one call launches
+_NCU_KERNELS = {
+    "tk_forward_subst": ("tri_chain_kernel<1", "tri_rows<", "tri_rows_cpl<1", "dense_chain<"),
+    "tk_backward_subst": ("tri_chain_kernel<0", "tri_rows<", "tri_rows_cpl<0", "dense_chain<"),
+    "tk_jacobi_sweep": ("tri_rows<", "dense_rows<"),
+    "tk_residual_restrict": ("tri_apply<2", "restrict_kernel"),
+}
+
+
+def ncu_traffic(call: str):
+    """DRAM bytes per call from the committed ncu summary (profiles/), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as fh:
+        summ = json.load(fh)
+    pats = _NCU_KERNELS.get(call)
+    if not pats:
+        return None, os.path.basename(files[-1])
+    if call == "tk_jacobi_sweep":   # the fine-level launch of the full capture
+        fine = [d for d in summ["full_capture"] if pats[0] in d["kernel"]]
+        if fine:
+            d = max(fine, key=lambda e: e["duration_us"])
+            return int((d["dram_read_MB"] + d["dram_write_MB"]) * 1e6), os.path.basename(files[-1])
+        return None, os.path.basename(files[-1])
+    tot = 0
+    for pat in pats:
+        for d in summ["launch_list"]:
+            if pat in d["kernel"]:
+                tot += d["dram_bytes_per_launch"]
+                break
+    return (tot or None), os.path.basename(files[-1])
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -293,11 +328,16 @@ def run_ours(args, rank, world, local_rank):
                 "h2d_bytes_per_step": int(r_host.nbytes), "d2h_bytes_per_step": int(r_host.nbytes),
                 "ms_per_step": e2e_ms, "api": "mg_preconditioner(h)(r) with pinned host r"},
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": ach,
-                     "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                     "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                     "traffic": ncu_traffic(dominant)[0], "traffic_source": ncu_traffic(dominant)[1],
                      "peak_kind": peak_kind, "launches_timed": n_dom,
                      "bytes_per_launch": b_dom, "ms_per_launch": ms_dom,
+                     "note": ("the Gauss-Seidel substitutions are serial in time (one CTA walks "
+                              "the coarse intervals): latency-bound, not HBM-bound"
+                              if "subst" in dominant else ""),
                      "fine_jacobi": {"achieved": ach_j, "frac": ach_j / hbm,
-                                     "bytes_per_launch": b_j, "ms_per_launch": ms_j}},
+                                     "bytes_per_launch": b_j, "ms_per_launch": ms_j,
+                                     "traffic": ncu_traffic("tk_jacobi_sweep")[0]}},
         "kernels": {k: {"calls": v["calls"], "ms": round(v["ms"], 4),
                         "share": round(v["ms"] / sum(x["ms"] for x in per.values()), 4),
                         "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}

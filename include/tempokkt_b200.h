@@ -88,6 +88,11 @@ typedef struct tk_level {
     int32_t row1;
     const double* halo_u;
     const double* halo_mu;
+    /* TRI: transposed dense inverse of the scalar Q_z system reduced to the
+     * cyclic-reduction cut level (tk_tri_cut_nodes(n_u)^2 doubles, i.e. the
+     * (active, active) block of Q_z^{-1}).  Required once L->fac holds
+     * factor records: D^{-1} then runs as an rhs-only solve. */
+    const double* qz_w;
 } tk_level;
 
 /* --- library ------------------------------------------------------------ */
@@ -125,6 +130,10 @@ int tk_backward_subst(const tk_level* L, const double* r, double* delta, void* s
 int64_t tk_subst_factor_len(const tk_level* L);
 int64_t tk_subst_scratch_len(const tk_level* L);
 int tk_subst_factor(const tk_level* L, void* stream);
+/* TRI: cut level / active-node count of the record-based local solves, and
+ * the node indices (0-based) of the active nodes (host memory, out[cut_nodes]). */
+int32_t tk_tri_cut_nodes(int32_t n_u);
+int tk_tri_cut_indices(int32_t n_u, int32_t* out);
 
 /* --- transfers (multigrid.py:272-300) ------------------------------------- */
 /* xc = R xf  (injection for u,v,lam,mu; 2-interval average for z)    restrict_kkt multigrid.py:272 */

@@ -38,6 +38,7 @@ class TkLevel(C.Structure):
         ("kappa", _d), ("qz_cr", _p),
         ("fac", _p), ("scratch", _p),
         ("row0", _i32), ("row1", _i32), ("halo_u", _p), ("halo_mu", _p),
+        ("qz_w", _p),
     ]
 
 
@@ -56,6 +57,8 @@ _SIGS = {
     "tk_subst_factor_len": (_i64, [C.POINTER(TkLevel)]),
     "tk_subst_scratch_len": (_i64, [C.POINTER(TkLevel)]),
     "tk_subst_factor": (C.c_int, [C.POINTER(TkLevel), _p]),
+    "tk_tri_cut_nodes": (_i32, [_i32]),
+    "tk_tri_cut_indices": (C.c_int, [_i32, _p]),
     "tk_restrict": (C.c_int, [_i32, _i32, _i32, _p, _p, _p]),
     "tk_prolong_add": (C.c_int, [_i32, _i32, _i32, _p, _p, _p]),
     "tk_restrict_slab": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _p, _p, _p]),

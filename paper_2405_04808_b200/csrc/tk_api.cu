@@ -29,6 +29,8 @@ int64_t tri_smem_bytes(int n);
 int64_t tri_fac_len(const tk_level*);
 int64_t tri_scratch_len(const tk_level*);
 int64_t dense_fac_len(const tk_level*);
+int32_t tri_cut_nodes(int n);
+int32_t tri_cut_level(int n);
 int64_t dense_scratch_len(const tk_level*);
 int transfer_launch(int, int, int, int, int, int, const double*, const double*, const double*,
                     double*, cudaStream_t);
@@ -150,6 +152,15 @@ int64_t tk_subst_scratch_len(const tk_level* L) {
 
 int tk_subst_factor(const tk_level* L, void* stream) {
     return level_op(L, 12, 12, nullptr, nullptr, nullptr, 1.0, stream);
+}
+
+int32_t tk_tri_cut_nodes(int32_t n_u) { return n_u >= 1 ? tri_cut_nodes(n_u) : 0; }
+
+int tk_tri_cut_indices(int32_t n_u, int32_t* out) {
+    TK_CHECK_ARG(n_u >= 1 && out, "tk_tri_cut_indices: bad arguments");
+    const int c = tri_cut_level(n_u), a = tri_cut_nodes(n_u);
+    for (int m = 0; m < a; ++m) out[m] = ((m + 1) << c) - 1;
+    return TK_OK;
 }
 
 int tk_restrict(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xf, double* xc,

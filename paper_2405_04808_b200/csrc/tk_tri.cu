@@ -42,9 +42,12 @@ struct TView {
     const double* cr;
     double kappa;
     Slab sl;
+    const double* fac;   // factor records of the slab's stages (or null)
+    const double* qzw;   // scalar reduced-system inverse at the cut (with fac)
     TView(const tk_level* L)
         : lay(L->n_steps, L->n_u, L->n_z), n(L->n_u), K(L->K), C(L->C), Qm(L->Qm), Ql(L->Ql),
-          Qz(L->Qz), cr(L->qz_cr), kappa(L->kappa), sl(L, Lay(L->n_steps, L->n_u, L->n_z)) {}
+          Qz(L->Qz), cr(L->qz_cr), kappa(L->kappa), sl(L, Lay(L->n_steps, L->n_u, L->n_z)),
+          fac(L->fac), qzw(L->qz_w) {}
     // stage diagonals of global block row i (stage arrays start at the slab's first row)
     __device__ const double* Ki(int i, int n_) const { return K + (size_t)(i - sl.r0) * 3 * n_; }
     __device__ const double* Ci(int i, int n_) const { return C + (size_t)(i - sl.r0) * 3 * n_; }
@@ -476,19 +479,22 @@ __device__ __forceinline__ int lvl_pos(int n, int j) {
 // Extra dynamic smem after the 16 node arrays: the 2A x 4A augmented matrix
 // of the reduced system and a pivot column (Gauss-Jordan, no pivoting needed:
 // the reduced system is symmetric quasi-definite).
-template <int NT>
-__global__ void tri_factor_kernel(TView V, double* __restrict__ fac) {
+// GW: the 16 node arrays live in global scratch (one slice per CTA) for n
+// too large for shared memory.
+template <int NT, bool GW>
+__global__ void tri_factor_kernel(TView V, double* __restrict__ fac, double* gwork) {
     extern __shared__ __align__(16) double sm[];
     const Lay& L = V.lay;
     const int n = dimn<NT>(V);
     const int tid = threadIdx.x, nth = blockDim.x;
-    const TriSm S(sm, n);
+    const TriSm S(GW ? gwork + (size_t)blockIdx.x * kTriArrays * padded(n) : sm, n);
     const int c = cut_level(n), A = cut_nodes(n), M = 2 * A, M2 = 2 * M;
-    double* G = sm + kTriArrays * padded(n);     // [M][2M]
-    double* fcol = G + M * M2;                   // [M]
+    double* G = GW ? sm : sm + kTriArrays * padded(n);   // [M][2M]
+    double* fcol = G + M * M2;                           // [M]
     using K = CrSolve<false>;
     const double* cinv = V.cr;
-    for (int i = blockIdx.x; i < L.N; i += gridDim.x) {
+    const int s1 = V.sl.r1 < L.N ? V.sl.r1 : L.N;         // stages of the slab
+    for (int i = V.sl.r0 + blockIdx.x; i < s1; i += gridDim.x) {
         tri_init_de(V, n, i, S);
         __syncthreads();
         for (int lev = 0; lev < c; ++lev) {      // partial factorisation: levels < c
@@ -532,7 +538,7 @@ __global__ void tri_factor_kernel(TView V, double* __restrict__ fac) {
             for (int col = tid; col < M2; col += nth) G[k * M2 + col] /= piv;
             __syncthreads();
         }
-        double* out = fac + (size_t)i * fac_record(n);
+        double* out = fac + (size_t)(i - V.sl.r0) * fac_record(n);
         const double* Cm = (i >= 1) ? V.Ci(i, n) : nullptr;
         for (int j = tid; j < n; j += nth) {
             const int lev = __ffs(j + 1) - 1;
@@ -619,11 +625,32 @@ __device__ __forceinline__ void cr_rhs_up(const double* fb, int n, int np, int l
     f1[P] = x1;
 }
 
+// scalar cyclic reduction of Qz w = fw with precomputed coefficients
+// cr = [3][n] = (inv_d, e_up, e_lo) at each node's elimination level
+__device__ __forceinline__ void scal_down(double* fw, const double* cr, int n, int lev, int m) {
+    const int s = 1 << lev;
+    const int j = 2 * s - 1 + 2 * s * m, p = j - s, q = j + s;
+    double w = fw[PI(j)] - cr[n + p] * cr[p] * fw[PI(p)];
+    if (q < n) w -= cr[2 * n + q] * cr[q] * fw[PI(q)];
+    fw[PI(j)] = w;
+}
+__device__ __forceinline__ void scal_up(double* fw, const double* cr, int n, int lev, int m) {
+    const int s = 1 << lev;
+    const int p = s - 1 + 2 * s * m;
+    double w = fw[PI(p)];
+    if (p - s >= 0) w -= cr[2 * n + p] * fw[PI(p - s)];
+    if (p + s < n) w -= cr[n + p] * fw[PI(p + s)];
+    fw[PI(p)] = cr[p] * w;
+}
+
 // rhs-only solve with a factor record: cyclic-reduction levels below the cut
 // (CTA-wide while more than 32 nodes are eliminated, then in warp 0), the
-// reduced system by the dense inverse W, and the back-substitution.
+// reduced system by the dense inverse W, and the back-substitution.  With
+// fw != null the scalar Qz system (coefficients cr, reduced inverse qzw at
+// the cut) is solved alongside, sharing the barriers.
 __device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0, double* part,
-                                       bool prof = false) {
+                                       bool prof = false, double* fw = nullptr,
+                                       const double* cr = nullptr, const double* qzw = nullptr) {
     const int tid = threadIdx.x, nth = blockDim.x;
     const int np = padded(n);
     const int c = cut_level(n), A = cut_nodes(n), M = 2 * A;
@@ -634,7 +661,10 @@ __device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0, doub
     for (int lev = 0; lev < kMaxLev; ++lev) {   // CTA-wide levels
         if (lev >= lw) break;
         const int ck = kept_count(n, lev);
-        for (int m = tid; m < ck; m += nth) cr_rhs_down(fb, n, np, lev, off, m, f0);
+        for (int m = tid; m < ck; m += nth) {
+            cr_rhs_down(fb, n, np, lev, off, m, f0);
+            if (fw) scal_down(fw, cr, n, lev, m);
+        }
         off += lvl_count(n, lev);
         __syncthreads();
     }
@@ -646,38 +676,65 @@ __device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0, doub
             for (int l = 0; l < kMaxLev; ++l) {
                 if (l < lw) continue;
                 if (l >= c) break;
-                if (tid < kept_count(n, l)) cr_rhs_down(fb, n, np, l, o, tid, f0);
+                if (tid < kept_count(n, l)) {
+                    cr_rhs_down(fb, n, np, l, o, tid, f0);
+                    if (fw) scal_down(fw, cr, n, l, tid);
+                }
                 o += lvl_count(n, l);
                 __syncwarp();
             }
         }
         __syncthreads();
     }
+    if (fw) {   // scalar reduced system: w_a = (Qz^{-1})_aa fw_a (qzw transposed)
+        double x = 0.0;
+        if (tid < A) {
+            for (int m = 0; m < A; ++m) x = fma(qzw[m * A + tid], fw[PI(((m + 1) << c) - 1)], x);
+        }
+        __syncthreads();
+        if (tid < A) fw[PI(((tid + 1) << c) - 1)] = x;
+    }
     // dense solve of the reduced system: x = W g on the A active nodes.  Row r
     // is split over G = nth / M thread groups (column chunks); partial sums
     // meet in the shared scratch `part` ([blockDim.x] doubles).
     {
         const double* Wt = fb + kFacRows * n;
-        const int G = (nth / M) > 0 ? nth / M : 1;
-        const int r = tid % M, grp = tid / M;
-        double acc0 = 0.0, acc1 = 0.0;
-        if (grp < G && tid < G * M) {
-            const int nodes = A;           // columns come in (u, lam) pairs per node
-            const int per = (nodes + G - 1) / G;
-            const int m0 = grp * per, m1 = min(nodes, m0 + per);
-            for (int m = m0; m < m1; ++m) {
-                const int J = PI(((m + 1) << c) - 1);
-                acc0 = fma(Wt[(2 * m) * M + r], f0[J], acc0);
-                acc1 = fma(Wt[(2 * m + 1) * M + r], f1[J], acc1);
+        if (nth >= M) {
+            const int G = nth / M;
+            const int r = tid % M, grp = tid / M;
+            double acc0 = 0.0, acc1 = 0.0;
+            if (grp < G) {
+                const int per = (A + G - 1) / G;   // columns come in (u, lam) pairs per node
+                const int m0 = grp * per, m1 = min(A, m0 + per);
+                for (int m = m0; m < m1; ++m) {
+                    const int J = PI(((m + 1) << c) - 1);
+                    acc0 = fma(Wt[(2 * m) * M + r], f0[J], acc0);
+                    acc1 = fma(Wt[(2 * m + 1) * M + r], f1[J], acc1);
+                }
+                part[tid] = acc0 + acc1;
             }
-            part[tid] = acc0 + acc1;
-        }
-        __syncthreads();
-        if (tid < M) {
-            double x = 0.0;
-            for (int g = 0; g < G; ++g) x += part[g * M + tid];
-            const int J = PI(((tid >> 1) + 1 << c) - 1);
-            (tid & 1 ? f1 : f0)[J] = x;
+            __syncthreads();
+            if (tid < M) {
+                double x = 0.0;
+                for (int g = 0; g < G; ++g) x += part[g * M + tid];
+                const int J = PI(((tid >> 1) + 1 << c) - 1);
+                (tid & 1 ? f1 : f0)[J] = x;
+            }
+        } else {                           // fewer threads than rows: whole rows per thread
+            for (int r = tid; r < M; r += nth) {
+                double acc0 = 0.0, acc1 = 0.0;
+                for (int m = 0; m < A; ++m) {
+                    const int J = PI(((m + 1) << c) - 1);
+                    acc0 = fma(Wt[(2 * m) * M + r], f0[J], acc0);
+                    acc1 = fma(Wt[(2 * m + 1) * M + r], f1[J], acc1);
+                }
+                part[r] = acc0 + acc1;
+            }
+            __syncthreads();
+            for (int r = tid; r < M; r += nth) {
+                const int J = PI(((r >> 1) + 1 << c) - 1);
+                (r & 1 ? f1 : f0)[J] = part[r];
+            }
         }
         __syncthreads();
     }
@@ -691,7 +748,10 @@ __device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0, doub
                 if (l >= c || l < lw) continue;
                 const int ce = lvl_count(n, l);
                 o -= ce;
-                if (tid < ce) cr_rhs_up(fb, n, np, l, o, tid, f0);
+                if (tid < ce) {
+                    cr_rhs_up(fb, n, np, l, o, tid, f0);
+                    if (fw) scal_up(fw, cr, n, l, tid);
+                }
                 __syncwarp();
             }
         }
@@ -703,7 +763,10 @@ __device__ __forceinline__ void cr_rhs(int n, const double* fb, double* f0, doub
         if (lev >= lw) continue;
         const int ce = lvl_count(n, lev);
         off -= ce;
-        for (int m = tid; m < ce; m += nth) cr_rhs_up(fb, n, np, lev, off, m, f0);
+        for (int m = tid; m < ce; m += nth) {
+            cr_rhs_up(fb, n, np, lev, off, m, f0);
+            if (fw) scal_up(fw, cr, n, lev, m);
+        }
         __syncthreads();
     }
     TKP(5, prof);
@@ -853,6 +916,129 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Record-based local solve: the same block row operation as tri_block, with
+// the (u,lam) factorisation read from the interval's precomputed record
+// (rhs-only cyclic reduction + dense cut solve) instead of being recomputed.
+// Shared memory: f0 f1 fw sv srv (padded node arrays) + one partial-sum row.
+// ---------------------------------------------------------------------------
+static constexpr int kRecArrays = 5;
+
+template <int NT>
+__device__ __forceinline__ void tri_block_rec(const TView& V, int i, const double* b,
+                                              const double* x, const double* uprev,
+                                              const double* munext, double* out, double omega,
+                                              const double* xupd, double* sm) {
+    const Lay& L = V.lay;
+    const int n = dimn<NT>(V), np = padded(n);
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const bool has_vm = i >= 1, has_uzl = i < L.N;
+    double* f0 = sm;
+    double* f1 = sm + np;
+    double* fw = sm + 2 * np;
+    double* sv = sm + 3 * np;
+    double* srv = sm + 4 * np;
+    double* part = sm + 5 * np;
+    const double kap = V.kappa;
+    const double* Qv = (i == L.N) ? V.Ql : V.Qm;
+    const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;
+    const double* Qz = V.Qz;
+    const double* K = has_uzl ? V.Ki(i, n) : nullptr;
+    const double* C = (has_uzl && has_vm) ? V.Ci(i, n) : nullptr;
+    const int64_t bs = V.sl.base;
+    const int64_t ov = L.off_v(i) - bs, ou = L.off_u(i) - bs, oz = L.off_z(i) - bs,
+                  om = L.off_mu(i) - bs, ol = L.off_l(i) - bs;
+    for (int j = tid; j < n; j += nth) {
+        const int J = PI(j);
+        double rv = 0.0, ru = 0.0, rz = 0.0, rm = 0.0, rl = 0.0;
+        if (has_vm) { rv = b[ov + j]; rm = b[om + j]; }
+        if (has_uzl) { ru = b[ou + j]; rz = b[oz + j]; rl = b[ol + j]; }
+        if (x) {
+            if (has_vm) {
+                double av = tmv(Qv, n, x + ov, j) - x[om + j];
+                if (C) av += tmtv(C, n, x + ol, j);
+                rv -= av;
+                rm += x[ov + j];
+            }
+            if (has_uzl) {
+                ru -= tmv(Qu, n, x + ou, j) + tmtv(K, n, x + ol, j);
+                rz -= tmv(Qz, n, x + oz, j) + kap * tmv(Qz, n, x + ol, j);
+                double al = tmv(K, n, x + ou, j) + kap * tmv(Qz, n, x + oz, j);
+                if (C) al += tmv(C, n, x + ov, j);
+                rl -= al;
+            }
+        }
+        if (has_vm && uprev) rm -= uprev[j];
+        if (has_uzl && munext) ru -= munext[j];
+        if (has_vm) { sv[J] = -rm; srv[J] = rv; }
+        if (has_uzl) { f0[J] = ru; f1[J] = rl - kap * rz; fw[J] = rz; }
+    }
+    __syncthreads();
+    if (!has_uzl) {  // last block (v_N, mu_N): mu = Qv v - r_v
+        for (int j = tid; j < n; j += nth) {
+            const double dv = sv[PI(j)];
+            const double dm = tmv_s(Qv, n, sv, j) - srv[PI(j)];
+            out[ov + j] = (xupd ? xupd[ov + j] : 0.0) + omega * dv;
+            out[om + j] = (xupd ? xupd[om + j] : 0.0) + omega * dm;
+        }
+        __syncthreads();
+        return;
+    }
+    if (C) {
+        for (int j = tid; j < n; j += nth) f1[PI(j)] -= tmv_s(C, n, sv, j);
+        __syncthreads();
+    }
+    const double* fb = V.fac + (size_t)(i - V.sl.r0) * fac_record(n);
+    cr_rhs(n, fb, f0, part, false, fw, V.cr, V.qzw);
+    for (int j = tid; j < n; j += nth) {
+        const int J = PI(j);
+        const double du = f0[J], dl = f1[J];
+        const double dz = fw[J] - kap * dl;
+        out[ou + j] = (xupd ? xupd[ou + j] : 0.0) + omega * du;
+        out[oz + j] = (xupd ? xupd[oz + j] : 0.0) + omega * dz;
+        out[ol + j] = (xupd ? xupd[ol + j] : 0.0) + omega * dl;
+        if (has_vm) {
+            const double dv = sv[J];
+            double dm = tmv_s(Qv, n, sv, j) - srv[J];
+            if (C) dm += tmtv_s(C, n, f1, j);
+            out[ov + j] = (xupd ? xupd[ov + j] : 0.0) + omega * dv;
+            out[om + j] = (xupd ? xupd[om + j] : 0.0) + omega * dm;
+        }
+    }
+    __syncthreads();
+}
+
+int64_t tri_rec_smem_bytes(int n) { return ((int64_t)kRecArrays * padded(n) + 256) * 8; }
+
+// Parallel over block rows with records: jacobi (x may be null) or D^{-1} b.
+template <int NT>
+__global__ void __launch_bounds__(256, 2) tri_rows_rec(TView V, const double* __restrict__ b,
+                                                       const double* __restrict__ x,
+                                                       double* __restrict__ y, double omega) {
+    extern __shared__ __align__(16) double sm[];
+    const Lay& L = V.lay;
+    for (int i = V.sl.r0 + blockIdx.x; i < V.sl.r1; i += gridDim.x) {
+        const double* uprev = x ? V.sl.uprev(L, x, i) : nullptr;
+        const double* munext = x ? V.sl.munext(L, x, i) : nullptr;
+        tri_block_rec<NT>(V, i, b, x, uprev, munext, y, omega, x, sm);
+    }
+}
+
+// Pass 3 of the substitution with records.
+template <bool FWD, int NT>
+__global__ void __launch_bounds__(256, 2) tri_rows_rec_cpl(TView V, const double* __restrict__ r,
+                                                           const double* __restrict__ chain,
+                                                           double* __restrict__ y) {
+    extern __shared__ __align__(16) double sm[];
+    const Lay& L = V.lay;
+    const int n = dimn<NT>(V);
+    for (int i = blockIdx.x; i <= L.N; i += gridDim.x) {
+        const double* uprev = (FWD && i >= 1) ? chain + (size_t)(i - 1) * n : nullptr;
+        const double* munext = (!FWD && i < L.N) ? chain + (size_t)(i + 1) * n : nullptr;
+        tri_block_rec<NT>(V, i, r, nullptr, uprev, munext, y, 1.0, nullptr, sm);
+    }
+}
+
 // Pass 3: parallel solves with the chain as the continuity coupling.
 template <bool FWD, int NT>
 __global__ void __launch_bounds__(256, 3) tri_rows_cpl(TView V, const double* __restrict__ r,
@@ -874,8 +1060,26 @@ extern "C" int tk_debug_prof(long long* out16) {
 }
 #endif
 
-int64_t tri_fac_len(const tk_level* Lv) { return (int64_t)Lv->n_steps * fac_record(Lv->n_u); }
-int64_t tri_scratch_len(const tk_level* Lv) { return (int64_t)(Lv->n_steps + 1) * Lv->n_u; }
+int64_t tri_fac_len(const tk_level* Lv) {
+    const int r0 = Lv->row0;
+    const int r1 = Lv->row1 > 0 ? Lv->row1 : Lv->n_steps + 1;
+    const int stages = (r1 < Lv->n_steps ? r1 : Lv->n_steps) - r0;
+    return (int64_t)(stages > 1 ? stages : 1) * fac_record(Lv->n_u);
+}
+// chain buffer (N+1)*n; for n too large for the shared-memory factor kernel
+// also room for a persistent grid of global node-array slices
+int64_t tri_scratch_len(const tk_level* Lv) {
+    const int n = Lv->n_u;
+    const int64_t chain = (int64_t)(Lv->n_steps + 1) * n;
+    const int M = 2 * cut_nodes(n);
+    const int64_t fsm = (int64_t)kTriArrays * padded(n) * 8 + (int64_t)(M * 2 * M + M) * 8;
+    if (fsm <= 227 * 1024) return chain;
+    const int64_t work = (int64_t)148 * 2 * kTriArrays * padded(n);
+    return chain > work ? chain : work;
+}
+
+int32_t tri_cut_nodes(int n) { return cut_nodes(n); }
+int32_t tri_cut_level(int n) { return cut_level(n); }
 
 enum TriApply { T_APPLY = 0, T_APPLY_DIAG = 1, T_RESIDUAL = 2 };
 
@@ -929,6 +1133,20 @@ int64_t tri_smem_bytes(int n) {
     return (int64_t)kTriArrays * padded(n) * (int64_t)sizeof(double);
 }
 
+// threads per CTA of the record-based rows kernels (TK_REC_THREADS overrides)
+static int tri_rec_threads(int n) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = getenv("TK_REC_THREADS");
+        forced = e ? atoi(e) : 0;
+    }
+    if (forced >= 32) return forced;
+    int t = (n / 4 + 31) / 32 * 32;
+    if (t < 32) t = 32;
+    if (t > 128) t = 128;
+    return t;
+}
+
 static int tri_threads(int n) {
     int t = (n / 2 + 31) / 32 * 32;
     if (t < 32) t = 32;
@@ -965,8 +1183,17 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
         cudaFuncSetAttribute(tri_subst<true, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(tri_subst<false, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              mx);
-        cudaFuncSetAttribute(tri_factor_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             mx);
+        cudaFuncSetAttribute(tri_factor_kernel<NT, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_factor_kernel<NT, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_rows_rec<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_rows_rec<NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        cudaFuncSetAttribute(tri_rows_rec_cpl<true, NT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_rows_rec_cpl<false, NT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(tri_rows_cpl<true, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              mx);
         cudaFuncSetAttribute(tri_rows_cpl<false, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -993,12 +1220,21 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
     }
     const int th = tri_threads(n);
     const bool fast = Lv->fac != nullptr && Lv->scratch != nullptr;
+    const bool rec = Lv->fac != nullptr && Lv->qz_w != nullptr;   // record-based D^{-1}
+    const int64_t rsm = tri_rec_smem_bytes(n);
+    const int rth = tri_rec_threads(n);
+    if (!rec && smem == 0) {
+        set_error("tri family: n_u=%d needs factor records (tk_subst_factor + qz_w)", n);
+        return TK_ERR_UNSUPPORTED;
+    }
     switch (op) {
         case 3:  // diag solve
-            tri_rows<NT><<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
+            if (rec) tri_rows_rec<NT><<<rows, rth, rsm, s>>>(V, b, nullptr, y, 1.0);
+            else tri_rows<NT><<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
             break;
         case 4:  // jacobi
-            tri_rows<NT><<<rows, th, smem, s>>>(V, b, x, y, omega);
+            if (rec) tri_rows_rec<NT><<<rows, rth, rsm, s>>>(V, b, x, y, omega);
+            else tri_rows<NT><<<rows, th, smem, s>>>(V, b, x, y, omega);
             break;
         case 10:
         case 11: {
@@ -1009,7 +1245,8 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                 break;
             }
             // pass 1: a = D^{-1} r into y
-            tri_rows<NT><<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
+            if (rec) tri_rows_rec<NT><<<rows, rth, rsm, s>>>(V, b, nullptr, y, 1.0);
+            else tri_rows<NT><<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
             // pass 2: serial chain on the coupling vector
             const int cth = tri_chain_threads(n);
             const int np = padded(n);
@@ -1028,8 +1265,13 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                 else tri_chain_kernel<false, false, NT><<<1, cth, direct, s>>>(V, y, fac, chn);
             }
             // pass 3: parallel solves with the chain coupling
-            if (fwd) tri_rows_cpl<true, NT><<<rows, th, smem, s>>>(V, b, chn, y);
-            else tri_rows_cpl<false, NT><<<rows, th, smem, s>>>(V, b, chn, y);
+            if (rec) {
+                if (fwd) tri_rows_rec_cpl<true, NT><<<rows, rth, rsm, s>>>(V, b, chn, y);
+                else tri_rows_rec_cpl<false, NT><<<rows, rth, rsm, s>>>(V, b, chn, y);
+            } else {
+                if (fwd) tri_rows_cpl<true, NT><<<rows, th, smem, s>>>(V, b, chn, y);
+                else tri_rows_cpl<false, NT><<<rows, th, smem, s>>>(V, b, chn, y);
+            }
             break;
         }
         case 12:  // factor
@@ -1039,13 +1281,22 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             }
             {
                 const int M = 2 * cut_nodes(n);
-                const int64_t fsm = smem + (int64_t)(M * 2 * M + M) * 8;
-                if (fsm > 227 * 1024) {
-                    set_error("tk_subst_factor: n_u=%d needs %lld bytes of shared memory", n,
-                              (long long)fsm);
-                    return TK_ERR_UNSUPPORTED;
+                const int64_t gsm = (int64_t)(M * 2 * M + M) * 8;
+                const int64_t fsm = (smem ? smem : (int64_t)1 << 40) + gsm;
+                const int nst = V.sl.r1 - V.sl.r0 < Lv->n_steps ? V.sl.r1 - V.sl.r0 : Lv->n_steps;
+                if (fsm <= 227 * 1024) {
+                    tri_factor_kernel<NT, false><<<nst, th, fsm, s>>>(V, Lv->fac, nullptr);
+                } else {
+                    // node arrays in global scratch (large n): a persistent grid
+                    const int64_t per = (int64_t)kTriArrays * padded(n);
+                    const int grid = (int)(tri_scratch_len(Lv) / per);
+                    if (!Lv->scratch || grid < 1) {
+                        set_error("tk_subst_factor: n_u=%d needs the level's scratch buffer", n);
+                        return TK_ERR_ARG;
+                    }
+                    tri_factor_kernel<NT, true><<<grid < nst ? grid : nst, th, gsm, s>>>(
+                        V, Lv->fac, Lv->scratch);
                 }
-                tri_factor_kernel<NT><<<Lv->n_steps, th, fsm, s>>>(V, Lv->fac);
             }
             break;
         default: set_error("tri: bad op %d", op); return TK_ERR_ARG;
@@ -1074,8 +1325,8 @@ int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, dou
         else tri_apply<T_RESIDUAL><<<grid, th, 0, s>>>(V, b, x, y);
         return check_launch("tri_apply");
     }
-    if (tri_smem_bytes(n) == 0) {
-        set_error("tri family kernels support 2 <= n_u <= 1664 (got %d)", n);
+    if (n < 2 || n > 4096) {
+        set_error("tri family kernels support 2 <= n_u <= 4096 (got %d)", n);
         return TK_ERR_UNSUPPORTED;
     }
     switch (n) {
@@ -1084,6 +1335,7 @@ int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, dou
         case 256: return tri_launch_t<256>(Lv, op, b, x, y, omega, s);
         case 512: return tri_launch_t<512>(Lv, op, b, x, y, omega, s);
         case 1024: return tri_launch_t<1024>(Lv, op, b, x, y, omega, s);
+        case 2048: return tri_launch_t<2048>(Lv, op, b, x, y, omega, s);
         default: return tri_launch_t<0>(Lv, op, b, x, y, omega, s);
     }
 }

@@ -125,6 +125,7 @@ class StageBlocks:
     Qz_inv: Optional[torch.Tensor] = None
     kappa: float = 0.0
     qz_cr: Optional[torch.Tensor] = None
+    qz_w: Optional[torch.Tensor] = None
     host_weights: dict = field(default_factory=dict, repr=False)
     # time slab: global block rows [row0, row1) of a level with n_global steps
     # (row1 == 0: the whole level); K/C/B then hold stages [row0, min(row1, N)).
@@ -168,12 +169,19 @@ def _weights(family, q_mid, q_last, q_z, kappa):
                     Qz_inv=dev.to_device(np.linalg.inv(q_z)), kappa=0.0, qz_cr=None,
                     host_weights=hw)
     qz3 = np.ascontiguousarray(_tri_diags(q_z))
+    lib = _lib.load()
+    n = q_z.shape[0]
     cr = np.empty_like(qz3)
-    _lib.check(_lib.load().tk_cr_scalar_factor(q_z.shape[0], qz3.ctypes.data, cr.ctypes.data),
-               "tk_cr_scalar_factor")
+    _lib.check(lib.tk_cr_scalar_factor(n, qz3.ctypes.data, cr.ctypes.data), "tk_cr_scalar_factor")
+    # (active, active) block of Qz^{-1} at the cyclic-reduction cut, transposed:
+    # the inverse of the scalar system reduced onto the active nodes
+    a = int(lib.tk_tri_cut_nodes(n))
+    idx = np.empty(a, dtype=np.int32)
+    _lib.check(lib.tk_tri_cut_indices(n, idx.ctypes.data), "tk_tri_cut_indices")
+    qzw = np.ascontiguousarray(np.linalg.inv(q_z)[np.ix_(idx, idx)].T)
     return dict(Qm=dev.to_device(_tri_diags(q_mid)), Ql=dev.to_device(_tri_diags(q_last)),
                 Qz=dev.to_device(qz3), kappa=float(kappa), qz_cr=dev.to_device(cr),
-                host_weights=hw)
+                qz_w=dev.to_device(qzw), host_weights=hw)
 
 
 def _problem_weights(p: ProblemSpec, dt: float, n: int):
@@ -344,6 +352,19 @@ class BlockTriKKT:
         self.level.fac = self._fac.data_ptr()
         self.level.scratch = self._scratch.data_ptr()
         dev.call("tk_subst_factor", self.lref, dev.stream())
+        # TRI: the records also drive every D^{-1} (Jacobi, diagonal solve)
+        if self.stage.qz_w is not None and os.environ.get("TK_NO_RECORDS") != "1":
+            self.level.qz_w = self.stage.qz_w.data_ptr()
+
+    def ensure_records(self, force: bool = False) -> None:
+        """TRI levels whose node arrays do not fit in shared memory (n_u > 1664,
+        or ``force``/``TK_RECORDS_ALL=1``): precompute the per-interval factor
+        records once so that every local solve runs rhs-only.  Smaller levels
+        refactor on the fly, which moves fewer HBM bytes per sweep."""
+        if self.family != FAMILY_TRI:
+            return
+        if force or self.n_u > 1664 or os.environ.get("TK_RECORDS_ALL") == "1":
+            self.ensure_subst()
 
     @property
     def dim(self) -> int:

@@ -127,8 +127,9 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
     if restart < 1:
         raise ValueError("restart must be >= 1")
     if x0 is None:
-        x = dev.zeros(n)
         r = b.clone()                      # b - A*0, bitwise
+        x = torch.empty_like(b)
+        ops.scale_into(0.0, r, x)          # x = 0 (signed zeros add exactly)
     else:
         x = dev.to_device(x0).clone()
         if x.shape != (n,):
@@ -207,7 +208,8 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
             if Z is not None:
                 ops.gemv_t_add(Z, yt, x)
             else:
-                vy = dev.zeros(n)
+                vy = torch.empty_like(b)
+                ops.scale_into(0.0, V[0], vy)
                 ops.gemv_t_add(V, yt, vy)
                 ops.axpy(1.0, vy if prec is None else dev.to_device(prec(vy)), x)
         del V, Z
@@ -218,7 +220,7 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
             raise Breakdown("zero Arnoldi norm with nonzero residual")
         if true_norm <= target or total >= max_iters or broke:
             break
-    if not bool(torch.isfinite(x).all()):
+    if not math.isfinite(ops.nrm2(x)):
         raise NonFiniteValue("non-finite solution vector")
     final_rel = ops.nrm2(_residual(op, b, x)) / beta0
     report = SolveReport(iterations=total, residual_history=history,

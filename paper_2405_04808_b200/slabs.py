@@ -282,13 +282,16 @@ class CudaBackend:
     # level construction -------------------------------------------------
     def slab_level(self, p, dt, u, v, z, rows):
         from .kkt import BlockTriKKT, build_stage_blocks
-        return BlockTriKKT(build_stage_blocks(p, dt, u, v, z, rows=rows))
+        a = BlockTriKKT(build_stage_blocks(p, dt, u, v, z, rows=rows))
+        a.ensure_records()
+        return a
 
     def full_coarse(self, p, dt, u, v, z, coarse_tol, coarse_max_iters):
         from .kkt import DiagonalSolver, assemble_kkt, build_stage_blocks
         from .multigrid import MgHierarchy, MgLevel
         st = build_stage_blocks(p, dt, u, v, z)
         a = assemble_kkt(st)
+        a.ensure_records()
         return MgHierarchy(levels=[MgLevel(st.n_steps, dt, st, a, DiagonalSolver(a))],
                            transfers=[], coarse_tol=coarse_tol,
                            coarse_max_iters=coarse_max_iters)

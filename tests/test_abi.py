@@ -13,7 +13,7 @@ from conftest import ROOT, load_golden, product_problem, rel, CASES
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "tempokkt_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(tk_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|const char\*)\s+(tk_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_header():

@@ -1,0 +1,63 @@
+"""GPU vs oracle at spatial sizes that exercise every cyclic-reduction path:
+several CTA-wide and warp levels, the dense cut solve with more rows than
+threads, non-power-of-two n, and both the on-the-fly and the record-based
+local solves."""
+
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(n_u, n=16, theta=0.5, seed=0):
+    import paper_2405_04808_b200 as P
+    from oracle import tk_oracle as O
+    grid = P.TimeGrid(1.0, n)
+    p = P.build_burgers(P.BurgersConfig(n_elems=n_u + 1, theta=theta, u0_kind="sinstep"), grid)
+    op = O.burgers(n_u=n_u, nu=1e-2, alpha=0.1, theta=theta, u0_kind="sinstep")
+    rng = np.random.default_rng(seed)
+    u = P.forward_solve(p, np.zeros((n, n_u)), grid).states
+    v = u + 0.01 * rng.standard_normal(u.shape)
+    z = 0.1 * rng.standard_normal((n, n_u))
+    return P, O, p, op, grid, u, v, z, rng
+
+
+@pytest.mark.parametrize("n_u", [64, 100, 128, 256])
+@pytest.mark.parametrize("records", [False, True])
+def test_operator_and_smoothers(n_u, records):
+    P, O, p, op, grid, u, v, z, rng = _case(n_u)
+    st = P.build_stage_blocks(p, grid.dt, u, v, z)
+    a = P.assemble_kkt(st)
+    if records:
+        a.ensure_records(force=True)
+    ost = O.build_stages(op, grid.dt, u, v, z)
+    oa = O.Kkt(ost)
+    od = O.DiagSolve(oa)
+    x = rng.standard_normal(a.dim)
+    b = rng.standard_normal(a.dim)
+    assert rel(a.apply(x), oa.apply(x)) < 1e-13
+    assert rel(P.DiagonalSolver(a).solve_all(b), od.all(b)) < 1e-11
+    assert rel(P.jacobi_apply(a, None, b, x, 2), O.jacobi(oa, od, b, x, 2)) < 1e-11
+    assert rel(P.fgs_apply(a, None, b, x), O.fgs(oa, od, b, x)) < 1e-11
+    assert rel(P.bgs_apply(a, None, b, x), O.bgs(oa, od, b, x)) < 1e-11
+    assert rel(P.sgs_apply(a, None, b, x), O.sgs(oa, od, b, x)) < 1e-11
+
+
+@pytest.mark.parametrize("n_u", [64, 128])
+def test_cycle_and_solve(n_u):
+    P, O, p, op, grid, u, v, z, rng = _case(n_u, n=32)
+    h = P.build_hierarchy(p, u, v, z, grid, 3, sweeps=1, coarse_tol=1e-2)
+    oh = O.build_hierarchy(op, u, v, z, 32, grid.dt, 3, sweeps=1, coarse_tol=1e-2)
+    b = rng.standard_normal(h.levels[0].kkt.dim)
+    assert rel(P.cycle(h, 0, b), O.cycle(oh, 0, b)) < 1e-10
+    assert h.stats.iters == oh.coarse_iters
+    h.stats = type(h.stats)()
+    oh.coarse_iters = oh.coarse_calls = 0
+    x, rep = P.fgmres(h.levels[0].kkt.as_operator(), P.mg_preconditioner(h), b, rel_tol=1e-8,
+                      max_iters=60)
+    xo, orep = O.fgmres(oh.levels[0].kkt.apply, O.mg_prec(oh), b, rel_tol=1e-8, max_iters=60)
+    assert rep.iterations == orep.iterations
+    assert h.stats.iters == oh.coarse_iters
+    assert rel(x, xo) < 1e-10
