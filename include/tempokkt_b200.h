@@ -93,6 +93,15 @@ typedef struct tk_level {
      * (active, active) block of Q_z^{-1}).  Required once L->fac holds
      * factor records: D^{-1} then runs as an rhs-only solve. */
     const double* qz_w;
+    /* TRI: time-chunked coupling chain (see tk_chain_prod).  With chain_chunk
+     * = Lc > 0 and chain_prod filled by tk_chain_prod, the serial n_u-vector
+     * chain of the substitutions runs as: all chunks of Lc intervals in
+     * parallel from a zero start -> a short serial carry over the chunk ends
+     * with the precomputed chunk propagators -> all chunks again from their
+     * true start.  chain_chunk = 0: one serial chain. */
+    double* chain_prod;
+    int32_t chain_chunk;
+    int32_t chain_pad_;
 } tk_level;
 
 /* --- library ------------------------------------------------------------ */
@@ -134,6 +143,15 @@ int tk_subst_factor(const tk_level* L, void* stream);
  * the node indices (0-based) of the active nodes (host memory, out[cut_nodes]). */
 int32_t tk_tri_cut_nodes(int32_t n_u);
 int tk_tri_cut_indices(int32_t n_u, int32_t* out);
+/* TRI chunked chain: default chunk length for (n_u, n_steps) (0 = keep the
+ * chain serial), the size in doubles of L->chain_prod for L->chain_chunk, and
+ * the one-off computation of the chunk propagators Pi_c = T_hi-1 ... T_lo
+ * (T_i: u_{i-1} -> u_i of the homogeneous forward chain; the backward chain
+ * uses Pi_c^T since the local (u,lam) systems are symmetric).  Needs L->fac
+ * (tk_subst_factor) first. */
+int32_t tk_chain_chunk_default(int32_t n_u, int32_t n_steps);
+int64_t tk_chain_prod_len(const tk_level* L);
+int tk_chain_prod(const tk_level* L, void* stream);
 
 /* --- transfers (multigrid.py:272-300) ------------------------------------- */
 /* xc = R xf  (injection for u,v,lam,mu; 2-interval average for z)    restrict_kkt multigrid.py:272 */

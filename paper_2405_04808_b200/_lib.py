@@ -39,6 +39,7 @@ class TkLevel(C.Structure):
         ("fac", _p), ("scratch", _p),
         ("row0", _i32), ("row1", _i32), ("halo_u", _p), ("halo_mu", _p),
         ("qz_w", _p),
+        ("chain_prod", _p), ("chain_chunk", _i32), ("chain_pad_", _i32),
     ]
 
 
@@ -58,6 +59,9 @@ _SIGS = {
     "tk_subst_scratch_len": (_i64, [C.POINTER(TkLevel)]),
     "tk_subst_factor": (C.c_int, [C.POINTER(TkLevel), _p]),
     "tk_tri_cut_nodes": (_i32, [_i32]),
+    "tk_chain_chunk_default": (_i32, [_i32, _i32]),
+    "tk_chain_prod_len": (_i64, [C.POINTER(TkLevel)]),
+    "tk_chain_prod": (C.c_int, [C.POINTER(TkLevel), _p]),
     "tk_tri_cut_indices": (C.c_int, [_i32, _p]),
     "tk_restrict": (C.c_int, [_i32, _i32, _i32, _p, _p, _p]),
     "tk_prolong_add": (C.c_int, [_i32, _i32, _i32, _p, _p, _p]),

@@ -31,6 +31,8 @@ int64_t tri_scratch_len(const tk_level*);
 int64_t dense_fac_len(const tk_level*);
 int32_t tri_cut_nodes(int n);
 int32_t tri_cut_level(int n);
+int32_t tri_chain_chunk_default(int n, int N);
+int64_t tri_chain_prod_len(const tk_level*);
 int64_t dense_scratch_len(const tk_level*);
 int transfer_launch(int, int, int, int, int, int, const double*, const double*, const double*,
                     double*, cudaStream_t);
@@ -152,6 +154,25 @@ int64_t tk_subst_scratch_len(const tk_level* L) {
 
 int tk_subst_factor(const tk_level* L, void* stream) {
     return level_op(L, 12, 12, nullptr, nullptr, nullptr, 1.0, stream);
+}
+
+int32_t tk_chain_chunk_default(int32_t n_u, int32_t n_steps) {
+    return tri_chain_chunk_default(n_u, n_steps);
+}
+
+int64_t tk_chain_prod_len(const tk_level* L) {
+    if (check_level(L)) return -1;
+    return L->family == TK_FAMILY_TRI ? tri_chain_prod_len(L) : 0;
+}
+
+int tk_chain_prod(const tk_level* L, void* stream) {
+    int rc = check_level(L);
+    if (rc) return rc;
+    if (L->family != TK_FAMILY_TRI) {
+        set_error("tk_chain_prod: only the TRI family chunks its chain");
+        return TK_ERR_UNSUPPORTED;
+    }
+    return tri_launch(L, 13, nullptr, nullptr, nullptr, 1.0, as_stream(stream));
 }
 
 int32_t tk_tri_cut_nodes(int32_t n_u) { return n_u >= 1 ? tri_cut_nodes(n_u) : 0; }

@@ -21,6 +21,11 @@
 // the cyclic-reduction level loops unroll.
 #include "tk_common.cuh"
 
+#include <cooperative_groups.h>
+#include <math.h>
+
+namespace cg = cooperative_groups;
+
 namespace tk {
 
 __host__ __device__ __forceinline__ constexpr int PI(int j) { return j + (j >> 4); }
@@ -800,14 +805,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         : "memory");
 }
 
-// Serial coupling chain (one CTA).  FWD: chain[i] = u_i, BWD: chain[i] = mu_i.
+// Coupling chain over the steps of one time chunk (one CTA per chunk).
+// FWD: chain[i] = u_i, BWD: chain[i] = mu_i; step k handles interval
+// FWD ? 1+k : N-1-k.  The chunks partition the intervals 1..N-1 into runs of
+// Lc (the same runs in both directions, so the backward chunk propagator is
+// the transpose of the forward one); chunk c = cbase + blockIdx.x.  The chunk
+// holding step 0 starts from the seed a_{i0} (and writes chain[i0]); the
+// others start from starts[c*n] (zero when starts is null).  ends != null:
+// the chunk's last value goes to ends[c*n].  HOM: homogeneous chain (a = 0)
+// from the unit vector e_y (y = blockIdx.y); its end value is column y of the
+// chunk propagator Pi_c, written to ends[(c*n + y)*n] (row y of Pi_c^T).
 // `a` = D^{-1} r from pass 1.  STAGED: the next interval's record and
 // a-segment are TMA bulk-copied into the other half of a double buffer while
 // the current interval is solved.  The output of step k and the right-hand
 // side of step k+1 are formed in one pass (two ping-pong rhs buffers).
-template <bool FWD, bool STAGED, int NT>
+template <bool FWD, bool STAGED, bool HOM, int NT>
 __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
-                                 const double* __restrict__ fac, double* __restrict__ chain) {
+                                 const double* __restrict__ fac, double* __restrict__ chain,
+                                 int Lc, int cbase, const double* __restrict__ starts,
+                                 double* __restrict__ ends) {
     extern __shared__ __align__(16) double sm[];
     __shared__ __align__(8) uint64_t bars[2];
     const Lay& L = V.lay;
@@ -820,16 +836,27 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
     double* fbase = STAGED ? sm + 2 * brec : sm;
     double* fr[2] = {fbase, fbase + 2 * np};
     const int K = N - 1;  // chain steps after the seed
+    const int c = cbase + blockIdx.x;
+    const int lo = c * Lc, hi = min(K, lo + Lc);
+    const int k0 = FWD ? lo : K - hi, k1 = FWD ? hi : K - lo;
+    const bool seed = !HOM && k0 == 0;
     auto blk = [&](int k) { return FWD ? 1 + k : N - 1 - k; };
     auto aseg = [&](int i) { return a + (FWD ? L.off_u(i) : L.off_mu(i)); };
     auto record = [&](int k) -> const double* {
-        return STAGED ? ((k & 1) ? buf1 : buf0) : fac + (size_t)blk(k) * rec;
+        return STAGED ? (((k - k0) & 1) ? buf1 : buf0) : fac + (size_t)blk(k) * rec;
     };
     auto aval = [&](int k) -> const double* { return STAGED ? record(k) + rec : aseg(blk(k)); };
     const int i0 = FWD ? 0 : N;
-    const double* s0 = aseg(i0);
-    for (int j = tid; j < n; j += nth) chain[(size_t)i0 * n + j] = s0[j];
-    if (K <= 0) return;
+    const double* s0 = seed ? aseg(i0) : (HOM ? nullptr : (starts ? starts + (size_t)c * n : nullptr));
+    const int ey = blockIdx.y;
+    auto startv = [&](int j) -> double {
+        if (HOM) return j == ey ? 1.0 : 0.0;
+        return s0 ? s0[j] : 0.0;
+    };
+    if (seed) {
+        for (int j = tid; j < n; j += nth) chain[(size_t)i0 * n + j] = s0[j];
+    }
+    if (k0 >= k1) return;
     const int pt = nth - 1;        // the thread issuing the TMA prefetches
     if (STAGED && tid == pt) {
         mbar_init(&bars[0], 1);
@@ -838,75 +865,82 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
     }
     __syncthreads();
     auto prefetch = [&](int k) {
-        double* b = (k & 1) ? buf1 : buf0;
-        uint64_t* bar = &bars[k & 1];
+        const int t = k - k0;
+        double* b = (t & 1) ? buf1 : buf0;
+        uint64_t* bar = &bars[t & 1];
         const int i = blk(k);
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        mbar_expect_tx(bar, (unsigned)(brec * sizeof(double)));
+        mbar_expect_tx(bar, (unsigned)((HOM ? rec : brec) * sizeof(double)));
         tma_g2s(b, fac + (size_t)i * rec, (unsigned)(rec * sizeof(double)), bar);
-        tma_g2s(b + rec, aseg(i), (unsigned)(n * sizeof(double)), bar);
+        if (!HOM) tma_g2s(b + rec, aseg(i), (unsigned)(n * sizeof(double)), bar);
     };
-    if (STAGED && tid == pt) prefetch(0);
+    if (STAGED && tid == pt) prefetch(k0);
     if (STAGED) mbar_wait(&bars[0], 0u);
-    {   // right-hand side of step 0 from the seed
-        const double* fb = record(0);
+    {   // right-hand side of the first step from the start vector
+        const double* fb = record(k0);
         const double *Cs = fb + 11 * n, *Cd = fb + 12 * n, *Cp = fb + 13 * n;
         double* f0 = fr[0];
         double* f1 = f0 + np;
         for (int j = tid; j < n; j += nth) {
             const int J = PI(j);
             if (FWD) {
-                double cv = Cd[j] * s0[j];
-                if (j > 0) cv += Cs[j] * s0[j - 1];
-                if (j < n - 1) cv += Cp[j] * s0[j + 1];
+                double cv = Cd[j] * startv(j);
+                if (j > 0) cv += Cs[j] * startv(j - 1);
+                if (j < n - 1) cv += Cp[j] * startv(j + 1);
                 f0[J] = 0.0;
                 f1[J] = -cv;
             } else {
-                f0[J] = -s0[j];
+                f0[J] = -startv(j);
                 f1[J] = 0.0;
             }
         }
     }
     __syncthreads();
-    for (int k = 0; k < K; ++k) {
+    double* eout = ends ? (HOM ? ends + ((size_t)c * n + ey) * n : ends + (size_t)c * n) : nullptr;
+    for (int k = k0; k < k1; ++k) {
+        const int t = k - k0;
         const int i = blk(k);
-        const bool prof = (k == K / 2);
+        const bool prof = !HOM && (k == K / 2);
         TKP(0, prof);
-        if (STAGED && tid == pt && k + 1 < K) prefetch(k + 1);
+        if (STAGED && tid == pt && k + 1 < k1) prefetch(k + 1);
         const double* fb = record(k);
-        const double* ai = aval(k);
-        double* f0 = fr[k & 1];
+        const double* ai = HOM ? nullptr : aval(k);
+        double* f0 = fr[t & 1];
         double* f1 = f0 + np;
         TKP(1, prof);
         cr_rhs(n, fb, f0, fbase + 4 * np, prof);
-        const bool more = k + 1 < K;
-        if (STAGED && more) mbar_wait(&bars[(k + 1) & 1], (unsigned)(((k + 1) >> 1) & 1));
+        const bool more = k + 1 < k1;
+        if (STAGED && more) mbar_wait(&bars[(t + 1) & 1], (unsigned)(((t + 1) >> 1) & 1));
         const double* fbn = more ? record(k + 1) : fb;
-        double* g0 = fr[(k + 1) & 1];
+        double* g0 = fr[(t + 1) & 1];
         double* g1 = g0 + np;
         const double *Cs = fb + 11 * n, *Cd = fb + 12 * n, *Cp = fb + 13 * n;
         const double *Ns = fbn + 11 * n, *Nd = fbn + 12 * n, *Np = fbn + 13 * n;
         for (int j = tid; j < n; j += nth) {
             const int J = PI(j);
             if (FWD) {   // u_i = a + u-part; next rhs (0, -C_{i+1} u_i)
-                const double val = ai[j] + f0[J];
-                chain[(size_t)i * n + j] = val;
+                const double val = HOM ? f0[J] : ai[j] + f0[J];
+                if (!HOM) chain[(size_t)i * n + j] = val;
                 if (more) {
                     double cv = Nd[j] * val;
-                    if (j > 0) cv += Ns[j] * (ai[j - 1] + f0[PI(j - 1)]);
-                    if (j < n - 1) cv += Np[j] * (ai[j + 1] + f0[PI(j + 1)]);
+                    if (j > 0) cv += Ns[j] * (HOM ? f0[PI(j - 1)] : ai[j - 1] + f0[PI(j - 1)]);
+                    if (j < n - 1) cv += Np[j] * (HOM ? f0[PI(j + 1)] : ai[j + 1] + f0[PI(j + 1)]);
                     g0[J] = 0.0;
                     g1[J] = -cv;
+                } else if (eout) {
+                    eout[j] = val;
                 }
             } else {     // mu_i = a + C^T lam; next rhs (-mu_i, 0)
                 double ct = Cd[j] * f1[J];
                 if (j > 0) ct += Cp[j - 1] * f1[PI(j - 1)];
                 if (j < n - 1) ct += Cs[j + 1] * f1[PI(j + 1)];
-                const double val = ai[j] + ct;
-                chain[(size_t)i * n + j] = val;
+                const double val = HOM ? ct : ai[j] + ct;
+                if (!HOM) chain[(size_t)i * n + j] = val;
                 if (more) {
                     g0[J] = -val;
                     g1[J] = 0.0;
+                } else if (eout) {
+                    eout[j] = val;
                 }
             }
         }
@@ -914,6 +948,86 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
         __syncthreads();
         TKP(6, prof);
     }
+}
+
+// Serial carry over the chunk ends (one cluster of kCarryCtas CTAs):
+//   U = ends[first];  for each next chunk c in chain order:
+//     starts[c] = U;  U = ends[c] + M_c U
+// with M_c = Pi_c (forward) or Pi_c^T (backward), row-major n x n.  Each CTA
+// owns a block of rows of the matvec; the new U is broadcast into every CTA's
+// shared copy through distributed shared memory (ping-pong buffers), one
+// cluster barrier per chunk.
+static constexpr int kCarryCtas = 8;
+template <bool FWD>
+__global__ void __cluster_dims__(kCarryCtas, 1, 1) __launch_bounds__(1024, 1)
+    tri_chain_carry(int n, int nc, const double* __restrict__ M, const double* __restrict__ ends,
+                    double* __restrict__ starts) {
+    extern __shared__ __align__(16) double sm[];   // U ping-pong [2][n]
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int rpc = (n + kCarryCtas - 1) / kCarryCtas;
+    const int r0 = rank * rpc, r1 = min(n, r0 + rpc);
+    const int first = FWD ? 0 : nc - 1;
+    for (int j = tid; j < n; j += blockDim.x) sm[j] = ends[(size_t)first * n + j];
+    cl.sync();
+    for (int t = 1; t < nc; ++t) {
+        const int c = FWD ? t : nc - 1 - t;
+        const double* cur = sm + ((t - 1) & 1) * n;
+        double* nxt = sm + (t & 1) * n;
+        for (int j = r0 + tid; j < r1; j += blockDim.x) starts[(size_t)c * n + j] = cur[j];
+        if (t == nc - 1) break;
+        const double* Mc = M + (size_t)c * n * n;
+        const double* ec = ends + (size_t)c * n;
+        for (int r = r0 + warp; r < r1; r += nw) {
+            const double* row = Mc + (size_t)r * n;
+            double acc = 0.0;
+            for (int k = lane; k < n; k += 32) acc = fma(row[k], cur[k], acc);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane < kCarryCtas) {
+                double* dst = cl.map_shared_rank(nxt, lane);
+                dst[r] = ec[r] + acc;
+            }
+        }
+        cl.sync();
+    }
+}
+
+// out[b][c][r] = in[b][r][c] for count n x n matrices
+__global__ void tri_transpose(const double* __restrict__ in, double* __restrict__ out, int n) {
+    __shared__ double tile[32][33];
+    const size_t off = (size_t)blockIdx.z * n * n;
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int gr = by + r, gc = bx + threadIdx.x;
+        if (gr < n && gc < n) tile[r][threadIdx.x] = in[off + (size_t)gr * n + gc];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int gr = bx + r, gc = by + threadIdx.x;
+        if (gr < n && gc < n) out[off + (size_t)gr * n + gc] = tile[threadIdx.x][r];
+    }
+}
+
+int32_t tri_chain_chunk_default(int n, int N) {
+    const int K = N - 1;
+    if (n < 2 || K < 24) return 0;
+    int lc = (int)ceil(sqrt(K / 2.0));
+    const int need = (K + 147) / 148;    // at most one chunk per SM
+    if (lc < need) lc = need;
+    if (lc < 4) lc = 4;
+    return lc;
+}
+static int chain_nc(int N, int Lc) {
+    const int K = N - 1;
+    if (Lc <= 0 || K <= 0) return 1;
+    return (K + Lc - 1) / Lc;
+}
+int64_t tri_chain_prod_len(const tk_level* Lv) {
+    if (Lv->chain_chunk <= 0) return 0;
+    const int64_t n = Lv->n_u, nc = chain_nc(Lv->n_steps, Lv->chain_chunk);
+    return 2 * nc * n * n + 2 * nc * n;
 }
 
 // ---------------------------------------------------------------------------
@@ -1206,14 +1320,19 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                              cudaSharedmemCarveoutMaxShared);
         // the chain kernels also hold two static mbarriers
         const int mxc = mx - 1024;
-        cudaFuncSetAttribute(tri_chain_kernel<true, true, NT>,
+        cudaFuncSetAttribute(tri_chain_kernel<true, true, false, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
-        cudaFuncSetAttribute(tri_chain_kernel<false, true, NT>,
+        cudaFuncSetAttribute(tri_chain_kernel<false, true, false, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
-        cudaFuncSetAttribute(tri_chain_kernel<true, false, NT>,
+        cudaFuncSetAttribute(tri_chain_kernel<true, false, false, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
-        cudaFuncSetAttribute(tri_chain_kernel<false, false, NT>,
+        cudaFuncSetAttribute(tri_chain_kernel<false, false, false, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
+        cudaFuncSetAttribute(tri_chain_kernel<true, false, true, NT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, mxc);
+        cudaFuncSetAttribute(tri_chain_kernel<true, false, true, NT>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_status(e, "tri: cudaFuncSetAttribute");
         attr_done = true;
@@ -1247,7 +1366,7 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             // pass 1: a = D^{-1} r into y
             if (rec) tri_rows_rec<NT><<<rows, rth, rsm, s>>>(V, b, nullptr, y, 1.0);
             else tri_rows<NT><<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
-            // pass 2: serial chain on the coupling vector
+            // pass 2: the chain on the coupling vector (serial, or time-chunked)
             const int cth = tri_chain_threads(n);
             const int np = padded(n);
             const int64_t staged = (int64_t)(2 * (fac_record(n) + n) + 4 * np + 256) * 8;
@@ -1255,14 +1374,36 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             // TMA bulk copies need 16-byte aligned sources and sizes: n even and
             // even segment offsets (always true for the Burgers layout, nz == nu)
             const bool aligned = (n % 2 == 0) && (Lv->n_z % 2 == 0);
+            const bool stg = aligned && staged <= 227 * 1024 - 1024;
+            const int64_t csm = stg ? staged : direct;
             double* fac = Lv->fac;
             double* chn = Lv->scratch;
-            if (aligned && staged <= 227 * 1024 - 1024) {
-                if (fwd) tri_chain_kernel<true, true, NT><<<1, cth, staged, s>>>(V, y, fac, chn);
-                else tri_chain_kernel<false, true, NT><<<1, cth, staged, s>>>(V, y, fac, chn);
+            const int N = Lv->n_steps;
+            const bool chunked = Lv->chain_prod != nullptr && Lv->chain_chunk > 0;
+            const int Lc = chunked ? Lv->chain_chunk : (N > 1 ? N - 1 : 1);
+            const int nc = chain_nc(N, Lc);
+            double* P = Lv->chain_prod;
+            double* PT = chunked ? P + (size_t)nc * n * n : nullptr;
+            double* E = chunked ? PT + (size_t)nc * n * n : nullptr;
+            double* S = chunked ? E + (size_t)nc * n : nullptr;
+            auto chain_launch = [&](int grid, int cbase, const double* st, double* en) {
+                if (grid <= 0) return;
+                if (stg) {
+                    if (fwd) tri_chain_kernel<true, true, false, NT><<<grid, cth, csm, s>>>(V, y, fac, chn, Lc, cbase, st, en);
+                    else tri_chain_kernel<false, true, false, NT><<<grid, cth, csm, s>>>(V, y, fac, chn, Lc, cbase, st, en);
+                } else {
+                    if (fwd) tri_chain_kernel<true, false, false, NT><<<grid, cth, csm, s>>>(V, y, fac, chn, Lc, cbase, st, en);
+                    else tri_chain_kernel<false, false, false, NT><<<grid, cth, csm, s>>>(V, y, fac, chn, Lc, cbase, st, en);
+                }
+            };
+            if (!chunked || nc == 1) {
+                chain_launch(1, 0, nullptr, nullptr);
             } else {
-                if (fwd) tri_chain_kernel<true, false, NT><<<1, cth, direct, s>>>(V, y, fac, chn);
-                else tri_chain_kernel<false, false, NT><<<1, cth, direct, s>>>(V, y, fac, chn);
+                chain_launch(nc, 0, nullptr, E);                 // all chunks from zero
+                const int64_t usm = (int64_t)2 * n * 8;
+                if (fwd) tri_chain_carry<true><<<kCarryCtas, 1024, usm, s>>>(n, nc, P, E, S);
+                else tri_chain_carry<false><<<kCarryCtas, 1024, usm, s>>>(n, nc, PT, E, S);
+                chain_launch(nc - 1, fwd ? 1 : 0, S, nullptr);   // non-seed chunks again
             }
             // pass 3: parallel solves with the chain coupling
             if (rec) {
@@ -1299,6 +1440,23 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                 }
             }
             break;
+        case 13: {  // chunk propagators Pi_c (c = 1..nc-2) and their transposes
+            if (!Lv->fac || !Lv->chain_prod || Lv->chain_chunk <= 0) {
+                set_error("tk_chain_prod: needs fac, chain_prod and chain_chunk > 0");
+                return TK_ERR_ARG;
+            }
+            const int N = Lv->n_steps, Lc = Lv->chain_chunk, nc = chain_nc(N, Lc);
+            if (nc <= 2) break;
+            double* P = Lv->chain_prod;
+            double* PT = P + (size_t)nc * n * n;
+            const int cth = tri_chain_threads(n);
+            const int64_t direct = (int64_t)(4 * padded(n) + 256) * 8;
+            dim3 g(nc - 2, n);
+            tri_chain_kernel<true, false, true, NT><<<g, cth, direct, s>>>(V, nullptr, Lv->fac, nullptr, Lc, 1, nullptr, PT);
+            dim3 tg((n + 31) / 32, (n + 31) / 32, nc);
+            tri_transpose<<<tg, dim3(32, 8), 0, s>>>(PT, P, n);
+            break;
+        }
         default: set_error("tri: bad op %d", op); return TK_ERR_ARG;
     }
     return check_launch("tri_rows");

@@ -323,6 +323,7 @@ class BlockTriKKT:
         self.lref = C.byref(self.level)
         self._fac = None
         self._scratch = None
+        self._chain = None
 
     # --- slab geometry (local offsets of the boundary segments) -------------
     def seg_offset(self, kind: str, row: int) -> int:
@@ -338,10 +339,19 @@ class BlockTriKKT:
         return start + off
 
     def ensure_subst(self) -> None:
-        """Precompute the Gauss-Seidel chain factors once (tk_subst_factor);
-        afterwards tk_forward_subst / tk_backward_subst run as parallel solve
-        -> serial coupling chain -> parallel solve.  ``TK_SERIAL_SUBST=1``
-        keeps the plain serial kernels (used by tests to cross-check)."""
+        """Precompute the Gauss-Seidel chain data once: the per-interval factor
+        records (tk_subst_factor) and, for TRI levels long enough to gain from
+        it, the time-chunk propagators of the coupling chain (tk_chain_prod).
+        Afterwards tk_forward_subst / tk_backward_subst run as parallel solve
+        -> (chunked) coupling chain -> parallel solve.  ``TK_SERIAL_SUBST=1``
+        keeps the plain serial kernels (used by tests to cross-check);
+        ``TK_CHAIN_CHUNK=Lc`` overrides the chunk length (0: serial chain)."""
+        if os.environ.get("TK_SERIAL_SUBST") == "1":
+            return
+        self._ensure_fac()
+        self._ensure_chain()
+
+    def _ensure_fac(self) -> None:
         if self._fac is not None or os.environ.get("TK_SERIAL_SUBST") == "1":
             return
         lib = _lib.load()
@@ -356,6 +366,21 @@ class BlockTriKKT:
         if self.stage.qz_w is not None and os.environ.get("TK_NO_RECORDS") != "1":
             self.level.qz_w = self.stage.qz_w.data_ptr()
 
+    def _ensure_chain(self) -> None:
+        if self._chain is not None or self.family != FAMILY_TRI or self.is_slab:
+            return
+        lib = _lib.load()
+        env = os.environ.get("TK_CHAIN_CHUNK")
+        lc = int(env) if env is not None else int(lib.tk_chain_chunk_default(self.n_u, self.n_steps))
+        self._chain = ()
+        if lc <= 0:
+            return
+        self.level.chain_chunk = lc
+        n = int(lib.tk_chain_prod_len(self.lref))
+        self._chain = dev.empty(max(n, 1))
+        self.level.chain_prod = self._chain.data_ptr()
+        dev.call("tk_chain_prod", self.lref, dev.stream())
+
     def ensure_records(self, force: bool = False) -> None:
         """TRI levels whose node arrays do not fit in shared memory (n_u > 1664,
         or ``force``/``TK_RECORDS_ALL=1``): precompute the per-interval factor
@@ -364,7 +389,7 @@ class BlockTriKKT:
         if self.family != FAMILY_TRI:
             return
         if force or self.n_u > 1664 or os.environ.get("TK_RECORDS_ALL") == "1":
-            self.ensure_subst()
+            self._ensure_fac()
 
     @property
     def dim(self) -> int:

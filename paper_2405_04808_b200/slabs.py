@@ -292,6 +292,7 @@ class CudaBackend:
         st = build_stage_blocks(p, dt, u, v, z)
         a = assemble_kkt(st)
         a.ensure_records()
+        a.ensure_subst()
         return MgHierarchy(levels=[MgLevel(st.n_steps, dt, st, a, DiagonalSolver(a))],
                            transfers=[], coarse_tol=coarse_tol,
                            coarse_max_iters=coarse_max_iters)

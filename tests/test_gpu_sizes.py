@@ -61,3 +61,43 @@ def test_cycle_and_solve(n_u):
     assert rep.iterations == orep.iterations
     assert h.stats.iters == oh.coarse_iters
     assert rel(x, xo) < 1e-10
+
+
+@pytest.mark.parametrize("lc", [1, 3, 4, 7, 31, 62, 63, 100])
+def test_chunked_chain(lc, monkeypatch):
+    """Time-chunked coupling chain (zero-start chunks -> carry with the chunk
+    propagators -> re-run) against the oracle's serial substitutions, for
+    chunk lengths giving one, two, and many chunks and a ragged last chunk."""
+    monkeypatch.setenv("TK_CHAIN_CHUNK", str(lc))
+    P, O, p, op, grid, u, v, z, rng = _case(64, n=64)
+    st = P.build_stage_blocks(p, grid.dt, u, v, z)
+    a = P.assemble_kkt(st)
+    a.ensure_subst()
+    assert a.level.chain_chunk == lc
+    oa = O.Kkt(O.build_stages(op, grid.dt, u, v, z))
+    od = O.DiagSolve(oa)
+    x = rng.standard_normal(a.dim)
+    b = rng.standard_normal(a.dim)
+    assert rel(P.fgs_apply(a, None, b, x), O.fgs(oa, od, b, x)) < 1e-11
+    assert rel(P.bgs_apply(a, None, b, x), O.bgs(oa, od, b, x)) < 1e-11
+    assert rel(P.sgs_apply(a, None, b, x), O.sgs(oa, od, b, x)) < 1e-11
+
+
+def test_chunked_coarse_cycle():
+    """Default chunking on a 64-interval coarse level inside a V-cycle and
+    the preconditioned FGMRES: same coarse and outer iteration counts."""
+    P, O, p, op, grid, u, v, z, rng = _case(64, n=128)
+    h = P.build_hierarchy(p, u, v, z, grid, 2, sweeps=1, coarse_tol=1e-2)
+    assert h.levels[-1].kkt.level.chain_chunk > 0
+    oh = O.build_hierarchy(op, u, v, z, 128, grid.dt, 2, sweeps=1, coarse_tol=1e-2)
+    b = rng.standard_normal(h.levels[0].kkt.dim)
+    assert rel(P.cycle(h, 0, b), O.cycle(oh, 0, b)) < 1e-10
+    assert h.stats.iters == oh.coarse_iters
+    h.stats = type(h.stats)()
+    oh.coarse_iters = oh.coarse_calls = 0
+    x, rep = P.fgmres(h.levels[0].kkt.as_operator(), P.mg_preconditioner(h), b, rel_tol=1e-8,
+                      max_iters=40)
+    xo, orep = O.fgmres(oh.levels[0].kkt.apply, O.mg_prec(oh), b, rel_tol=1e-8, max_iters=40)
+    assert rep.iterations == orep.iterations
+    assert h.stats.iters == oh.coarse_iters
+    assert rel(x, xo) < 1e-10
