@@ -90,8 +90,8 @@ typedef struct tk_level {
     const double* halo_mu;
     /* TRI: transposed dense inverse of the scalar Q_z system reduced to the
      * cyclic-reduction cut level (tk_tri_cut_nodes(n_u)^2 doubles, i.e. the
-     * (active, active) block of Q_z^{-1}).  Required once L->fac holds
-     * factor records: D^{-1} then runs as an rhs-only solve. */
+     * (active, active) block of Q_z^{-1}).  Required by every TRI local
+     * solve; with factor records in L->fac, D^{-1} runs rhs-only. */
     const double* qz_w;
     /* TRI: time-chunked coupling chain (see tk_chain_prod).  With chain_chunk
      * = Lc > 0 and chain_prod filled by tk_chain_prod, the serial n_u-vector
@@ -101,8 +101,13 @@ typedef struct tk_level {
      * true start.  chain_chunk = 0: one serial chain. */
     double* chain_prod;
     int32_t chain_chunk;
-    int32_t chain_pad_;
+    /* TK_FLAG_ONTHEFLY: TRI local solves (Jacobi, diagonal solve, the
+     * parallel passes of the substitutions) refactor on the fly even when
+     * L->fac holds factor records. */
+    int32_t flags;
 } tk_level;
+
+#define TK_FLAG_ONTHEFLY 1
 
 /* --- library ------------------------------------------------------------ */
 const char* tk_version(void);

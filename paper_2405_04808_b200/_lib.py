@@ -28,6 +28,9 @@ _i32 = C.c_int32
 _i64 = C.c_int64
 
 
+TK_FLAG_ONTHEFLY = 1
+
+
 class TkLevel(C.Structure):
     """Mirror of ``struct tk_level`` (include/tempokkt_b200.h)."""
     _fields_ = [
@@ -39,7 +42,7 @@ class TkLevel(C.Structure):
         ("fac", _p), ("scratch", _p),
         ("row0", _i32), ("row1", _i32), ("halo_u", _p), ("halo_mu", _p),
         ("qz_w", _p),
-        ("chain_prod", _p), ("chain_chunk", _i32), ("chain_pad_", _i32),
+        ("chain_prod", _p), ("chain_chunk", _i32), ("flags", _i32),
     ]
 
 

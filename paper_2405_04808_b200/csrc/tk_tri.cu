@@ -23,6 +23,7 @@
 
 #include <cooperative_groups.h>
 #include <math.h>
+#include <string.h>
 
 namespace cg = cooperative_groups;
 
@@ -35,6 +36,23 @@ __host__ __device__ __forceinline__ constexpr int ilog2(int n) {
 }
 
 static constexpr int kMaxLev = 12;   // n <= 4096
+
+static constexpr int kFacRows = 14;
+
+// Cut level c of the chain's cyclic reduction: levels below c run as usual;
+// the reduced system on the A = n >> c <= 32 active nodes left at level c is
+// solved with its precomputed dense inverse W (2A x 2A, stored transposed).
+__host__ __device__ __forceinline__ constexpr int cut_level(int n) {
+    int c = 0;
+    while ((n >> c) > 32) ++c;
+    return c;
+}
+__host__ __device__ __forceinline__ constexpr int cut_nodes(int n) { return n >> cut_level(n); }
+// doubles per interval record: P, M1, M2 (levels < c, level order), C, W^T
+__host__ __device__ __forceinline__ constexpr int fac_record(int n) {
+    return kFacRows * n + 4 * cut_nodes(n) * cut_nodes(n);
+}
+
 
 struct TView {
     Lay lay;
@@ -249,59 +267,205 @@ struct CrSolve {
     }
 };
 
+// One CTA-wide cyclic-reduction level (factorisation + rhs) with a single
+// barrier.  Kept node j = 2s-1+2sm eliminates both neighbours p = j-s and
+// q = j+s itself (each pivot is inverted by the two kept nodes that border
+// it), so no separate elimination phase is needed.  j records for its upper
+// neighbour q the lower coupling L_q = E_j (before updating E_j) and, after
+// the barrier (when nobody reads the raw pivot any more), the inverse P_q in
+// q's D slot; kept node m = 0 does the same for p = s-1.  The scalar Q_z
+// reduction of fw rides along with the precomputed coefficients cr.
+template <int KPT>
+__device__ __forceinline__ void cr_level(const TriSm& S, int n, int lev,
+                                         const double* __restrict__ cr) {
+    const double* cinv = cr;
+    const double* cup = cr + n;
+    const double* clo = cr + 2 * n;
+    const int s = 1 << lev, tid = threadIdx.x, nth = blockDim.x;
+    const int ck = kept_count(n, lev);
+    double qa[KPT], qb[KPT], qc[KPT];
+    int qi[KPT];
+    double p0a = 0.0, p0b = 0.0, p0c = 0.0;
+    int p0i = -1;
+#pragma unroll
+    for (int t = 0; t < KPT; ++t) {
+        qi[t] = -1;
+        qa[t] = qb[t] = qc[t] = 0.0;
+        const int m = tid + t * nth;
+        if (m < ck) {
+            const int j = 2 * s - 1 + 2 * s * m, p = j - s, q = j + s;
+            const int J = PI(j), P = PI(p);
+            double pa, pb, pc;
+            {
+                const double a = S.Da()[P], b = S.Db()[P], c = S.Dc()[P];
+                const double id = 1.0 / (a * c - b * b);
+                pa = c * id; pb = -b * id; pc = a * id;
+            }
+            if (m == 0) {
+                p0a = pa; p0b = pb; p0c = pc; p0i = P;
+                S.L0()[P] = 0.0; S.L1()[P] = 0.0; S.L2()[P] = 0.0; S.L3()[P] = 0.0;
+            }
+            double da = S.Da()[J], db = S.Db()[J], dc = S.Dc()[J];
+            double g0 = S.f0()[J], g1 = S.f1()[J];
+            double w = S.fw()[J] - cup[p] * cinv[p] * S.fw()[P];
+            {   // lower neighbour p: coupling E_p (row p, col j)
+                const double e0 = S.E0()[P], e1 = S.E1()[P], e2 = S.E2()[P], e3 = S.E3()[P];
+                const double t00 = e0 * pa + e2 * pb, t01 = e0 * pb + e2 * pc;
+                const double t10 = e1 * pa + e3 * pb, t11 = e1 * pb + e3 * pc;
+                da -= t00 * e0 + t01 * e2;
+                db -= t00 * e1 + t01 * e3;
+                dc -= t10 * e1 + t11 * e3;
+                const double h0 = S.f0()[P], h1 = S.f1()[P];
+                g0 -= t00 * h0 + t01 * h1;
+                g1 -= t10 * h0 + t11 * h1;
+            }
+            double n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0;
+            if (q < n) {   // upper neighbour q: coupling E_j (row j, col q)
+                const int Qi = PI(q);
+                double xa, xb, xc;
+                {
+                    const double a = S.Da()[Qi], b = S.Db()[Qi], c = S.Dc()[Qi];
+                    const double id = 1.0 / (a * c - b * b);
+                    xa = c * id; xb = -b * id; xc = a * id;
+                }
+                const double e0 = S.E0()[J], e1 = S.E1()[J], e2 = S.E2()[J], e3 = S.E3()[J];
+                S.L0()[Qi] = e0; S.L1()[Qi] = e1; S.L2()[Qi] = e2; S.L3()[Qi] = e3;
+                const double t00 = e0 * xa + e1 * xb, t01 = e0 * xb + e1 * xc;
+                const double t10 = e2 * xa + e3 * xb, t11 = e2 * xb + e3 * xc;
+                da -= t00 * e0 + t01 * e1;
+                db -= t00 * e2 + t01 * e3;
+                dc -= t10 * e2 + t11 * e3;
+                const double h0 = S.f0()[Qi], h1 = S.f1()[Qi];
+                g0 -= t00 * h0 + t01 * h1;
+                g1 -= t10 * h0 + t11 * h1;
+                w -= clo[q] * cinv[q] * S.fw()[Qi];
+                if (q + s < n) {
+                    const double k0 = S.E0()[Qi], k1 = S.E1()[Qi], k2 = S.E2()[Qi], k3 = S.E3()[Qi];
+                    n0 = -(t00 * k0 + t01 * k2);
+                    n1 = -(t00 * k1 + t01 * k3);
+                    n2 = -(t10 * k0 + t11 * k2);
+                    n3 = -(t10 * k1 + t11 * k3);
+                }
+                qa[t] = xa; qb[t] = xb; qc[t] = xc; qi[t] = Qi;
+            }
+            S.Da()[J] = da; S.Db()[J] = db; S.Dc()[J] = dc;
+            S.E0()[J] = n0; S.E1()[J] = n1; S.E2()[J] = n2; S.E3()[J] = n3;
+            S.f0()[J] = g0; S.f1()[J] = g1; S.fw()[J] = w;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < KPT; ++t) {
+        if (qi[t] >= 0) { S.Da()[qi[t]] = qa[t]; S.Db()[qi[t]] = qb[t]; S.Dc()[qi[t]] = qc[t]; }
+    }
+    if (p0i >= 0) { S.Da()[p0i] = p0a; S.Db()[p0i] = p0b; S.Dc()[p0i] = p0c; }
+}
+
+// The A <= 32 nodes left at the cut level, solved by parallel cyclic
+// reduction in warp 0 with one node per lane (registers + shuffles, no
+// back-substitution): each step eliminates the couplings at distance s with
+// the neighbours' inverted pivots; the system stays symmetric, so the lower
+// neighbour's upper coupling is this lane's lower coupling transposed.
+__device__ __forceinline__ void pcr_tail(const TriSm& S, int c, int A) {
+    const unsigned F = 0xffffffffu;
+    const int m = threadIdx.x & 31;
+    const bool act = m < A;
+    const int J = act ? PI(((m + 1) << c) - 1) : 0;
+    double da = 1.0, db = 0.0, dc = 1.0, u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0, f0 = 0.0, f1 = 0.0;
+    if (act) {
+        da = S.Da()[J]; db = S.Db()[J]; dc = S.Dc()[J];
+        u0 = S.E0()[J]; u1 = S.E1()[J]; u2 = S.E2()[J]; u3 = S.E3()[J];
+        f0 = S.f0()[J]; f1 = S.f1()[J];
+    }
+    // lower coupling (row m, col m-1) = E_{m-1}^T
+    double l0 = __shfl_up_sync(F, u0, 1), l1 = __shfl_up_sync(F, u2, 1);
+    double l2 = __shfl_up_sync(F, u1, 1), l3 = __shfl_up_sync(F, u3, 1);
+    if (m == 0) { l0 = 0.0; l1 = 0.0; l2 = 0.0; l3 = 0.0; }
+    for (int s = 1; s < A; s <<= 1) {
+        const double id = 1.0 / (da * dc - db * db);
+        const double ia = dc * id, ib = -db * id, ic = da * id;
+        const double La = __shfl_up_sync(F, ia, s), Lb = __shfl_up_sync(F, ib, s),
+                     Lc = __shfl_up_sync(F, ic, s);
+        const double Ll0 = __shfl_up_sync(F, l0, s), Ll1 = __shfl_up_sync(F, l1, s),
+                     Ll2 = __shfl_up_sync(F, l2, s), Ll3 = __shfl_up_sync(F, l3, s);
+        const double Lf0 = __shfl_up_sync(F, f0, s), Lf1 = __shfl_up_sync(F, f1, s);
+        const double Ua = __shfl_down_sync(F, ia, s), Ub = __shfl_down_sync(F, ib, s),
+                     Uc = __shfl_down_sync(F, ic, s);
+        const double Uu0 = __shfl_down_sync(F, u0, s), Uu1 = __shfl_down_sync(F, u1, s),
+                     Uu2 = __shfl_down_sync(F, u2, s), Uu3 = __shfl_down_sync(F, u3, s);
+        const double Uf0 = __shfl_down_sync(F, f0, s), Uf1 = __shfl_down_sync(F, f1, s);
+        double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
+        double b00 = 0.0, b01 = 0.0, b10 = 0.0, b11 = 0.0;
+        if (m >= s) {          // alpha = -Lo P_{m-s}
+            a00 = -(l0 * La + l1 * Lb); a01 = -(l0 * Lb + l1 * Lc);
+            a10 = -(l2 * La + l3 * Lb); a11 = -(l2 * Lb + l3 * Lc);
+        }
+        if (m + s < A) {       // beta = -Up P_{m+s}
+            b00 = -(u0 * Ua + u1 * Ub); b01 = -(u0 * Ub + u1 * Uc);
+            b10 = -(u2 * Ua + u3 * Ub); b11 = -(u2 * Ub + u3 * Uc);
+        }
+        da += a00 * l0 + a01 * l1 + b00 * u0 + b01 * u1;
+        db += a00 * l2 + a01 * l3 + b00 * u2 + b01 * u3;
+        dc += a10 * l2 + a11 * l3 + b10 * u2 + b11 * u3;
+        f0 += a00 * Lf0 + a01 * Lf1 + b00 * Uf0 + b01 * Uf1;
+        f1 += a10 * Lf0 + a11 * Lf1 + b10 * Uf0 + b11 * Uf1;
+        l0 = a00 * Ll0 + a01 * Ll2; l1 = a00 * Ll1 + a01 * Ll3;
+        l2 = a10 * Ll0 + a11 * Ll2; l3 = a10 * Ll1 + a11 * Ll3;
+        u0 = b00 * Uu0 + b01 * Uu2; u1 = b00 * Uu1 + b01 * Uu3;
+        u2 = b10 * Uu0 + b11 * Uu2; u3 = b10 * Uu1 + b11 * Uu3;
+    }
+    const double id = 1.0 / (da * dc - db * db);
+    if (act) {
+        S.f0()[J] = (dc * f0 - db * f1) * id;
+        S.f1()[J] = (da * f1 - db * f0) * id;
+    }
+}
+
+// Scalar Q_z system reduced to the cut: w_a = (Q_z^{-1})_aa fw_a (qzw
+// transposed), one warp.
+__device__ __forceinline__ void scal_cut(const TriSm& S, int c, int A,
+                                         const double* __restrict__ qzw) {
+    const int a = threadIdx.x & 31;
+    double x = 0.0;
+    if (a < A) {
+        for (int m = 0; m < A; ++m) x = fma(qzw[m * A + a], S.fw()[PI(((m + 1) << c) - 1)], x);
+    }
+    __syncwarp();
+    if (a < A) S.fw()[PI(((a + 1) << c) - 1)] = x;
+}
+
 // Block cyclic reduction of the symmetric quasi-definite 2x2-block tridiagonal
 // system held in S (D sym (a,b,c), E upper coupling, f rhs), jointly with the
-// scalar reduction of Qz w = fw using precomputed coefficients cr = [3][n]
-// (inv_d, e_up, e_lo per node at its elimination level).  With RHS=false only
-// the factorisation is performed.  Solutions overwrite f0/f1/fw.  Levels with
-// more than 32 eliminated nodes run CTA-wide (two barriers per level); the
-// deeper levels, the root and their back-substitution run in warp 0 with
-// __syncwarp only.
-template <bool RHS>
-__device__ __forceinline__ void cr_solve(int n, const TriSm& S, const double* __restrict__ cr) {
-    using K = CrSolve<RHS>;
+// scalar reduction of Qz w = fw (coefficients cr; reduced inverse qzw at the
+// cut).  Levels below the cut run CTA-wide with one barrier each; the <= 32
+// nodes at the cut by parallel cyclic reduction in warp 0 while warp 1 (or
+// warp 0 afterwards) applies the scalar reduced inverse; then the CTA-wide
+// back-substitution.  Solutions overwrite f0/f1/fw.
+template <int KPT>
+__device__ __forceinline__ void cr_solve(int n, const TriSm& S, const double* __restrict__ cr,
+                                         const double* __restrict__ qzw) {
+    using K = CrSolve<true>;
     const int tid = threadIdx.x, nth = blockDim.x;
     const double* cinv = cr;
     const double* cup = cr + n;
     const double* clo = cr + 2 * n;
-    const int top = ilog2(n);
-    const int lw = cta_levels(n);
+    const int c = cut_level(n), A = cut_nodes(n);
 #pragma unroll
     for (int lev = 0; lev < kMaxLev; ++lev) {
-        if (lev >= lw) break;
-        const int ce = lvl_count(n, lev);
-        for (int m = tid; m < ce; m += nth) K::elim(S, n, lev, m);
-        __syncthreads();
-        const int ck = kept_count(n, lev);
-        for (int m = tid; m < ck; m += nth) K::keep(S, n, lev, m, cinv, cup, clo);
-        __syncthreads();
-    }
-    if (tid < 32) {
-#pragma unroll
-        for (int l = 0; l < kMaxLev; ++l) {
-            if (l < lw) continue;
-            if (l >= top) break;
-            if (tid < lvl_count(n, l)) K::elim(S, n, l, tid);
-            __syncwarp();
-            if (tid < kept_count(n, l)) K::keep(S, n, l, tid, cinv, cup, clo);
-            __syncwarp();
-        }
-        if (tid == 0) K::root(S, n, cinv);
-        __syncwarp();
-        if (RHS) {
-#pragma unroll
-            for (int l = kMaxLev - 1; l >= 0; --l) {
-                if (l >= top || l < lw) continue;
-                if (tid < lvl_count(n, l)) K::back(S, n, l, tid, cinv, cup, clo);
-                __syncwarp();
-            }
-        }
+        if (lev >= c) break;
+        cr_level<KPT>(S, n, lev, cr);
     }
     __syncthreads();
-    if (!RHS) return;
+    if (tid < 32) {
+        pcr_tail(S, c, A);
+        if (nth <= 32) scal_cut(S, c, A, qzw);
+    } else if (tid < 64) {
+        scal_cut(S, c, A, qzw);
+    }
+    __syncthreads();
 #pragma unroll
     for (int lev = kMaxLev - 1; lev >= 0; --lev) {
-        if (lev >= lw) continue;
+        if (lev >= c) continue;
         const int ce = lvl_count(n, lev);
         for (int m = tid; m < ce; m += nth) K::back(S, n, lev, m, cinv, cup, clo);
         __syncthreads();
@@ -397,7 +561,7 @@ __device__ __forceinline__ void tri_block(const TView& V, int i, const double* b
     }
     tri_init_de(V, n, i, S);
     __syncthreads();
-    cr_solve<true>(n, S, V.cr);
+    cr_solve<(NT > 0 ? (NT / 2 + 127) / 128 : 4)>(n, S, V.cr, V.qzw);
     for (int j = tid; j < n; j += nth) {
         const int J = PI(j);
         const double du = S.f0()[J], dl = S.f1()[J];
@@ -454,22 +618,6 @@ __global__ void tri_subst(TView V, const double* __restrict__ r, double* d) {
 // TMA bulk-staged in a double buffer so only the recurrences of the current
 // interval sit on the serial critical path.
 // ---------------------------------------------------------------------------
-static constexpr int kFacRows = 14;
-
-// Cut level c of the chain's cyclic reduction: levels below c run as usual;
-// the reduced system on the A = n >> c <= 32 active nodes left at level c is
-// solved with its precomputed dense inverse W (2A x 2A, stored transposed).
-__host__ __device__ __forceinline__ constexpr int cut_level(int n) {
-    int c = 0;
-    while ((n >> c) > 32) ++c;
-    return c;
-}
-__host__ __device__ __forceinline__ constexpr int cut_nodes(int n) { return n >> cut_level(n); }
-// doubles per interval record: P, M1, M2 (levels < c, level order), C, W^T
-__host__ __device__ __forceinline__ constexpr int fac_record(int n) {
-    return kFacRows * n + 4 * cut_nodes(n) * cut_nodes(n);
-}
-
 // Level order of the factor rows: node j = s-1 + 2s*m (s = 2^l) is eliminated
 // at level l = ctz(j+1) with index m = (j+1) >> (l+1); level l occupies
 // [lvl_off(l), lvl_off(l+1)).  Every CR level then reads a contiguous run.
@@ -579,7 +727,16 @@ __device__ long long g_tk_prof[16];
     do {                                                                 \
         if ((cond) && threadIdx.x == 0) g_tk_prof[slot] = clock64();     \
     } while (0)
+#define TKA(slot, v)                                                     \
+    do {                                                                 \
+        if (threadIdx.x == 0 && blockIdx.x == 0) g_tk_prof[slot] += (v); \
+    } while (0)
+#define TKCLK() clock64()
 #else
+#define TKA(slot, v) \
+    do {             \
+    } while (0)
+#define TKCLK() 0LL
 #define TKP(slot, cond) \
     do {                \
     } while (0)
@@ -950,47 +1107,197 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
     }
 }
 
-// Serial carry over the chunk ends (one cluster of kCarryCtas CTAs):
+// shared::cluster address of the same shared-memory location in CTA `rank`
+__device__ __forceinline__ unsigned mapa_u32(unsigned a, unsigned rank) {
+    unsigned d;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(d) : "r"(a), "r"(rank));
+    return d;
+}
+// 8-byte store into a peer CTA's shared memory that completes 8 transaction
+// bytes on the peer's mbarrier
+__device__ __forceinline__ void st_async_f64(unsigned raddr, double v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n"
+                 ::"r"(raddr), "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+
+// Serial carry over the chunk ends (one thread-block cluster):
 //   U = ends[first];  for each next chunk c in chain order:
 //     starts[c] = U;  U = ends[c] + M_c U
 // with M_c = Pi_c (forward) or Pi_c^T (backward), row-major n x n.  Each CTA
-// owns a block of rows of the matvec; the new U is broadcast into every CTA's
-// shared copy through distributed shared memory (ping-pong buffers), one
-// cluster barrier per chunk.
-static constexpr int kCarryCtas = 8;
+// owns a block of rows of the matvec and pushes every new entry of U into
+// all CTAs' shared copies with st.async; each copy (ping-pong by step) has
+// an mbarrier expecting the n*8 bytes of one U, so the only synchronisation
+// per chunk is that transaction count (no cluster-wide barrier).  staged:
+// the CTA's row block of the next M_c is TMA bulk-copied into shared memory
+// as soon as the current one has been consumed.
 template <bool FWD>
-__global__ void __cluster_dims__(kCarryCtas, 1, 1) __launch_bounds__(1024, 1)
+__global__ void __launch_bounds__(1024, 1)
     tri_chain_carry(int n, int nc, const double* __restrict__ M, const double* __restrict__ ends,
-                    double* __restrict__ starts) {
-    extern __shared__ __align__(16) double sm[];   // U ping-pong [2][n]
+                    double* __restrict__ starts, int staged) {
+    extern __shared__ __align__(16) double sm[];   // U ping-pong [2][n], row block
+    __shared__ __align__(8) uint64_t tbar;          // TMA row block
+    __shared__ __align__(8) uint64_t ubar[2];       // U copies
     cg::cluster_group cl = cg::this_cluster();
+    const int CS = (int)cl.num_blocks();
     const int rank = (int)cl.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    const int rpc = (n + kCarryCtas - 1) / kCarryCtas;
-    const int r0 = rank * rpc, r1 = min(n, r0 + rpc);
+    const int rpc = (n + CS - 1) / CS;
+    const int r0 = min(n, rank * rpc), r1 = min(n, r0 + rpc);
+    double* blk = sm + 2 * n;
+    const unsigned bytes = (unsigned)((size_t)(r1 - r0) * n * sizeof(double));
+    const bool stg = staged && bytes > 0;
+    const unsigned ubytes = (unsigned)(n * sizeof(double));
+    auto chunk_at = [&](int t) { return FWD ? t : nc - 1 - t; };
+    auto issue = [&](int t) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_tx(&tbar, bytes);
+        tma_g2s(blk, M + (size_t)chunk_at(t) * n * n + (size_t)r0 * n, bytes, &tbar);
+    };
+    if (tid == 0) {
+        mbar_init(&tbar, 1);
+        mbar_init(&ubar[0], 1);
+        mbar_init(&ubar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (stg && tid == 0 && nc > 2) issue(1);
     const int first = FWD ? 0 : nc - 1;
     for (int j = tid; j < n; j += blockDim.x) sm[j] = ends[(size_t)first * n + j];
-    cl.sync();
+    cl.sync();   // every CTA's barriers are initialised before any st.async
+    unsigned tphase = 0;
     for (int t = 1; t < nc; ++t) {
-        const int c = FWD ? t : nc - 1 - t;
+        const int c = chunk_at(t);
+        long long c0 = TKCLK();
+        if (t >= 2) mbar_wait(&ubar[(t - 1) & 1], (unsigned)(((t - 2) >> 1) & 1));
+        long long c1 = TKCLK();
+        TKA(8, c1 - c0);
         const double* cur = sm + ((t - 1) & 1) * n;
-        double* nxt = sm + (t & 1) * n;
         for (int j = r0 + tid; j < r1; j += blockDim.x) starts[(size_t)c * n + j] = cur[j];
         if (t == nc - 1) break;
-        const double* Mc = M + (size_t)c * n * n;
+        if (tid == 0) mbar_expect_tx(&ubar[t & 1], ubytes);   // arm the copy of U_t
+        c0 = TKCLK();
+        if (stg) { mbar_wait(&tbar, tphase); tphase ^= 1u; }
+        c1 = TKCLK();
+        TKA(9, c1 - c0);
+        const double* src = stg ? blk : M + (size_t)c * n * n + (size_t)r0 * n;
         const double* ec = ends + (size_t)c * n;
+        const unsigned nxt = smem_u32(sm + (t & 1) * n);
+        const unsigned bar = smem_u32(&ubar[t & 1]);
         for (int r = r0 + warp; r < r1; r += nw) {
-            const double* row = Mc + (size_t)r * n;
-            double acc = 0.0;
-            for (int k = lane; k < n; k += 32) acc = fma(row[k], cur[k], acc);
+            const double* row = src + (size_t)(r - r0) * n;
+            const double e = ec[r];
+            double a0 = 0.0, a1 = 0.0;
+            int k = lane;
+            for (; k + 32 < n; k += 64) {
+                a0 = fma(row[k], cur[k], a0);
+                a1 = fma(row[k + 32], cur[k + 32], a1);
+            }
+            if (k < n) a0 = fma(row[k], cur[k], a0);
+            double acc = a0 + a1;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane < kCarryCtas) {
-                double* dst = cl.map_shared_rank(nxt, lane);
-                dst[r] = ec[r] + acc;
-            }
+            const double v = e + acc;
+            for (int d = lane; d < CS; d += 32)
+                st_async_f64(mapa_u32(nxt + 8u * r, d), v, mapa_u32(bar, d));
         }
-        cl.sync();
+        TKA(10, TKCLK() - c1);
+        if (stg) {
+            __syncthreads();   // row block consumed: refill with the next chunk's
+            if (tid == 0 && t + 1 < nc - 1) issue(t + 1);
+        }
+    }
+    cl.sync();   // no CTA leaves while peers may still write into it
+}
+
+// Grid-wide variant of the carry (one CTA per SM, cooperative launch): CTA g
+// owns rows [g R, g R + R) of every M_c.  Its row blocks are streamed by TMA
+// into a ring of D shared-memory slots up to D chunks ahead, so the HBM
+// traffic (n^2 doubles per chunk) runs at full-chip bandwidth off the serial
+// path.  U_t goes through global memory (Ug, read with .cg loads) and one
+// arrival counter (release/acquire) per chunk; the last CTA out resets the
+// counters for the next launch.  D == 0: rows are loaded directly.
+static constexpr int kCarryRing = 8;
+template <bool FWD>
+__global__ void __launch_bounds__(256, 1)
+    tri_chain_carry_grid(int n, int nc, const double* __restrict__ M,
+                         const double* __restrict__ ends, double* __restrict__ starts,
+                         double* Ug, unsigned* cnt, int R, int D) {
+    extern __shared__ __align__(16) double sm[];   // ring [D][R*n], then U [n]
+    __shared__ __align__(8) uint64_t bars[kCarryRing];
+    const int G = gridDim.x, g = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int r0 = min(n, g * R), r1 = min(n, r0 + R);
+    const size_t slot = (size_t)R * n;
+    double* Us = sm + (size_t)D * slot;
+    const unsigned bytes = (unsigned)((size_t)(r1 - r0) * n * sizeof(double));
+    const int T = nc - 2;   // chunks with a matvec: t = 1..T
+    auto chunk_at = [&](int t) { return FWD ? t : nc - 1 - t; };
+    auto issue = [&](int t) {   // row block of step t into slot (t-1) % D
+        const int sl = (t - 1) % D;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_tx(&bars[sl], bytes);
+        tma_g2s(sm + sl * slot, M + (size_t)chunk_at(t) * n * n + (size_t)r0 * n, bytes, &bars[sl]);
+    };
+    if (D > 0 && tid == 0) {
+        for (int k = 0; k < D; ++k) mbar_init(&bars[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (D > 0 && bytes > 0 && tid == 0)
+        for (int t = 1; t <= min(D, T); ++t) issue(t);
+    const int first = FWD ? 0 : nc - 1;
+    for (int t = 1; t < nc; ++t) {
+        const int c = chunk_at(t);
+        const double* curg = (t == 1) ? ends + (size_t)first * n : Ug + (size_t)(t - 1) * n;
+        long long c0 = TKCLK();
+        if (t >= 2) {
+            if (tid == 0) {
+                const unsigned target = (unsigned)(t - 1) * (unsigned)G;
+                unsigned v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
+                } while (v < target);
+            }
+            __syncthreads();
+        }
+        long long c1 = TKCLK();
+        TKA(8, c1 - c0);
+        for (int j = tid; j < n; j += blockDim.x) Us[j] = __ldcg(curg + j);
+        __syncthreads();
+        long long c2 = TKCLK();
+        TKA(11, c2 - c1);
+        for (int j = r0 + tid; j < r1; j += blockDim.x) starts[(size_t)c * n + j] = Us[j];
+        if (t == nc - 1) break;
+        const int sl = D > 0 ? (t - 1) % D : 0;
+        if (D > 0 && bytes > 0) mbar_wait(&bars[sl], (unsigned)(((t - 1) / D) & 1));
+        c1 = TKCLK();
+        TKA(9, c1 - c2);
+        const double* src = D > 0 ? sm + sl * slot : M + (size_t)c * n * n + (size_t)r0 * n;
+        const double* ec = ends + (size_t)c * n;
+        for (int r = r0 + warp; r < r1; r += nw) {
+            const double* row = src + (size_t)(r - r0) * n;
+            double acc = 0.0;
+            for (int k = lane; k < n; k += 32) acc = fma(row[k], Us[k], acc);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) __stcg(Ug + (size_t)t * n + r, ec[r] + acc);
+        }
+        __syncthreads();
+        TKA(10, TKCLK() - c1);
+        if (tid == 0) {
+            if (D > 0 && bytes > 0 && t + D <= T) issue(t + D);
+            __threadfence();
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(cnt) : "memory");
+        }
+    }
+    if (tid == 0) {   // last CTA out resets the counters
+        __threadfence();
+        const unsigned prev = atomicAdd(cnt + 1, 1u);
+        if (prev == (unsigned)G - 1) {
+            atomicExch(cnt, 0u);
+            atomicExch(cnt + 1, 0u);
+        }
     }
 }
 
@@ -1027,7 +1334,7 @@ static int chain_nc(int N, int Lc) {
 int64_t tri_chain_prod_len(const tk_level* Lv) {
     if (Lv->chain_chunk <= 0) return 0;
     const int64_t n = Lv->n_u, nc = chain_nc(Lv->n_steps, Lv->chain_chunk);
-    return 2 * nc * n * n + 2 * nc * n;
+    return 2 * nc * n * n + 3 * nc * n + 4;   // P, P^T, ends, starts, U_t, counters
 }
 
 // ---------------------------------------------------------------------------
@@ -1262,6 +1569,12 @@ static int tri_rec_threads(int n) {
 }
 
 static int tri_threads(int n) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = getenv("TK_ROWS_THREADS");
+        forced = e ? atoi(e) : 0;
+    }
+    if (forced >= 32 && forced <= 256) return forced;
     int t = (n / 2 + 31) / 32 * 32;
     if (t < 32) t = 32;
     if (t > 256) t = 256;
@@ -1279,6 +1592,97 @@ static int tri_chain_threads(int n) {
     if (t < 32) t = 32;
     if (t > 256) t = 256;
     return t;
+}
+
+// Launch the chunk carry as one cluster: 16 CTAs (non-portable) when that
+// fits, else 8; the row blocks are TMA-staged when they fit in shared memory.
+static int carry_launch(bool fwd, int n, int nc, const double* M, const double* E, double* S,
+                        cudaStream_t s) {
+    static int cs_ok = 0;   // cluster size verified for this process
+    auto base_for = [&](int) -> int64_t { return (int64_t)2 * n * 8; };   // U ping-pong
+    auto smem_for = [&](int cs) -> int64_t {
+        const int64_t rpc = (n + cs - 1) / cs;
+        return base_for(cs) + rpc * n * 8;
+    };
+    const int64_t lim = 227 * 1024 - 1024;
+    if (!cs_ok) {
+        for (void* f : {(void*)tri_chain_carry<true>, (void*)tri_chain_carry<false>}) {
+            cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+        }
+        cudaGetLastError();
+        cs_ok = 8;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 16; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(16); cfg.blockDim = dim3(1024); cfg.dynamicSmemBytes = (size_t)lim;
+        cfg.attrs = at; cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)tri_chain_carry<true>, &cfg) ==
+                cudaSuccess && ncl > 0)
+            cs_ok = 16;
+        cudaGetLastError();
+    }
+    int cs = cs_ok;
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = getenv("TK_CARRY_CTAS");
+        forced = e ? atoi(e) : 0;
+    }
+    if (forced == 8 || forced == 16) cs = forced < cs_ok ? forced : cs_ok;
+    int64_t smem = smem_for(cs);
+    const int staged = (n % 2 == 0) && smem <= lim && (smem - base_for(cs)) < (1 << 20);
+    if (!staged) smem = base_for(cs);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs); cfg.blockDim = dim3(1024); cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = s; cfg.attrs = at; cfg.numAttrs = 1;
+    cudaError_t e;
+    if (fwd) e = cudaLaunchKernelEx(&cfg, tri_chain_carry<true>, n, nc, M, E, S, staged);
+    else e = cudaLaunchKernelEx(&cfg, tri_chain_carry<false>, n, nc, M, E, S, staged);
+    return cuda_status(e, "tri_chain_carry");
+}
+
+// carry implementation: 1 = one cluster, 0 = grid-wide.  Default: the
+// cluster while its row blocks can be TMA-staged (n <= 640), else the grid
+// (bandwidth: n^2 doubles per chunk).  TK_CARRY=cluster|grid overrides.
+static int carry_mode(int n) {
+    static int m = -1;
+    if (m < 0) {
+        const char* e = getenv("TK_CARRY");
+        m = !e ? 2 : (!strcmp(e, "cluster") ? 1 : 0);
+    }
+    return m == 2 ? (n <= 640 ? 1 : 0) : m;
+}
+
+static int carry_grid_launch(bool fwd, int n, int nc, const double* M, const double* E, double* S,
+                             double* Ug, unsigned* cnt, cudaStream_t s) {
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (nsm <= 0) nsm = 148;
+        for (void* f : {(void*)tri_chain_carry_grid<true>, (void*)tri_chain_carry_grid<false>})
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaGetLastError();
+    }
+    const int R = (n + nsm - 1) / nsm;
+    const int G = (n + R - 1) / R;
+    const int64_t slot = (int64_t)R * n * 8;
+    int D = (int)((160 * 1024) / slot);
+    if (D > kCarryRing) D = kCarryRing;
+    if (n % 2) D = 0;                       // TMA needs 16-byte multiples
+    const int64_t smem = (int64_t)D * slot + (int64_t)n * 8;
+    int Ri = R, Di = D;
+    void* args[] = {(void*)&n, (void*)&nc, (void*)&M, (void*)&E, (void*)&S, (void*)&Ug,
+                    (void*)&cnt, (void*)&Ri, (void*)&Di};
+    const void* f = fwd ? (const void*)tri_chain_carry_grid<true> : (const void*)tri_chain_carry_grid<false>;
+    const cudaError_t e = cudaLaunchCooperativeKernel(f, dim3(G), dim3(256), args, (size_t)smem, s);
+    return cuda_status(e, "tri_chain_carry_grid");
 }
 
 template <int NT>
@@ -1339,7 +1743,11 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
     }
     const int th = tri_threads(n);
     const bool fast = Lv->fac != nullptr && Lv->scratch != nullptr;
-    const bool rec = Lv->fac != nullptr && Lv->qz_w != nullptr;   // record-based D^{-1}
+    if (!Lv->qz_w) {
+        set_error("tri family: level is missing qz_w");
+        return TK_ERR_ARG;
+    }
+    const bool rec = Lv->fac != nullptr && !(Lv->flags & TK_FLAG_ONTHEFLY);   // record-based D^{-1}
     const int64_t rsm = tri_rec_smem_bytes(n);
     const int rth = tri_rec_threads(n);
     if (!rec && smem == 0) {
@@ -1400,9 +1808,12 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                 chain_launch(1, 0, nullptr, nullptr);
             } else {
                 chain_launch(nc, 0, nullptr, E);                 // all chunks from zero
-                const int64_t usm = (int64_t)2 * n * 8;
-                if (fwd) tri_chain_carry<true><<<kCarryCtas, 1024, usm, s>>>(n, nc, P, E, S);
-                else tri_chain_carry<false><<<kCarryCtas, 1024, usm, s>>>(n, nc, PT, E, S);
+                double* Ug = S + (size_t)nc * n;
+                unsigned* cnt = (unsigned*)(Ug + (size_t)nc * n);
+                const int rc = carry_mode(n) == 1
+                                   ? carry_launch(fwd, n, nc, fwd ? P : PT, E, S, s)
+                                   : carry_grid_launch(fwd, n, nc, fwd ? P : PT, E, S, Ug, cnt, s);
+                if (rc) return rc;
                 chain_launch(nc - 1, fwd ? 1 : 0, S, nullptr);   // non-seed chunks again
             }
             // pass 3: parallel solves with the chain coupling
@@ -1446,6 +1857,11 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                 return TK_ERR_ARG;
             }
             const int N = Lv->n_steps, Lc = Lv->chain_chunk, nc = chain_nc(N, Lc);
+            {
+                double* cntp = Lv->chain_prod + 2 * (size_t)nc * n * n + 3 * (size_t)nc * n;
+                const cudaError_t e = cudaMemsetAsync(cntp, 0, 4 * sizeof(double), s);
+                if (e != cudaSuccess) return cuda_status(e, "tk_chain_prod: memset");
+            }
             if (nc <= 2) break;
             double* P = Lv->chain_prod;
             double* PT = P + (size_t)nc * n * n;

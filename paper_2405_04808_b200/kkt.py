@@ -319,7 +319,7 @@ class BlockTriKKT:
             Qz=dev.P(s.Qz), Qm_inv=dev.P(s.Qm_inv), Ql_inv=dev.P(s.Ql_inv),
             Qz_inv=dev.P(s.Qz_inv), kappa=s.kappa, qz_cr=dev.P(s.qz_cr),
             row0=self.row0, row1=0 if not self.is_slab else self.row1,
-            halo_u=dev.P(self.halo_u), halo_mu=dev.P(self.halo_mu))
+            halo_u=dev.P(self.halo_u), halo_mu=dev.P(self.halo_mu), qz_w=dev.P(s.qz_w))
         self.lref = C.byref(self.level)
         self._fac = None
         self._scratch = None
@@ -363,8 +363,8 @@ class BlockTriKKT:
         self.level.scratch = self._scratch.data_ptr()
         dev.call("tk_subst_factor", self.lref, dev.stream())
         # TRI: the records also drive every D^{-1} (Jacobi, diagonal solve)
-        if self.stage.qz_w is not None and os.environ.get("TK_NO_RECORDS") != "1":
-            self.level.qz_w = self.stage.qz_w.data_ptr()
+        if os.environ.get("TK_NO_RECORDS") == "1":
+            self.level.flags |= _lib.TK_FLAG_ONTHEFLY
 
     def _ensure_chain(self) -> None:
         if self._chain is not None or self.family != FAMILY_TRI or self.is_slab:
