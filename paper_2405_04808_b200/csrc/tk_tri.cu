@@ -19,7 +19,7 @@
 // compile-time constant (64..2048 are dispatched; NT = 0 is the generic
 // runtime-n build): shared-memory row offsets then fold into immediates and
 // the cyclic-reduction level loops unroll.
-#include "tk_common.cuh"
+#include "tk_tri.cuh"
 
 #include <cooperative_groups.h>
 #include <math.h>
@@ -28,12 +28,6 @@
 namespace cg = cooperative_groups;
 
 namespace tk {
-
-__host__ __device__ __forceinline__ constexpr int PI(int j) { return j + (j >> 4); }
-__host__ __device__ __forceinline__ constexpr int padded(int n) { return n + (n >> 4) + 1; }
-__host__ __device__ __forceinline__ constexpr int ilog2(int n) {
-    return n <= 1 ? 0 : 1 + ilog2(n >> 1);
-}
 
 static constexpr int kMaxLev = 12;   // n <= 4096
 
@@ -53,59 +47,6 @@ __host__ __device__ __forceinline__ constexpr int fac_record(int n) {
     return kFacRows * n + 4 * cut_nodes(n) * cut_nodes(n);
 }
 
-
-struct TView {
-    Lay lay;
-    int n;
-    const double* K;
-    const double* C;
-    const double* Qm;
-    const double* Ql;
-    const double* Qz;
-    const double* cr;
-    double kappa;
-    Slab sl;
-    const double* fac;   // factor records of the slab's stages (or null)
-    const double* qzw;   // scalar reduced-system inverse at the cut (with fac)
-    TView(const tk_level* L)
-        : lay(L->n_steps, L->n_u, L->n_z), n(L->n_u), K(L->K), C(L->C), Qm(L->Qm), Ql(L->Ql),
-          Qz(L->Qz), cr(L->qz_cr), kappa(L->kappa), sl(L, Lay(L->n_steps, L->n_u, L->n_z)),
-          fac(L->fac), qzw(L->qz_w) {}
-    // stage diagonals of global block row i (stage arrays start at the slab's first row)
-    __device__ const double* Ki(int i, int n_) const { return K + (size_t)(i - sl.r0) * 3 * n_; }
-    __device__ const double* Ci(int i, int n_) const { return C + (size_t)(i - sl.r0) * 3 * n_; }
-};
-
-template <int NT>
-__device__ __forceinline__ int dimn(const TView& V) { return NT > 0 ? NT : V.n; }
-
-// (A x)_j for a tridiagonal A stored [3][n] = (sub, diag, sup); x in global memory
-__device__ __forceinline__ double tmv(const double* A, int n, const double* x, int j) {
-    double s = A[n + j] * x[j];
-    if (j > 0) s += A[j] * x[j - 1];
-    if (j < n - 1) s += A[2 * n + j] * x[j + 1];
-    return s;
-}
-// (A^T x)_j
-__device__ __forceinline__ double tmtv(const double* A, int n, const double* x, int j) {
-    double s = A[n + j] * x[j];
-    if (j > 0) s += A[2 * n + j - 1] * x[j - 1];
-    if (j < n - 1) s += A[j + 1] * x[j + 1];
-    return s;
-}
-// same with x in padded shared memory
-__device__ __forceinline__ double tmv_s(const double* A, int n, const double* xs, int j) {
-    double s = A[n + j] * xs[PI(j)];
-    if (j > 0) s += A[j] * xs[PI(j - 1)];
-    if (j < n - 1) s += A[2 * n + j] * xs[PI(j + 1)];
-    return s;
-}
-__device__ __forceinline__ double tmtv_s(const double* A, int n, const double* xs, int j) {
-    double s = A[n + j] * xs[PI(j)];
-    if (j > 0) s += A[2 * n + j - 1] * xs[PI(j - 1)];
-    if (j < n - 1) s += A[j + 1] * xs[PI(j + 1)];
-    return s;
-}
 
 static constexpr int kTriArrays = 16;
 
@@ -1685,6 +1626,21 @@ static int carry_grid_launch(bool fwd, int n, int nc, const double* M, const dou
     return cuda_status(e, "tri_chain_carry_grid");
 }
 
+int part_nodes_per_lane(int n);
+int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, double* y,
+                double omega, const double* chain, cudaStream_t s);
+
+// warp-per-row partitioned solves (tk_tri_part.cu) for 32 < n <= 512;
+// TK_PART=0 selects the CTA-wide cyclic-reduction kernels instead
+static bool use_part(int n) {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("TK_PART");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on && part_nodes_per_lane(n) > 0;
+}
+
 template <int NT>
 static int tri_launch_t(const tk_level* Lv, int op, const double* b, const double* x, double* y,
                         double omega, cudaStream_t s) {
@@ -1756,10 +1712,12 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
     }
     switch (op) {
         case 3:  // diag solve
+            if (!rec && use_part(n)) return part_launch(Lv, 0, b, nullptr, y, 1.0, nullptr, s);
             if (rec) tri_rows_rec<NT><<<rows, rth, rsm, s>>>(V, b, nullptr, y, 1.0);
             else tri_rows<NT><<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
             break;
         case 4:  // jacobi
+            if (!rec && use_part(n)) return part_launch(Lv, 0, b, x, y, omega, nullptr, s);
             if (rec) tri_rows_rec<NT><<<rows, rth, rsm, s>>>(V, b, x, y, omega);
             else tri_rows<NT><<<rows, th, smem, s>>>(V, b, x, y, omega);
             break;
@@ -1772,7 +1730,10 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                 break;
             }
             // pass 1: a = D^{-1} r into y
-            if (rec) tri_rows_rec<NT><<<rows, rth, rsm, s>>>(V, b, nullptr, y, 1.0);
+            if (!rec && use_part(n)) {
+                const int rc = part_launch(Lv, 0, b, nullptr, y, 1.0, nullptr, s);
+                if (rc) return rc;
+            } else if (rec) tri_rows_rec<NT><<<rows, rth, rsm, s>>>(V, b, nullptr, y, 1.0);
             else tri_rows<NT><<<rows, th, smem, s>>>(V, b, nullptr, y, 1.0);
             // pass 2: the chain on the coupling vector (serial, or time-chunked)
             const int cth = tri_chain_threads(n);
@@ -1820,6 +1781,9 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             if (rec) {
                 if (fwd) tri_rows_rec_cpl<true, NT><<<rows, rth, rsm, s>>>(V, b, chn, y);
                 else tri_rows_rec_cpl<false, NT><<<rows, rth, rsm, s>>>(V, b, chn, y);
+            } else if (use_part(n)) {
+                const int rc = part_launch(Lv, fwd ? 1 : 2, b, nullptr, y, 1.0, chn, s);
+                if (rc) return rc;
             } else {
                 if (fwd) tri_rows_cpl<true, NT><<<rows, th, smem, s>>>(V, b, chn, y);
                 else tri_rows_cpl<false, NT><<<rows, th, smem, s>>>(V, b, chn, y);

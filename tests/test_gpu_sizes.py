@@ -24,7 +24,7 @@ def _case(n_u, n=16, theta=0.5, seed=0):
     return P, O, p, op, grid, u, v, z, rng
 
 
-@pytest.mark.parametrize("n_u", [64, 100, 128, 256])
+@pytest.mark.parametrize("n_u", [33, 64, 100, 128, 256, 300, 512])
 @pytest.mark.parametrize("records", [False, True])
 def test_operator_and_smoothers(n_u, records):
     P, O, p, op, grid, u, v, z, rng = _case(n_u)
