@@ -1,5 +1,5 @@
 // TRI family: partitioned local KKT solves (one CTA per block row, four
-// nodes per thread).
+// nodes per thread, everything in registers).
 //
 // Same block-row operation as tri_block (tk_tri.cu; reference kkt.py:298-389
 // DiagonalSolver.solve_all, smoothers.py:61-76 jacobi_apply): residual,
@@ -8,22 +8,23 @@
 // after the first), the nodes are partitioned into T = 32W contiguous chunks
 // of four, one per thread:
 //
-//   * every thread eliminates its chunk's three interior nodes by two Thomas
-//     sweeps in registers: bottom-up (the first interior node in terms of the
-//     two chunk interfaces) and top-down (factors T_k = D'_k^{-1} U_k and
-//     D'_k^{-1} kept in registers for the back-substitution),
-//   * the T interface nodes (the last node of every chunk) form a 2x2-block
-//     tridiagonal system, solved by parallel cyclic reduction with a
-//     ping-pong shared exchange (one barrier per step),
+//   * phase 1: the thread forms the residual of its chunk in registers from
+//     16-byte loads (the vector data of the row was staged into the thread's
+//     own shared-memory slots by cp.async while the previous row was solved;
+//     the stage data K, C comes from L2, prefetched by a TMA bulk prefetch),
+//   * two Thomas sweeps over the chunk's three interior nodes: bottom-up (the
+//     first interior node in terms of the two chunk interfaces) and top-down
+//     (factors T_k = D'_k^{-1} U_k and D'_k^{-1} kept for the back-substitution),
+//   * the T interface nodes (the last node of every chunk) form a symmetric
+//     2x2-block tridiagonal system, solved by parallel cyclic reduction with
+//     a ping-pong shared exchange (one barrier per step),
 //   * a forward rhs sweep with the known left interface and a
-//     back-substitution recover the interior.
+//     back-substitution recover the interior; the output is written with
+//     16-byte stores.
 //
 // The scalar system Q_z w = r_z rides along through the same steps.  The grid
-// is persistent (a few CTAs per SM loop over the block rows), so loads of one
-// CTA overlap the solves of the others.  Nodes >= n pad the system to 4T
-// nodes with identity blocks.  Node j lives at PI(j) = j + j/16 in the node
-// arrays: conflict-free both for the coalesced phases (thread t on node
-// t + T s) and the chunk phases (thread t on node 4t + k).
+// is persistent (two CTAs per SM loop over the block rows).  Nodes >= n pad
+// the system to 4T nodes with identity blocks.
 #include "tk_tri.cuh"
 
 namespace tk {
@@ -31,15 +32,19 @@ namespace tk {
 namespace {
 
 constexpr int kChunk = 4;        // nodes per thread
-constexpr int kNodeArrays = 7;   // F0 F1 FW KD KS KB SV
-constexpr int kXch = 13;         // doubles per thread in one exchange slot
+#ifndef TK_PART_STAGE
+#define TK_PART_STAGE 1          // cp.async staging of the next row's vectors
+#endif
+#ifndef TK_PART_MINB
+#define TK_PART_MINB 2           // CTAs per SM the W=4 build is register-limited to
+#endif
+constexpr bool kStage = TK_PART_STAGE != 0;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kPX = 19;          // symmetric PCR: published doubles per row
+constexpr int kSgC = 12, kSgN = 12;   // staged chunk arrays / neighbour values per thread
+constexpr int kFac = 9;          // per interior node: T_k (4), D'_k^{-1} (3), scalar t_k, 1/d'_k
 
 struct S2 { double a, b, c; };   // symmetric [[a b][b c]]
-
-__device__ __forceinline__ S2 inv_s2(double a, double b, double c) {
-    const double id = 1.0 / (a * c - b * b);
-    return {c * id, -b * id, a * id};
-}
 
 }  // namespace
 
@@ -47,43 +52,262 @@ template <int W>
 struct PartCta {
     static constexpr int T = 32 * W;          // threads = chunks = interface nodes
     static constexpr int P = kChunk * T;      // padded system size
-    static constexpr int PP = P + P / 16 + 1; // padded node-array length
     static constexpr int64_t smem_bytes() {
-        return ((int64_t)kNodeArrays * PP + (int64_t)kXch * T) * 8;
+        return ((int64_t)(2 * kPX + (kStage ? 4 * kSgC + kSgN : 0)) * T) * 8;
     }
-    static constexpr int min_blocks() { return W >= 8 ? 1 : 12 / W; }
+    static constexpr int min_blocks() { return W >= 8 ? 1 : (TK_PART_MINB * 4) / W; }
 };
+
+// Four consecutive nodes [j0, j0+4) of segment p + o (zero beyond n).
+// FULL: n is a multiple of four chunks and every segment is 16-byte aligned.
+template <bool FULL>
+__device__ __forceinline__ void ld4(const double* __restrict__ p, int64_t o, int j0, int n,
+                                    bool on, double (&r)[4]) {
+    if (!on) { r[0] = r[1] = r[2] = r[3] = 0.0; return; }
+    const double* a = p + o + j0;
+    if (FULL || (j0 + 3 < n && ((reinterpret_cast<uintptr_t>(a) & 15) == 0))) {
+        const double2 u = *reinterpret_cast<const double2*>(a);
+        const double2 v = *reinterpret_cast<const double2*>(a + 2);
+        r[0] = u.x; r[1] = u.y; r[2] = v.x; r[3] = v.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = (j0 + k < n) ? a[k] : 0.0;
+    }
+}
+template <bool FULL>
+__device__ __forceinline__ void st4(double* __restrict__ p, int64_t o, int j0, int n,
+                                    const double (&r)[4]) {
+    double* a = p + o + j0;
+    if (FULL || (j0 + 3 < n && ((reinterpret_cast<uintptr_t>(a) & 15) == 0))) {
+        *reinterpret_cast<double2*>(a) = make_double2(r[0], r[1]);
+        *reinterpret_cast<double2*>(a + 2) = make_double2(r[2], r[3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (j0 + k < n) a[k] = r[k];
+    }
+}
+// single node j of segment p + o (zero outside [0, n))
+__device__ __forceinline__ double ld1(const double* __restrict__ p, int64_t o, int j, int n,
+                                      bool on) {
+    return (on && j >= 0 && j < n) ? p[o + j] : 0.0;
+}
+
+// L2 prefetch of [p, p + len) doubles (TMA bulk prefetch; 16-byte granules)
+__device__ __forceinline__ void pf_l2(const double* p, int64_t len) {
+    if (!p || len <= 0) return;
+    uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+    uintptr_t e = (reinterpret_cast<uintptr_t>(p + len) + 15) & ~(uintptr_t)15;
+    while (a < e) {
+        const uint32_t sz = (uint32_t)((e - a) > (1u << 20) ? (1u << 20) : (e - a));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(sz) : "memory");
+        a += sz;
+    }
+}
+
+// 1/x without the IEEE slow path: MUFU estimate + two Newton steps
+__device__ __forceinline__ double frcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+__device__ __forceinline__ S2 inv_s2f(double a, double b, double c) {
+    const double id = frcp(a * c - b * b);
+    return {c * id, -b * id, a * id};
+}
+
+
+// cp.async (LDGSTS) staging of the next block row's vector data: every thread
+// copies exactly the nodes it reads later into its own slots, so only its own
+// wait_group is needed (no barrier).  8-byte copies zero-fill out-of-range nodes.
+__device__ __forceinline__ void cpa16(double* dst, const double* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa8(double* dst, const double* src, bool on) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(on ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <bool FULL>
+__device__ __forceinline__ void stage4(double* dst, const double* p, int64_t o, int j0, int n, bool on,
+                                       const double* dummy) {
+    if (FULL && on) {
+        cpa16(dst, p + o + j0);
+        cpa16(dst + 2, p + o + j0 + 2);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool v = on && j0 + k < n;
+            cpa8(dst + k, v ? p + o + j0 + k : dummy, v);
+        }
+    }
+}
+__device__ __forceinline__ void stage1(double* dst, const double* p, int64_t o, int j, int n, bool on,
+                                       const double* dummy) {
+    const bool v = on && j >= 0 && j < n;
+    cpa8(dst, v ? p + o + j : dummy, v);
+}
+
+// vector sources of block row i (slab-relative offsets; couplings per MODE)
+struct RowSrc {
+    int64_t ov, ou, oz, om, ol;
+    const double* uprev;
+    const double* munext;
+    bool has_vm, has_uzl;
+};
+template <int MODE>
+__device__ __forceinline__ RowSrc row_src(const TView& V, const double* x, const double* chain, int i) {
+    const Lay& L = V.lay;
+    const int64_t bs = V.sl.base;
+    RowSrc r;
+    r.has_vm = i >= 1;
+    r.has_uzl = i < L.N;
+    r.ov = L.off_v(i) - bs; r.ou = L.off_u(i) - bs; r.oz = L.off_z(i) - bs;
+    r.om = L.off_mu(i) - bs; r.ol = L.off_l(i) - bs;
+    r.uprev = nullptr;
+    r.munext = nullptr;
+    if (MODE == 0) {
+        if (x) { r.uprev = V.sl.uprev(L, x, i); r.munext = V.sl.munext(L, x, i); }
+    } else if (MODE == 1) {
+        if (i >= 1) r.uprev = chain + (size_t)(i - 1) * V.n;
+    } else {
+        if (i < L.N) r.munext = chain + (size_t)(i + 1) * V.n;
+    }
+    return r;
+}
+// staged arrays (chunk nodes): b v m u z l, x v u z l m, uprev, munext;
+// neighbours: b_m, x_v, uprev at j0-1 / j0+4, then x u z l at j0-1 / j0+4
+template <bool FULL, int T>
+__device__ __forceinline__ void stage_row(double* SG, const RowSrc& r, const double* b, const double* x,
+                                          bool hx, int n, int j0) {
+    const int t = threadIdx.x;
+    double* c = SG + 4 * t;                   // [kSgC][4T]
+    double* nb = SG + kSgC * 4 * T + t;       // [kSgN][T]
+    const int jL = j0 - 1, jR = j0 + 4;
+    stage4<FULL>(c + 0 * 4 * T, b, r.ov, j0, n, r.has_vm, b);
+    stage4<FULL>(c + 1 * 4 * T, b, r.om, j0, n, r.has_vm, b);
+    stage4<FULL>(c + 2 * 4 * T, b, r.ou, j0, n, r.has_uzl, b);
+    stage4<FULL>(c + 3 * 4 * T, b, r.oz, j0, n, r.has_uzl, b);
+    stage4<FULL>(c + 4 * 4 * T, b, r.ol, j0, n, r.has_uzl, b);
+    stage1(nb + 0 * T, b, r.om, jL, n, r.has_vm, b);
+    stage1(nb + 1 * T, b, r.om, jR, n, r.has_vm, b);
+    const bool up = r.has_vm && r.uprev != nullptr, mn = r.has_uzl && r.munext != nullptr;
+    stage4<FULL>(c + 10 * 4 * T, r.uprev, 0, j0, n, up, b);
+    stage4<FULL>(c + 11 * 4 * T, r.munext, 0, j0, n, mn, b);
+    stage1(nb + 4 * T, r.uprev, 0, jL, n, up, b);
+    stage1(nb + 5 * T, r.uprev, 0, jR, n, up, b);
+    if (hx) {
+        stage4<FULL>(c + 5 * 4 * T, x, r.ov, j0, n, r.has_vm, b);
+        stage4<FULL>(c + 6 * 4 * T, x, r.ou, j0, n, r.has_uzl, b);
+        stage4<FULL>(c + 7 * 4 * T, x, r.oz, j0, n, r.has_uzl, b);
+        stage4<FULL>(c + 8 * 4 * T, x, r.ol, j0, n, r.has_uzl, b);
+        stage4<FULL>(c + 9 * 4 * T, x, r.om, j0, n, r.has_vm, b);
+        stage1(nb + 2 * T, x, r.ov, jL, n, r.has_vm, b);
+        stage1(nb + 3 * T, x, r.ov, jR, n, r.has_vm, b);
+        stage1(nb + 6 * T, x, r.ou, jL, n, r.has_uzl, b);
+        stage1(nb + 7 * T, x, r.ou, jR, n, r.has_uzl, b);
+        stage1(nb + 8 * T, x, r.oz, jL, n, r.has_uzl, b);
+        stage1(nb + 9 * T, x, r.oz, jR, n, r.has_uzl, b);
+        stage1(nb + 10 * T, x, r.ol, jL, n, r.has_uzl, b);
+        stage1(nb + 11 * T, x, r.ol, jR, n, r.has_uzl, b);
+    }
+    cpa_commit();
+}
+
+
+#ifdef TK_PROF
+// per-phase cycles of CTA 0 / thread 0, accumulated over its block rows
+__device__ long long g_part_prof[10];
+#define TKPP(slot)                                                          \
+    do {                                                                    \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                          \
+            const long long c_ = clock64();                                 \
+            if (slot > 0) g_part_prof[slot] += c_ - g_part_last;            \
+            g_part_last = c_;                                               \
+        }                                                                   \
+    } while (0)
+extern "C" int tk_debug_part_prof(long long* out10) {
+    const int e = cudaMemcpyFromSymbol(out10, g_part_prof, sizeof(long long) * 10);
+    long long z[10] = {0};
+    cudaMemcpyToSymbol(g_part_prof, z, sizeof(z));
+    return e == cudaSuccess ? 0 : 2;
+}
+#else
+#define TKPP(slot) \
+    do {           \
+    } while (0)
+#endif
 
 // MODE 0: Jacobi / D^{-1} b (couplings from x through the slab);
 // MODE 1 / 2: pass 3 of the forward / backward substitution (coupling from
 // the chain vector, no update).
-template <int W, int MODE>
+//
+// Every phase works in chunk order: thread t owns nodes [4t, 4t+4) of every
+// segment, loaded with two 16-byte loads per segment (all of a block row's
+// loads are independent, so a CTA has its whole row in flight at once) and
+// kept in registers through the solve; the neighbours j0-1 and j0+4 come
+// from single loads (L1 hits: the adjacent threads load those lines).
+template <int W, int MODE, bool FULL>
 __global__ void __launch_bounds__(32 * W, PartCta<W>::min_blocks())
 tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ x,
               double* __restrict__ y, double omega, const double* __restrict__ chain) {
     using Cf = PartCta<W>;
-    constexpr int T = Cf::T, PP = Cf::PP;
-    constexpr int NA = kChunk;           // nodes per thread, both layouts
+    constexpr int T = Cf::T;
+    constexpr int NA = kChunk;
     extern __shared__ __align__(16) double sm[];
     const Lay& L = V.lay;
-    const int n = V.n;
+    const int n = FULL ? Cf::P : V.n;
     const int tid = threadIdx.x;
+    __builtin_assume(tid < T);
     const double kap = V.kappa, k2 = kap * kap;
     const double* Qz = V.Qz;
-
-    double* F0 = sm;
-    double* F1 = sm + PP;
-    double* FW = sm + 2 * PP;
-    double* KD = sm + 3 * PP;   // K diag
-    double* KS = sm + 4 * PP;   // K sup  K_{j,j+1}
-    double* KB = sm + 5 * PP;   // K sub  K_{j+1,j}
-    double* SV = sm + 6 * PP;   // v (coalesced phases)
-    double* XB[2] = {KD, sm + kNodeArrays * PP};   // exchange slots (slot 0 over KD..SV)
+    double* PX[2] = {sm, sm + kPX * T};    // PCR ping-pong slots
+    double* XB[1] = {PX[1]};               // exchange 1 (12 per thread; PX[1] is first written at step 2)
+    double* SG = sm + 2 * kPX * T;         // staged vector data of the next row [kSgC*4 + kSgN][T]
+    double* XO = nullptr;                  // interface solution (a PCR slot)
+    double* LAM = nullptr;                 // first lam of every chunk (the other PCR slot)
 
     const int j0 = kChunk * tid;
+    const int jL = j0 - 1, jR = j0 + NA;
+#ifdef TK_PROF
+    long long g_part_last = 0;
+#endif
     const int64_t bs = V.sl.base;
+    // constant weights at the chunk nodes (diagonal, super-diagonal)
+    double qzd[NA], qzs[NA], qzb[NA];
+    ld4<FULL>(Qz, n, j0, n, true, qzd);
+    ld4<FULL>(Qz, 2 * n, j0, n, true, qzs);
+    ld4<FULL>(Qz, 0, j0, n, true, qzb);
+    const double qzsL = ld1(Qz, 2 * n, jL, n, true), qzbR = ld1(Qz, 0, jR, n, true);
+
+    if (kStage && V.sl.r0 + (int)blockIdx.x < V.sl.r1)
+        stage_row<FULL, T>(SG, row_src<MODE>(V, x, chain, V.sl.r0 + blockIdx.x), b, x,
+                           MODE == 0 && x != nullptr, n, j0);
     for (int i = V.sl.r0 + blockIdx.x; i < V.sl.r1; i += gridDim.x) {
+        if (kStage) cpa_wait();
         const bool has_vm = i >= 1, has_uzl = i < L.N;
+        if (tid == 0 && i + (int)gridDim.x < V.sl.r1) {   // next row's stage data -> L2
+            const int i2 = i + gridDim.x;
+            if (!kStage) {
+                const int64_t q0 = L.start(i2) - bs;
+                const int64_t q1 = (i2 == L.N ? L.dim() : L.start(i2 + 1)) - bs;
+                pf_l2(b + q0, q1 - q0);
+                if (MODE == 0 && x) pf_l2(x + q0, q1 - q0);
+            }
+            if (i2 < L.N) {
+                pf_l2(V.Ki(i2, n), 3 * n);
+                if (i2 >= 1) pf_l2(V.Ci(i2, n), 3 * n);
+            }
+        }
         const double* Qv = (i == L.N) ? V.Ql : V.Qm;
         const double* Qu = (i == L.N - 1) ? V.Ql : V.Qm;
         const double* K = has_uzl ? V.Ki(i, n) : nullptr;
@@ -99,157 +323,203 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         } else {
             if (i < L.N) munext = chain + (size_t)(i + 1) * n;
         }
-        const double* xu = MODE == 0 ? x : nullptr;
         const bool hx = MODE == 0 && x != nullptr;
+        const bool hc = C != nullptr;
+        TKPP(0);
 
-        // ---- phase A (coalesced): residual and K diagonals.  All loads are
-        // predicated on warp-uniform flags (no branches), so the compiler can
-        // batch them across the NA nodes of a thread.
-        double pm[NA];
+        // ---- phase 1: residual of the chunk in registers
+        double f0[NA], f1[NA], fw[NA], pm[NA], kd[NA], ks[NA], kb[NA];
+        double ksL, kbR;
+        {
+            const double* sgc = SG + 4 * tid;
+            const double* sgn = SG + kSgC * 4 * T + tid;
+            auto g4 = [&](int a, double (&r)[NA]) {
+                if (kStage) {
+                    const double2 u = *reinterpret_cast<const double2*>(sgc + a * 4 * T);
+                    const double2 v = *reinterpret_cast<const double2*>(sgc + a * 4 * T + 2);
+                    r[0] = u.x; r[1] = u.y; r[2] = v.x; r[3] = v.y;
+                    return;
+                }
+                const bool up = has_vm && uprev != nullptr, mnx = has_uzl && munext != nullptr;
+                switch (a) {
+                    case 0: ld4<FULL>(b, ov, j0, n, has_vm, r); break;
+                    case 1: ld4<FULL>(b, om, j0, n, has_vm, r); break;
+                    case 2: ld4<FULL>(b, ou, j0, n, has_uzl, r); break;
+                    case 3: ld4<FULL>(b, oz, j0, n, has_uzl, r); break;
+                    case 4: ld4<FULL>(b, ol, j0, n, has_uzl, r); break;
+                    case 5: ld4<FULL>(x, ov, j0, n, has_vm, r); break;
+                    case 6: ld4<FULL>(x, ou, j0, n, has_uzl, r); break;
+                    case 7: ld4<FULL>(x, oz, j0, n, has_uzl, r); break;
+                    case 8: ld4<FULL>(x, ol, j0, n, has_uzl, r); break;
+                    case 9: ld4<FULL>(x, om, j0, n, has_vm, r); break;
+                    case 10: ld4<FULL>(uprev, 0, j0, n, up, r); break;
+                    default: ld4<FULL>(munext, 0, j0, n, mnx, r); break;
+                }
+            };
+            auto g1 = [&](int a) -> double {
+                if (kStage) return sgn[a * T];
+                const bool up = has_vm && uprev != nullptr;
+                switch (a) {
+                    case 0: return ld1(b, om, jL, n, has_vm);
+                    case 1: return ld1(b, om, jR, n, has_vm);
+                    case 2: return ld1(x, ov, jL, n, has_vm);
+                    case 3: return ld1(x, ov, jR, n, has_vm);
+                    case 4: return ld1(uprev, 0, jL, n, up);
+                    case 5: return ld1(uprev, 0, jR, n, up);
+                    case 6: return ld1(x, ou, jL, n, has_uzl);
+                    case 7: return ld1(x, ou, jR, n, has_uzl);
+                    case 8: return ld1(x, oz, jL, n, has_uzl);
+                    case 9: return ld1(x, oz, jR, n, has_uzl);
+                    case 10: return ld1(x, ol, jL, n, has_uzl);
+                    default: return ld1(x, ol, jR, n, has_uzl);
+                }
+            };
+            double rv[NA], rm[NA], xv[NA], up[NA];
+            g4(0, rv);
+            g4(1, rm);
+            g4(2, f0);
+            g4(3, fw);
+            g4(4, f1);
+            ld4<FULL>(K, n, j0, n, has_uzl, kd);
+            ld4<FULL>(K, 2 * n, j0, n, has_uzl, ks);
+            ld4<FULL>(K, 0, j0, n, has_uzl, kb);
+            ksL = ld1(K, 2 * n, jL, n, has_uzl);
+            kbR = ld1(K, 0, jR, n, has_uzl);
+            if (hx) g4(5, xv); else xv[0] = xv[1] = xv[2] = xv[3] = 0.0;
+            g4(10, up);
+            // v at the chunk and its two neighbours
+            double vv[NA];
+            const double bmL = g1(0), bmR = g1(1);
+            const double xvL = hx ? g1(2) : 0.0, xvR = hx ? g1(3) : 0.0;
+            const double upL = g1(4), upR = g1(5);
 #pragma unroll
-        for (int t = 0; t < NA; ++t) {
-            const int j = tid + T * t;
-            const bool in = j < n;
-            const int jj = in ? j : n - 1;
-            const int jm = jj > 0 ? jj - 1 : jj, jp = jj < n - 1 ? jj + 1 : jj;
-            const bool lo = in && jj > 0, hi = in && jj < n - 1;
-            const bool vm = in && has_vm, uz = in && has_uzl, cc = in && C != nullptr;
-            double rv = vm ? b[ov + jj] : 0.0;
-            double rm = vm ? b[om + jj] : 0.0;
-            double ru = uz ? b[ou + jj] : 0.0;
-            double rz = uz ? b[oz + jj] : 0.0;
-            double rl = uz ? b[ol + jj] : 0.0;
-            const double kd = uz ? K[n + jj] : 0.0;
-            const double ks = (uz && hi) ? K[2 * n + jj] : 0.0;
-            const double kb = (uz && hi) ? K[jp] : 0.0;
+            for (int k = 0; k < NA; ++k) vv[k] = -((rm[k] + xv[k]) - up[k]);
+            const double vL = -((bmL + xvL) - upL), vR = -((bmR + xvR) - upR);
             if (hx) {
-                const double ksm = (uz && lo) ? K[2 * n + jm] : 0.0;
-                const double kbj = (uz && lo) ? K[jj] : 0.0;
-                const double cd = cc ? C[n + jj] : 0.0;
-                const double cs = (cc && hi) ? C[2 * n + jj] : 0.0;
-                const double cb = (cc && lo) ? C[jj] : 0.0;
-                const double csm = (cc && lo) ? C[2 * n + jm] : 0.0;
-                const double cbp = (cc && hi) ? C[jp] : 0.0;
-                const double xv0 = vm ? x[ov + jj] : 0.0;
-                const double xvm = (vm && lo) ? x[ov + jm] : 0.0;
-                const double xvp = (vm && hi) ? x[ov + jp] : 0.0;
-                const double xm0 = vm ? x[om + jj] : 0.0;
-                const double xu0 = uz ? x[ou + jj] : 0.0;
-                const double xum = (uz && lo) ? x[ou + jm] : 0.0;
-                const double xup = (uz && hi) ? x[ou + jp] : 0.0;
-                const double xz0 = uz ? x[oz + jj] : 0.0;
-                const double xzm = (uz && lo) ? x[oz + jm] : 0.0;
-                const double xzp = (uz && hi) ? x[oz + jp] : 0.0;
-                const double xl0 = uz ? x[ol + jj] : 0.0;
-                const double xlm = (uz && lo) ? x[ol + jm] : 0.0;
-                const double xlp = (uz && hi) ? x[ol + jp] : 0.0;
-                const double up = (vm && uprev) ? uprev[jj] : 0.0;
-                const double mn = (uz && munext) ? munext[jj] : 0.0;
-                // weights (L1-resident)
-                const double qvd = Qv[n + jj], qvb = lo ? Qv[jj] : 0.0, qvs = hi ? Qv[2 * n + jj] : 0.0;
-                const double qud = Qu[n + jj], qub = lo ? Qu[jj] : 0.0, qus = hi ? Qu[2 * n + jj] : 0.0;
-                const double qzd = Qz[n + jj], qzb = lo ? Qz[jj] : 0.0, qzs = hi ? Qz[2 * n + jj] : 0.0;
-                if (has_vm) {
-                    double av = (qvd * xv0 + qvb * xvm + qvs * xvp) - xm0;
-                    av += cd * xl0 + csm * xlm + cbp * xlp;
-                    rv -= av;
-                    rm += xv0;
-                    rm -= up;
-                }
-                if (has_uzl) {
-                    ru -= (qud * xu0 + qub * xum + qus * xup) + (kd * xl0 + ksm * xlm + kb * xlp);
-                    ru -= mn;
-                    const double qzz = qzd * xz0 + qzb * xzm + qzs * xzp;
-                    rz -= qzz + kap * (qzd * xl0 + qzb * xlm + qzs * xlp);
-                    double al = (kd * xu0 + kbj * xum + ks * xup) + kap * qzz;
-                    al += cd * xv0 + cb * xvm + cs * xvp;
-                    rl -= al;
-                }
-            } else {
-                if (vm && uprev) rm -= uprev[jj];
-                if (uz && munext) ru -= munext[jj];
-            }
-            if (!in) { rv = rm = ru = rz = rl = 0.0; }
-            const int q = PI(j);
-            pm[t] = rv;
-            SV[q] = -rm;
-            F0[q] = ru;
-            F1[q] = rl - kap * rz;
-            FW[q] = rz;
-            KD[q] = kd;
-            KS[q] = ks;
-            KB[q] = kb;
-        }
-        __syncthreads();
-        // ---- phase B (coalesced): v, the C v coupling, the mu part without C^T lam
-        if (has_vm) {
-            double xo[NA], xm[NA];
+                double xu[NA], xz[NA], xl[NA], xm[NA], mn[NA];
+                g4(6, xu);
+                g4(7, xz);
+                g4(8, xl);
+                g4(9, xm);
+                g4(11, mn);
+                const double xuL = g1(6), xuR = g1(7);
+                const double xzL = g1(8), xzR = g1(9);
+                const double xlL = g1(10), xlR = g1(11);
+                double cd[NA], cs[NA], cb[NA], qvd[NA], qvs[NA], qvb[NA], qud[NA], qus[NA], qub[NA];
+                ld4<FULL>(C, n, j0, n, hc, cd);
+                ld4<FULL>(C, 2 * n, j0, n, hc, cs);
+                ld4<FULL>(C, 0, j0, n, hc, cb);
+                const double csL = ld1(C, 2 * n, jL, n, hc), cbR = ld1(C, 0, jR, n, hc);
+                ld4<FULL>(Qv, n, j0, n, true, qvd);
+                ld4<FULL>(Qv, 2 * n, j0, n, true, qvs);
+                ld4<FULL>(Qv, 0, j0, n, true, qvb);
+                ld4<FULL>(Qu, n, j0, n, true, qud);
+                ld4<FULL>(Qu, 2 * n, j0, n, true, qus);
+                ld4<FULL>(Qu, 0, j0, n, true, qub);
 #pragma unroll
-            for (int t = 0; t < NA; ++t) {
-                const int j = tid + T * t;
-                xo[t] = (xu && j < n) ? xu[ov + j] : 0.0;
-                xm[t] = (xu && j < n && !has_uzl) ? xu[om + j] : 0.0;
-            }
-#pragma unroll
-            for (int t = 0; t < NA; ++t) {
-                const int j = tid + T * t;
-                if (j < n) {
-                    const double vj = SV[PI(j)];
-                    const double vm = j > 0 ? SV[PI(j - 1)] : 0.0;
-                    const double vp = j < n - 1 ? SV[PI(j + 1)] : 0.0;
-                    double qv = Qv[n + j] * vj;
-                    if (j > 0) qv += Qv[j] * vm;
-                    if (j < n - 1) qv += Qv[2 * n + j] * vp;
-                    pm[t] = qv - pm[t];
-                    if (C) {
-                        double cv = C[n + j] * vj;
-                        if (j > 0) cv += C[j] * vm;
-                        if (j < n - 1) cv += C[2 * n + j] * vp;
-                        F1[PI(j)] -= cv;
+                for (int k = 0; k < NA; ++k) {
+                    const int j = j0 + k;
+                    const bool lo = j > 0, hi = j < n - 1;
+                    const double xvm = k > 0 ? xv[k - 1] : xvL, xvp = k < NA - 1 ? xv[k + 1] : xvR;
+                    const double xum = k > 0 ? xu[k - 1] : xuL, xup = k < NA - 1 ? xu[k + 1] : xuR;
+                    const double xzm = k > 0 ? xz[k - 1] : xzL, xzp = k < NA - 1 ? xz[k + 1] : xzR;
+                    const double xlm = k > 0 ? xl[k - 1] : xlL, xlp = k < NA - 1 ? xl[k + 1] : xlR;
+                    const double ksm = k > 0 ? ks[k - 1] : ksL, kbp = k < NA - 1 ? kb[k + 1] : kbR;
+                    const double csm = k > 0 ? cs[k - 1] : csL, cbp = k < NA - 1 ? cb[k + 1] : cbR;
+                    const double qb = lo ? 1.0 : 0.0, qs = hi ? 1.0 : 0.0;
+                    if (has_vm) {
+                        double av = (qvd[k] * xv[k] + qb * qvb[k] * xvm + qs * qvs[k] * xvp) - xm[k];
+                        if (hc) av += cd[k] * xl[k] + qb * csm * xlm + qs * cbp * xlp;
+                        rv[k] -= av;
                     }
-                    y[ov + j] = xo[t] + omega * vj;
-                    if (!has_uzl) y[om + j] = xm[t] + omega * pm[t];
+                    if (has_uzl) {
+                        f0[k] -= (qud[k] * xu[k] + qb * qub[k] * xum + qs * qus[k] * xup) +
+                                 (kd[k] * xl[k] + qb * ksm * xlm + qs * kbp * xlp);
+                        f0[k] -= mn[k];
+                        const double qzz = qzd[k] * xz[k] + qb * qzb[k] * xzm + qs * qzs[k] * xzp;
+                        fw[k] -= qzz + kap * (qzd[k] * xl[k] + qb * qzb[k] * xlm + qs * qzs[k] * xlp);
+                        double al = (kd[k] * xu[k] + qb * kb[k] * xum + qs * ks[k] * xup) + kap * qzz;
+                        if (hc) al += cd[k] * xv[k] + qb * cb[k] * xvm + qs * cs[k] * xvp;
+                        f1[k] -= al;
+                    }
                 }
+            } else if (has_uzl && munext) {
+                double mn[NA];
+                g4(11, mn);
+#pragma unroll
+                for (int k = 0; k < NA; ++k) f0[k] -= mn[k];
+            }
+            // v, the mu part without C^T lam, C v into the lam row
+            double qvd[NA], qvs[NA], qvb[NA], cd[NA], cs[NA], cb[NA];
+            ld4<FULL>(Qv, n, j0, n, has_vm, qvd);
+            ld4<FULL>(Qv, 2 * n, j0, n, has_vm, qvs);
+            ld4<FULL>(Qv, 0, j0, n, has_vm, qvb);
+            ld4<FULL>(C, n, j0, n, hc, cd);
+            ld4<FULL>(C, 2 * n, j0, n, hc, cs);
+            ld4<FULL>(C, 0, j0, n, hc, cb);
+#pragma unroll
+            for (int k = 0; k < NA; ++k) {
+                const int j = j0 + k;
+                const bool in = j < n, lo = j > 0, hi = j < n - 1;
+                const double vm = (k > 0 ? vv[k - 1] : vL) * (lo ? 1.0 : 0.0);
+                const double vp = (k < NA - 1 ? vv[k + 1] : vR) * (hi ? 1.0 : 0.0);
+                pm[k] = (qvd[k] * vv[k] + qvb[k] * vm + qvs[k] * vp) - rv[k];
+                f1[k] = f1[k] - kap * fw[k];
+                if (hc) f1[k] -= cd[k] * vv[k] + cb[k] * vm + cs[k] * vp;
+                if (!in) { f0[k] = f1[k] = fw[k] = pm[k] = vv[k] = 0.0; }
+            }
+            if (has_vm) {
+                double o[NA];
+                if (hx) {
+#pragma unroll
+                    for (int k = 0; k < NA; ++k) o[k] = xv[k] + omega * vv[k];
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NA; ++k) o[k] = omega * vv[k];
+                }
+                st4<FULL>(y, ov, j0, n, o);
             }
         }
-        if (!has_uzl) {   // last block (v_N, mu_N) is done
-            __syncthreads();
+        TKPP(1);
+        if (!has_uzl) {   // last block (v_N, mu_N): mu = Qv v - r_v
+            double xm[NA], o[NA];
+            ld4<FULL>(x, om, j0, n, hx, xm);
+#pragma unroll
+            for (int k = 0; k < NA; ++k) o[k] = xm[k] + omega * pm[k];
+            st4<FULL>(y, om, j0, n, o);
             continue;
         }
-        __syncthreads();
 
-        // ---- chunk phase.  D_k = [[Qu, K], [K, -k^2 Qz]]_kk,
+        // ---- chunk solve.  D_k = [[Qu, K], [K, -k^2 Qz]]_kk,
         // U_k = [[Qu_{k,k+1}, K_{k+1,k}], [K_{k,k+1}, -k^2 Qz_{k,k+1}]]; the
         // scalar system has diagonal Qz_kk and coupling Qz_{k,k+1}.
-        auto Dget = [&](int j, double& a, double& bb, double& c) {
-            const bool in = j < n;
-            a = in ? Qu[n + j] : 1.0;
-            bb = KD[PI(j)];
-            c = in ? -k2 * Qz[n + j] : -1.0;
+        double qud[NA], qus[NA];
+        ld4<FULL>(Qu, n, j0, n, true, qud);
+        ld4<FULL>(Qu, 2 * n, j0, n, true, qus);
+        const double qusL = ld1(Qu, 2 * n, jL, n, true);
+        auto Dk = [&](int k, double& a, double& bb, double& c) {
+            const bool in = j0 + k < n;
+            a = in ? qud[k] : 1.0;
+            bb = kd[k];
+            c = in ? -k2 * qzd[k] : -1.0;
         };
-        auto Uget = [&](int j, double& u0, double& u1, double& u2, double& u3) {
+        auto Uk = [&](int k, double& u0, double& u1, double& u2, double& u3) {   // k = -1..NA-1
+            const int j = j0 + k;
             const bool cpl = j >= 0 && j < n - 1;
-            u0 = cpl ? Qu[2 * n + j] : 0.0;
-            u1 = cpl ? KB[PI(j)] : 0.0;
-            u2 = cpl ? KS[PI(j)] : 0.0;
-            u3 = cpl ? -k2 * Qz[2 * n + j] : 0.0;
+            u0 = cpl ? (k >= 0 ? qus[k] : qusL) : 0.0;
+            u1 = cpl ? (k + 1 < NA ? kb[k + 1] : kbR) : 0.0;
+            u2 = cpl ? (k >= 0 ? ks[k] : ksL) : 0.0;
+            u3 = cpl ? -k2 * (k >= 0 ? qzs[k] : qzsL) : 0.0;
         };
-        auto dzs = [&](int j) -> double { return j < n ? Qz[n + j] : 1.0; };
-        auto ezs = [&](int j) -> double { return (j >= 0 && j < n - 1) ? Qz[2 * n + j] : 0.0; };
-
-        double fa[NA], fb[NA], fw[NA];
-#pragma unroll
-        for (int k = 0; k < NA; ++k) {
-            const int q = PI(j0 + k);
-            fa[k] = F0[q];
-            fb[k] = F1[q];
-            fw[k] = FW[q];
-        }
-        // couplings needed after the exchange slot 0 (over KD..SV) is reused
+        auto dzs = [&](int k) -> double { return j0 + k < n ? qzd[k] : 1.0; };
+        auto ezs = [&](int k) -> double {   // coupling (j0+k, j0+k+1), k = -1..NA-1
+            const int j = j0 + k;
+            return (j >= 0 && j < n - 1) ? (k >= 0 ? qzs[k] : qzsL) : 0.0;
+        };
         double ul0, ul1, ul2, ul3, ur0, ur1, ur2, ur3;
-        Uget(j0 - 1, ul0, ul1, ul2, ul3);            // left interface -> node 0
-        Uget(j0 + NA - 1, ur0, ur1, ur2, ur3);       // own interface -> next chunk
-        const double sel = ezs(j0 - 1), ser = ezs(j0 + NA - 1);
+        Uk(-1, ul0, ul1, ul2, ul3);
+        Uk(NA - 1, ur0, ur1, ur2, ur3);
+        const double sel = ezs(-1), ser = ezs(NA - 1);
 
         // step A (bottom-up over the interior): y_0 = iDh (h + H x_R - U_{-1}^T x_L)
         double ha, hb, H00, H01, H10, H11;
@@ -257,84 +527,86 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         double s_idh, s_hh, s_Hh;
         {
             double da, db, dc;
-            Dget(j0 + NA - 2, da, db, dc);
-            ha = fa[NA - 2];
-            hb = fb[NA - 2];
+            Dk(NA - 2, da, db, dc);
+            ha = f0[NA - 2];
+            hb = f1[NA - 2];
             double u0, u1, u2, u3;
-            Uget(j0 + NA - 2, u0, u1, u2, u3);
+            Uk(NA - 2, u0, u1, u2, u3);
             H00 = -u0; H01 = -u1; H10 = -u2; H11 = -u3;
-            double sd = dzs(j0 + NA - 2);
+            double sd = dzs(NA - 2);
             s_hh = fw[NA - 2];
-            s_Hh = -ezs(j0 + NA - 2);
+            s_Hh = -ezs(NA - 2);
 #pragma unroll
             for (int k = NA - 2; k >= 1; --k) {
-                const S2 iv = inv_s2(da, db, dc);
-                Uget(j0 + k - 1, u0, u1, u2, u3);
+                const S2 iv = inv_s2f(da, db, dc);
+                Uk(k - 1, u0, u1, u2, u3);
                 const double s00 = iv.a * u0 + iv.b * u1, s01 = iv.a * u2 + iv.b * u3;
                 const double s10 = iv.b * u0 + iv.c * u1, s11 = iv.b * u2 + iv.c * u3;
                 double a, bb, c;
-                Dget(j0 + k - 1, a, bb, c);
+                Dk(k - 1, a, bb, c);
                 da = a - (u0 * s00 + u1 * s10);
                 db = bb - (u0 * s01 + u1 * s11);
                 dc = c - (u2 * s01 + u3 * s11);
-                const double nha = fa[k - 1] - (s00 * ha + s10 * hb);
-                const double nhb = fb[k - 1] - (s01 * ha + s11 * hb);
+                const double nha = f0[k - 1] - (s00 * ha + s10 * hb);
+                const double nhb = f1[k - 1] - (s01 * ha + s11 * hb);
                 ha = nha; hb = nhb;
                 const double n00 = -(s00 * H00 + s10 * H10), n01 = -(s00 * H01 + s10 * H11);
                 const double n10 = -(s01 * H00 + s11 * H10), n11 = -(s01 * H01 + s11 * H11);
                 H00 = n00; H01 = n01; H10 = n10; H11 = n11;
-                // scalar
-                const double e = ezs(j0 + k - 1);
-                const double sb = e / sd;
-                sd = dzs(j0 + k - 1) - e * sb;
+                const double e = ezs(k - 1);
+                const double sb = e * frcp(sd);
+                sd = dzs(k - 1) - e * sb;
                 s_hh = fw[k - 1] - sb * s_hh;
                 s_Hh = -sb * s_Hh;
             }
-            iDh = inv_s2(da, db, dc);
-            s_idh = 1.0 / sd;
+            iDh = inv_s2f(da, db, dc);
+            s_idh = frcp(sd);
         }
         // step B (top-down): T_k, D'_k^{-1} in registers
-        double Tt[NA - 1][4], Ti[NA - 1][3], st[NA - 1], sid[NA - 1];
+        double FSr[kFac][NA - 1];   // chunk factors (registers)
+        auto fs = [&](int a, int k) -> double& { return FSr[a][k]; };
         double pa, pb, pc, ga, gb, F00, F01, F10, F11, s_dp, s_g, s_F;
         {
-            Dget(j0, pa, pb, pc);
-            ga = fa[0];
-            gb = fb[0];
+            Dk(0, pa, pb, pc);
+            ga = f0[0];
+            gb = f1[0];
             F00 = -ul0; F01 = -ul2; F10 = -ul1; F11 = -ul3;
-            s_dp = dzs(j0);
+            s_dp = dzs(0);
             s_g = fw[0];
             s_F = -sel;
 #pragma unroll
             for (int k = 1; k < NA; ++k) {
-                const S2 iv = inv_s2(pa, pb, pc);
+                const S2 iv = inv_s2f(pa, pb, pc);
                 double u0, u1, u2, u3;
-                Uget(j0 + k - 1, u0, u1, u2, u3);
+                Uk(k - 1, u0, u1, u2, u3);
                 const double t00 = iv.a * u0 + iv.b * u2, t01 = iv.a * u1 + iv.b * u3;
                 const double t10 = iv.b * u0 + iv.c * u2, t11 = iv.b * u1 + iv.c * u3;
-                Tt[k - 1][0] = t00; Tt[k - 1][1] = t01; Tt[k - 1][2] = t10; Tt[k - 1][3] = t11;
-                Ti[k - 1][0] = iv.a; Ti[k - 1][1] = iv.b; Ti[k - 1][2] = iv.c;
+                fs(0, k - 1) = t00; fs(1, k - 1) = t01; fs(2, k - 1) = t10; fs(3, k - 1) = t11;
+                fs(4, k - 1) = iv.a; fs(5, k - 1) = iv.b; fs(6, k - 1) = iv.c;
                 double a, bb, c;
-                Dget(j0 + k, a, bb, c);
+                Dk(k, a, bb, c);
                 pa = a - (u0 * t00 + u2 * t10);
                 pb = bb - (u0 * t01 + u2 * t11);
                 pc = c - (u1 * t01 + u3 * t11);
-                const double nga = fa[k] - (t00 * ga + t10 * gb);
-                const double ngb = fb[k] - (t01 * ga + t11 * gb);
+                const double nga = f0[k] - (t00 * ga + t10 * gb);
+                const double ngb = f1[k] - (t01 * ga + t11 * gb);
                 ga = nga; gb = ngb;
                 const double n00 = -(t00 * F00 + t10 * F10), n01 = -(t00 * F01 + t10 * F11);
                 const double n10 = -(t01 * F00 + t11 * F10), n11 = -(t01 * F01 + t11 * F11);
                 F00 = n00; F01 = n01; F10 = n10; F11 = n11;
-                // scalar
-                const double e = ezs(j0 + k - 1);
-                const double tt = e / s_dp;
-                st[k - 1] = tt;
-                sid[k - 1] = 1.0 / s_dp;
-                s_dp = dzs(j0 + k) - e * tt;
+                const double e = ezs(k - 1);
+                const double idp = frcp(s_dp);
+                const double tt = e * idp;
+                fs(7, k - 1) = tt;
+                fs(8, k - 1) = idp;
+                s_dp = dzs(k) - e * tt;
                 s_g = fw[k] - tt * s_g;
                 s_F = -tt * s_F;
             }
         }
-        __syncthreads();   // KD..SV are dead: exchange slot 0 may overwrite them
+        TKPP(2);
+        if (kStage && i + (int)gridDim.x < V.sl.r1)   // the next row's vectors -> this thread's slots
+            stage_row<FULL, T>(SG, row_src<MODE>(V, x, chain, i + gridDim.x), b, x, hx, n, j0);
         // exchange 1: this chunk's bottom-up results for the previous chunk
         {
             double* E = XB[0];
@@ -344,9 +616,11 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             E[9 * T + tid] = s_idh; E[10 * T + tid] = s_hh; E[11 * T + tid] = s_Hh;
         }
         __syncthreads();
-        // step C: interface rows  A X_{l-1} + B X_l + C X_{l+1} = R  (block and scalar)
-        double B00, B01, B10, B11, C00, C01, C10, C11, A00, A01, A10, A11, R0, R1;
-        double sA, sB, sC, sR;
+        TKPP(3);
+        // step C: symmetric interface rows  C_{l-1}^T X_{l-1} + B_l X_l + C_l X_{l+1} = R_l
+        // (B symmetric; the lower coupling is the transposed upper coupling of the
+        // row below), block and scalar
+        double B00, B01, B11, C00, C01, C10, C11, R0, R1, sB, sC, sR;
         {
             const double* E = XB[0];
             const int nx = tid + 1 < T ? tid + 1 : tid;   // last chunk: coupling is zero
@@ -357,162 +631,167 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             const double nsi = E[9 * T + nx], nsh = E[10 * T + nx], nsH = E[11 * T + nx];
             const double v00 = ur0 * na + ur1 * nb, v01 = ur0 * nb + ur1 * nc;
             const double v10 = ur2 * na + ur3 * nb, v11 = ur2 * nb + ur3 * nc;
-            B00 = pa - (v00 * ur0 + v01 * ur1); B01 = pb - (v00 * ur2 + v01 * ur3);
-            B10 = pb - (v10 * ur0 + v11 * ur1); B11 = pc - (v10 * ur2 + v11 * ur3);
+            B00 = pa - (v00 * ur0 + v01 * ur1);
+            B01 = pb - (v00 * ur2 + v01 * ur3);
+            B11 = pc - (v10 * ur2 + v11 * ur3);
             C00 = v00 * nH00 + v01 * nH10; C01 = v00 * nH01 + v01 * nH11;
             C10 = v10 * nH00 + v11 * nH10; C11 = v10 * nH01 + v11 * nH11;
-            A00 = -F00; A01 = -F01; A10 = -F10; A11 = -F11;
             R0 = ga - (v00 * nha + v01 * nhb);
             R1 = gb - (v10 * nha + v11 * nhb);
             const double rho = ser * nsi;
-            sA = -s_F;
             sB = s_dp - ser * rho;
             sC = rho * nsH;
             sR = s_g - rho * nsh;
         }
-        // parallel cyclic reduction over the T interface rows (ping-pong slots)
-        int slot = 1;
+        // the output's loads, issued early: their latency overlaps the interface solve
+        const bool hxu = MODE == 0 && x != nullptr;
+        double oxu[NA], oxz[NA], oxl[NA], oxm[NA], ocd[NA], ocs[NA], ocb[NA];
+        ld4<FULL>(x, ou, j0, n, hxu, oxu);
+        ld4<FULL>(x, oz, j0, n, hxu, oxz);
+        ld4<FULL>(x, ol, j0, n, hxu, oxl);
+        ld4<FULL>(x, om, j0, n, hxu && has_vm, oxm);
+        ld4<FULL>(C, n, j0, n, hc, ocd);
+        ld4<FULL>(C, 2 * n, j0, n, hc, ocs);
+        ld4<FULL>(C, 0, j0, n, hc, ocb);
+        const double ocsL = ld1(C, 2 * n, jL, n, hc), ocbR = ld1(C, 0, jR, n, hc);
+        TKPP(4);
+        // symmetric parallel cyclic reduction (ping-pong slots, one barrier per step).
+        // Row l publishes G = C^T B^{-1} C, g = C^T B^{-1} R (for row l+s) and
+        // B^{-1}, q = B^{-1} R, P = B^{-1} C (for row l-s).
+        {
+            int slot = 0;
 #pragma unroll
-        for (int s = 1; s < T; s <<= 1) {
-            const double id = 1.0 / (B00 * B11 - B01 * B10);
-            const double i00 = B11 * id, i01 = -B01 * id, i10 = -B10 * id, i11 = B00 * id;
-            const double isb = 1.0 / sB;
-            double* E = XB[slot];
-            E[0 * T + tid] = i00 * A00 + i01 * A10; E[1 * T + tid] = i00 * A01 + i01 * A11;
-            E[2 * T + tid] = i10 * A00 + i11 * A10; E[3 * T + tid] = i10 * A01 + i11 * A11;
-            E[4 * T + tid] = i00 * C00 + i01 * C10; E[5 * T + tid] = i00 * C01 + i01 * C11;
-            E[6 * T + tid] = i10 * C00 + i11 * C10; E[7 * T + tid] = i10 * C01 + i11 * C11;
-            E[8 * T + tid] = i00 * R0 + i01 * R1;   E[9 * T + tid] = i10 * R0 + i11 * R1;
-            E[10 * T + tid] = isb * sA; E[11 * T + tid] = isb * sC; E[12 * T + tid] = isb * sR;
+            for (int s = 1; s < T; s <<= 1) {
+                double* E = PX[slot];
+                {
+                    const S2 iv = inv_s2f(B00, B01, B11);
+                    const double q0 = iv.a * R0 + iv.b * R1, q1 = iv.b * R0 + iv.c * R1;
+                    const double p00 = iv.a * C00 + iv.b * C10, p01 = iv.a * C01 + iv.b * C11;
+                    const double p10 = iv.b * C00 + iv.c * C10, p11 = iv.b * C01 + iv.c * C11;
+                    E[0 * T + tid] = C00 * p00 + C10 * p10;
+                    E[1 * T + tid] = C00 * p01 + C10 * p11;
+                    E[2 * T + tid] = C01 * p01 + C11 * p11;
+                    E[3 * T + tid] = C00 * q0 + C10 * q1;
+                    E[4 * T + tid] = C01 * q0 + C11 * q1;
+                    E[5 * T + tid] = iv.a; E[6 * T + tid] = iv.b; E[7 * T + tid] = iv.c;
+                    E[8 * T + tid] = q0; E[9 * T + tid] = q1;
+                    E[10 * T + tid] = p00; E[11 * T + tid] = p01;
+                    E[12 * T + tid] = p10; E[13 * T + tid] = p11;
+                    const double ib = frcp(sB);
+                    const double sq = sR * ib, sp = sC * ib;
+                    E[14 * T + tid] = sC * sp; E[15 * T + tid] = sC * sq;
+                    E[16 * T + tid] = ib; E[17 * T + tid] = sq; E[18 * T + tid] = sp;
+                }
+                __syncthreads();
+                if (tid >= s) {
+                    const int m = tid - s;
+                    B00 -= E[0 * T + m]; B01 -= E[1 * T + m]; B11 -= E[2 * T + m];
+                    R0 -= E[3 * T + m]; R1 -= E[4 * T + m];
+                    sB -= E[14 * T + m]; sR -= E[15 * T + m];
+                }
+                if (tid + s < T) {
+                    const int m = tid + s;
+                    const double ia = E[5 * T + m], ib = E[6 * T + m], ic = E[7 * T + m];
+                    const double q0 = E[8 * T + m], q1 = E[9 * T + m];
+                    const double p00 = E[10 * T + m], p01 = E[11 * T + m];
+                    const double p10 = E[12 * T + m], p11 = E[13 * T + m];
+                    // K = C iB
+                    const double k00 = C00 * ia + C01 * ib, k01 = C00 * ib + C01 * ic;
+                    const double k10 = C10 * ia + C11 * ib, k11 = C10 * ib + C11 * ic;
+                    B00 -= k00 * C00 + k01 * C01;
+                    B01 -= k00 * C10 + k01 * C11;
+                    B11 -= k10 * C10 + k11 * C11;
+                    R0 -= C00 * q0 + C01 * q1;
+                    R1 -= C10 * q0 + C11 * q1;
+                    const double n00 = -(C00 * p00 + C01 * p10), n01 = -(C00 * p01 + C01 * p11);
+                    const double n10 = -(C10 * p00 + C11 * p10), n11 = -(C10 * p01 + C11 * p11);
+                    C00 = n00; C01 = n01; C10 = n10; C11 = n11;
+                    const double sib = E[16 * T + m], ssq = E[17 * T + m], ssp = E[18 * T + m];
+                    sB -= sC * sC * sib;
+                    sR -= sC * ssq;
+                    sC = -sC * ssp;
+                } else {
+                    C00 = C01 = C10 = C11 = 0.0;
+                    sC = 0.0;
+                }
+                slot ^= 1;
+            }
+            const S2 iv = inv_s2f(B00, B01, B11);
+            double* E = PX[slot];
+            E[tid] = iv.a * R0 + iv.b * R1;
+            E[T + tid] = iv.b * R0 + iv.c * R1;
+            E[2 * T + tid] = sR * frcp(sB);
             __syncthreads();
-            double mc00 = 0, mc01 = 0, mc10 = 0, mc11 = 0, ma00 = 0, ma01 = 0, ma10 = 0, ma11 = 0;
-            double mr0 = 0, mr1 = 0, msa = 0, msc = 0, msr = 0;
-            double pa00 = 0, pa01 = 0, pa10 = 0, pa11 = 0, pc00 = 0, pc01 = 0, pc10 = 0, pc11 = 0;
-            double pr0 = 0, pr1 = 0, psa = 0, psc = 0, psr = 0;
-            if (tid >= s) {
-                const int m = tid - s;
-                ma00 = E[0 * T + m]; ma01 = E[1 * T + m]; ma10 = E[2 * T + m]; ma11 = E[3 * T + m];
-                mc00 = E[4 * T + m]; mc01 = E[5 * T + m]; mc10 = E[6 * T + m]; mc11 = E[7 * T + m];
-                mr0 = E[8 * T + m]; mr1 = E[9 * T + m];
-                msa = E[10 * T + m]; msc = E[11 * T + m]; msr = E[12 * T + m];
-            }
-            if (tid + s < T) {
-                const int m = tid + s;
-                pa00 = E[0 * T + m]; pa01 = E[1 * T + m]; pa10 = E[2 * T + m]; pa11 = E[3 * T + m];
-                pc00 = E[4 * T + m]; pc01 = E[5 * T + m]; pc10 = E[6 * T + m]; pc11 = E[7 * T + m];
-                pr0 = E[8 * T + m]; pr1 = E[9 * T + m];
-                psa = E[10 * T + m]; psc = E[11 * T + m]; psr = E[12 * T + m];
-            }
-            // B -= A (iB C)_{l-s} + C (iB A)_{l+s};  A <- -A (iB A)_{l-s};  C <- -C (iB C)_{l+s}
-            B00 -= (A00 * mc00 + A01 * mc10) + (C00 * pa00 + C01 * pa10);
-            B01 -= (A00 * mc01 + A01 * mc11) + (C00 * pa01 + C01 * pa11);
-            B10 -= (A10 * mc00 + A11 * mc10) + (C10 * pa00 + C11 * pa10);
-            B11 -= (A10 * mc01 + A11 * mc11) + (C10 * pa01 + C11 * pa11);
-            R0 -= (A00 * mr0 + A01 * mr1) + (C00 * pr0 + C01 * pr1);
-            R1 -= (A10 * mr0 + A11 * mr1) + (C10 * pr0 + C11 * pr1);
-            const double nA00 = -(A00 * ma00 + A01 * ma10), nA01 = -(A00 * ma01 + A01 * ma11);
-            const double nA10 = -(A10 * ma00 + A11 * ma10), nA11 = -(A10 * ma01 + A11 * ma11);
-            const double nC00 = -(C00 * pc00 + C01 * pc10), nC01 = -(C00 * pc01 + C01 * pc11);
-            const double nC10 = -(C10 * pc00 + C11 * pc10), nC11 = -(C10 * pc01 + C11 * pc11);
-            A00 = nA00; A01 = nA01; A10 = nA10; A11 = nA11;
-            C00 = nC00; C01 = nC01; C10 = nC10; C11 = nC11;
-            sB -= sA * msc + sC * psa;
-            sR -= sA * msr + sC * psr;
-            sA = -sA * msa;
-            sC = -sC * psc;
-            slot ^= 1;
+            XO = E;
+            LAM = PX[slot ^ 1];
         }
-        double X0, X1, sX;
-        {
-            const double id = 1.0 / (B00 * B11 - B01 * B10);
-            X0 = (B11 * R0 - B01 * R1) * id;
-            X1 = (B00 * R1 - B10 * R0) * id;
-            sX = sR / sB;
-        }
-        // exchange 2: interface values for the next chunk
-        {
-            double* E = XB[slot];
-            E[tid] = X0; E[T + tid] = X1; E[2 * T + tid] = sX;
-        }
-        __syncthreads();
+        TKPP(5);
+        const double X0 = XO[tid], X1 = XO[T + tid], sX = XO[2 * T + tid];
         double xl0 = 0.0, xl1 = 0.0, sxl = 0.0;
-        if (tid > 0) {
-            const double* E = XB[slot];
-            xl0 = E[tid - 1]; xl1 = E[T + tid - 1]; sxl = E[2 * T + tid - 1];
-        }
-        // steps D/E: rhs sweep with the left interface, back-substitution
+        if (tid > 0) { xl0 = XO[tid - 1]; xl1 = XO[T + tid - 1]; sxl = XO[2 * T + tid - 1]; }
+        // steps D/E: rhs sweep with the left interface, back-substitution (registers)
+        double yu[NA], yl[NA], yw[NA];
         {
             double g0[NA - 1], g1[NA - 1], gs[NA - 1];
-#pragma unroll
-            for (int k = 0; k < NA - 1; ++k) {   // rhs again from the node arrays
-                const int q = PI(j0 + k);
-                g0[k] = F0[q];
-                g1[k] = F1[q];
-                gs[k] = FW[q];
-            }
-            g0[0] -= ul0 * xl0 + ul2 * xl1;
-            g1[0] -= ul1 * xl0 + ul3 * xl1;
-            gs[0] -= sel * sxl;
+            g0[0] = f0[0] - (ul0 * xl0 + ul2 * xl1);
+            g1[0] = f1[0] - (ul1 * xl0 + ul3 * xl1);
+            gs[0] = fw[0] - sel * sxl;
 #pragma unroll
             for (int k = 1; k < NA - 1; ++k) {
-                const double* t = Tt[k - 1];
-                g0[k] -= t[0] * g0[k - 1] + t[2] * g1[k - 1];
-                g1[k] -= t[1] * g0[k - 1] + t[3] * g1[k - 1];
-                gs[k] -= st[k - 1] * gs[k - 1];
+                g0[k] = f0[k] - (fs(0, k - 1) * g0[k - 1] + fs(2, k - 1) * g1[k - 1]);
+                g1[k] = f1[k] - (fs(1, k - 1) * g0[k - 1] + fs(3, k - 1) * g1[k - 1]);
+                gs[k] = fw[k] - fs(7, k - 1) * gs[k - 1];
             }
-            double ya = X0, yb = X1, ys = sX;
-            {
-                const int q = PI(j0 + NA - 1);
-                F0[q] = X0; F1[q] = X1; FW[q] = sX;
-            }
+            yu[NA - 1] = X0; yl[NA - 1] = X1; yw[NA - 1] = sX;
 #pragma unroll
             for (int k = NA - 2; k >= 0; --k) {
-                const double* t = Tt[k];
-                const double* iv = Ti[k];
-                const double na = iv[0] * g0[k] + iv[1] * g1[k] - (t[0] * ya + t[1] * yb);
-                const double nb = iv[1] * g0[k] + iv[2] * g1[k] - (t[2] * ya + t[3] * yb);
-                ys = sid[k] * gs[k] - st[k] * ys;
-                ya = na; yb = nb;
-                const int q = PI(j0 + k);
-                F0[q] = na; F1[q] = nb; FW[q] = ys;
+                const double t00 = fs(0, k), t01 = fs(1, k), t10 = fs(2, k), t11 = fs(3, k);
+                const double ia = fs(4, k), ib = fs(5, k), ic = fs(6, k);
+                yu[k] = ia * g0[k] + ib * g1[k] - (t00 * yu[k + 1] + t01 * yl[k + 1]);
+                yl[k] = ib * g0[k] + ic * g1[k] - (t10 * yu[k + 1] + t11 * yl[k + 1]);
+                yw[k] = fs(8, k) * gs[k] - fs(7, k) * yw[k + 1];
             }
         }
-        __syncthreads();
-        // ---- output (coalesced)
+        TKPP(6);
+        // exchange 3: first lam of every chunk (the C^T lam coupling of the previous chunk)
         {
-            double xo[NA][5];
-#pragma unroll
-            for (int t = 0; t < NA; ++t) {
-                const int j = tid + T * t;
-                const bool in = xu && j < n;
-                xo[t][0] = in ? xu[ou + j] : 0.0;
-                xo[t][1] = in ? xu[oz + j] : 0.0;
-                xo[t][2] = in ? xu[ol + j] : 0.0;
-                xo[t][3] = (in && has_vm) ? xu[om + j] : 0.0;
-            }
-#pragma unroll
-            for (int t = 0; t < NA; ++t) {
-                const int j = tid + T * t;
-                if (j < n) {
-                    const int q = PI(j);
-                    const double du = F0[q], dl = F1[q];
-                    const double dzv = FW[q] - kap * dl;
-                    y[ou + j] = xo[t][0] + omega * du;
-                    y[oz + j] = xo[t][1] + omega * dzv;
-                    y[ol + j] = xo[t][2] + omega * dl;
-                    if (has_vm) {
-                        double dm = pm[t];
-                        if (C) {
-                            dm += C[n + j] * dl;
-                            if (j > 0) dm += C[2 * n + j - 1] * F1[PI(j - 1)];
-                            if (j < n - 1) dm += C[j + 1] * F1[PI(j + 1)];
-                        }
-                        y[om + j] = xo[t][3] + omega * dm;
-                    }
-                }
-            }
+            LAM[tid] = yl[0];
         }
         __syncthreads();
+        const double lamR = (tid + 1 < T) ? LAM[tid + 1] : 0.0;
+        TKPP(7);
+        // ---- output (chunk order)
+        {
+            double o[NA];
+#pragma unroll
+            for (int k = 0; k < NA; ++k) o[k] = oxu[k] + omega * yu[k];
+            st4<FULL>(y, ou, j0, n, o);
+#pragma unroll
+            for (int k = 0; k < NA; ++k) o[k] = oxz[k] + omega * (yw[k] - kap * yl[k]);
+            st4<FULL>(y, oz, j0, n, o);
+#pragma unroll
+            for (int k = 0; k < NA; ++k) o[k] = oxl[k] + omega * yl[k];
+            st4<FULL>(y, ol, j0, n, o);
+            if (has_vm) {
+#pragma unroll
+                for (int k = 0; k < NA; ++k) {
+                    const int j = j0 + k;
+                    const double lm = k > 0 ? yl[k - 1] : xl1;   // lam at j-1 (left interface)
+                    const double lp = k < NA - 1 ? yl[k + 1] : lamR;
+                    double dm = pm[k];
+                    if (hc) {
+                        dm += ocd[k] * yl[k];
+                        if (j > 0) dm += (k > 0 ? ocs[k - 1] : ocsL) * lm;
+                        if (j < n - 1) dm += (k < NA - 1 ? ocb[k + 1] : ocbR) * lp;
+                    }
+                    o[k] = oxm[k] + omega * dm;
+                }
+                st4<FULL>(y, om, j0, n, o);
+            }
+        }
+        TKPP(8);
+        __syncthreads();
+        TKPP(9);
     }
 }
 
@@ -528,7 +807,7 @@ static int part_warps(int n) {
 
 int part_nodes_per_lane(int n) { return part_warps(n) ? kChunk : 0; }
 
-template <int W, int MODE>
+template <int W, int MODE, bool FULL>
 static int part_launch_t(const tk_level* Lv, const double* b, const double* x, double* y,
                          double omega, const double* chain, cudaStream_t s) {
     using Cf = PartCta<W>;
@@ -536,15 +815,15 @@ static int part_launch_t(const tk_level* Lv, const double* b, const double* x, d
     static int nsm = 0;
     const int64_t smem = Cf::smem_bytes();
     if (!per_sm) {
-        cudaFuncSetAttribute(tri_rows_part<W, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(tri_rows_part<W, MODE, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        cudaFuncSetAttribute(tri_rows_part<W, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        cudaFuncSetAttribute(tri_rows_part<W, MODE, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         int per = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tri_rows_part<W, MODE>, 32 * W,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tri_rows_part<W, MODE, FULL>, 32 * W,
                                                       (size_t)smem);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_status(e, "tri_rows_part: attributes");
@@ -559,18 +838,29 @@ static int part_launch_t(const tk_level* Lv, const double* b, const double* x, d
     int grid = rows;
     const int cap = nsm * per_sm;
     if (grid > cap) grid = cap;
-    tri_rows_part<W, MODE><<<grid, 32 * W, smem, s>>>(V, b, x, y, omega, chain);
+    tri_rows_part<W, MODE, FULL><<<grid, 32 * W, smem, s>>>(V, b, x, y, omega, chain);
     return check_launch("tri_rows_part");
 }
 
 // mode 0: rows (jacobi / D^{-1} b), 1/2: substitution pass 3 forward/backward
 int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, double* y,
                 double omega, const double* chain, cudaStream_t s) {
-#define TK_PART_CASE(WW)                                                              \
-    case WW:                                                                          \
-        if (mode == 0) return part_launch_t<WW, 0>(Lv, b, x, y, omega, chain, s);     \
-        if (mode == 1) return part_launch_t<WW, 1>(Lv, b, x, y, omega, chain, s);     \
-        return part_launch_t<WW, 2>(Lv, b, x, y, omega, chain, s);
+#define TK_PART_CASE(WW)                                                                   \
+    case WW:                                                                               \
+        if (full) {                                                                        \
+            if (mode == 0) return part_launch_t<WW, 0, true>(Lv, b, x, y, omega, chain, s);  \
+            if (mode == 1) return part_launch_t<WW, 1, true>(Lv, b, x, y, omega, chain, s);  \
+            return part_launch_t<WW, 2, true>(Lv, b, x, y, omega, chain, s);                 \
+        }                                                                                  \
+        if (mode == 0) return part_launch_t<WW, 0, false>(Lv, b, x, y, omega, chain, s);     \
+        if (mode == 1) return part_launch_t<WW, 1, false>(Lv, b, x, y, omega, chain, s);     \
+        return part_launch_t<WW, 2, false>(Lv, b, x, y, omega, chain, s);
+    // FULL: every chunk is complete and every segment 16-byte aligned
+    const int w = part_warps(Lv->n_u);
+    auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    const bool full = w > 0 && Lv->n_u == kChunk * 32 * w && Lv->n_u % 2 == 0 && Lv->n_z % 2 == 0 &&
+                      al(b) && al(x) && al(y) && al(chain) && al(Lv->K) && al(Lv->C) &&
+                      al(Lv->Qm) && al(Lv->Ql) && al(Lv->Qz) && al(Lv->halo_u) && al(Lv->halo_mu);
     switch (part_warps(Lv->n_u)) {
         TK_PART_CASE(1)
         TK_PART_CASE(2)
