@@ -26,6 +26,7 @@ int check_launch(const char* where) { return cuda_status(cudaGetLastError(), whe
 int dense_launch(const tk_level*, int, const double*, const double*, double*, double, cudaStream_t);
 int tri_launch(const tk_level*, int, const double*, const double*, double*, double, cudaStream_t);
 int64_t tri_smem_bytes(int n);
+int tri_resrestrict_launch(const tk_level*, const double*, const double*, double*, cudaStream_t);
 int64_t tri_fac_len(const tk_level*);
 int64_t tri_scratch_len(const tk_level*);
 int64_t dense_fac_len(const tk_level*);
@@ -220,6 +221,12 @@ int tk_prolong_add_slab(int32_t n_fine, int32_t n_u, int32_t n_z, int32_t row0, 
 int tk_residual_restrict(const tk_level* L, const double* b, const double* x, double* rc,
                          double* work, void* stream) {
     TK_CHECK_ARG(b && x && rc && work, "tk_residual_restrict: null vector");
+    {
+        const int e = check_level(L);
+        if (e) return e;
+    }
+    if (L->family == TK_FAMILY_TRI)   // fused: the fine residual never reaches HBM
+        return tri_resrestrict_launch(L, b, x, rc, as_stream(stream));
     int rcode = level_op(L, 2, 2, b, x, work, 1.0, stream);
     if (rcode) return rcode;
     return transfer_launch(1, L->n_steps, L->n_u, L->n_z, L->row0, L->row1, work, nullptr,
