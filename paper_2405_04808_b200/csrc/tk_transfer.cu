@@ -104,6 +104,76 @@ __global__ void prolong_add_kernel(Lay Lf, Lay Lc, int64_t fbase, int64_t flen, 
     }
 }
 
+
+// Row-based prolong-add: one CTA per fine block row; every segment of the row
+// is one kind at one fine time, so its (at most two) coarse source segments
+// are located once per CTA and the row is streamed with 16-byte accesses
+// when the layout allows.
+__device__ __forceinline__ const double* coarse_seg(const Lay& Lc, const double* xc, int64_t cbase,
+                                                    int64_t clen, const double* hprev,
+                                                    const double* hnext, int kind, int t) {
+    const int64_t g = kind_off(Lc, kind, t);
+    const int64_t l = g - cbase;
+    if (l >= 0 && l < clen) return xc + l;
+    if (l < 0) return hprev + (kind == KU ? 0 : Lc.nu);   // previous slab: (u, lam)
+    return hnext + (kind == KV ? 0 : Lc.nu);                // next slab: (v, mu)
+}
+
+__global__ void __launch_bounds__(256) prolong_rows_kernel(Lay Lf, Lay Lc, int64_t fbase, int r0,
+                                                           int r1, int64_t cbase, int64_t clen,
+                                                           const double* __restrict__ xc,
+                                                           const double* __restrict__ hprev,
+                                                           const double* __restrict__ hnext,
+                                                           double* __restrict__ xf, bool vec) {
+    for (int i = r0 + blockIdx.x; i < r1; i += gridDim.x) {
+        // segments of row i: kind, fine time, offset
+        int kinds[5], ts[5];
+        int64_t offs[5];
+        int ns = 0;
+        auto add = [&](int k, int t, int64_t o) { kinds[ns] = k; ts[ns] = t; offs[ns] = o; ++ns; };
+        if (i >= 1) add(KV, i, Lf.off_v(i));
+        if (i < Lf.N) { add(KU, i + 1, Lf.off_u(i)); add(KZ, i + 1, Lf.off_z(i)); }
+        if (i >= 1) add(KM, i, Lf.off_mu(i));
+        if (i < Lf.N) add(KL, i + 1, Lf.off_l(i));
+        for (int q = 0; q < ns; ++q) {
+            const int kind = kinds[q], t = ts[q];
+            const int len = kind == KZ ? Lf.nz : Lf.nu;
+            double* dst = xf + (offs[q] - fbase);
+            const double* a;
+            const double* b = nullptr;
+            if (kind == KZ) {
+                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, KZ, (t + 1) / 2);
+            } else if ((t & 1) == 0) {
+                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, t / 2);
+            } else if (t == 1) {
+                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, 1);
+            } else {
+                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, (t - 1) / 2);
+                b = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, (t + 1) / 2);
+            }
+            if (vec) {   // every segment 16-byte aligned, len even
+                const int h = len / 2;
+                for (int k = threadIdx.x; k < h; k += blockDim.x) {
+                    double2 d = reinterpret_cast<double2*>(dst)[k];
+                    const double2 u = reinterpret_cast<const double2*>(a)[k];
+                    if (b) {
+                        const double2 w = reinterpret_cast<const double2*>(b)[k];
+                        d.x = d.x + 0.5 * (u.x + w.x);
+                        d.y = d.y + 0.5 * (u.y + w.y);
+                    } else {
+                        d.x = d.x + u.x;
+                        d.y = d.y + u.y;
+                    }
+                    reinterpret_cast<double2*>(dst)[k] = d;
+                }
+            } else {
+                for (int k = threadIdx.x; k < len; k += blockDim.x)
+                    dst[k] = dst[k] + (b ? 0.5 * (a[k] + b[k]) : a[k]);
+            }
+        }
+    }
+}
+
 // fine rows [r0, r1) -> coarse rows [r0/2, r1/2) (through N/2 for the last slab)
 static void slab_geom(const Lay& Lf, const Lay& Lc, int r0, int r1, int64_t& fbase,
                       int64_t& flen, int64_t& cbase, int64_t& clen) {
@@ -136,8 +206,13 @@ int transfer_launch(int restrict_op, int n_fine, int nu, int nz, int r0, int r1,
             set_error("prolong_add: slab [%d, %d) needs its coarse halo segments", r0, r1);
             return TK_ERR_ARG;
         }
-        prolong_add_kernel<<<grid_for(flen, th, 148 * 32), th, 0, s>>>(
-            Lf, Lc, fbase, flen, cbase, clen, in, hprev, hnext, out);
+        auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        const bool vec = (nu % 2 == 0) && (nz % 2 == 0) && (fbase % 2 == 0) && (cbase % 2 == 0) &&
+                         al(in) && al(out) && al(hprev) && al(hnext);
+        const int rows = r1 - r0;
+        const int pth = nu >= 512 ? 256 : 128;
+        prolong_rows_kernel<<<rows < (1 << 30) ? rows : (1 << 30), pth, 0, s>>>(
+            Lf, Lc, fbase, r0, r1, cbase, clen, in, hprev, hnext, out, vec);
     }
     return check_launch("transfer");
 }
