@@ -33,11 +33,16 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 
 
 # ncu-measured DRAM traffic per C-ABI call: which CUDA kernels one call launches
+# (launch-list patterns), or the fine-level launch of the `--set full` capture
 _NCU_KERNELS = {
-    "tk_forward_subst": ("tri_chain_kernel<1", "tri_rows<", "tri_rows_cpl<1", "dense_chain<"),
-    "tk_backward_subst": ("tri_chain_kernel<0", "tri_rows<", "tri_rows_cpl<0", "dense_chain<"),
-    "tk_jacobi_sweep": ("tri_rows<", "dense_rows<"),
-    "tk_residual_restrict": ("tri_apply<2", "restrict_kernel"),
+    "tk_forward_subst": ("tri_chain_kernel<1", "tri_chain_carry<1", "tri_rows_rec<", "tri_rows_rec_cpl<1"),
+    "tk_backward_subst": ("tri_chain_kernel<0", "tri_chain_carry<0", "tri_rows_rec<", "tri_rows_rec_cpl<0"),
+}
+_NCU_FULL = {
+    "tk_jacobi_sweep": "tri_rows_part",
+    "tk_residual_restrict": "tri_resrestrict",
+    "tk_prolong_add": "prolong_rows_kernel",
+    "tk_kkt_apply": "tri_apply<0",
 }
 
 
@@ -47,24 +52,25 @@ def ncu_traffic(call: str):
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
     if not files:
         return None, None
+    src = os.path.basename(files[-1])
     with open(files[-1]) as fh:
         summ = json.load(fh)
-    pats = _NCU_KERNELS.get(call)
-    if not pats:
-        return None, os.path.basename(files[-1])
-    if call == "tk_jacobi_sweep":   # the fine-level launch of the full capture
-        fine = [d for d in summ["full_capture"] if pats[0] in d["kernel"]]
+    if call in _NCU_FULL:
+        fine = [d for d in summ["full_capture"] if _NCU_FULL[call] in d["kernel"]]
         if fine:
             d = max(fine, key=lambda e: e["duration_us"])
-            return int((d["dram_read_MB"] + d["dram_write_MB"]) * 1e6), os.path.basename(files[-1])
-        return None, os.path.basename(files[-1])
+            return int((d["dram_read_MB"] + d["dram_write_MB"]) * 1e6), src
+        return None, src
+    pats = _NCU_KERNELS.get(call)
+    if not pats:
+        return None, src
     tot = 0
     for pat in pats:
         for d in summ["launch_list"]:
             if pat in d["kernel"]:
                 tot += d["dram_bytes_per_launch"]
                 break
-    return (tot or None), os.path.basename(files[-1])
+    return (tot or None), src
 
 
 def load_peaks():
@@ -230,8 +236,30 @@ def run_ours(args, rank, world, local_rank):
         d["calls"] += 1
         d["ms"] += ms
         d["bytes"] += roofline.algorithmic_bytes(nm, a)
+    fine_recs = {}
+    for nm, a, e0, e1 in dev.INSTR.records:   # fine-level launch of each HBM kernel
+        if nm in ("tk_jacobi_sweep", "tk_residual_restrict"):
+            lvl = roofline.dim_of(a[0]._obj)
+        elif nm == "tk_prolong_add":
+            lvl = int(a[0]) * (4 * int(a[1]) + int(a[2]))
+        else:
+            continue
+        cur = fine_recs.get(nm)
+        if cur is None or lvl > cur[0]:
+            fine_recs[nm] = (lvl, [(a, e0.elapsed_time(e1))])
+        elif lvl == cur[0]:
+            cur[1].append((a, e0.elapsed_time(e1)))
     dev.INSTR.timed, dev.INSTR.records = None, []
     dominant = max(per, key=lambda k: per[k]["ms"])
+    # the fine-level KKT mat-vec (the outer Krylov operator), timed on its own
+    a0 = h.levels[0].kkt
+    y0 = dev.empty(a0.dim)
+    dev.INSTR.timed, dev.INSTR.records = {"tk_kkt_apply"}, []
+    for _ in range(5):
+        dev.call("tk_kkt_apply", a0.lref, dev.P(r_dev), dev.P(y0), dev.stream())
+    torch.cuda.synchronize()
+    fine_recs["tk_kkt_apply"] = (a0.dim, [(a, s_.elapsed_time(t_)) for _, a, s_, t_ in dev.INSTR.records[1:]])
+    dev.INSTR.timed, dev.INSTR.records = None, []
 
     # timed region: K V-cycles, CUDA events on the launching stream; the
     # dominant kernel's launches are bracketed by events for the roofline
@@ -267,6 +295,14 @@ def run_ours(args, rank, world, local_rank):
 
     peaks, peak_kind = load_peaks()
     hbm = float(peaks["hbm_gbs"])
+    hbm_kernels = {}
+    for nm, (_, rs) in fine_recs.items():
+        byts = sum(roofline.algorithmic_bytes(nm, a) for a, _ in rs) / len(rs)
+        ms = sum(m for _, m in rs) / len(rs)
+        achk = byts / (ms * 1e-3) / 1e9
+        hbm_kernels[nm] = {"level": "fine", "bytes_per_launch": byts, "ms_per_launch": ms,
+                           "achieved_GBps": achk, "frac": achk / hbm,
+                           "ncu_kernel": _NCU_FULL.get(nm), "traffic": ncu_traffic(nm)[0]}
     b_dom, ms_dom, n_dom = kernel_stats(dominant)
     ach = b_dom / (ms_dom * 1e-3) / 1e9
     b_j, ms_j, n_j = kernel_stats("tk_jacobi_sweep", fine_only=True)
@@ -338,6 +374,7 @@ def run_ours(args, rank, world, local_rank):
                      "fine_jacobi": {"achieved": ach_j, "frac": ach_j / hbm,
                                      "bytes_per_launch": b_j, "ms_per_launch": ms_j,
                                      "traffic": ncu_traffic("tk_jacobi_sweep")[0]}},
+        "hbm_kernels": hbm_kernels,
         "kernels": {k: {"calls": v["calls"], "ms": round(v["ms"], 4),
                         "share": round(v["ms"] / sum(x["ms"] for x in per.values()), 4),
                         "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}

@@ -51,7 +51,20 @@ def to_host(x: torch.Tensor) -> np.ndarray:
 
 
 # kernels launched per C-ABI call (for the bench's gpu_launches claim)
-KERNELS_PER_CALL = {"tk_residual_restrict": 2, "tk_dot": 2, "tk_nrm2": 2}
+KERNELS_PER_CALL = {"tk_dot": 2, "tk_nrm2": 2}
+
+
+def _launches(name, args) -> int:
+    if name in ("tk_residual_restrict", "tk_forward_subst", "tk_backward_subst"):
+        lv = getattr(args[0], "_obj", None)
+        tri = lv is not None and lv.family == _lib.FAMILY_TRI
+        if name == "tk_residual_restrict":
+            return 1 if tri else 2          # fused TRI kernel / residual + restrict
+        if not tri:
+            return 3                        # rows, chain, coupled rows
+        chunked = lv.chain_prod is not None and lv.chain_chunk > 0
+        return 5 if chunked else 3          # rows, chunk chains, carry, re-run, coupled rows
+    return KERNELS_PER_CALL.get(name, 1)
 
 
 class _Instrument:
@@ -81,7 +94,7 @@ def call(name: str, *args) -> None:
         rc = getattr(lib, name)(*args)
     _lib.check(rc, name)
     if ins.counting:
-        ins.launches += KERNELS_PER_CALL.get(name, 1)
+        ins.launches += _launches(name, args)
 
 
 def P(t) -> int:

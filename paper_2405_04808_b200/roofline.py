@@ -9,8 +9,9 @@ constant weights counted as cache hits (0 bytes).  ``dim = N*(4nu+nz)``.
   diag solve / subst       8*dim*2 + stage
   apply / apply_diag       8*dim*2 + stage ;  residual 8*dim*3 + stage
   residual_restrict        DENSE: residual + restrict as separate passes;
-                           TRI (fused): 8*(b rows kept by R + x + coarse_dim) + stage,
-                           b kept = 3 of the 5 segments of every fine row
+                           TRI (fused): 8*N*(2nu+nz) of b (v,mu,z of even rows, u,lam,z
+                           of odd rows) + 8*N*(3nu+nz) of x + 8*coarse_dim written
+                           + 3/4 of the stage data (C of even rows, K and C of odd rows)
   restrict                 8*(coarse_dim + Nc*nz) read + 8*coarse_dim write
   prolong_add              8*(2*fine_dim + coarse_dim)
   dot 16n, nrm2 8n, axpy 24n, scale_into 16n, rsub 24n, gemv_t_add 8n(k+2)
@@ -50,8 +51,9 @@ def algorithmic_bytes(name: str, args) -> int:
         L = _lvl(args[0])
         nc = L.n_steps // 2
         cdim = nc * (4 * L.n_u + L.n_z)
-        if L.family == 1:   # fused kernel
-            return 8 * (L.n_steps * (2 * L.n_u + L.n_z) + dim_of(L) + cdim) + stage_bytes(L)
+        if L.family == 1:   # fused kernel: the parts the restriction keeps
+            N, nu, nz = L.n_steps, L.n_u, L.n_z
+            return 8 * (N * (2 * nu + nz) + N * (3 * nu + nz) + cdim) + (3 * stage_bytes(L)) // 4
         return 8 * dim_of(L) * 3 + stage_bytes(L) + 8 * (2 * cdim + nc * L.n_z)
     if name in ("tk_restrict", "tk_prolong_add"):
         nf, nu, nz = args[0], args[1], args[2]
