@@ -23,6 +23,7 @@ from .smoothers import (bgs_apply, fgs_apply, jacobi_apply, sgs_apply,
                         smoother_preconditioner)
 from .multigrid import (MgHierarchy, TransferOps, build_hierarchy, coarse_solve, cycle,
                         default_levels, mg_preconditioner)
+from .pipeline import HostPipeline
 
 __all__ = [
     "Breakdown", "ConfigError", "DimensionMismatch", "IndivisibleSteps", "NativeLibraryError",
@@ -35,5 +36,5 @@ __all__ = [
     "LinearOperator", "Preconditioner", "SolveReport", "fgmres", "gmres",
     "bgs_apply", "fgs_apply", "jacobi_apply", "sgs_apply", "smoother_preconditioner",
     "MgHierarchy", "TransferOps", "build_hierarchy", "coarse_solve", "cycle",
-    "default_levels", "mg_preconditioner",
+    "default_levels", "mg_preconditioner", "HostPipeline",
 ]

@@ -39,6 +39,9 @@ constexpr int kChunk = 4;        // nodes per thread
 #define TK_PART_MINB 2           // CTAs per SM the W=4 build is register-limited to
 #endif
 constexpr bool kStage = TK_PART_STAGE != 0;
+#ifndef TK_PART_EARLY
+#define TK_PART_EARLY 1          // issue the output's loads before the interface solve
+#endif
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kPX = 19;          // symmetric PCR: published doubles per row
 constexpr int kSgC = 12, kSgN = 12;   // staged chunk arrays / neighbour values per thread
@@ -643,6 +646,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             sC = rho * nsH;
             sR = s_g - rho * nsh;
         }
+#if TK_PART_EARLY
         // the output's loads, issued early: their latency overlaps the interface solve
         const bool hxu = MODE == 0 && x != nullptr;
         double oxu[NA], oxz[NA], oxl[NA], oxm[NA], ocd[NA], ocs[NA], ocb[NA];
@@ -655,6 +659,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         ld4<FULL>(C, 0, j0, n, hc, ocb);
         const double ocsL = ld1(C, 2 * n, jL, n, hc), ocbR = ld1(C, 0, jR, n, hc);
         TKPP(4);
+#endif
         // symmetric parallel cyclic reduction (ping-pong slots, one barrier per step).
         // Row l publishes G = C^T B^{-1} C, g = C^T B^{-1} R (for row l+s) and
         // B^{-1}, q = B^{-1} R, P = B^{-1} C (for row l-s).
@@ -760,6 +765,20 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         __syncthreads();
         const double lamR = (tid + 1 < T) ? LAM[tid + 1] : 0.0;
         TKPP(7);
+#if !TK_PART_EARLY
+        // the output's loads, issued early: their latency overlaps the interface solve
+        const bool hxu = MODE == 0 && x != nullptr;
+        double oxu[NA], oxz[NA], oxl[NA], oxm[NA], ocd[NA], ocs[NA], ocb[NA];
+        ld4<FULL>(x, ou, j0, n, hxu, oxu);
+        ld4<FULL>(x, oz, j0, n, hxu, oxz);
+        ld4<FULL>(x, ol, j0, n, hxu, oxl);
+        ld4<FULL>(x, om, j0, n, hxu && has_vm, oxm);
+        ld4<FULL>(C, n, j0, n, hc, ocd);
+        ld4<FULL>(C, 2 * n, j0, n, hc, ocs);
+        ld4<FULL>(C, 0, j0, n, hc, ocb);
+        const double ocsL = ld1(C, 2 * n, jL, n, hc), ocbR = ld1(C, 0, jR, n, hc);
+        TKPP(4);
+#endif
         // ---- output (chunk order)
         {
             double o[NA];
