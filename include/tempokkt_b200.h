@@ -38,7 +38,7 @@ extern "C" {
 
 /*
  * One level of the operator ladder (replaces BlockTriKKT + DiagonalSolver,
- * kkt.py:194-389, built per level by multigrid.py:358-410).
+ * kkt.py:194-389, built per level by multigrid.py:190-242).
  *
  * Stage data are the reference's StageBlocks (kkt.py:53-80):
  *   DENSE: K,C [N][nu][nu], B [N][nu][nz], row-major (same as numpy).
@@ -120,7 +120,7 @@ int64_t tk_tri_smem_bytes(int32_t n_u);
 /* --- the operator (kkt.py) ---------------------------------------------- */
 /* y = A x                        replaces BlockTriKKT.apply        kkt.py:228 */
 int tk_kkt_apply(const tk_level* L, const double* x, double* y, void* stream);
-/* r = b - A x                    replaces `b - a.apply(x)`   smoothers.py:74, multigrid.py:456 */
+/* r = b - A x                    replaces `b - a.apply(x)`   smoothers.py:74, multigrid.py:288 */
 int tk_kkt_residual(const tk_level* L, const double* b, const double* x, double* r,
                     void* stream);
 /* y = D x (no continuity couplings) replaces split_parts' D        kkt.py:400 and smoothers.py:142-151 */
@@ -158,12 +158,12 @@ int32_t tk_chain_chunk_default(int32_t n_u, int32_t n_steps);
 int64_t tk_chain_prod_len(const tk_level* L);
 int tk_chain_prod(const tk_level* L, void* stream);
 
-/* --- transfers (multigrid.py:272-300) ------------------------------------- */
-/* xc = R xf  (injection for u,v,lam,mu; 2-interval average for z)    restrict_kkt multigrid.py:272 */
+/* --- transfers (multigrid.py:104-132) ------------------------------------- */
+/* xc = R xf  (injection for u,v,lam,mu; 2-interval average for z)    restrict_kkt multigrid.py:104 */
 int tk_restrict(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xf, double* xc,
                 void* stream);
 /* xf += P xc (linear interpolation / piecewise-constant copy)  prolong_kkt + `x + t.prolong_kkt(e)`
- * multigrid.py:283 and :465 */
+ * multigrid.py:115 and :297 */
 int tk_prolong_add(int32_t n_fine, int32_t n_u, int32_t n_z, const double* xc, double* xf,
                    void* stream);
 /* Slab versions for the time-sharded hierarchy: [row0, row1) are FINE block
@@ -178,7 +178,7 @@ int tk_restrict_slab(int32_t n_fine, int32_t n_u, int32_t n_z, int32_t row0, int
 int tk_prolong_add_slab(int32_t n_fine, int32_t n_u, int32_t n_z, int32_t row0, int32_t row1,
                         const double* xc, const double* halo_prev_ul,
                         const double* halo_next_vm, double* xf, void* stream);
-/* rc = R (b - A x)  (work: fine-sized scratch; honours the level's slab)  multigrid.py:456 */
+/* rc = R (b - A x)  (work: fine-sized scratch; honours the level's slab)  multigrid.py:288 */
 int tk_residual_restrict(const tk_level* L, const double* b, const double* x, double* rc,
                          double* work, void* stream);
 
@@ -202,7 +202,7 @@ int tk_gemv_t_add(int64_t n, int32_t k, const double* V, int64_t ld, const doubl
 int tk_stage_vanderpol(int32_t n_steps, double dt, double theta, double mu, int32_t n_controls,
                        const double* u0, const double* u, const double* v, const double* z,
                        double* K, double* C, double* B, void* stream);
-/* Burgers (problems.py:425): TRI diagonals of K, C at (v_{i-1}, u_i, z_i). */
+/* Burgers (problems.py:149): TRI diagonals of K, C at (v_{i-1}, u_i, z_i). */
 int tk_stage_burgers(int32_t n_steps, int32_t n_u, double dt, double theta, double nu,
                      const double* u0, const double* u, const double* v, double* K, double* C,
                      void* stream);

@@ -53,7 +53,7 @@ class Problem:
 
 
 def vanderpol(mu=1.0, alpha=0.1, n_controls=2, u0=(1.0, 1.0), theta=1.0) -> Problem:
-    """van der Pol oscillator (problems.py:318-373).  ``n_controls=2`` is the
+    """van der Pol oscillator (problems.py:42-97).  ``n_controls=2`` is the
     reference's F_z = I; ``n_controls=1`` is the single control entering the
     second equation (BASELINE configs 0 and 3)."""
     def f(u, z):
@@ -80,14 +80,14 @@ def _tridiag(n, lo, di, hi):
 
 
 def burgers_convection(u):
-    """Galerkin convection vector (problems.py:395-400)."""
+    """Galerkin convection vector (problems.py:119-124)."""
     up = np.concatenate([u[1:], [0.0]])
     um = np.concatenate([[0.0], u[:-1]])
     return (up * up + u * up - u * um - um * um) / 6.0
 
 
 def burgers_convection_jac(u):
-    """Its Jacobian (problems.py:403-414)."""
+    """Its Jacobian (problems.py:127-138)."""
     n = u.shape[0]
     up = np.concatenate([u[1:], [0.0]])
     um = np.concatenate([[0.0], u[:-1]])
@@ -97,7 +97,7 @@ def burgers_convection_jac(u):
 
 def burgers(n_u=127, nu=1e-2, alpha=0.1, theta=0.5, u0_kind="step") -> Problem:
     """1D viscous Burgers, P1 finite elements, interior nodes only
-    (problems.py:425-473).  ``n_u`` interior nodes => ``n_u + 1`` elements.
+    (problems.py:149-197).  ``n_u`` interior nodes => ``n_u + 1`` elements.
     ``u0_kind='step'`` is the reference's initial step; ``'sinstep'`` is
     BASELINE's ``sin(pi x)`` for x <= 0.5, else 0."""
     n = n_u
@@ -511,7 +511,7 @@ STATE_KINDS = ("u", "v", "lam", "mu")
 
 
 def restrict_kkt(lf: Layout, lc: Layout, x):
-    """multigrid.py:272-281: injection at even fine nodes, control average."""
+    """multigrid.py:104-113: injection at even fine nodes, control average."""
     out = np.empty(lc.dim)
     for k in STATE_KINDS:
         out[lc.rows[k]] = x[lf.rows[k][1::2]]
@@ -521,7 +521,7 @@ def restrict_kkt(lf: Layout, lc: Layout, x):
 
 
 def prolong_kkt(lf: Layout, lc: Layout, x):
-    """multigrid.py:283-300: linear interpolation / piecewise-constant copy."""
+    """multigrid.py:115-132: linear interpolation / piecewise-constant copy."""
     out = np.empty(lf.dim)
     for k in STATE_KINDS:
         rc, rf = lc.rows[k], lf.rows[k]
@@ -558,7 +558,7 @@ class Hierarchy:
 
 
 def default_levels(n_steps, coarsest=16):
-    """multigrid.py:348-355."""
+    """multigrid.py:180-187."""
     levels, n = 1, n_steps
     while n % 2 == 0 and n // 2 >= coarsest:
         n //= 2
@@ -568,7 +568,7 @@ def default_levels(n_steps, coarsest=16):
 
 def build_hierarchy(p: Problem, u, v, z, n, dt, levels, sweeps=4, omega=1.0,
                     cycle_kind="v", coarse_tol=1e-2, coarse_max_iters=401):
-    """Rediscretised ladder (multigrid.py:358-410)."""
+    """Rediscretised ladder (multigrid.py:190-242)."""
     if n % (1 << (levels - 1)) != 0:
         raise ValueError("indivisible steps")
     lv = []
@@ -587,7 +587,7 @@ def build_hierarchy(p: Problem, u, v, z, n, dt, levels, sweeps=4, omega=1.0,
 
 
 def coarse_solve(h: Hierarchy, r):
-    """SGS-preconditioned GMRES from zero (multigrid.py:413-428)."""
+    """SGS-preconditioned GMRES from zero (multigrid.py:245-260)."""
     lev = h.levels[-1]
     zero = np.zeros(lev.kkt.dim)
     x, rep = gmres(lev.kkt.apply, lambda q: sgs(lev.kkt, lev.dsolve, q, zero), r,
@@ -598,7 +598,7 @@ def coarse_solve(h: Hierarchy, r):
 
 
 def cycle(h: Hierarchy, level, b, x0=None, kind=None):
-    """Algorithm 1 generalised to V/F/W (multigrid.py:437-469)."""
+    """Algorithm 1 generalised to V/F/W (multigrid.py:269-301)."""
     kind = h.cycle_kind if kind is None else kind
     lev = h.levels[level]
     if level == len(h.levels) - 1:
@@ -620,5 +620,5 @@ def cycle(h: Hierarchy, level, b, x0=None, kind=None):
 
 
 def mg_prec(h: Hierarchy):
-    """multigrid.py:472-479."""
+    """multigrid.py:304-311."""
     return lambda r: cycle(h, 0, r)

@@ -11,7 +11,7 @@ linearisation point is the forward march under the stated control (u = v);
 the right-hand side is i.i.d. N(0,1) in fp64 from ``numpy.random.default_rng(seed)``
 over the whole KKT dimension N*(4 N_u + N_z).  Solver: (F)GMRES tol 1e-8,
 V-cycle with 1 pre- and 1 post-sweep of block Jacobi, coarse SGS-GMRES at
-the reference's default tolerance 1e-2 (multigrid.py:335).  Controls are
+the reference's default tolerance 1e-2 (multigrid.py:167).  Controls are
 sampled at the interval end points t_i = i*dt (i = 1..N) where the reference
 indexes z_i (timedisc.py:6-8).
 """

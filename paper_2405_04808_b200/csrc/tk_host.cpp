@@ -1,6 +1,6 @@
 // Host-side setup routines of libtempokkt_b200.so (CPU, no CUDA calls):
 //  * theta-method forward marches with per-step Newton (timedisc.py:152-191)
-//    for van der Pol (problems.py:318-373) and P1 Burgers (problems.py:425-473),
+//    for van der Pol (problems.py:42-97) and P1 Burgers (problems.py:149-197),
 //    exploiting the 2x2 / tridiagonal Jacobian instead of a dense LU;
 //  * scalar cyclic-reduction coefficients for the constant control weight.
 // These run once per hierarchy build, outside the timed hot path.

@@ -13,7 +13,7 @@ __device__ __forceinline__ double M_(double a, double b) { return __dmul_rn(a, b
 __device__ __forceinline__ double A_(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double S_(double a, double b) { return __dsub_rn(a, b); }
 
-// F_u of van der Pol (problems.py:332-336)
+// F_u of van der Pol (problems.py:56-60)
 __device__ __forceinline__ void vdp_fu(double mu, const double* u, double f[4]) {
     f[0] = 0.0;
     f[1] = 1.0;
@@ -50,7 +50,7 @@ __global__ void stage_vdp_kernel(int N, double dt, double theta, double mu, int 
     }
 }
 
-// Burgers F_u = -nu*A_stiff - J_conv(u) (problems.py:403-414, 442-443),
+// Burgers F_u = -nu*A_stiff - J_conv(u) (problems.py:127-138, 166-167),
 // P1 elements on n interior nodes, h = 1/(n+1).  Writes diagonals of
 // out = sgn*M + c*F_u(w) as [3][n].
 __device__ __forceinline__ void burgers_row(int n, double h, double nu, const double* w, int j,

@@ -1,4 +1,4 @@
-// Time-level transfers on the reference layout (multigrid.py:263-300):
+// Time-level transfers on the reference layout (multigrid.py:95-132):
 // states/multipliers (u, v, lam, mu) use injection down / linear interpolation
 // up; piecewise-constant controls use 2-interval averages down / copies up.
 //

@@ -1,5 +1,5 @@
 // TRI family: per-interval KKT blocks whose sub-blocks are tridiagonal in
-// space (P1 finite elements, 1D Burgers: problems.py:425-473).
+// space (P1 finite elements, 1D Burgers: problems.py:149-197).
 //
 // One CTA owns one block row (time interval) of the Figure-3 operator.  The
 // local KKT block (kkt.py:298-312) is solved exactly, without the dense

@@ -1,6 +1,6 @@
 // TRI family: fused residual + restriction, rc = R (b - A x)
-// (multigrid.py:449-456 `restrict_kkt(b - a.apply(x))`, transfers
-// multigrid.py:272-280).
+// (multigrid.py:281-288 `restrict_kkt(b - a.apply(x))`, transfers
+// multigrid.py:104-112).
 //
 // The restriction keeps the states/multipliers of the even fine time levels
 // and averages the controls of each fine pair, so coarse block row c needs

@@ -1,5 +1,5 @@
-"""Problem builders: van der Pol (problems.py:300-373) and 1D viscous Burgers
-with P1 finite elements (problems.py:376-473).
+"""Problem builders: van der Pol (problems.py:24-97) and 1D viscous Burgers
+with P1 finite elements (problems.py:100-197).
 
 Each returns a :class:`ProblemSpec` with the reference's Python callables
 (so generic code paths and tests can evaluate F) plus a ``native`` tag that
@@ -61,7 +61,7 @@ def _vdp_callables(mu, nc):
 def build_vanderpol(cfg: VanDerPolConfig, g: TimeGrid, theta: float = 1.0,
                     with_targets: bool = True) -> ProblemSpec:
     """Two-state oscillator; tracking data from the same oscillator with
-    damping ``data_mu`` at zero control (problems.py:318-373)."""
+    damping ``data_mu`` at zero control (problems.py:42-97)."""
     nc = cfg.n_controls
     u0 = np.array(cfg.u_init, dtype=np.float64)
     fe, fu, fz, fh = _vdp_callables(cfg.mu, nc)
@@ -124,7 +124,7 @@ def burgers_convection_jac(u):
 
 def build_burgers(cfg: BurgersConfig, g: TimeGrid) -> ProblemSpec:
     """P1 FE semi-discretisation, interior nodes only, N_z = N_u
-    (problems.py:425-473)."""
+    (problems.py:149-197)."""
     n = cfg.n_elems - 1
     h = 1.0 / cfg.n_elems
     mass = tridiag(n, h / 6.0, 4.0 * h / 6.0, h / 6.0)

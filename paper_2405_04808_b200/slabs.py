@@ -7,7 +7,7 @@ sweep a rank exchanges one u segment and one mu segment with each neighbour
 (the continuity couplings, kkt.py:221-247); prolongation exchanges the
 neighbours' edge coarse (u, lam) / (v, mu) segments; the coarsest level is
 gathered onto rank 0, solved there by the serial-in-time SGS-GMRES
-(multigrid.py:413-428) and the correction scattered back; Krylov dots are
+(multigrid.py:245-260) and the correction scattered back; Krylov dots are
 local partial sums + one allreduce.
 
 Communication goes through a small ``Comm`` interface: ``TorchComm`` wraps

@@ -68,7 +68,7 @@ def test_transfers_and_coarse(golden_case):
     lf, lc = h.levels[0].kkt.lay, h.levels[1].kkt.lay
     assert np.array_equal(O.restrict_kkt(lf, lc, g["x"]), g["restrict_x"])
     assert np.array_equal(O.prolong_kkt(lf, lc, g["xc"]), g["prolong_xc"])
-    # restrict o prolong = identity (multigrid.py:176-178)
+    # restrict o prolong = identity (multigrid.py:8-10)
     assert np.array_equal(O.restrict_kkt(lf, lc, O.prolong_kkt(lf, lc, g["xc"])), g["xc"])
     xcs = O.coarse_solve(h, g["coarse_r"])
     assert h.coarse_iters == int(g["coarse_iters"])
