@@ -197,6 +197,16 @@ int tk_rsub(int64_t n, const double* b, double* y, void* stream);
 int tk_gemv_t_add(int64_t n, int32_t k, const double* V, int64_t ld, const double* c,
                   double* x, void* stream);
 
+/* One modified Gram-Schmidt Arnoldi step, replacing the inner loop of
+ * krylov.py:77-191 (`for i in range(j+1): h = dot(V_i, w); w -= h V_i`,
+ * `hj1 = norm2(w)`, `V_{j+1} = w / hj1`) by ONE cooperative launch with a grid
+ * barrier per basis vector.  V: rows 0..j+1 of length n, leading dimension
+ * ld; w is updated in place; h (device, >= j+2 doubles) receives
+ * h_0..h_j, h_{j+1}; V_{j+1} is written when h_{j+1} != 0.  Bitwise equal to
+ * the tk_dot / tk_axpy / tk_nrm2 / tk_scale_into sequence. */
+int tk_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ld, double* w, double* h,
+                   double* work, void* stream);
+
 /* --- setup: stage linearisation on the device (timedisc.py:133, kkt.py:100) - */
 /* van der Pol: K,C,B at (v_{i-1}, u_i, z_i), v_{-1} = u0.  n_controls in {1,2}. */
 int tk_stage_vanderpol(int32_t n_steps, double dt, double theta, double mu, int32_t n_controls,

@@ -78,6 +78,7 @@ _SIGS = {
     "tk_scale_into": (C.c_int, [_i64, _d, _p, _p, _p]),
     "tk_rsub": (C.c_int, [_i64, _p, _p, _p]),
     "tk_gemv_t_add": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _p]),
+    "tk_arnoldi_mgs": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _p, _p]),
     "tk_stage_vanderpol": (C.c_int, [_i32, _d, _d, _d, _i32, _p, _p, _p, _p, _p, _p, _p, _p]),
     "tk_stage_burgers": (C.c_int, [_i32, _i32, _d, _d, _d, _p, _p, _p, _p, _p, _p]),
     "tk_forward_vanderpol_host": (C.c_int, [_i32, _d, _d, _d, _i32, _p, _p, _d, _p]),

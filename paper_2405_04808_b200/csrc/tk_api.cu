@@ -41,6 +41,7 @@ int64_t reduce_work_len();
 int dot_launch(int64_t, const double*, const double*, double*, double*, int, cudaStream_t);
 int vec_launch(int, int64_t, double, const double*, double*, cudaStream_t);
 int gemv_t_add_launch(int64_t, int, const double*, int64_t, const double*, double*, cudaStream_t);
+int arnoldi_launch(int64_t, int, double*, int64_t, double*, double*, double*, cudaStream_t);
 int stage_vdp_launch(int, double, double, double, int, const double*, const double*,
                      const double*, const double*, double*, double*, double*, cudaStream_t);
 int stage_burgers_launch(int, int, double, double, double, const double*, const double*,
@@ -259,6 +260,13 @@ int tk_scale_into(int64_t n, double a, const double* x, double* y, void* stream)
 int tk_rsub(int64_t n, const double* b, double* y, void* stream) {
     TK_CHECK_ARG(b && y, "tk_rsub: null vector");
     return vec_launch(2, n, 0.0, b, y, as_stream(stream));
+}
+
+int tk_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ld, double* w, double* h,
+                   double* work, void* stream) {
+    TK_CHECK_ARG(V && w && h && work && n >= 0 && j >= 0 && ld >= n,
+                 "tk_arnoldi_mgs: bad arguments");
+    return arnoldi_launch(n, j, V, ld, w, h, work, as_stream(stream));
 }
 
 int tk_gemv_t_add(int64_t n, int32_t k, const double* V, int64_t ld, const double* c, double* x,

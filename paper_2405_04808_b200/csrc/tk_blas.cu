@@ -2,6 +2,8 @@
 // Reductions are deterministic: a fixed grid of kReduceBlocks CTAs, each
 // summing a fixed grid-stride slice, then one CTA summing the partials in a
 // fixed tree order, so repeated solves are bitwise reproducible.
+#include <cooperative_groups.h>
+
 #include "tk_common.cuh"
 
 namespace tk {
@@ -80,7 +82,115 @@ __global__ void gemv_t_add_kernel(int64_t n, int kk, const double* __restrict__ 
     }
 }
 
-int64_t reduce_work_len() { return kReduceBlocks; }
+// ---------------------------------------------------------------------------
+// One modified Gram-Schmidt Arnoldi step in a single cooperative launch
+// (krylov.py:77-191, the inner `for i in range(j+1)` loop, the norm and the
+// normalisation of the next basis vector):
+//   for i = 0..j:  h_i = <V_i, w>;  w -= h_i V_i
+//   h_{j+1} = ||w||;  V_{j+1} = (1 / h_{j+1}) w
+// Pass i fuses the update with h_{i-1} into the reduction for h_i, so the
+// sequential MGS chain costs one grid barrier per basis vector instead of a
+// dot launch, a host round trip and an axpy launch.  The grid (kReduceBlocks
+// CTAs of kReduceThreads), the per-thread element order, the two accumulators
+// and the reduction trees are exactly those of dot_partial/sum_partials and
+// axpy_kernel's fma, so h and w are bitwise identical to the unfused
+// sequence tk_dot / tk_axpy / tk_nrm2 / tk_scale_into.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_xor_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// sum_partials' tree (1024 threads = 32 virtual warps) evaluated by one CTA
+__device__ __forceinline__ double reduce_partials(const double* __restrict__ part, double* sh) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    constexpr int NW = kReduceThreads / 32;
+    for (int vw = w; vw < 32; vw += NW) {
+        const int k = 32 * vw + l;
+        double v = k < kReduceBlocks ? __ldcg(part + k) : 0.0;
+        v = warp_xor_sum(v);
+        if (l == 0) sh[vw] = v;
+    }
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = warp_xor_sum(sh[l]);
+        if (l == 0) sh[32] = r;
+    }
+    __syncthreads();
+    r = sh[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kReduceThreads, 4)
+arnoldi_mgs_kernel(int64_t n, int j, double* __restrict__ V, int64_t ld, double* __restrict__ w,
+                   double* __restrict__ h, double* __restrict__ part) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[kReduceThreads / 32 + 34];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t k0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double hp = 0.0;   // h_{i-1}
+    for (int i = 0; i <= j + 1; ++i) {
+        const double* Vp = i > 0 ? V + (int64_t)(i - 1) * ld : nullptr;   // update with h_{i-1}
+        const double* Vi = i <= j ? V + (int64_t)i * ld : nullptr;         // dot against V_i (or w)
+        const double a = -hp;
+        double acc = 0.0, acc2 = 0.0;
+        int64_t k = k0;
+        for (; k + stride < n; k += 2 * stride) {
+            double w0 = w[k], w1 = w[k + stride];
+            if (Vp) {
+                w0 = fma(a, Vp[k], w0);
+                w1 = fma(a, Vp[k + stride], w1);
+                w[k] = w0;
+                w[k + stride] = w1;
+            }
+            acc = fma(Vi ? Vi[k] : w0, w0, acc);
+            acc2 = fma(Vi ? Vi[k + stride] : w1, w1, acc2);
+        }
+        if (k < n) {
+            double w0 = w[k];
+            if (Vp) {
+                w0 = fma(a, Vp[k], w0);
+                w[k] = w0;
+            }
+            acc = fma(Vi ? Vi[k] : w0, w0, acc);
+        }
+        acc += acc2;
+        // block_sum<kReduceThreads>
+        acc = warp_xor_sum(acc);
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        double s = (threadIdx.x < kReduceThreads / 32) ? sh[threadIdx.x] : 0.0;
+        if ((threadIdx.x >> 5) == 0) s = warp_xor_sum(s);
+        double* pslot = part + (i & 1) * kReduceBlocks;
+        if (threadIdx.x == 0) __stcg(pslot + blockIdx.x, s);
+        __syncthreads();
+        grid.sync();
+        double hi = reduce_partials(pslot, sh);
+        if (i == j + 1) hi = sqrt(hi);
+        if (blockIdx.x == 0 && threadIdx.x == 0) h[i] = hi;
+        hp = hi;
+    }
+    // V_{j+1} = (1 / h_{j+1}) w  (scale_into_kernel's a * x[k])
+    if (hp != 0.0) {
+        const double inv = 1.0 / hp;
+        double* Vn = V + (int64_t)(j + 1) * ld;
+        for (int64_t k = k0; k < n; k += stride) Vn[k] = inv * w[k];
+    }
+}
+
+int arnoldi_launch(int64_t n, int j, double* V, int64_t ld, double* w, double* h, double* work,
+                   cudaStream_t s) {
+    void* args[] = {(void*)&n, (void*)&j, (void*)&V, (void*)&ld, (void*)&w, (void*)&h, (void*)&work};
+    const cudaError_t e = cudaLaunchCooperativeKernel((const void*)arnoldi_mgs_kernel,
+                                                      dim3(kReduceBlocks), dim3(kReduceThreads),
+                                                      args, 0, s);
+    return cuda_status(e, "arnoldi_mgs_kernel");
+}
+
+int64_t reduce_work_len() { return 2 * kReduceBlocks; }
 
 int dot_launch(int64_t n, const double* x, const double* y, double* out, double* work,
                int take_sqrt, cudaStream_t s) {

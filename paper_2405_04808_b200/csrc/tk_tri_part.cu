@@ -31,7 +31,10 @@ namespace tk {
 
 namespace {
 
-constexpr int kChunk = 4;        // nodes per thread
+#ifndef TK_PART_CHUNK
+#define TK_PART_CHUNK 4          // nodes per thread (even)
+#endif
+constexpr int kChunk = TK_PART_CHUNK;
 #ifndef TK_PART_STAGE
 #define TK_PART_STAGE 1          // cp.async staging of the next row's vectors
 #endif
@@ -56,37 +59,43 @@ struct PartCta {
     static constexpr int T = 32 * W;          // threads = chunks = interface nodes
     static constexpr int P = kChunk * T;      // padded system size
     static constexpr int64_t smem_bytes() {
-        return ((int64_t)(2 * kPX + (kStage ? 4 * kSgC + kSgN : 0)) * T) * 8;
+        return ((int64_t)(2 * kPX + (kStage ? kChunk * kSgC + kSgN : 0)) * T) * 8;
     }
-    static constexpr int min_blocks() { return W >= 8 ? 1 : (TK_PART_MINB * 4) / W; }
+    static constexpr int min_blocks() { return (TK_PART_MINB * 4) / W > 1 ? (TK_PART_MINB * 4) / W : 1; }
 };
 
-// Four consecutive nodes [j0, j0+4) of segment p + o (zero beyond n).
-// FULL: n is a multiple of four chunks and every segment is 16-byte aligned.
-template <bool FULL>
+// NA consecutive nodes [j0, j0+NA) of segment p + o (zero beyond n), NA even.
+// FULL: n is a multiple of the chunk count and every segment is 16-byte aligned.
+template <bool FULL, int NA>
 __device__ __forceinline__ void ld4(const double* __restrict__ p, int64_t o, int j0, int n,
-                                    bool on, double (&r)[4]) {
-    if (!on) { r[0] = r[1] = r[2] = r[3] = 0.0; return; }
+                                    bool on, double (&r)[NA]) {
+    if (!on) {
+#pragma unroll
+        for (int k = 0; k < NA; ++k) r[k] = 0.0;
+        return;
+    }
     const double* a = p + o + j0;
-    if (FULL || (j0 + 3 < n && ((reinterpret_cast<uintptr_t>(a) & 15) == 0))) {
-        const double2 u = *reinterpret_cast<const double2*>(a);
-        const double2 v = *reinterpret_cast<const double2*>(a + 2);
-        r[0] = u.x; r[1] = u.y; r[2] = v.x; r[3] = v.y;
+    if (FULL || (j0 + NA - 1 < n && ((reinterpret_cast<uintptr_t>(a) & 15) == 0))) {
+#pragma unroll
+        for (int k = 0; k < NA; k += 2) {
+            const double2 u = *reinterpret_cast<const double2*>(a + k);
+            r[k] = u.x; r[k + 1] = u.y;
+        }
     } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) r[k] = (j0 + k < n) ? a[k] : 0.0;
+        for (int k = 0; k < NA; ++k) r[k] = (j0 + k < n) ? a[k] : 0.0;
     }
 }
-template <bool FULL>
+template <bool FULL, int NA>
 __device__ __forceinline__ void st4(double* __restrict__ p, int64_t o, int j0, int n,
-                                    const double (&r)[4]) {
+                                    const double (&r)[NA]) {
     double* a = p + o + j0;
-    if (FULL || (j0 + 3 < n && ((reinterpret_cast<uintptr_t>(a) & 15) == 0))) {
-        *reinterpret_cast<double2*>(a) = make_double2(r[0], r[1]);
-        *reinterpret_cast<double2*>(a + 2) = make_double2(r[2], r[3]);
+    if (FULL || (j0 + NA - 1 < n && ((reinterpret_cast<uintptr_t>(a) & 15) == 0))) {
+#pragma unroll
+        for (int k = 0; k < NA; k += 2) *reinterpret_cast<double2*>(a + k) = make_double2(r[k], r[k + 1]);
     } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < NA; ++k)
             if (j0 + k < n) a[k] = r[k];
     }
 }
@@ -144,11 +153,11 @@ template <bool FULL>
 __device__ __forceinline__ void stage4(double* dst, const double* p, int64_t o, int j0, int n, bool on,
                                        const double* dummy) {
     if (FULL && on) {
-        cpa16(dst, p + o + j0);
-        cpa16(dst + 2, p + o + j0 + 2);
+#pragma unroll
+        for (int k = 0; k < kChunk; k += 2) cpa16(dst + k, p + o + j0 + k);
     } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kChunk; ++k) {
             const bool v = on && j0 + k < n;
             cpa8(dst + k, v ? p + o + j0 + k : dummy, v);
         }
@@ -193,27 +202,28 @@ template <bool FULL, int T>
 __device__ __forceinline__ void stage_row(double* SG, const RowSrc& r, const double* b, const double* x,
                                           bool hx, int n, int j0) {
     const int t = threadIdx.x;
-    double* c = SG + 4 * t;                   // [kSgC][4T]
-    double* nb = SG + kSgC * 4 * T + t;       // [kSgN][T]
-    const int jL = j0 - 1, jR = j0 + 4;
-    stage4<FULL>(c + 0 * 4 * T, b, r.ov, j0, n, r.has_vm, b);
-    stage4<FULL>(c + 1 * 4 * T, b, r.om, j0, n, r.has_vm, b);
-    stage4<FULL>(c + 2 * 4 * T, b, r.ou, j0, n, r.has_uzl, b);
-    stage4<FULL>(c + 3 * 4 * T, b, r.oz, j0, n, r.has_uzl, b);
-    stage4<FULL>(c + 4 * 4 * T, b, r.ol, j0, n, r.has_uzl, b);
+    constexpr int CT = kChunk * T;
+    double* c = SG + kChunk * t;              // [kSgC][kChunk*T]
+    double* nb = SG + kSgC * CT + t;          // [kSgN][T]
+    const int jL = j0 - 1, jR = j0 + kChunk;
+    stage4<FULL>(c + 0 * CT, b, r.ov, j0, n, r.has_vm, b);
+    stage4<FULL>(c + 1 * CT, b, r.om, j0, n, r.has_vm, b);
+    stage4<FULL>(c + 2 * CT, b, r.ou, j0, n, r.has_uzl, b);
+    stage4<FULL>(c + 3 * CT, b, r.oz, j0, n, r.has_uzl, b);
+    stage4<FULL>(c + 4 * CT, b, r.ol, j0, n, r.has_uzl, b);
     stage1(nb + 0 * T, b, r.om, jL, n, r.has_vm, b);
     stage1(nb + 1 * T, b, r.om, jR, n, r.has_vm, b);
     const bool up = r.has_vm && r.uprev != nullptr, mn = r.has_uzl && r.munext != nullptr;
-    stage4<FULL>(c + 10 * 4 * T, r.uprev, 0, j0, n, up, b);
-    stage4<FULL>(c + 11 * 4 * T, r.munext, 0, j0, n, mn, b);
+    stage4<FULL>(c + 10 * CT, r.uprev, 0, j0, n, up, b);
+    stage4<FULL>(c + 11 * CT, r.munext, 0, j0, n, mn, b);
     stage1(nb + 4 * T, r.uprev, 0, jL, n, up, b);
     stage1(nb + 5 * T, r.uprev, 0, jR, n, up, b);
     if (hx) {
-        stage4<FULL>(c + 5 * 4 * T, x, r.ov, j0, n, r.has_vm, b);
-        stage4<FULL>(c + 6 * 4 * T, x, r.ou, j0, n, r.has_uzl, b);
-        stage4<FULL>(c + 7 * 4 * T, x, r.oz, j0, n, r.has_uzl, b);
-        stage4<FULL>(c + 8 * 4 * T, x, r.ol, j0, n, r.has_uzl, b);
-        stage4<FULL>(c + 9 * 4 * T, x, r.om, j0, n, r.has_vm, b);
+        stage4<FULL>(c + 5 * CT, x, r.ov, j0, n, r.has_vm, b);
+        stage4<FULL>(c + 6 * CT, x, r.ou, j0, n, r.has_uzl, b);
+        stage4<FULL>(c + 7 * CT, x, r.oz, j0, n, r.has_uzl, b);
+        stage4<FULL>(c + 8 * CT, x, r.ol, j0, n, r.has_uzl, b);
+        stage4<FULL>(c + 9 * CT, x, r.om, j0, n, r.has_vm, b);
         stage1(nb + 2 * T, x, r.ov, jL, n, r.has_vm, b);
         stage1(nb + 3 * T, x, r.ov, jR, n, r.has_vm, b);
         stage1(nb + 6 * T, x, r.ou, jL, n, r.has_uzl, b);
@@ -334,13 +344,15 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         double f0[NA], f1[NA], fw[NA], pm[NA], kd[NA], ks[NA], kb[NA];
         double ksL, kbR;
         {
-            const double* sgc = SG + 4 * tid;
-            const double* sgn = SG + kSgC * 4 * T + tid;
+            const double* sgc = SG + kChunk * tid;
+            const double* sgn = SG + kSgC * kChunk * T + tid;
             auto g4 = [&](int a, double (&r)[NA]) {
                 if (kStage) {
-                    const double2 u = *reinterpret_cast<const double2*>(sgc + a * 4 * T);
-                    const double2 v = *reinterpret_cast<const double2*>(sgc + a * 4 * T + 2);
-                    r[0] = u.x; r[1] = u.y; r[2] = v.x; r[3] = v.y;
+#pragma unroll
+                    for (int k = 0; k < NA; k += 2) {
+                        const double2 u = *reinterpret_cast<const double2*>(sgc + a * kChunk * T + k);
+                        r[k] = u.x; r[k + 1] = u.y;
+                    }
                     return;
                 }
                 const bool up = has_vm && uprev != nullptr, mnx = has_uzl && munext != nullptr;
@@ -388,7 +400,11 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             ld4<FULL>(K, 0, j0, n, has_uzl, kb);
             ksL = ld1(K, 2 * n, jL, n, has_uzl);
             kbR = ld1(K, 0, jR, n, has_uzl);
-            if (hx) g4(5, xv); else xv[0] = xv[1] = xv[2] = xv[3] = 0.0;
+            if (hx) g4(5, xv);
+            else {
+#pragma unroll
+                for (int k = 0; k < NA; ++k) xv[k] = 0.0;
+            }
             g4(10, up);
             // v at the chunk and its two neighbours
             double vv[NA];

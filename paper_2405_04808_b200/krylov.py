@@ -24,6 +24,9 @@ from . import device as dev
 from .errors import Breakdown, DimensionMismatch, NonFiniteValue
 
 BREAKDOWN_TOL = 1e-14
+# MGS Arnoldi step as one cooperative launch (tk_arnoldi_mgs) instead of
+# j+1 dot/axpy pairs with a host round trip each; bitwise identical
+FUSED_ARNOLDI = True
 
 
 @dataclass
@@ -59,6 +62,8 @@ class VecOps:
         lib = _lib.load()
         self.work = dev.empty(int(lib.tk_reduce_work_len()))
         self.scal = dev.empty(8)
+        self.hdev = None
+        self.hpin = None
 
     def dot_dev(self, x, y, slot=0):
         dev.call("tk_dot", x.numel(), dev.P(x), dev.P(y), self.scal[slot:].data_ptr(),
@@ -78,6 +83,21 @@ class VecOps:
 
     def scale_into(self, a, x, y):
         dev.call("tk_scale_into", x.numel(), float(a), dev.P(x), dev.P(y), dev.stream())
+
+    def arnoldi(self, V, j, w):
+        """MGS step against V[0..j] in one launch (tk_arnoldi_mgs): returns
+        h_0..h_{j+1} as numpy (one device->host copy); w is orthogonalised
+        in place and V[j+1] = w / h_{j+1}."""
+        k = j + 2
+        if self.hdev is None or self.hdev.numel() < k:
+            m = max(k, 2 * (self.hdev.numel() if self.hdev is not None else 64))
+            self.hdev = dev.empty(m)
+            self.hpin = torch.empty(m, dtype=torch.float64).pin_memory()
+        dev.call("tk_arnoldi_mgs", w.numel(), j, dev.P(V), V.stride(0), dev.P(w),
+                 dev.P(self.hdev), dev.P(self.work), dev.stream())
+        self.hpin[:k].copy_(self.hdev[:k], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.hpin[:k].numpy().copy()
 
     def gemv_t_add(self, V, c, x):
         """x += V[:k]^T c (V rows contiguous)."""
@@ -168,12 +188,17 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
                 if Z is not None:
                     Z[j].copy_(zj)
                     zj = Z[j]
-            w = op(zj)
-            for i in range(j + 1):
-                hij = ops.dot(V[i], w)
-                H[i, j] = hij
-                ops.axpy(-hij, V[i], w)
-            hj1 = ops.nrm2(w)
+            w = dev.to_device(op(zj))
+            if FUSED_ARNOLDI:     # one launch + one copy per step (V[j+1] written too)
+                hcol = ops.arnoldi(V, j, w)
+                H[:j + 1, j] = hcol[:j + 1]
+                hj1 = float(hcol[j + 1])
+            else:
+                for i in range(j + 1):
+                    hij = ops.dot(V[i], w)
+                    H[i, j] = hij
+                    ops.axpy(-hij, V[i], w)
+                hj1 = ops.nrm2(w)
             H[j + 1, j] = hj1
             if not math.isfinite(hj1) or not np.isfinite(H[:j + 1, j]).all():
                 raise NonFiniteValue("non-finite Hessenberg entry in Arnoldi")
@@ -199,7 +224,8 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
                 break
             if est <= target or total >= max_iters:
                 break
-            ops.scale_into(1.0 / hj1, w, V[j + 1])
+            if not FUSED_ARNOLDI:
+                ops.scale_into(1.0 / hj1, w, V[j + 1])
         if jd > 0:
             y = np.zeros(jd)
             for i in range(jd - 1, -1, -1):

@@ -62,6 +62,9 @@ def algorithmic_bytes(name: str, args) -> int:
         if name == "tk_restrict":
             return 8 * (2 * cdim + (nf // 2) * nz)
         return 8 * (2 * fdim + cdim)
+    if name == "tk_arnoldi_mgs":   # V_0..V_j and V_j+1 once, w read+written per pass
+        n, j = int(args[0]), int(args[1])
+        return 8 * n * ((j + 2) + 2 * (j + 2))
     n = int(args[0])
     return {"tk_dot": 16 * n, "tk_nrm2": 8 * n, "tk_axpy": 24 * n, "tk_scale_into": 16 * n,
             "tk_rsub": 24 * n}.get(name, 8 * n * ((int(args[1]) + 2) if name == "tk_gemv_t_add"

@@ -1,0 +1,70 @@
+"""GPU: the fused Arnoldi step (tk_arnoldi_mgs) against the unfused
+dot/axpy/nrm2/scale_into sequence of the same kernels, and MG-(F)GMRES with
+it against the reference's golden solves (krylov.py:77-210)."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, product_problem, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _mk(n, k, seed):
+    import torch
+    g = torch.Generator().manual_seed(seed)
+    V = torch.randn(k + 2, n, generator=g, dtype=torch.float64).cuda()
+    w = torch.randn(n, generator=g, dtype=torch.float64).cuda()
+    return V, w
+
+
+@pytest.mark.parametrize("n", [1, 37, 151552, 151553, 1 << 20, 3_000_017])
+@pytest.mark.parametrize("j", [0, 1, 5])
+def test_arnoldi_step_bitwise(n, j):
+    import torch
+    from paper_2405_04808_b200.krylov import vec_ops
+    ops = vec_ops()
+    V, w = _mk(n, j, 1000 * j + n % 997)
+    V2, w2 = V.clone(), w.clone()
+    h = ops.arnoldi(V, j, w)
+    ref = []
+    for i in range(j + 1):
+        hij = ops.dot(V2[i], w2)
+        ref.append(hij)
+        ops.axpy(-hij, V2[i], w2)
+    hj1 = ops.nrm2(w2)
+    ref.append(hj1)
+    ops.scale_into(1.0 / hj1, w2, V2[j + 1])
+    torch.cuda.synchronize()
+    assert np.array_equal(h, np.array(ref))
+    assert torch.equal(w, w2)
+    assert torch.equal(V[j + 1], V2[j + 1])
+
+
+@pytest.mark.parametrize("outer", ["fgmres", "gmres"])
+def test_fused_solve_bitwise_and_golden(outer):
+    """Whole MG-preconditioned solve with and without the fused step: same
+    bits; and against the reference's golden solve of BASELINE configs[1]
+    (reduced nx): identical iteration counts, 1e-10 solutions."""
+    import paper_2405_04808_b200 as P
+    from paper_2405_04808_b200 import krylov
+    g = load_golden("cfg1_burgers")
+    p, grid = product_problem(g)
+    res = {}
+    for fused in (True, False):
+        krylov.FUSED_ARNOLDI = fused
+        try:
+            h = P.build_hierarchy(p, g["u"], g["v"], g["z"], grid, int(g["levels"]),
+                                  sweeps=int(g["sweeps"]), cycle_kind="v", coarse_tol=1e-2)
+            fn = P.fgmres if outer == "fgmres" else P.gmres
+            x, rep = fn(h.levels[0].kkt.as_operator(), P.mg_preconditioner(h), g["b"],
+                        rel_tol=1e-8, max_iters=401)
+            res[fused] = (x, rep, h.stats.iters)
+        finally:
+            krylov.FUSED_ARNOLDI = True
+    (x1, r1, c1), (x0, r0, c0) = res[True], res[False]
+    assert np.array_equal(x1, x0)
+    assert r1.iterations == r0.iterations and c1 == c0
+    assert r1.iterations == int(g[f"{outer}_iters"])
+    assert c1 == int(g[f"{outer}_coarse_iters"])
+    assert rel(x1, g[f"{outer}_x"]) < 1e-10

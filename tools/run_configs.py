@@ -46,17 +46,27 @@ def main():
                    hierarchy_s=round(t_h, 2), vcycle_ms=round(ms, 3),
                    coarse_its_per_cycle=h.stats.iters / k,
                    tsdof_per_s=s.grid.n_steps * s.dof_per_step / (ms * 1e-3))
+        print(json.dumps(out), flush=True)
         if solve:
+            # (F)GMRES keeps V and Z: size the restart to the free HBM
+            free, _ = torch.cuda.mem_get_info()
+            per_it = 2 * s.dim * 8
+            m_fit = int(0.85 * free // per_it) - 2
+            restart = None if m_fit >= S["max_iters"] + 1 else max(2, m_fit)
+            out = dict(config=i, name=s.describe(), restart=restart)
             h.stats = type(h.stats)()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             x, rep = P.fgmres(h.levels[0].kkt.as_operator(), prec, r, rel_tol=S["rel_tol"],
-                              max_iters=S["max_iters"],
-                              restart=None if s.dim * 8 * 2 * 402 < 60e9 else 50)
+                              max_iters=S["max_iters"], restart=restart)
             torch.cuda.synchronize()
             out.update(solve_s=round(time.perf_counter() - t0, 3), iters=rep.iterations,
-                       final_rel=rep.final_relative_residual)
-        print(json.dumps(out), flush=True)
+                       final_rel=rep.final_relative_residual,
+                       coarse_its_avg=h.stats.average)
+            print(json.dumps(out), flush=True)
+            del x
+        del h, r, prec
+        torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":
