@@ -137,6 +137,13 @@ int tk_jacobi_sweep(const tk_level* L, const double* b, const double* x_in, doub
 int tk_forward_subst(const tk_level* L, const double* r, double* delta, void* stream);
 /* (D - U) delta = r, serial in time   replaces _backward_subst smoothers.py:95 */
 int tk_backward_subst(const tk_level* L, const double* r, double* delta, void* stream);
+/* d = (D - U)^{-1} D w, the second half of the symmetric Gauss-Seidel
+ * (smoothers.py:130-152: `(D-U)^{-1} D (D-L)^{-1} r` with w = (D-L)^{-1} r).
+ * Pass 1 of the backward substitution would form D^{-1} (D w) = w, so the
+ * coupling chain starts from w and the parallel pass solves a zero rhs on top
+ * of w.  TRI levels with factor records (after tk_subst_factor); other levels
+ * return TK_ERR_UNSUPPORTED. */
+int tk_sgs_back_half(const tk_level* L, const double* w, double* d, void* stream);
 /* Sizes (in doubles) of L->fac and L->scratch, and the one-off factorisation
  * filling L->fac (TRI: per-interval cyclic-reduction factors of the (u,lam)
  * system + C_i; DENSE: the n_u x n_u chain matrices P_u D_i^{-1} E_mu and
@@ -196,6 +203,16 @@ int tk_rsub(int64_t n, const double* b, double* y, void* stream);
 /* x += V^T c: V is k rows of length n with leading dimension ld; c on device */
 int tk_gemv_t_add(int64_t n, int32_t k, const double* V, int64_t ld, const double* c,
                   double* x, void* stream);
+
+/* dst = src (n doubles) by a kernel, not a copy engine: with src or dst in
+ * mapped pinned host memory (tk_host_device_ptr) the Krylov scalars cross
+ * PCIe without queueing behind bulk host<->device copies of other streams. */
+int tk_copy_kernel(int64_t n, const double* src, double* dst, void* stream);
+/* Mapped pinned host memory (cudaHostAllocMapped): host and device addresses. */
+int tk_host_alloc_mapped(int64_t bytes, void** host, void** dptr);
+int tk_host_free(void* host);
+/* Device address of pinned (cudaHostAlloc'd / torch pin_memory) host memory. */
+int tk_host_device_ptr(void* host, void** dptr);
 
 /* One modified Gram-Schmidt Arnoldi step, replacing the inner loop of
  * krylov.py:77-191 (`for i in range(j+1): h = dot(V_i, w); w -= h V_i`,

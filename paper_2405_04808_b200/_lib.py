@@ -58,6 +58,7 @@ _SIGS = {
     "tk_jacobi_sweep": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _d, _p]),
     "tk_forward_subst": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
     "tk_backward_subst": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
+    "tk_sgs_back_half": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
     "tk_subst_factor_len": (_i64, [C.POINTER(TkLevel)]),
     "tk_subst_scratch_len": (_i64, [C.POINTER(TkLevel)]),
     "tk_subst_factor": (C.c_int, [C.POINTER(TkLevel), _p]),
@@ -79,6 +80,10 @@ _SIGS = {
     "tk_rsub": (C.c_int, [_i64, _p, _p, _p]),
     "tk_gemv_t_add": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _p]),
     "tk_arnoldi_mgs": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _p, _p]),
+    "tk_copy_kernel": (C.c_int, [_i64, _p, _p, _p]),
+    "tk_host_device_ptr": (C.c_int, [_p, C.POINTER(C.c_void_p)]),
+    "tk_host_alloc_mapped": (C.c_int, [_i64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "tk_host_free": (C.c_int, [_p]),
     "tk_stage_vanderpol": (C.c_int, [_i32, _d, _d, _d, _i32, _p, _p, _p, _p, _p, _p, _p, _p]),
     "tk_stage_burgers": (C.c_int, [_i32, _i32, _d, _d, _d, _p, _p, _p, _p, _p, _p]),
     "tk_forward_vanderpol_host": (C.c_int, [_i32, _d, _d, _d, _i32, _p, _p, _d, _p]),

@@ -42,6 +42,7 @@ int dot_launch(int64_t, const double*, const double*, double*, double*, int, cud
 int vec_launch(int, int64_t, double, const double*, double*, cudaStream_t);
 int gemv_t_add_launch(int64_t, int, const double*, int64_t, const double*, double*, cudaStream_t);
 int arnoldi_launch(int64_t, int, double*, int64_t, double*, double*, double*, cudaStream_t);
+int copy_small_launch(int64_t, const double*, double*, cudaStream_t);
 int stage_vdp_launch(int, double, double, double, int, const double*, const double*,
                      const double*, const double*, double*, double*, double*, cudaStream_t);
 int stage_burgers_launch(int, int, double, double, double, const double*, const double*,
@@ -142,6 +143,17 @@ int tk_forward_subst(const tk_level* L, const double* r, double* delta, void* st
 int tk_backward_subst(const tk_level* L, const double* r, double* delta, void* stream) {
     TK_CHECK_ARG(r && delta && r != delta, "tk_backward_subst: bad vectors");
     return level_op(L, 11, 11, r, nullptr, delta, 1.0, stream);
+}
+
+int tk_sgs_back_half(const tk_level* L, const double* w, double* d, void* stream) {
+    TK_CHECK_ARG(w && d && w != d, "tk_sgs_back_half: bad vectors");
+    int rc = check_level(L);
+    if (rc) return rc;
+    if (L->family != TK_FAMILY_TRI) {
+        set_error("tk_sgs_back_half: TRI levels only (use apply_diag + backward_subst)");
+        return TK_ERR_UNSUPPORTED;
+    }
+    return tri_launch(L, 14, w, nullptr, d, 1.0, as_stream(stream));
 }
 
 int64_t tk_subst_factor_len(const tk_level* L) {
@@ -260,6 +272,27 @@ int tk_scale_into(int64_t n, double a, const double* x, double* y, void* stream)
 int tk_rsub(int64_t n, const double* b, double* y, void* stream) {
     TK_CHECK_ARG(b && y, "tk_rsub: null vector");
     return vec_launch(2, n, 0.0, b, y, as_stream(stream));
+}
+
+int tk_copy_kernel(int64_t n, const double* src, double* dst, void* stream) {
+    TK_CHECK_ARG(src && dst && n >= 0, "tk_copy_kernel: bad arguments");
+    if (n == 0) return TK_OK;
+    return copy_small_launch(n, src, dst, as_stream(stream));
+}
+
+int tk_host_alloc_mapped(int64_t bytes, void** host, void** dptr) {
+    TK_CHECK_ARG(bytes > 0 && host && dptr, "tk_host_alloc_mapped: bad arguments");
+    int rc = cuda_status(cudaHostAlloc(host, (size_t)bytes, cudaHostAllocMapped | cudaHostAllocPortable),
+                         "cudaHostAlloc");
+    if (rc) return rc;
+    return cuda_status(cudaHostGetDevicePointer(dptr, *host, 0), "cudaHostGetDevicePointer");
+}
+
+int tk_host_free(void* host) { return cuda_status(cudaFreeHost(host), "cudaFreeHost"); }
+
+int tk_host_device_ptr(void* host, void** dptr) {
+    TK_CHECK_ARG(host && dptr, "tk_host_device_ptr: bad arguments");
+    return cuda_status(cudaHostGetDevicePointer(dptr, host, 0), "cudaHostGetDevicePointer");
 }
 
 int tk_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ld, double* w, double* h,

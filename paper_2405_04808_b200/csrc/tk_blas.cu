@@ -192,6 +192,19 @@ int arnoldi_launch(int64_t n, int j, double* V, int64_t ld, double* w, double* h
 
 int64_t reduce_work_len() { return 2 * kReduceBlocks; }
 
+// dst[k] = src[k] with SM loads/stores: used for the few Krylov scalars that
+// cross between host and device through mapped pinned memory, so they never
+// queue behind bulk copies on the copy engines (HostPipeline)
+__global__ void copy_small_kernel(int64_t n, const double* __restrict__ src, double* __restrict__ dst) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        dst[k] = src[k];
+}
+
+int copy_small_launch(int64_t n, const double* src, double* dst, cudaStream_t s) {
+    copy_small_kernel<<<grid_for(n, 256, 64), 256, 0, s>>>(n, src, dst);
+    return check_launch("copy_small");
+}
+
 int dot_launch(int64_t n, const double* x, const double* y, double* out, double* work,
                int take_sqrt, cudaStream_t s) {
     dot_partial<<<kReduceBlocks, kReduceThreads, 0, s>>>(n, x, y, work);

@@ -209,6 +209,11 @@ int transfer_launch(int restrict_op, int n_fine, int nu, int nz, int r0, int r1,
         auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
         const bool vec = (nu % 2 == 0) && (nz % 2 == 0) && (fbase % 2 == 0) && (cbase % 2 == 0) &&
                          al(in) && al(out) && al(hprev) && al(hnext);
+        if (nu < 32) {   // tiny rows (van der Pol): one thread per fine element
+            prolong_add_kernel<<<grid_for(flen, th, 148 * 32), th, 0, s>>>(
+                Lf, Lc, fbase, flen, cbase, clen, in, hprev, hnext, out);
+            return check_launch("transfer");
+        }
         const int rows = r1 - r0;
         const int pth = nu >= 512 ? 256 : 128;
         prolong_rows_kernel<<<rows < (1 << 30) ? rows : (1 << 30), pth, 0, s>>>(

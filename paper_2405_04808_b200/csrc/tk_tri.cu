@@ -463,8 +463,10 @@ __device__ __forceinline__ void tri_block(const TView& V, int i, const double* b
     for (int j = tid; j < n; j += nth) {
         const int J = PI(j);
         double rv = 0.0, ru = 0.0, rz = 0.0, rm = 0.0, rl = 0.0;
-        if (has_vm) { rv = b[ov + j]; rm = b[om + j]; }
-        if (has_uzl) { ru = b[ou + j]; rz = b[oz + j]; rl = b[ol + j]; }
+        if (b) {
+            if (has_vm) { rv = b[ov + j]; rm = b[om + j]; }
+            if (has_uzl) { ru = b[ou + j]; rz = b[oz + j]; rl = b[ol + j]; }
+        }
         if (x) {
             if (has_vm) {
                 double av = tmv(Qv, n, x + ov, j) - x[om + j];
@@ -1313,8 +1315,10 @@ __device__ __forceinline__ void tri_block_rec(const TView& V, int i, const doubl
     for (int j = tid; j < n; j += nth) {
         const int J = PI(j);
         double rv = 0.0, ru = 0.0, rz = 0.0, rm = 0.0, rl = 0.0;
-        if (has_vm) { rv = b[ov + j]; rm = b[om + j]; }
-        if (has_uzl) { ru = b[ou + j]; rz = b[oz + j]; rl = b[ol + j]; }
+        if (b) {
+            if (has_vm) { rv = b[ov + j]; rm = b[om + j]; }
+            if (has_uzl) { ru = b[ou + j]; rz = b[oz + j]; rl = b[ol + j]; }
+        }
         if (x) {
             if (has_vm) {
                 double av = tmv(Qv, n, x + ov, j) - x[om + j];
@@ -1398,6 +1402,21 @@ __global__ void __launch_bounds__(256, 2) tri_rows_rec_cpl(TView V, const double
         const double* uprev = (FWD && i >= 1) ? chain + (size_t)(i - 1) * n : nullptr;
         const double* munext = (!FWD && i < L.N) ? chain + (size_t)(i + 1) * n : nullptr;
         tri_block_rec<NT>(V, i, r, nullptr, uprev, munext, y, 1.0, nullptr, sm);
+    }
+}
+
+// Pass 3 of the SGS back half (D-U)^{-1} D w:  y_i = w_i - D_i^{-1} U_i y_{i+1}
+// (zero rhs, the chain's mu_{i+1} as the coupling, w as the update base).
+template <int NT>
+__global__ void __launch_bounds__(256, 2) tri_rows_rec_sgsb(TView V, const double* __restrict__ w,
+                                                            const double* __restrict__ chain,
+                                                            double* __restrict__ y) {
+    extern __shared__ __align__(16) double sm[];
+    const Lay& L = V.lay;
+    const int n = dimn<NT>(V);
+    for (int i = blockIdx.x; i <= L.N; i += gridDim.x) {
+        const double* munext = i < L.N ? chain + (size_t)(i + 1) * n : nullptr;
+        tri_block_rec<NT>(V, i, nullptr, nullptr, nullptr, munext, y, 1.0, w, sm);
     }
 }
 
@@ -1666,6 +1685,7 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                              cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(tri_rows_rec_cpl<true, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(tri_rows_rec_sgsb<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(tri_rows_rec_cpl<false, NT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(tri_rows_cpl<true, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1722,15 +1742,26 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             else tri_rows<NT><<<rows, th, smem, s>>>(V, b, x, y, omega);
             break;
         case 10:
-        case 11: {
+        case 11:
+        case 14: {
+            // 14: second half of the symmetric Gauss-Seidel, d = (D-U)^{-1} D w
+            // (smoothers.py:130-152) with w = b: pass 1 would compute
+            // D^{-1} (D w) = w, so the chain starts from w itself and pass 3
+            // solves with a zero rhs on top of w
             const bool fwd = op == 10;
+            const bool sgsb = op == 14;
+            if (sgsb && !(fast && rec)) {
+                set_error("sgs back half needs the level's factor records");
+                return TK_ERR_UNSUPPORTED;
+            }
             if (!fast) {
                 if (fwd) tri_subst<true, NT><<<1, th, smem, s>>>(V, b, y);
                 else tri_subst<false, NT><<<1, th, smem, s>>>(V, b, y);
                 break;
             }
             // pass 1: a = D^{-1} r into y
-            if (!rec && use_part(n)) {
+            if (sgsb) {
+            } else if (!rec && use_part(n)) {
                 const int rc = part_launch(Lv, 0, b, nullptr, y, 1.0, nullptr, s);
                 if (rc) return rc;
             } else if (rec) tri_rows_rec<NT><<<rows, rth, rsm, s>>>(V, b, nullptr, y, 1.0);
@@ -1755,14 +1786,15 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             double* PT = chunked ? P + (size_t)nc * n * n : nullptr;
             double* E = chunked ? PT + (size_t)nc * n * n : nullptr;
             double* S = chunked ? E + (size_t)nc * n : nullptr;
+            const double* av = sgsb ? b : y;   // D^{-1} r of pass 1 (or w itself)
             auto chain_launch = [&](int grid, int cbase, const double* st, double* en) {
                 if (grid <= 0) return;
                 if (stg) {
-                    if (fwd) tri_chain_kernel<true, true, false, NT><<<grid, cth, csm, s>>>(V, y, fac, chn, Lc, cbase, st, en);
-                    else tri_chain_kernel<false, true, false, NT><<<grid, cth, csm, s>>>(V, y, fac, chn, Lc, cbase, st, en);
+                    if (fwd) tri_chain_kernel<true, true, false, NT><<<grid, cth, csm, s>>>(V, av, fac, chn, Lc, cbase, st, en);
+                    else tri_chain_kernel<false, true, false, NT><<<grid, cth, csm, s>>>(V, av, fac, chn, Lc, cbase, st, en);
                 } else {
-                    if (fwd) tri_chain_kernel<true, false, false, NT><<<grid, cth, csm, s>>>(V, y, fac, chn, Lc, cbase, st, en);
-                    else tri_chain_kernel<false, false, false, NT><<<grid, cth, csm, s>>>(V, y, fac, chn, Lc, cbase, st, en);
+                    if (fwd) tri_chain_kernel<true, false, false, NT><<<grid, cth, csm, s>>>(V, av, fac, chn, Lc, cbase, st, en);
+                    else tri_chain_kernel<false, false, false, NT><<<grid, cth, csm, s>>>(V, av, fac, chn, Lc, cbase, st, en);
                 }
             };
             if (!chunked || nc == 1) {
@@ -1778,7 +1810,9 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                 chain_launch(nc - 1, fwd ? 1 : 0, S, nullptr);   // non-seed chunks again
             }
             // pass 3: parallel solves with the chain coupling
-            if (rec) {
+            if (sgsb) {
+                tri_rows_rec_sgsb<NT><<<rows, rth, rsm, s>>>(V, b, chn, y);
+            } else if (rec) {
                 if (fwd) tri_rows_rec_cpl<true, NT><<<rows, rth, rsm, s>>>(V, b, chn, y);
                 else tri_rows_rec_cpl<false, NT><<<rows, rth, rsm, s>>>(V, b, chn, y);
             } else if (use_part(n)) {

@@ -55,9 +55,12 @@ KERNELS_PER_CALL = {"tk_dot": 2, "tk_nrm2": 2}
 
 
 def _launches(name, args) -> int:
-    if name in ("tk_residual_restrict", "tk_forward_subst", "tk_backward_subst"):
+    if name in ("tk_residual_restrict", "tk_forward_subst", "tk_backward_subst",
+                "tk_sgs_back_half"):
         lv = getattr(args[0], "_obj", None)
         tri = lv is not None and lv.family == _lib.FAMILY_TRI
+        if name == "tk_sgs_back_half":
+            return 4                        # chunk chains, carry, re-run, coupled rows
         if name == "tk_residual_restrict":
             return 1 if tri else 2          # fused TRI kernel / residual + restrict
         if not tri:

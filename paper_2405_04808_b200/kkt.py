@@ -381,6 +381,12 @@ class BlockTriKKT:
         self.level.chain_prod = self._chain.data_ptr()
         dev.call("tk_chain_prod", self.lref, dev.stream())
 
+    @property
+    def has_records(self) -> bool:
+        """Factor records present (tk_subst_factor ran), so the substitutions
+        run as parallel solve -> chain -> parallel solve."""
+        return self._fac is not None
+
     def ensure_records(self, force: bool = False) -> None:
         """TRI levels whose node arrays do not fit in shared memory (n_u > 1664,
         or ``force``/``TK_RECORDS_ALL=1``): precompute the per-interval factor

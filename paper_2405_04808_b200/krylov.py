@@ -12,6 +12,7 @@ as numpy).
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 from typing import Callable
@@ -55,28 +56,67 @@ class SolveReport:
     final_relative_residual: float = float("nan")
 
 
+class MappedScalars:
+    """Pinned host memory mapped into the device address space
+    (tk_host_alloc_mapped).  Reduction kernels write their scalars straight
+    into it and the host reads them after a stream synchronisation; uploads
+    go through tk_copy_kernel.  No scalar crosses PCIe on a copy engine, so
+    the Krylov recurrence never queues behind a bulk host<->device copy of
+    another stream (HostPipeline)."""
+
+    def __init__(self, n: int):
+        lib = _lib.load()
+        h, d = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(lib.tk_host_alloc_mapped(8 * n, ctypes.byref(h), ctypes.byref(d)),
+                   "tk_host_alloc_mapped")
+        self.n = n
+        self.host_ptr, self.dev_ptr = h.value, d.value
+        self.host = np.ctypeslib.as_array((ctypes.c_double * n).from_address(h.value))
+
+    def dptr(self, k: int = 0) -> int:
+        return self.dev_ptr + 8 * k
+
+    def __del__(self):
+        try:
+            _lib.load().tk_host_free(ctypes.c_void_p(self.host_ptr))
+        except Exception:
+            pass
+
+
+def _sync():
+    torch.cuda.current_stream().synchronize()
+
+
 class VecOps:
-    """Thin wrapper over the BLAS-1 kernels with a reusable scalar buffer."""
+    """Thin wrapper over the BLAS-1 kernels; scalars live in mapped pinned
+    memory (MappedScalars)."""
 
     def __init__(self):
         lib = _lib.load()
         self.work = dev.empty(int(lib.tk_reduce_work_len()))
         self.scal = dev.empty(8)
-        self.hdev = None
-        self.hpin = None
+        self.ms = MappedScalars(8)
+        self.hmap = None        # Hessenberg column (grown on demand)
+        self.cdev = None        # uploaded gemv coefficients
+        self.cmap = None
 
     def dot_dev(self, x, y, slot=0):
+        """<x, y> into the device scalar self.scal[slot] (no host sync)."""
         dev.call("tk_dot", x.numel(), dev.P(x), dev.P(y), self.scal[slot:].data_ptr(),
                  dev.P(self.work), dev.stream())
         return self.scal[slot]
 
     def dot(self, x, y) -> float:
-        return float(self.dot_dev(x, y).item())
+        dev.call("tk_dot", x.numel(), dev.P(x), dev.P(y), self.ms.dptr(0), dev.P(self.work),
+                 dev.stream())
+        _sync()
+        return float(self.ms.host[0])
 
     def nrm2(self, x) -> float:
-        dev.call("tk_nrm2", x.numel(), dev.P(x), self.scal.data_ptr(), dev.P(self.work),
+        dev.call("tk_nrm2", x.numel(), dev.P(x), self.ms.dptr(1), dev.P(self.work),
                  dev.stream())
-        return float(self.scal[0].item())
+        _sync()
+        return float(self.ms.host[1])
 
     def axpy(self, a, x, y):
         dev.call("tk_axpy", x.numel(), float(a), dev.P(x), dev.P(y), dev.stream())
@@ -86,25 +126,32 @@ class VecOps:
 
     def arnoldi(self, V, j, w):
         """MGS step against V[0..j] in one launch (tk_arnoldi_mgs): returns
-        h_0..h_{j+1} as numpy (one device->host copy); w is orthogonalised
-        in place and V[j+1] = w / h_{j+1}."""
+        h_0..h_{j+1} (written by the kernel into mapped host memory); w is
+        orthogonalised in place and V[j+1] = w / h_{j+1}."""
         k = j + 2
-        if self.hdev is None or self.hdev.numel() < k:
-            m = max(k, 2 * (self.hdev.numel() if self.hdev is not None else 64))
-            self.hdev = dev.empty(m)
-            self.hpin = torch.empty(m, dtype=torch.float64).pin_memory()
+        if self.hmap is None or self.hmap.n < k:
+            self.hmap = MappedScalars(max(k, 2 * (self.hmap.n if self.hmap else 64)))
         dev.call("tk_arnoldi_mgs", w.numel(), j, dev.P(V), V.stride(0), dev.P(w),
-                 dev.P(self.hdev), dev.P(self.work), dev.stream())
-        self.hpin[:k].copy_(self.hdev[:k], non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return self.hpin[:k].numpy().copy()
+                 self.hmap.dptr(), dev.P(self.work), dev.stream())
+        _sync()
+        return self.hmap.host[:k].copy()
 
     def gemv_t_add(self, V, c, x):
-        """x += V[:k]^T c (V rows contiguous)."""
-        k = int(c.numel())
+        """x += V[:k]^T c (V rows contiguous; c numpy or torch)."""
+        k = int(c.numel()) if isinstance(c, torch.Tensor) else int(np.size(c))
         if k == 0:
             return
-        cd = dev.to_device(c)
+        if isinstance(c, torch.Tensor) and c.is_cuda:
+            cd = c.contiguous()
+        else:
+            if self.cmap is None or self.cmap.n < k:
+                self.cmap = MappedScalars(max(k, 2 * (self.cmap.n if self.cmap else 64)))
+                self.cdev = dev.empty(self.cmap.n)
+            _sync()                      # the previous upload has been consumed
+            self.cmap.host[:k] = np.asarray(c.cpu() if isinstance(c, torch.Tensor) else c,
+                                            dtype=np.float64)
+            dev.call("tk_copy_kernel", k, self.cmap.dptr(), dev.P(self.cdev), dev.stream())
+            cd = self.cdev
         dev.call("tk_gemv_t_add", x.numel(), k, dev.P(V), V.stride(0), dev.P(cd), dev.P(x),
                  dev.stream())
 
@@ -230,7 +277,7 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
             y = np.zeros(jd)
             for i in range(jd - 1, -1, -1):
                 y[i] = (g[i] - H[i, i + 1:jd] @ y[i + 1:jd]) / H[i, i]
-            yt = torch.from_numpy(y)
+            yt = y
             if Z is not None:
                 ops.gemv_t_add(Z, yt, x)
             else:

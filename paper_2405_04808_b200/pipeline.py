@@ -24,13 +24,21 @@ from . import device as dev
 
 
 class HostPipeline:
-    def __init__(self, prec: Callable, dim: int):
+    """``depth`` device input buffers; copy-ins are enqueued ``depth - 1``
+    steps ahead so the host->device engine streams back to back while the
+    V-cycles run (the preconditioner's Krylov scalars use mapped memory, not
+    the copy engines, so they never queue behind these copies)."""
+
+    def __init__(self, prec: Callable, dim: int, depth: int = 3):
+        if depth < 2:
+            raise ValueError("depth must be >= 2")
         self.prec = prec
         self.dim = dim
+        self.depth = depth
         self.h2d = torch.cuda.Stream()
         self.d2h = torch.cuda.Stream()
         self.comp = torch.cuda.current_stream()
-        self.din = [dev.empty(dim), dev.empty(dim)]
+        self.din = [dev.empty(dim) for _ in range(depth)]
 
     def run(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
             start_event: torch.cuda.Event = None) -> None:
@@ -42,26 +50,27 @@ class HostPipeline:
         n = len(inputs)
         if n == 0:
             return
-        copied = [torch.cuda.Event() for _ in range(2)]
-        consumed = [torch.cuda.Event() for _ in range(2)]
-        done = [None] * n
+        D = self.depth
+        copied = [torch.cuda.Event() for _ in range(D)]
+        consumed = [torch.cuda.Event() for _ in range(D)]
 
         if start_event is not None:
             self.h2d.wait_event(start_event)
 
         def copy_in(k):
-            s = k & 1
+            s = k % D
             with torch.cuda.stream(self.h2d):
-                if k >= 2:
-                    self.h2d.wait_event(consumed[s])   # the V-cycle of step k-2 read din[s]
+                if k >= D:
+                    self.h2d.wait_event(consumed[s])   # the V-cycle of step k-D read din[s]
                 self.din[s].copy_(inputs[k], non_blocking=True)
                 copied[s].record(self.h2d)
 
-        copy_in(0)
+        for k in range(min(D - 1, n)):
+            copy_in(k)
         for k in range(n):
-            s = k & 1
-            if k + 1 < n:
-                copy_in(k + 1)
+            s = k % D
+            if k + D - 1 < n:
+                copy_in(k + D - 1)
             self.comp.wait_event(copied[s])
             out = self.prec(self.din[s])
             consumed[s].record(self.comp)
@@ -71,5 +80,4 @@ class HostPipeline:
                 self.d2h.wait_event(ev)
                 outputs[k].copy_(out, non_blocking=True)
                 out.record_stream(self.d2h)
-            done[k] = out
         self.comp.wait_stream(self.d2h)

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 from . import device as dev
 from .errors import DimensionMismatch
-from .kkt import BlockTriKKT, DiagonalSolver
+from .kkt import FAMILY_TRI, BlockTriKKT, DiagonalSolver
 from .krylov import Preconditioner
 
 SMOOTHER_KINDS = ("jacobi", "fgs", "bgs", "sgs")
@@ -85,8 +85,14 @@ def bgs_apply(a: BlockTriKKT, dfac, b, x):
 
 
 def sgs_zero(a: BlockTriKKT, r, out=None):
-    """P_sgs^{-1} r = (D-U)^{-1} D (D-L)^{-1} r, i.e. sgs_apply from x = 0."""
+    """P_sgs^{-1} r = (D-U)^{-1} D (D-L)^{-1} r, i.e. sgs_apply from x = 0.
+    TRI levels with factor records fuse `D` and the backward substitution's
+    D^{-1} (tk_sgs_back_half: the backward chain starts from w itself)."""
     w = forward_subst(a, r)
+    if a.family == FAMILY_TRI and a.has_records and not a.is_slab:
+        d = dev.empty(a.dim) if out is None else out
+        dev.call("tk_sgs_back_half", a.lref, dev.P(w), dev.P(d), dev.stream())
+        return d
     y = a.apply_diag(w)
     return backward_subst(a, y, out=out)
 

@@ -68,3 +68,29 @@ def test_fused_solve_bitwise_and_golden(outer):
     assert r1.iterations == int(g[f"{outer}_iters"])
     assert c1 == int(g[f"{outer}_coarse_iters"])
     assert rel(x1, g[f"{outer}_x"]) < 1e-10
+
+
+def test_cfg1_full_size_solve_vs_reference():
+    """BASELINE configs[1] at FULL size (Burgers nx=128, nt=1024, 4-level
+    V(1,1), FGMRES 1e-8 / 401 its) against the record of the reference's own
+    solve (tests/golden/make_cfg1_full.py, 29 min on the CPU): same outer and
+    coarse iteration counts, residual history and solution fingerprint within
+    1e-10."""
+    import paper_2405_04808_b200 as P
+    from paper_2405_04808_b200 import configs
+    g = load_golden("cfg1_full_solve")
+    s = configs.build_setup(1)
+    S = s.solver
+    h = P.build_hierarchy(s.problem, s.u, s.v, s.z, s.grid, s.levels, sweeps=S["sweeps"],
+                          cycle_kind=S["cycle"], coarse_tol=S["coarse_tol"])
+    b = s.rhs()
+    assert abs(np.linalg.norm(b) - float(g["b_norm"])) <= 1e-12 * float(g["b_norm"])
+    x, rep = P.fgmres(h.levels[0].kkt.as_operator(), P.mg_preconditioner(h), b,
+                      rel_tol=S["rel_tol"], max_iters=S["max_iters"])
+    assert rep.iterations == int(g["fgmres_iters"])
+    assert h.stats.calls == int(g["coarse_calls"]) and h.stats.iters == int(g["coarse_iters"])
+    hist = np.array(rep.residual_history)
+    assert rel(hist, g["fgmres_hist"]) < 1e-10
+    assert abs(rep.final_relative_residual - float(g["fgmres_rel"])) < 1e-10
+    assert rel(x[::int(g["x_stride"])], g["x_sample"]) < 1e-10
+    assert abs(np.linalg.norm(x) - float(g["x_norm"])) < 1e-10 * float(g["x_norm"])
