@@ -923,7 +923,7 @@ template <bool FWD, bool STAGED, bool HOM, int NT>
 __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
                                  const double* __restrict__ fac, double* __restrict__ chain,
                                  int Lc, int cbase, const double* __restrict__ starts,
-                                 double* __restrict__ ends) {
+                                 double* __restrict__ ends, int span = 1) {
     extern __shared__ __align__(16) double sm[];
     __shared__ __align__(8) uint64_t bars[2];
     const Lay& L = V.lay;
@@ -936,8 +936,10 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
     double* fbase = STAGED ? sm + 2 * brec : sm;
     double* fr[2] = {fbase, fbase + 2 * np};
     const int K = N - 1;  // chain steps after the seed
-    const int c = cbase + blockIdx.x;
-    const int lo = c * Lc, hi = min(K, lo + Lc);
+    const int c = cbase + blockIdx.x * span;
+    int hi0 = min(K, c * Lc + span * Lc);
+    if (span > 1) hi0 = min(hi0, ((K + Lc - 1) / Lc - 1) * Lc);   // groups stop before the last chunk
+    const int lo = c * Lc, hi = hi0;
     const int k0 = FWD ? lo : K - hi, k1 = FWD ? hi : K - lo;
     const bool seed = !HOM && k0 == 0;
     auto blk = [&](int k) { return FWD ? 1 + k : N - 1 - k; };
@@ -996,7 +998,7 @@ __global__ void tri_chain_kernel(TView V, const double* __restrict__ a,
         }
     }
     __syncthreads();
-    double* eout = ends ? (HOM ? ends + ((size_t)c * n + ey) * n : ends + (size_t)c * n) : nullptr;
+    double* eout = ends ? (HOM ? ends + ((size_t)(c / span) * n + ey) * n : ends + (size_t)c * n) : nullptr;
     for (int k = k0; k < k1; ++k) {
         const int t = k - k0;
         const int i = blk(k);
@@ -1153,6 +1155,109 @@ __global__ void __launch_bounds__(1024, 1)
     cl.sync();   // no CTA leaves while peers may still write into it
 }
 
+// Grouped carry (two-level scan of the chunk recurrence).  The transitions
+// over chunks 1..nc-2 are split into groups of G consecutive chunks (group g:
+// chunks [1+gG, min(nc-2, (g+1)G)]), one thread-block cluster per group.
+//   mode 1 (phase A, all groups at once): run the group's transitions from
+//     zero -- or, for the group first in chain order, from the exact seed
+//     ends[first] (writing the exact starts) -- and store the group's end
+//     value in GE[g];
+//   phase B (tri_chain_carry over the groups with the group propagators Phi_g
+//     and GE as the ends): exact group starts GS[g];
+//   mode 2 (phase C, all groups but the first in chain order): re-run the
+//     transitions from GS[g], writing the exact chunk starts.
+// The group last in chain order also writes the start of the final chunk.
+// Serial depth: 2G + nc/G matvecs instead of nc.
+template <bool FWD>
+__global__ void __launch_bounds__(1024, 1)
+    tri_chain_carry_seg(int n, int nc, int G, int mode, const double* __restrict__ M,
+                        const double* __restrict__ ends, double* __restrict__ starts,
+                        double* __restrict__ GE, const double* __restrict__ GS, int staged) {
+    extern __shared__ __align__(16) double sm[];   // U ping-pong [2][n], row block
+    __shared__ __align__(8) uint64_t tbar;
+    __shared__ __align__(8) uint64_t ubar[2];
+    cg::cluster_group cl = cg::this_cluster();
+    const int CS = (int)cl.num_blocks();
+    const int rank = (int)cl.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int ng = (nc - 2 + G - 1) / G;
+    const int q = blockIdx.x / CS;
+    const int gi = (mode == 2 && FWD) ? q + 1 : q;
+    const bool first = FWD ? gi == 0 : gi == ng - 1;
+    const bool last = FWD ? gi == ng - 1 : gi == 0;
+    const int lo = 1 + gi * G, hi = min(nc - 2, (gi + 1) * G);
+    const int L = hi - lo + 1;
+    auto chunk_of = [&](int t) { return FWD ? lo + t : hi - t; };
+    const int rpc = (n + CS - 1) / CS;
+    const int r0 = min(n, rank * rpc), r1 = min(n, r0 + rpc);
+    double* blk = sm + 2 * n;
+    const unsigned bytes = (unsigned)((size_t)(r1 - r0) * n * sizeof(double));
+    const bool stg = staged && bytes > 0;
+    const unsigned ubytes = (unsigned)(n * sizeof(double));
+    auto issue = [&](int t) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_tx(&tbar, bytes);
+        tma_g2s(blk, M + (size_t)chunk_of(t) * n * n + (size_t)r0 * n, bytes, &tbar);
+    };
+    if (tid == 0) {
+        mbar_init(&tbar, 1);
+        mbar_init(&ubar[0], 1);
+        mbar_init(&ubar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (stg && tid == 0 && L > 0) issue(0);
+    const double* init = mode == 2 ? GS + (size_t)gi * n
+                                   : (first ? ends + (size_t)(FWD ? 0 : nc - 1) * n : nullptr);
+    for (int j = tid; j < n; j += blockDim.x) sm[j] = init ? init[j] : 0.0;
+    cl.sync();   // every CTA's barriers are initialised before any st.async
+    const bool wstart = mode == 2 || first;
+    unsigned tphase = 0;
+    for (int t = 0; t < L; ++t) {   // transition t: U_{t+1} = E_c + M_c U_t
+        const int c = chunk_of(t);
+        if (t >= 1) mbar_wait(&ubar[t & 1], (unsigned)(((t - 1) >> 1) & 1));
+        const double* cur = sm + (t & 1) * n;
+        if (wstart)
+            for (int j = r0 + tid; j < r1; j += blockDim.x) starts[(size_t)c * n + j] = cur[j];
+        if (tid == 0) mbar_expect_tx(&ubar[(t + 1) & 1], ubytes);   // arm the copy of U_{t+1}
+        if (stg) { mbar_wait(&tbar, tphase); tphase ^= 1u; }
+        const double* src = stg ? blk : M + (size_t)c * n * n + (size_t)r0 * n;
+        const double* ec = ends + (size_t)c * n;
+        const unsigned nxt = smem_u32(sm + ((t + 1) & 1) * n);
+        const unsigned bar = smem_u32(&ubar[(t + 1) & 1]);
+        for (int r = r0 + warp; r < r1; r += nw) {
+            const double* row = src + (size_t)(r - r0) * n;
+            const double e = ec[r];
+            double a0 = 0.0, a1 = 0.0;
+            int k = lane;
+            for (; k + 32 < n; k += 64) {
+                a0 = fma(row[k], cur[k], a0);
+                a1 = fma(row[k + 32], cur[k + 32], a1);
+            }
+            if (k < n) a0 = fma(row[k], cur[k], a0);
+            double acc = a0 + a1;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            const double v = e + acc;
+            for (int d = lane; d < CS; d += 32)
+                st_async_f64(mapa_u32(nxt + 8u * r, d), v, mapa_u32(bar, d));
+        }
+        if (stg) {
+            __syncthreads();   // row block consumed: refill with the next transition's
+            if (tid == 0 && t + 1 < L) issue(t + 1);
+        }
+    }
+    if (L > 0) mbar_wait(&ubar[L & 1], (unsigned)(((L - 1) >> 1) & 1));
+    const double* fin = sm + (L & 1) * n;
+    if (mode == 1)
+        for (int j = r0 + tid; j < r1; j += blockDim.x) GE[(size_t)gi * n + j] = fin[j];
+    if (last && (mode == 2 || first)) {
+        const int cf = FWD ? nc - 1 : 0;
+        for (int j = r0 + tid; j < r1; j += blockDim.x) starts[(size_t)cf * n + j] = fin[j];
+    }
+    cl.sync();   // no CTA leaves while peers may still write into it
+}
+
 // Grid-wide variant of the carry (one CTA per SM, cooperative launch): CTA g
 // owns rows [g R, g R + R) of every M_c.  Its row blocks are streamed by TMA
 // into a ring of D shared-memory slots up to D chunks ahead, so the HBM
@@ -1260,9 +1365,40 @@ __global__ void tri_transpose(const double* __restrict__ in, double* __restrict_
     }
 }
 
+static int carry_mode(int n);
+// group size of the two-level carry for nc chunks (0: single serial carry).
+// At most 9 groups: one 16-CTA cluster per group must be co-resident.
+// TK_CARRY_GROUP overrides (0 disables).
+static int carry_group(int n, int nc) {
+    static int forced = -2;
+    if (forced == -2) {
+        const char* e = getenv("TK_CARRY_GROUP");
+        forced = e ? atoi(e) : -1;
+    }
+    const int T = nc - 2;   // transitions
+    if (forced >= 0) return (forced >= 2 && T >= 2 * forced) ? forced : 0;
+    if (carry_mode(n) != 1 || T <= 12) return 0;
+    int g = (int)sqrt((double)T);
+    const int need = (T + 8) / 9;
+    return g < need ? need : g;
+}
+static int chain_ng(int nc, int G) { return G > 0 ? (nc - 2 + G - 1) / G : 0; }
+
 int32_t tri_chain_chunk_default(int n, int N) {
     const int K = N - 1;
     if (n < 2 || K < 24) return 0;
+    if (carry_mode(n) == 1 && K >= 128) {
+        // grouped carry: phases A and C stream every chunk propagator (n^2
+        // doubles each) once, so fewer, longer chunks than the latency-only
+        // optimum (K/2)^(1/3); measured on configs[2] (n=512, K=511): Lc = 12
+        // (203 us per substitution) vs 7 (264) and 20 (232)
+        int lc = (int)ceil(sqrt(K / 4.0));
+        const int need = (K + 147) / 148;
+        if (lc < need) lc = need;
+        if (lc < 4) lc = 4;
+        const int nc = (K + lc - 1) / lc;
+        if (carry_group(n, nc) > 0) return lc;
+    }
     int lc = (int)ceil(sqrt(K / 2.0));
     const int need = (K + 147) / 148;    // at most one chunk per SM
     if (lc < need) lc = need;
@@ -1277,7 +1413,9 @@ static int chain_nc(int N, int Lc) {
 int64_t tri_chain_prod_len(const tk_level* Lv) {
     if (Lv->chain_chunk <= 0) return 0;
     const int64_t n = Lv->n_u, nc = chain_nc(Lv->n_steps, Lv->chain_chunk);
-    return 2 * nc * n * n + 3 * nc * n + 4;   // P, P^T, ends, starts, U_t, counters
+    const int64_t ng = chain_ng((int)nc, carry_group((int)n, (int)nc));
+    // P, P^T, ends, starts, U_t, counters | Phi, Phi^T, group ends, group starts
+    return 2 * nc * n * n + 3 * nc * n + 4 + 2 * ng * n * n + 2 * ng * n;
 }
 
 // ---------------------------------------------------------------------------
@@ -1556,8 +1694,10 @@ static int tri_chain_threads(int n) {
 
 // Launch the chunk carry as one cluster: 16 CTAs (non-portable) when that
 // fits, else 8; the row blocks are TMA-staged when they fit in shared memory.
+// seg_mode 1/2: the grouped carry's phase A / C (clusters = groups).
 static int carry_launch(bool fwd, int n, int nc, const double* M, const double* E, double* S,
-                        cudaStream_t s) {
+                        cudaStream_t s, int seg_mode = 0, int G = 0, double* GE = nullptr,
+                        const double* GS = nullptr) {
     static int cs_ok = 0;   // cluster size verified for this process
     auto base_for = [&](int) -> int64_t { return (int64_t)2 * n * 8; };   // U ping-pong
     auto smem_for = [&](int cs) -> int64_t {
@@ -1566,7 +1706,8 @@ static int carry_launch(bool fwd, int n, int nc, const double* M, const double* 
     };
     const int64_t lim = 227 * 1024 - 1024;
     if (!cs_ok) {
-        for (void* f : {(void*)tri_chain_carry<true>, (void*)tri_chain_carry<false>}) {
+        for (void* f : {(void*)tri_chain_carry<true>, (void*)tri_chain_carry<false>,
+                        (void*)tri_chain_carry_seg<true>, (void*)tri_chain_carry_seg<false>}) {
             cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
         }
@@ -1598,9 +1739,20 @@ static int carry_launch(bool fwd, int n, int nc, const double* M, const double* 
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(cs); cfg.blockDim = dim3(1024); cfg.dynamicSmemBytes = (size_t)smem;
+    int clusters = 1;
+    if (seg_mode) {
+        const int ng = chain_ng(nc, G);
+        clusters = seg_mode == 1 ? ng : ng - 1;
+        if (clusters <= 0) return TK_OK;
+    }
+    cfg.gridDim = dim3(cs * clusters); cfg.blockDim = dim3(1024); cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = s; cfg.attrs = at; cfg.numAttrs = 1;
     cudaError_t e;
+    if (seg_mode) {
+        if (fwd) e = cudaLaunchKernelEx(&cfg, tri_chain_carry_seg<true>, n, nc, G, seg_mode, M, E, S, GE, GS, staged);
+        else e = cudaLaunchKernelEx(&cfg, tri_chain_carry_seg<false>, n, nc, G, seg_mode, M, E, S, GE, GS, staged);
+        return cuda_status(e, "tri_chain_carry_seg");
+    }
     if (fwd) e = cudaLaunchKernelEx(&cfg, tri_chain_carry<true>, n, nc, M, E, S, staged);
     else e = cudaLaunchKernelEx(&cfg, tri_chain_carry<false>, n, nc, M, E, S, staged);
     return cuda_status(e, "tri_chain_carry");
@@ -1803,9 +1955,22 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                 chain_launch(nc, 0, nullptr, E);                 // all chunks from zero
                 double* Ug = S + (size_t)nc * n;
                 unsigned* cnt = (unsigned*)(Ug + (size_t)nc * n);
-                const int rc = carry_mode(n) == 1
-                                   ? carry_launch(fwd, n, nc, fwd ? P : PT, E, S, s)
-                                   : carry_grid_launch(fwd, n, nc, fwd ? P : PT, E, S, Ug, cnt, s);
+                const int G = carry_group(n, nc);
+                int rc;
+                if (G > 0) {   // two-level carry: groups from zero -> group starts -> groups again
+                    const int ng = chain_ng(nc, G);
+                    double* PhiF = reinterpret_cast<double*>(cnt) + 4;
+                    double* PhiT = PhiF + (size_t)ng * n * n;
+                    double* GE = PhiT + (size_t)ng * n * n;
+                    double* GS = GE + (size_t)ng * n;
+                    rc = carry_launch(fwd, n, nc, fwd ? P : PT, E, S, s, 1, G, GE, GS);
+                    if (!rc && ng >= 2) rc = carry_launch(fwd, n, ng, fwd ? PhiF : PhiT, GE, GS, s);
+                    if (!rc && ng >= 2) rc = carry_launch(fwd, n, nc, fwd ? P : PT, E, S, s, 2, G, GE, GS);
+                } else {
+                    rc = carry_mode(n) == 1
+                             ? carry_launch(fwd, n, nc, fwd ? P : PT, E, S, s)
+                             : carry_grid_launch(fwd, n, nc, fwd ? P : PT, E, S, Ug, cnt, s);
+                }
                 if (rc) return rc;
                 chain_launch(nc - 1, fwd ? 1 : 0, S, nullptr);   // non-seed chunks again
             }
@@ -1869,6 +2034,16 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             tri_chain_kernel<true, false, true, NT><<<g, cth, direct, s>>>(V, nullptr, Lv->fac, nullptr, Lc, 1, nullptr, PT);
             dim3 tg((n + 31) / 32, (n + 31) / 32, nc);
             tri_transpose<<<tg, dim3(32, 8), 0, s>>>(PT, P, n);
+            const int G = carry_group(n, nc);
+            if (G > 0) {   // group propagators Phi_g over chunks [1+gG, (g+1)G] (rows of Phi^T)
+                const int ng = chain_ng(nc, G);
+                double* PhiF = Lv->chain_prod + 2 * (size_t)nc * n * n + 3 * (size_t)nc * n + 4;
+                double* PhiT = PhiF + (size_t)ng * n * n;
+                dim3 gg(ng, n);
+                tri_chain_kernel<true, false, true, NT><<<gg, cth, direct, s>>>(V, nullptr, Lv->fac, nullptr, Lc, 1, nullptr, PhiT, G);
+                dim3 tg2((n + 31) / 32, (n + 31) / 32, ng);
+                tri_transpose<<<tg2, dim3(32, 8), 0, s>>>(PhiT, PhiF, n);
+            }
             break;
         }
         default: set_error("tri: bad op %d", op); return TK_ERR_ARG;
