@@ -35,8 +35,11 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 # ncu-measured DRAM traffic per C-ABI call: which CUDA kernels one call launches
 # (launch-list patterns), or the fine-level launch of the `--set full` capture
 _NCU_KERNELS = {
-    "tk_forward_subst": ("tri_chain_kernel<1", "tri_chain_carry<1", "tri_rows_rec<", "tri_rows_rec_cpl<1"),
+    "tk_forward_subst": ("tri_chain_kernel<1, 1", "tri_chain_carry_seg<1", "tri_chain_carry<1",
+                         "tri_rows_rec<", "tri_rows_rec_cpl<1"),
     "tk_backward_subst": ("tri_chain_kernel<0", "tri_chain_carry<0", "tri_rows_rec<", "tri_rows_rec_cpl<0"),
+    "tk_sgs_back_half": ("tri_chain_kernel<0", "tri_chain_carry_seg<0", "tri_chain_carry<0",
+                         "tri_rows_rec_sgsb"),
 }
 _NCU_FULL = {
     "tk_jacobi_sweep": "tri_rows_part",
@@ -224,8 +227,9 @@ def run_ours(args, rank, world, local_rank):
 
     # per-kernel breakdown from one untimed profiled step (events around every call)
     names = {"tk_jacobi_sweep", "tk_residual_restrict", "tk_prolong_add", "tk_forward_subst",
-             "tk_backward_subst", "tk_kkt_apply", "tk_kkt_apply_diag", "tk_kkt_residual",
-             "tk_dot", "tk_nrm2", "tk_axpy", "tk_scale_into", "tk_rsub", "tk_gemv_t_add"}
+             "tk_backward_subst", "tk_sgs_back_half", "tk_kkt_apply", "tk_kkt_apply_diag",
+             "tk_kkt_residual", "tk_dot", "tk_nrm2", "tk_axpy", "tk_scale_into", "tk_rsub",
+             "tk_gemv_t_add", "tk_arnoldi_mgs", "tk_copy_kernel"}
     dev.INSTR.timed, dev.INSTR.records = names, []
     prec(r_dev)
     torch.cuda.synchronize()

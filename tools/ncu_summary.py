@@ -30,11 +30,16 @@ def launches(path):
         elif m.startswith("dram__bytes"):
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
             per[k]["bytes"] += v * scale
-    tot = sum(d["ns"] for d in per.values())
+    # one-off hierarchy setup (stage linearisation, factor records, chunk and
+    # group propagators) is listed but excluded from the V-cycle shares
+    setup = ("tri_chain_kernel<1, 0, 1,", "tri_factor_kernel", "stage_", "tri_transpose")
+    is_setup = {k: any(s in k for s in setup) for k in per}
+    tot = sum(d["ns"] for k, d in per.items() if not is_setup[k])
     out = []
-    for k, d in sorted(per.items(), key=lambda kv: -kv[1]["ns"]):
-        out.append(dict(kernel=k, launches=int(d["n"]), total_us=round(d["ns"] / 1e3, 1),
-                        share=round(d["ns"] / tot, 4),
+    for k, d in sorted(per.items(), key=lambda kv: (is_setup[kv[0]], -kv[1]["ns"])):
+        out.append(dict(kernel=k, setup=is_setup[k], launches=int(d["n"]),
+                        total_us=round(d["ns"] / 1e3, 1),
+                        share=None if is_setup[k] else round(d["ns"] / tot, 4),
                         dram_bytes_per_launch=int(d["bytes"] / max(d["n"], 1)),
                         dram_GBps=round(d["bytes"] / max(d["ns"], 1), 1)))
     return out
@@ -85,7 +90,8 @@ if __name__ == "__main__":
     with open(prefix + "_summary.json", "w") as fh:
         json.dump({"launch_list": L, "full_capture": F}, fh, indent=1)
     with open(prefix + "_summary.txt", "w") as fh:
-        fh.write("# per-kernel totals from the ncu launch list (cold-cache, serialised)\n")
+        fh.write("# per-kernel totals from the ncu launch list of one V-cycle after the hierarchy\n"
+                 "# build (cold-cache, serialised); setup kernels listed last, share = of the V-cycle\n")
         for d in L:
             fh.write(json.dumps(d) + "\n")
         fh.write("\n# ncu --set full capture\n")
