@@ -1878,7 +1878,7 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
     const bool rec = Lv->fac != nullptr && !(Lv->flags & TK_FLAG_ONTHEFLY);   // record-based D^{-1}
     const int64_t rsm = tri_rec_smem_bytes(n);
     const int rth = tri_rec_threads(n);
-    if (!rec && smem == 0) {
+    if (!rec && smem == 0 && !use_part(n)) {
         set_error("tri family: n_u=%d needs factor records (tk_subst_factor + qz_w)", n);
         return TK_ERR_UNSUPPORTED;
     }
@@ -1904,6 +1904,10 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             const bool sgsb = op == 14;
             if (sgsb && !(fast && rec)) {
                 set_error("sgs back half needs the level's factor records");
+                return TK_ERR_UNSUPPORTED;
+            }
+            if (!fast && smem == 0) {
+                set_error("tri family: n_u=%d substitutions need factor records (tk_subst_factor)", n);
                 return TK_ERR_UNSUPPORTED;
             }
             if (!fast) {

@@ -25,6 +25,8 @@
 // The scalar system Q_z w = r_z rides along through the same steps.  The grid
 // is persistent (two CTAs per SM loop over the block rows).  Nodes >= n pad
 // the system to 4T nodes with identity blocks.
+#include <cooperative_groups.h>
+
 #include "tk_tri.cuh"
 
 namespace tk {
@@ -269,18 +271,40 @@ extern "C" int tk_debug_part_prof(long long* out10) {
 // loads are independent, so a CTA has its whole row in flight at once) and
 // kept in registers through the solve; the neighbours j0-1 and j0+4 come
 // from single loads (L1 hits: the adjacent threads load those lines).
-template <int W, int MODE, bool FULL>
+//
+// CL = 2 (n_u > 1024): a block row spans a 2-CTA cluster; CTA r owns chunks
+// [rT, (r+1)T) and the exchanges across the two halves (the neighbour
+// chunk's bottom-up results, the interface PCR partners, the left interface
+// value and the first lam of the right neighbour) read the peer's shared
+// memory (distributed shared memory) after cluster barriers.
+template <int W, int MODE, bool FULL, int CL>
 __global__ void __launch_bounds__(32 * W, PartCta<W>::min_blocks())
 tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ x,
               double* __restrict__ y, double omega, const double* __restrict__ chain) {
     using Cf = PartCta<W>;
     constexpr int T = Cf::T;
+    constexpr int TT = CL * T;                // interface nodes of a row
     constexpr int NA = kChunk;
     extern __shared__ __align__(16) double sm[];
     const Lay& L = V.lay;
-    const int n = FULL ? Cf::P : V.n;
+    const int n = FULL ? Cf::P * CL : V.n;
     const int tid = threadIdx.x;
     __builtin_assume(tid < T);
+    namespace cgs = cooperative_groups;
+    const int rank = CL > 1 ? (int)cgs::this_cluster().block_rank() : 0;
+    const int gt = rank * T + tid;            // chunk index within the row
+    const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+    auto csync = [&]() {
+        if (CL > 1) cgs::this_cluster().sync();
+        else __syncthreads();
+    };
+    // element k*T of buffer `base` for the chunk with row index g (own or peer smem)
+    auto at = [&](const double* base, int g) -> const double* {
+        if (CL == 1) return base + g;
+        const int o = g / T;
+        const double* p = o == rank ? base : cgs::this_cluster().map_shared_rank(base, o);
+        return p + (g - o * T);
+    };
     const double kap = V.kappa, k2 = kap * kap;
     const double* Qz = V.Qz;
     double* PX[2] = {sm, sm + kPX * T};    // PCR ping-pong slots
@@ -289,7 +313,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
     double* XO = nullptr;                  // interface solution (a PCR slot)
     double* LAM = nullptr;                 // first lam of every chunk (the other PCR slot)
 
-    const int j0 = kChunk * tid;
+    const int j0 = kChunk * gt;
     const int jL = j0 - 1, jR = j0 + NA;
 #ifdef TK_PROF
     long long g_part_last = 0;
@@ -302,14 +326,14 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
     ld4<FULL>(Qz, 0, j0, n, true, qzb);
     const double qzsL = ld1(Qz, 2 * n, jL, n, true), qzbR = ld1(Qz, 0, jR, n, true);
 
-    if (kStage && V.sl.r0 + (int)blockIdx.x < V.sl.r1)
-        stage_row<FULL, T>(SG, row_src<MODE>(V, x, chain, V.sl.r0 + blockIdx.x), b, x,
+    if (kStage && V.sl.r0 + cid < V.sl.r1)
+        stage_row<FULL, T>(SG, row_src<MODE>(V, x, chain, V.sl.r0 + cid), b, x,
                            MODE == 0 && x != nullptr, n, j0);
-    for (int i = V.sl.r0 + blockIdx.x; i < V.sl.r1; i += gridDim.x) {
+    for (int i = V.sl.r0 + cid; i < V.sl.r1; i += ncl) {
         if (kStage) cpa_wait();
         const bool has_vm = i >= 1, has_uzl = i < L.N;
-        if (tid == 0 && i + (int)gridDim.x < V.sl.r1) {   // next row's stage data -> L2
-            const int i2 = i + gridDim.x;
+        if (gt == 0 && i + ncl < V.sl.r1) {   // next row's stage data -> L2
+            const int i2 = i + ncl;
             if (!kStage) {
                 const int64_t q0 = L.start(i2) - bs;
                 const int64_t q1 = (i2 == L.N ? L.dim() : L.start(i2 + 1)) - bs;
@@ -624,8 +648,8 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             }
         }
         TKPP(2);
-        if (kStage && i + (int)gridDim.x < V.sl.r1)   // the next row's vectors -> this thread's slots
-            stage_row<FULL, T>(SG, row_src<MODE>(V, x, chain, i + gridDim.x), b, x, hx, n, j0);
+        if (kStage && i + ncl < V.sl.r1)   // the next row's vectors -> this thread's slots
+            stage_row<FULL, T>(SG, row_src<MODE>(V, x, chain, i + ncl), b, x, hx, n, j0);
         // exchange 1: this chunk's bottom-up results for the previous chunk
         {
             double* E = XB[0];
@@ -634,15 +658,15 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             E[5 * T + tid] = H00; E[6 * T + tid] = H01; E[7 * T + tid] = H10; E[8 * T + tid] = H11;
             E[9 * T + tid] = s_idh; E[10 * T + tid] = s_hh; E[11 * T + tid] = s_Hh;
         }
-        __syncthreads();
+        csync();
         TKPP(3);
         // step C: symmetric interface rows  C_{l-1}^T X_{l-1} + B_l X_l + C_l X_{l+1} = R_l
         // (B symmetric; the lower coupling is the transposed upper coupling of the
         // row below), block and scalar
         double B00, B01, B11, C00, C01, C10, C11, R0, R1, sB, sC, sR;
         {
-            const double* E = XB[0];
-            const int nx = tid + 1 < T ? tid + 1 : tid;   // last chunk: coupling is zero
+            const double* E = at(XB[0], gt + 1 < TT ? gt + 1 : gt);   // last chunk: coupling is zero
+            constexpr int nx = 0;
             const double na = E[0 * T + nx], nb = E[1 * T + nx], nc = E[2 * T + nx];
             const double nha = E[3 * T + nx], nhb = E[4 * T + nx];
             const double nH00 = E[5 * T + nx], nH01 = E[6 * T + nx];
@@ -682,7 +706,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         {
             int slot = 0;
 #pragma unroll
-            for (int s = 1; s < T; s <<= 1) {
+            for (int s = 1; s < TT; s <<= 1) {
                 double* E = PX[slot];
                 {
                     const S2 iv = inv_s2f(B00, B01, B11);
@@ -703,19 +727,21 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                     E[14 * T + tid] = sC * sp; E[15 * T + tid] = sC * sq;
                     E[16 * T + tid] = ib; E[17 * T + tid] = sq; E[18 * T + tid] = sp;
                 }
-                __syncthreads();
-                if (tid >= s) {
-                    const int m = tid - s;
-                    B00 -= E[0 * T + m]; B01 -= E[1 * T + m]; B11 -= E[2 * T + m];
-                    R0 -= E[3 * T + m]; R1 -= E[4 * T + m];
-                    sB -= E[14 * T + m]; sR -= E[15 * T + m];
+                csync();
+                if (gt >= s) {
+                    const double* Em = at(E, gt - s);
+                    constexpr int m = 0;
+                    B00 -= Em[0 * T + m]; B01 -= Em[1 * T + m]; B11 -= Em[2 * T + m];
+                    R0 -= Em[3 * T + m]; R1 -= Em[4 * T + m];
+                    sB -= Em[14 * T + m]; sR -= Em[15 * T + m];
                 }
-                if (tid + s < T) {
-                    const int m = tid + s;
-                    const double ia = E[5 * T + m], ib = E[6 * T + m], ic = E[7 * T + m];
-                    const double q0 = E[8 * T + m], q1 = E[9 * T + m];
-                    const double p00 = E[10 * T + m], p01 = E[11 * T + m];
-                    const double p10 = E[12 * T + m], p11 = E[13 * T + m];
+                if (gt + s < TT) {
+                    const double* Em = at(E, gt + s);
+                    constexpr int m = 0;
+                    const double ia = Em[5 * T + m], ib = Em[6 * T + m], ic = Em[7 * T + m];
+                    const double q0 = Em[8 * T + m], q1 = Em[9 * T + m];
+                    const double p00 = Em[10 * T + m], p01 = Em[11 * T + m];
+                    const double p10 = Em[12 * T + m], p11 = Em[13 * T + m];
                     // K = C iB
                     const double k00 = C00 * ia + C01 * ib, k01 = C00 * ib + C01 * ic;
                     const double k10 = C10 * ia + C11 * ib, k11 = C10 * ib + C11 * ic;
@@ -727,7 +753,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                     const double n00 = -(C00 * p00 + C01 * p10), n01 = -(C00 * p01 + C01 * p11);
                     const double n10 = -(C10 * p00 + C11 * p10), n11 = -(C10 * p01 + C11 * p11);
                     C00 = n00; C01 = n01; C10 = n10; C11 = n11;
-                    const double sib = E[16 * T + m], ssq = E[17 * T + m], ssp = E[18 * T + m];
+                    const double sib = Em[16 * T + m], ssq = Em[17 * T + m], ssp = Em[18 * T + m];
                     sB -= sC * sC * sib;
                     sR -= sC * ssq;
                     sC = -sC * ssp;
@@ -742,14 +768,17 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             E[tid] = iv.a * R0 + iv.b * R1;
             E[T + tid] = iv.b * R0 + iv.c * R1;
             E[2 * T + tid] = sR * frcp(sB);
-            __syncthreads();
+            csync();
             XO = E;
             LAM = PX[slot ^ 1];
         }
         TKPP(5);
         const double X0 = XO[tid], X1 = XO[T + tid], sX = XO[2 * T + tid];
         double xl0 = 0.0, xl1 = 0.0, sxl = 0.0;
-        if (tid > 0) { xl0 = XO[tid - 1]; xl1 = XO[T + tid - 1]; sxl = XO[2 * T + tid - 1]; }
+        if (gt > 0) {
+            const double* Xl = at(XO, gt - 1);
+            xl0 = Xl[0]; xl1 = Xl[T]; sxl = Xl[2 * T];
+        }
         // steps D/E: rhs sweep with the left interface, back-substitution (registers)
         double yu[NA], yl[NA], yw[NA];
         {
@@ -778,8 +807,8 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         {
             LAM[tid] = yl[0];
         }
-        __syncthreads();
-        const double lamR = (tid + 1 < T) ? LAM[tid + 1] : 0.0;
+        csync();
+        const double lamR = (gt + 1 < TT) ? *at(LAM, gt + 1) : 0.0;
         TKPP(7);
 #if !TK_PART_EARLY
         // the output's loads, issued early: their latency overlaps the interface solve
@@ -825,7 +854,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             }
         }
         TKPP(8);
-        __syncthreads();
+        csync();   // peers are done reading this CTA's exchange slots
         TKPP(9);
     }
 }
@@ -833,33 +862,36 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
 // ---------------------------------------------------------------------------
 // host dispatch
 // ---------------------------------------------------------------------------
+// warps per CTA and CTAs per row (cluster size): up to 8 warps (n_u <= 1024)
+// one CTA per row; 1024 < n_u <= 2048 a 2-CTA cluster of 8 warps each (one
+// CTA of 16 warps would need 512 threads x 255 registers)
 static int part_warps(int n) {
-    if (n <= 4 || n > 2048) return 0;
+    if (n <= 4 || n > 2 * kChunk * 32 * 8) return 0;
     int w = 1;
-    while (kChunk * 32 * w < n) w <<= 1;
+    while (kChunk * 32 * w < n && w < 8) w <<= 1;
     return w;
 }
+static int part_cluster(int n) { return n > kChunk * 32 * 8 ? 2 : 1; }
 
 int part_nodes_per_lane(int n) { return part_warps(n) ? kChunk : 0; }
 
-template <int W, int MODE, bool FULL>
+template <int W, int MODE, bool FULL, int CL>
 static int part_launch_t(const tk_level* Lv, const double* b, const double* x, double* y,
                          double omega, const double* chain, cudaStream_t s) {
     using Cf = PartCta<W>;
     static int per_sm = 0;
     static int nsm = 0;
     const int64_t smem = Cf::smem_bytes();
+    auto kern = tri_rows_part<W, MODE, FULL, CL>;
     if (!per_sm) {
-        cudaFuncSetAttribute(tri_rows_part<W, MODE, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        cudaFuncSetAttribute(tri_rows_part<W, MODE, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         int per = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tri_rows_part<W, MODE, FULL>, 32 * W,
-                                                      (size_t)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * W, (size_t)smem);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_status(e, "tri_rows_part: attributes");
         if (per < 1) {
@@ -870,41 +902,50 @@ static int part_launch_t(const tk_level* Lv, const double* b, const double* x, d
     }
     TView V(Lv);
     const int rows = V.sl.r1 - V.sl.r0;
-    int grid = rows;
-    const int cap = nsm * per_sm;
-    if (grid > cap) grid = cap;
-    tri_rows_part<W, MODE, FULL><<<grid, 32 * W, smem, s>>>(V, b, x, y, omega, chain);
-    return check_launch("tri_rows_part");
+    int clusters = rows;
+    const int cap = nsm * per_sm / CL;
+    if (clusters > cap) clusters = cap;
+    if (CL == 1) {
+        kern<<<clusters, 32 * W, smem, s>>>(V, b, x, y, omega, chain);
+        return check_launch("tri_rows_part");
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(clusters * CL); cfg.blockDim = dim3(32 * W); cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = s; cfg.attrs = at; cfg.numAttrs = 1;
+    return cuda_status(cudaLaunchKernelEx(&cfg, kern, V, b, x, y, omega, chain), "tri_rows_part (cluster)");
 }
 
 // mode 0: rows (jacobi / D^{-1} b), 1/2: substitution pass 3 forward/backward
 int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, double* y,
                 double omega, const double* chain, cudaStream_t s) {
-#define TK_PART_CASE(WW)                                                                   \
-    case WW:                                                                               \
-        if (full) {                                                                        \
-            if (mode == 0) return part_launch_t<WW, 0, true>(Lv, b, x, y, omega, chain, s);  \
-            if (mode == 1) return part_launch_t<WW, 1, true>(Lv, b, x, y, omega, chain, s);  \
-            return part_launch_t<WW, 2, true>(Lv, b, x, y, omega, chain, s);                 \
-        }                                                                                  \
-        if (mode == 0) return part_launch_t<WW, 0, false>(Lv, b, x, y, omega, chain, s);     \
-        if (mode == 1) return part_launch_t<WW, 1, false>(Lv, b, x, y, omega, chain, s);     \
-        return part_launch_t<WW, 2, false>(Lv, b, x, y, omega, chain, s);
+#define TK_PART_CASE(WW, CC)                                                                        \
+    if (w == WW && cl == CC) {                                                                      \
+        if (full) {                                                                                 \
+            if (mode == 0) return part_launch_t<WW, 0, true, CC>(Lv, b, x, y, omega, chain, s);     \
+            if (mode == 1) return part_launch_t<WW, 1, true, CC>(Lv, b, x, y, omega, chain, s);     \
+            return part_launch_t<WW, 2, true, CC>(Lv, b, x, y, omega, chain, s);                    \
+        }                                                                                           \
+        if (mode == 0) return part_launch_t<WW, 0, false, CC>(Lv, b, x, y, omega, chain, s);        \
+        if (mode == 1) return part_launch_t<WW, 1, false, CC>(Lv, b, x, y, omega, chain, s);        \
+        return part_launch_t<WW, 2, false, CC>(Lv, b, x, y, omega, chain, s);                       \
+    }
     // FULL: every chunk is complete and every segment 16-byte aligned
-    const int w = part_warps(Lv->n_u);
+    const int w = part_warps(Lv->n_u), cl = part_cluster(Lv->n_u);
     auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    const bool full = w > 0 && Lv->n_u == kChunk * 32 * w && Lv->n_u % 2 == 0 && Lv->n_z % 2 == 0 &&
+    const bool full = w > 0 && Lv->n_u == kChunk * 32 * w * cl && Lv->n_u % 2 == 0 && Lv->n_z % 2 == 0 &&
                       al(b) && al(x) && al(y) && al(chain) && al(Lv->K) && al(Lv->C) &&
                       al(Lv->Qm) && al(Lv->Ql) && al(Lv->Qz) && al(Lv->halo_u) && al(Lv->halo_mu);
-    switch (part_warps(Lv->n_u)) {
-        TK_PART_CASE(1)
-        TK_PART_CASE(2)
-        TK_PART_CASE(4)
-        TK_PART_CASE(8)
-        TK_PART_CASE(16)
-        default: set_error("tri_rows_part: unsupported n_u=%d", Lv->n_u); return TK_ERR_UNSUPPORTED;
-    }
+    TK_PART_CASE(1, 1)
+    TK_PART_CASE(2, 1)
+    TK_PART_CASE(4, 1)
+    TK_PART_CASE(8, 1)
+    TK_PART_CASE(8, 2)
 #undef TK_PART_CASE
+    set_error("tri_rows_part: unsupported n_u=%d", Lv->n_u);
+    return TK_ERR_UNSUPPORTED;
 }
 
 }  // namespace tk

@@ -388,13 +388,13 @@ class BlockTriKKT:
         return self._fac is not None
 
     def ensure_records(self, force: bool = False) -> None:
-        """TRI levels whose node arrays do not fit in shared memory (n_u > 1664,
+        """TRI levels beyond the partitioned on-the-fly solve (n_u > 2048,
         or ``force``/``TK_RECORDS_ALL=1``): precompute the per-interval factor
         records once so that every local solve runs rhs-only.  Smaller levels
         refactor on the fly, which moves fewer HBM bytes per sweep."""
         if self.family != FAMILY_TRI:
             return
-        if force or self.n_u > 1664 or os.environ.get("TK_RECORDS_ALL") == "1":
+        if force or self.n_u > 2048 or os.environ.get("TK_RECORDS_ALL") == "1":
             self._ensure_fac()
 
     @property

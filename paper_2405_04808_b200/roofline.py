@@ -40,8 +40,8 @@ def algorithmic_bytes(name: str, args) -> int:
         L = _lvl(args[0])
         nvec = 2 + (1 if args[2] else 0)
         return 8 * dim_of(L) * nvec + stage_bytes(L)
-    if name in ("tk_diag_solve", "tk_forward_subst", "tk_backward_subst", "tk_kkt_apply",
-                "tk_kkt_apply_diag"):
+    if name in ("tk_diag_solve", "tk_forward_subst", "tk_backward_subst", "tk_sgs_back_half",
+                "tk_kkt_apply", "tk_kkt_apply_diag"):
         L = _lvl(args[0])
         return 8 * dim_of(L) * 2 + stage_bytes(L)
     if name == "tk_kkt_residual":
@@ -65,6 +65,8 @@ def algorithmic_bytes(name: str, args) -> int:
     if name == "tk_arnoldi_mgs":   # V_0..V_j and V_j+1 once, w read+written per pass
         n, j = int(args[0]), int(args[1])
         return 8 * n * ((j + 2) + 2 * (j + 2))
+    if name == "tk_copy_kernel":
+        return 16 * int(args[0])
     n = int(args[0])
     return {"tk_dot": 16 * n, "tk_nrm2": 8 * n, "tk_axpy": 24 * n, "tk_scale_into": 16 * n,
             "tk_rsub": 24 * n}.get(name, 8 * n * ((int(args[1]) + 2) if name == "tk_gemv_t_add"

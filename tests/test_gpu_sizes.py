@@ -103,7 +103,7 @@ def test_chunked_coarse_cycle():
     assert rel(x, xo) < 1e-10
 
 
-@pytest.mark.parametrize("n_u", [1000, 1024, 2048])
+@pytest.mark.parametrize("n_u", [1000, 1024, 1100, 1536, 2048])
 def test_large_n_identities(n_u):
     """Large spatial sizes (BASELINE configs[4] has n_u = 2048), where dense
     oracle inverses are out of reach: the block-diagonal solve and the Jacobi
