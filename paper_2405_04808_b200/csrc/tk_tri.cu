@@ -36,9 +36,12 @@ static constexpr int kFacRows = 14;
 // Cut level c of the chain's cyclic reduction: levels below c run as usual;
 // the reduced system on the A = n >> c <= 32 active nodes left at level c is
 // solved with its precomputed dense inverse W (2A x 2A, stored transposed).
+#ifndef TK_CUT_A
+#define TK_CUT_A 32   // largest reduced system solved densely (nodes)
+#endif
 __host__ __device__ __forceinline__ constexpr int cut_level(int n) {
     int c = 0;
-    while ((n >> c) > 32) ++c;
+    while ((n >> c) > TK_CUT_A) ++c;
     return c;
 }
 __host__ __device__ __forceinline__ constexpr int cut_nodes(int n) { return n >> cut_level(n); }

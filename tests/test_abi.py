@@ -74,3 +74,30 @@ def test_configs_match_baseline_shapes():
     s1 = configs.build_setup(1, nt=64, nx=16)
     g1 = load_golden("cfg1_burgers")
     assert rel(s1.u, g1["fwd_states"]) < 1e-14
+
+
+def test_chain_sizing_without_gpu():
+    """Host-side sizing of the time-chunked coupling chain (no device work):
+    chunk length defaults, at most one chunk per SM, and the propagator
+    buffer length including the two-level carry's group propagators."""
+    from paper_2405_04808_b200 import _lib
+    lib = _lib.load()
+    # configs[2] coarsest level: n_u = 512, 512 intervals -> grouped carry, Lc = 12
+    assert lib.tk_chain_chunk_default(512, 512) == 12
+    assert lib.tk_chain_chunk_default(64, 16) == 0                 # too short to chunk
+    for n_u, N in [(64, 64), (128, 128), (512, 512), (512, 4096), (2048, 512)]:
+        lc = lib.tk_chain_chunk_default(n_u, N)
+        assert lc >= 4 and (N - 1 + lc - 1) // lc <= 148
+    lv = _lib.TkLevel(family=_lib.FAMILY_TRI, n_steps=512, n_u=512, n_z=512)
+    for f in ("K", "C", "Qm", "Ql", "Qz", "qz_cr"):   # never dereferenced by the sizing
+        setattr(lv, f, 16)
+    lv.chain_chunk = 12
+    nc = (511 + 11) // 12                                           # 43 chunks
+    ng = (nc - 2 + 6 - 1) // 6                                      # groups of 6 -> 7
+    n = 512
+    want = 2 * nc * n * n + 3 * nc * n + 4 + 2 * ng * n * n + 2 * ng * n
+    import ctypes
+    assert lib.tk_chain_prod_len(ctypes.byref(lv)) == want
+    lv.chain_chunk = 100                                            # 6 chunks: single carry
+    nc = (511 + 99) // 100
+    assert lib.tk_chain_prod_len(ctypes.byref(lv)) == 2 * nc * n * n + 3 * nc * n + 4
