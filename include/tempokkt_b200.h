@@ -103,11 +103,14 @@ typedef struct tk_level {
     int32_t chain_chunk;
     /* TK_FLAG_ONTHEFLY: TRI local solves (Jacobi, diagonal solve, the
      * parallel passes of the substitutions) refactor on the fly even when
-     * L->fac holds factor records. */
+     * L->fac holds factor records.  By default records drive them only where
+     * the partitioned on-the-fly solve cannot run (n_u > 2048);
+     * TK_FLAG_RECROWS forces the record-based kernels whenever records exist. */
     int32_t flags;
 } tk_level;
 
 #define TK_FLAG_ONTHEFLY 1
+#define TK_FLAG_RECROWS 2
 
 /* --- library ------------------------------------------------------------ */
 const char* tk_version(void);

@@ -29,6 +29,7 @@ _i64 = C.c_int64
 
 
 TK_FLAG_ONTHEFLY = 1
+TK_FLAG_RECROWS = 2
 
 
 class TkLevel(C.Structure):

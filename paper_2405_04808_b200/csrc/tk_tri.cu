@@ -1878,7 +1878,11 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
         set_error("tri family: level is missing qz_w");
         return TK_ERR_ARG;
     }
-    const bool rec = Lv->fac != nullptr && !(Lv->flags & TK_FLAG_ONTHEFLY);   // record-based D^{-1}
+    // record-based D^{-1} only where the partitioned on-the-fly solve cannot run
+    // (n_u > 2048): with 512 rows (configs[2] coarsest) tri_rows_part takes
+    // 19 us per pass against 26-29 us for the record-based kernels
+    const bool rec = Lv->fac != nullptr && !(Lv->flags & TK_FLAG_ONTHEFLY) &&
+                     (!use_part(n) || (Lv->flags & TK_FLAG_RECROWS));
     const int64_t rsm = tri_rec_smem_bytes(n);
     const int rth = tri_rec_threads(n);
     if (!rec && smem == 0 && !use_part(n)) {
@@ -1905,7 +1909,7 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             // solves with a zero rhs on top of w
             const bool fwd = op == 10;
             const bool sgsb = op == 14;
-            if (sgsb && !(fast && rec)) {
+            if (sgsb && !fast) {
                 set_error("sgs back half needs the level's factor records");
                 return TK_ERR_UNSUPPORTED;
             }

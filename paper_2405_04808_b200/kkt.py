@@ -396,6 +396,8 @@ class BlockTriKKT:
             return
         if force or self.n_u > 2048 or os.environ.get("TK_RECORDS_ALL") == "1":
             self._ensure_fac()
+            if force:            # the record-based row kernels even where tri_rows_part runs
+                self.level.flags |= _lib.TK_FLAG_RECROWS
 
     @property
     def dim(self) -> int:

@@ -291,6 +291,7 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
                 ops.scale_into(0.0, V[0], vy)
                 ops.gemv_t_add(V, yt, vy)
                 ops.axpy(1.0, vy if prec is None else dev.to_device(prec(vy)), x)
+        zj = w = None        # views of Z / V: drop them so the bases are freed before a restart
         del V, Z
         r = _residual(op, b, x)
         ops.nrm2_async(x, 2)              # the finiteness check rides on the next sync

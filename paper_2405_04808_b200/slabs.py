@@ -503,6 +503,34 @@ def bench_rank(args, rank, world, local_rank):
     ms = comm.allreduce_max(e0.elapsed_time(e1)) / args.steps
     launches = int(comm.allreduce_max(float(dev.INSTR.launches)))
     clocks = clk.stop() if clk else None
+    # roofline of the dominant kernel: this rank's fine-level Jacobi sweep over
+    # its slab (x present), CUDA events on the launching stream, slowest rank
+    from . import roofline
+    a0 = h.levels[0]
+    x0 = h.be.jacobi(a0, r_loc, None, 1.0)
+    h.exchange_x(0, x0)
+    for _ in range(2):
+        h.be.jacobi(a0, r_loc, x0, 1.0)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(5):
+        h.be.jacobi(a0, r_loc, x0, 1.0)
+    e1.record()
+    torch.cuda.synchronize()
+    jms = comm.allreduce_max(e0.elapsed_time(e1) / 5)
+    # algorithmic bytes of the slab: b, x in, x out + this slab's stage data
+    rows = min(a0.row1, a0.n_steps) - a0.row0
+    sb = roofline.stage_bytes(a0) * rows // a0.n_steps
+    jbytes = 8 * a0.dim * 3 + sb
+    try:
+        import json as _json
+        import os as _os
+        with open(_os.path.join(_os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))),
+                               "MEASURED_PEAKS.json")) as fh:
+            peak, peak_kind = float(_json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        peak, peak_kind = 6650.0, "fallback"
+    ach = jbytes / (jms * 1e-3) / 1e9
     # e2e: pinned host slice -> device, V-cycle, device -> pinned host, per rank
     out_host = torch.empty(ln, dtype=torch.float64).pin_memory()
     e2e_steps = max(2, min(args.steps, 5))
@@ -531,6 +559,10 @@ def bench_rank(args, rank, world, local_rank):
         "e2e": {"value": unknowns / (e2e_ms * 1e-3), "unit": "time-step*DoF/s",
                 "h2d_bytes_per_step": int(rhs.nbytes), "d2h_bytes_per_step": int(rhs.nbytes),
                 "ms_per_step": e2e_ms},
+        "roofline": {"bound": "hbm", "kernel": "tk_jacobi_sweep (fine level, per-rank slab)",
+                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": None, "peak_kind": peak_kind, "bytes_per_launch": jbytes,
+                     "ms_per_launch": jms},
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": None,

@@ -50,6 +50,7 @@ def main():
         if solve:
             # (F)GMRES keeps V and Z: size the restart to the free HBM
             free, _ = torch.cuda.mem_get_info()
+            free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
             per_it = 2 * s.dim * 8
             m_fit = int(0.85 * free // per_it) - 2
             restart = None if m_fit >= S["max_iters"] + 1 else max(2, m_fit)
