@@ -138,24 +138,26 @@ arnoldi_mgs_kernel(int64_t n, int j, double* __restrict__ V, int64_t ld, double*
         const double a = -hp;
         double acc = 0.0, acc2 = 0.0;
         int64_t k = k0;
+        // the basis vectors stream through L2 with evict-first loads so that w
+        // (re-read and re-written every pass) stays L2-resident for large n
         for (; k + stride < n; k += 2 * stride) {
             double w0 = w[k], w1 = w[k + stride];
             if (Vp) {
-                w0 = fma(a, Vp[k], w0);
-                w1 = fma(a, Vp[k + stride], w1);
+                w0 = fma(a, __ldcs(Vp + k), w0);
+                w1 = fma(a, __ldcs(Vp + k + stride), w1);
                 w[k] = w0;
                 w[k + stride] = w1;
             }
-            acc = fma(Vi ? Vi[k] : w0, w0, acc);
-            acc2 = fma(Vi ? Vi[k + stride] : w1, w1, acc2);
+            acc = fma(Vi ? __ldcs(Vi + k) : w0, w0, acc);
+            acc2 = fma(Vi ? __ldcs(Vi + k + stride) : w1, w1, acc2);
         }
         if (k < n) {
             double w0 = w[k];
             if (Vp) {
-                w0 = fma(a, Vp[k], w0);
+                w0 = fma(a, __ldcs(Vp + k), w0);
                 w[k] = w0;
             }
-            acc = fma(Vi ? Vi[k] : w0, w0, acc);
+            acc = fma(Vi ? __ldcs(Vi + k) : w0, w0, acc);
         }
         acc += acc2;
         // block_sum<kReduceThreads>

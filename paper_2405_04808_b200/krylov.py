@@ -227,8 +227,8 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
         V = torch.empty((m + 1, n), dtype=dev.F64, device=b.device)
         Z = torch.empty((m, n), dtype=dev.F64, device=b.device) \
             if (flexible and prec is not None) else None
-        H = np.zeros((m + 1, m)); cs = np.zeros(m); sn = np.zeros(m)
-        g = np.zeros(m + 1)
+        H = np.zeros((m + 1, m)); cs = [0.0] * m; sn = [0.0] * m
+        g = [0.0] * (m + 1)
         g[0] = beta
         ops.scale_into(1.0 / beta, r, V[0])
         jd = 0
@@ -244,28 +244,31 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
             w = dev.to_device(op(zj))
             if FUSED_ARNOLDI:     # one launch + one copy per step (V[j+1] written too)
                 hcol = ops.arnoldi(V, j, w)
-                H[:j + 1, j] = hcol[:j + 1]
-                hj1 = float(hcol[j + 1])
             else:
+                hcol = np.empty(j + 2)
                 for i in range(j + 1):
                     hij = ops.dot(V[i], w)
-                    H[i, j] = hij
+                    hcol[i] = hij
                     ops.axpy(-hij, V[i], w)
-                hj1 = ops.nrm2(w)
-            H[j + 1, j] = hj1
-            if not math.isfinite(hj1) or not np.isfinite(H[:j + 1, j]).all():
+                hcol[j + 1] = ops.nrm2(w)
+            hj1 = float(hcol[j + 1])
+            if not np.isfinite(hcol).all():
                 raise NonFiniteValue("non-finite Hessenberg entry in Arnoldi")
+            # Givens rotations on the new column as Python floats (same IEEE
+            # arithmetic as numpy scalars, without per-element array access)
+            col = hcol.tolist()
             for i in range(j):
-                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
-                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
-                H[i, j] = t
-            den = float(np.hypot(H[j, j], H[j + 1, j]))
+                a_, b_ = col[i], col[i + 1]
+                col[i] = cs[i] * a_ + sn[i] * b_
+                col[i + 1] = -sn[i] * a_ + cs[i] * b_
+            den = float(np.hypot(col[j], col[j + 1]))
             if den == 0.0:
                 raise Breakdown("zero diagonal in Givens elimination")
-            cs[j] = H[j, j] / den
-            sn[j] = H[j + 1, j] / den
-            H[j, j] = den
-            H[j + 1, j] = 0.0
+            cs[j] = col[j] / den
+            sn[j] = col[j + 1] / den
+            col[j] = den
+            col[j + 1] = 0.0
+            H[:j + 2, j] = col
             g[j + 1] = -sn[j] * g[j]
             g[j] = cs[j] * g[j]
             total += 1
@@ -282,7 +285,7 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
         if jd > 0:
             y = np.zeros(jd)
             for i in range(jd - 1, -1, -1):
-                y[i] = (g[i] - H[i, i + 1:jd] @ y[i + 1:jd]) / H[i, i]
+                y[i] = (np.float64(g[i]) - H[i, i + 1:jd] @ y[i + 1:jd]) / H[i, i]
             yt = y
             if Z is not None:
                 ops.gemv_t_add(Z, yt, x)
