@@ -189,6 +189,14 @@ int tk_prolong_add_slab(int32_t n_fine, int32_t n_u, int32_t n_z, int32_t row0, 
                         const double* xc, const double* halo_prev_ul,
                         const double* halo_next_vm, double* xf, void* stream);
 /* rc = R (b - A x)  (work: fine-sized scratch; honours the level's slab)  multigrid.py:288 */
+/* rc = R (b - A x) when x is ONE block-Jacobi sweep from zero (x = omega
+ * D^{-1} b, the V-cycle pre-smoothing with sweeps = 1, multigrid.py:284-288):
+ * D x = omega b, so b - A x = (1 - omega) b - (L + U) x reduces to the
+ * continuity couplings (r_mu(t) -= u_t, r_u(t) -= mu_t) -- b is not read for
+ * omega == 1 and x only at the injected u/mu segments.  Time slabs read the
+ * coupling partners outside the slab from L->halo_u / L->halo_mu. */
+int tk_residual_restrict_jacobi0(const tk_level* L, const double* b, const double* x,
+                                 double omega, double* rc, void* stream);
 int tk_residual_restrict(const tk_level* L, const double* b, const double* x, double* rc,
                          double* work, void* stream);
 

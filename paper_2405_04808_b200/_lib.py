@@ -73,6 +73,7 @@ _SIGS = {
     "tk_restrict_slab": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _p, _p, _p]),
     "tk_prolong_add_slab": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p]),
     "tk_residual_restrict": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p, _p]),
+    "tk_residual_restrict_jacobi0": (C.c_int, [C.POINTER(TkLevel), _p, _p, _d, _p, _p]),
     "tk_reduce_work_len": (_i64, []),
     "tk_dot": (C.c_int, [_i64, _p, _p, _p, _p, _p]),
     "tk_nrm2": (C.c_int, [_i64, _p, _p, _p, _p]),

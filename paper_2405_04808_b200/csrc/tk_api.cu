@@ -43,6 +43,8 @@ int vec_launch(int, int64_t, double, const double*, double*, cudaStream_t);
 int gemv_t_add_launch(int64_t, int, const double*, int64_t, const double*, double*, cudaStream_t);
 int arnoldi_launch(int64_t, int, double*, int64_t, double*, double*, double*, cudaStream_t);
 int copy_small_launch(int64_t, const double*, double*, cudaStream_t);
+int restrict_jacobi0_launch(int, int, int, int, int, const double*, const double*, const double*,
+                            const double*, double, double*, cudaStream_t);
 int stage_vdp_launch(int, double, double, double, int, const double*, const double*,
                      const double*, const double*, double*, double*, double*, cudaStream_t);
 int stage_burgers_launch(int, int, double, double, double, const double*, const double*,
@@ -244,6 +246,19 @@ int tk_residual_restrict(const tk_level* L, const double* b, const double* x, do
     if (rcode) return rcode;
     return transfer_launch(1, L->n_steps, L->n_u, L->n_z, L->row0, L->row1, work, nullptr,
                            nullptr, rc, as_stream(stream));
+}
+
+int tk_residual_restrict_jacobi0(const tk_level* L, const double* b, const double* x,
+                                 double omega, double* rc, void* stream) {
+    TK_CHECK_ARG(x && rc && (b || omega == 1.0), "tk_residual_restrict_jacobi0: null vector");
+    int e = check_level(L);
+    if (e) return e;
+    if (L->n_steps & 1) {
+        set_error("tk_residual_restrict_jacobi0: odd step count");
+        return TK_ERR_ARG;
+    }
+    return restrict_jacobi0_launch(L->n_steps, L->n_u, L->n_z, L->row0, L->row1, b, x, L->halo_u,
+                                   L->halo_mu, omega, rc, as_stream(stream));
 }
 
 int64_t tk_reduce_work_len(void) { return reduce_work_len(); }

@@ -174,6 +174,66 @@ __global__ void __launch_bounds__(256) prolong_rows_kernel(Lay Lf, Lay Lc, int64
     }
 }
 
+// rc = R (b - A x) for x = ONE block-Jacobi sweep from zero, x = omega D^{-1} b
+// (the pre-smoothing of every V-cycle level, multigrid.py:284-288).  Then
+// D x = omega b, so  b - A x = (1 - omega) b - (L + U) x: the only other
+// terms are the continuity couplings, r_mu(t) -= u_t and r_u(t) -= mu_t
+// (kkt.py:6-16).  Injection keeps fine time 2T for u, v, lam, mu and averages
+// z over 2T-1, 2T.  One thread per coarse element; b is not read when omega
+// == 1, and x only at the u and mu segments the coarse rows inject.
+static void slab_geom(const Lay& Lf, const Lay& Lc, int r0, int r1, int64_t& fbase,
+                      int64_t& flen, int64_t& cbase, int64_t& clen);
+
+// Time slab of fine rows [r0, r1): the coupling partners outside the slab are
+// the halo segments (u of row r0-1 = u_{r0}, mu of row r1 = mu_{r1}).
+__global__ void restrict_jacobi0_kernel(Lay Lf, Lay Lc, int64_t fbase, int64_t cbase, int64_t clen,
+                                        int r0, int r1, const double* __restrict__ b,
+                                        const double* __restrict__ x, const double* __restrict__ hu,
+                                        const double* __restrict__ hm, double omega,
+                                        double* __restrict__ rc) {
+    const double c1 = 1.0 - omega;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < clen;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        int kind, c, t;
+        decode(Lc, cbase + k, kind, c, t);
+        double v;
+        if (kind == KZ) {
+            v = c1 == 0.0 ? 0.0
+                          : c1 * (0.5 * (b[kind_off(Lf, KZ, 2 * t - 1) + c - fbase] +
+                                         b[kind_off(Lf, KZ, 2 * t) + c - fbase]));
+        } else {
+            const int ft = 2 * t;
+            v = c1 == 0.0 ? 0.0 : c1 * b[kind_off(Lf, kind, ft) + c - fbase];
+            if (kind == KM)        // u_{2t} lives in fine row 2t-1
+                v -= (ft - 1 >= r0) ? x[kind_off(Lf, KU, ft) + c - fbase] : hu[c];
+            else if (kind == KU)   // mu_{2t} lives in fine row 2t
+                v -= (ft < r1) ? x[kind_off(Lf, KM, ft) + c - fbase] : hm[c];
+        }
+        rc[k] = v;
+    }
+}
+
+int restrict_jacobi0_launch(int n_fine, int nu, int nz, int r0, int r1, const double* b,
+                            const double* x, const double* hu, const double* hm, double omega,
+                            double* rc, cudaStream_t s) {
+    Lay Lf(n_fine, nu, nz), Lc(n_fine / 2, nu, nz);
+    if (r1 <= 0) r1 = n_fine + 1;
+    if (r0 < 0 || r0 >= r1 || r1 > n_fine + 1 || (r0 & 1) || ((r1 & 1) && r1 != n_fine + 1)) {
+        set_error("restrict_jacobi0: bad fine slab [%d, %d) for N=%d (edges must be even)", r0, r1,
+                  n_fine);
+        return TK_ERR_ARG;
+    }
+    if ((r0 > 0 && !hu) || (r1 <= n_fine && !hm)) {
+        set_error("restrict_jacobi0: slab [%d, %d) needs its halo segments", r0, r1);
+        return TK_ERR_ARG;
+    }
+    int64_t fbase, flen, cbase, clen;
+    slab_geom(Lf, Lc, r0, r1, fbase, flen, cbase, clen);
+    restrict_jacobi0_kernel<<<grid_for(clen, 256, 148 * 32), 256, 0, s>>>(
+        Lf, Lc, fbase, cbase, clen, r0, r1, b, x, hu, hm, omega, rc);
+    return check_launch("restrict_jacobi0");
+}
+
 // fine rows [r0, r1) -> coarse rows [r0/2, r1/2) (through N/2 for the last slab)
 static void slab_geom(const Lay& Lf, const Lay& Lc, int r0, int r1, int64_t& fbase,
                       int64_t& flen, int64_t& cbase, int64_t& clen) {

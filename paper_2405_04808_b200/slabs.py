@@ -322,8 +322,12 @@ class CudaBackend:
         self.dev.call("tk_kkt_apply", a.lref, self.dev.P(x), self.dev.P(y), self.dev.stream())
         return y
 
-    def residual_restrict(self, a, b, x, coarse_len):
+    def residual_restrict(self, a, b, x, coarse_len, jacobi0_omega=None):
         rc = self.dev.empty(coarse_len)
+        if jacobi0_omega is not None:   # x = one sweep from zero: coupling terms only
+            self.dev.call("tk_residual_restrict_jacobi0", a.lref, self.dev.P(b), self.dev.P(x),
+                          float(jacobi0_omega), self.dev.P(rc), self.dev.stream())
+            return rc
         work = self.dev.empty(a.dim)
         self.dev.call("tk_residual_restrict", a.lref, self.dev.P(b), self.dev.P(x),
                       self.dev.P(rc), self.dev.P(work), self.dev.stream())
@@ -435,7 +439,10 @@ class SlabHierarchy:
         c0, c1 = self._coarse_rows(lvl, self.comm.rank)
         nc = self.plan.n_at(lvl + 1)
         clen = slab_span(nc, self.nu, self.nz, c0, c1)[1]
-        rc = self.be.residual_restrict(a, b, x, clen)
+        from . import multigrid
+        j0 = self.omega if (self.sweeps == 1 and multigrid.JACOBI0_RESIDUAL and
+                            getattr(self.be, "jacobi0", True)) else None
+        rc = self.be.residual_restrict(a, b, x, clen, j0)
         if lvl + 1 == len(self.levels):
             full = self.comm.gather(rc, self.coarse_sizes)
             ef = self.be.coarse_solve(self.coarse, full) if self.comm.rank == 0 else None

@@ -94,3 +94,26 @@ def test_cfg1_full_size_solve_vs_reference():
     assert abs(rep.final_relative_residual - float(g["fgmres_rel"])) < 1e-10
     assert rel(x[::int(g["x_stride"])], g["x_sample"]) < 1e-10
     assert abs(np.linalg.norm(x) - float(g["x_norm"])) < 1e-10 * float(g["x_norm"])
+
+
+@pytest.mark.parametrize("cfg,nt,nx", [(1, 256, 128), (0, 512, None)])
+def test_jacobi0_residual_restrict(cfg, nt, nx):
+    """The coupling-only residual-restrict after the zero-start pre-smoothing
+    sweep (tk_residual_restrict_jacobi0) against the general fused
+    residual-restrict: the V-cycles agree to roundoff, the coarse-solve
+    iteration counts are identical (TRI and DENSE families)."""
+    import paper_2405_04808_b200 as P
+    from paper_2405_04808_b200 import configs, multigrid
+    s = configs.build_setup(cfg, nt=nt, nx=nx, levels=3)
+    b = s.rhs()
+    out = {}
+    for flag in (True, False):
+        multigrid.JACOBI0_RESIDUAL = flag
+        try:
+            h = P.build_hierarchy(s.problem, s.u, s.v, s.z, s.grid, s.levels, sweeps=1,
+                                  coarse_tol=1e-2)
+            out[flag] = (P.cycle(h, 0, b), h.stats.iters)
+        finally:
+            multigrid.JACOBI0_RESIDUAL = True
+    assert out[True][1] == out[False][1]
+    assert rel(out[True][0], out[False][0]) < 1e-12

@@ -85,7 +85,9 @@ class OracleBackend:
         out = omega * d if x is None else x.numpy() + omega * d
         return torch.from_numpy(out.copy())
 
-    def residual_restrict(self, a, b, x, coarse_len):
+    def residual_restrict(self, a, b, x, coarse_len, jacobi0_omega=None):
+        # the oracle backend always forms the full residual (the coupling-only
+        # form after a zero-start sweep is the same vector in exact arithmetic)
         from oracle import tk_oracle as O
         r = b.numpy() - self._rows_of(a, a.k.apply(a.embed(x)))
         g = np.zeros(a.k.lay.dim)
