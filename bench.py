@@ -46,6 +46,7 @@ _NCU_FULL = {
     "tk_residual_restrict": "tri_resrestrict",
     "tk_prolong_add": "prolong_rows_kernel",
     "tk_kkt_apply": "tri_apply<0",
+    "tk_residual_restrict_jacobi0": "restrict_jacobi0_kernel",
 }
 
 
@@ -229,7 +230,7 @@ def run_ours(args, rank, world, local_rank):
     names = {"tk_jacobi_sweep", "tk_residual_restrict", "tk_prolong_add", "tk_forward_subst",
              "tk_backward_subst", "tk_sgs_back_half", "tk_kkt_apply", "tk_kkt_apply_diag",
              "tk_kkt_residual", "tk_dot", "tk_nrm2", "tk_axpy", "tk_scale_into", "tk_rsub",
-             "tk_gemv_t_add", "tk_arnoldi_mgs", "tk_copy_kernel"}
+             "tk_gemv_t_add", "tk_arnoldi_mgs", "tk_copy_kernel", "tk_residual_restrict_jacobi0"}
     dev.INSTR.timed, dev.INSTR.records = names, []
     prec(r_dev)
     torch.cuda.synchronize()
@@ -242,7 +243,7 @@ def run_ours(args, rank, world, local_rank):
         d["bytes"] += roofline.algorithmic_bytes(nm, a)
     fine_recs = {}
     for nm, a, e0, e1 in dev.INSTR.records:   # fine-level launch of each HBM kernel
-        if nm in ("tk_jacobi_sweep", "tk_residual_restrict"):
+        if nm in ("tk_jacobi_sweep", "tk_residual_restrict", "tk_residual_restrict_jacobi0"):
             lvl = roofline.dim_of(a[0]._obj)
         elif nm == "tk_prolong_add":
             lvl = int(a[0]) * (4 * int(a[1]) + int(a[2]))

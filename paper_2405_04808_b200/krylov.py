@@ -224,8 +224,11 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
         m = min(restart, max_iters - total)
         if m <= 0:
             break
-        V = torch.empty((m + 1, n), dtype=dev.F64, device=b.device)
-        Z = torch.empty((m, n), dtype=dev.F64, device=b.device) \
+        # bases grow on demand (doubling): a coarse solve that stops after a
+        # few iterations does not hold max_iters+1 vectors of HBM
+        cap = min(m, 16)
+        V = torch.empty((cap + 1, n), dtype=dev.F64, device=b.device)
+        Z = torch.empty((cap, n), dtype=dev.F64, device=b.device) \
             if (flexible and prec is not None) else None
         H = np.zeros((m + 1, m)); cs = [0.0] * m; sn = [0.0] * m
         g = [0.0] * (m + 1)
@@ -234,6 +237,16 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
         jd = 0
         broke = False
         for j in range(m):
+            if j + 1 > cap:
+                cap = min(m, 2 * cap)
+                V2 = torch.empty((cap + 1, n), dtype=dev.F64, device=b.device)
+                V2[:j + 1].copy_(V[:j + 1])
+                V = V2
+                if Z is not None:
+                    Z2 = torch.empty((cap, n), dtype=dev.F64, device=b.device)
+                    Z2[:j].copy_(Z[:j])
+                    Z = Z2
+                V2 = Z2 = None
             if prec is None:
                 zj = V[j]
             else:

@@ -55,6 +55,12 @@ def algorithmic_bytes(name: str, args) -> int:
             N, nu, nz = L.n_steps, L.n_u, L.n_z
             return 8 * (N * (2 * nu + nz) + N * (3 * nu + nz) + cdim) + (3 * stage_bytes(L)) // 4
         return 8 * dim_of(L) * 3 + stage_bytes(L) + 8 * (2 * cdim + nc * L.n_z)
+    if name == "tk_residual_restrict_jacobi0":   # coarse vector written, u/mu segments read
+        L = _lvl(args[0])
+        nc = L.n_steps // 2
+        cdim = nc * (4 * L.n_u + L.n_z)
+        extra = 0 if float(args[3]) == 1.0 else 8 * (cdim + nc * L.n_z)   # (1-omega) b
+        return 8 * cdim + 8 * 2 * L.n_u * nc + extra
     if name in ("tk_restrict", "tk_prolong_add"):
         nf, nu, nz = args[0], args[1], args[2]
         fdim = nf * (4 * nu + nz)

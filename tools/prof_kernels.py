@@ -27,5 +27,7 @@ rc = dev.empty(t.coarse_dim)
 work = dev.empty(a.dim)
 dev.call("tk_residual_restrict", a.lref, dev.P(b), dev.P(x1), dev.P(rc), dev.P(work), dev.stream())
 t.prolong_add(rc, x1)                             # prolong_rows_kernel
+dev.call("tk_residual_restrict_jacobi0", a.lref, dev.P(b), dev.P(x0), 1.0, dev.P(rc),
+         dev.stream())                            # restrict_jacobi0_kernel (x0 = D^-1 b)
 torch.cuda.synchronize()
 print("ok", s.describe())
