@@ -231,9 +231,22 @@ def run_ours(args, rank, world, local_rank):
              "tk_backward_subst", "tk_sgs_back_half", "tk_kkt_apply", "tk_kkt_apply_diag",
              "tk_kkt_residual", "tk_dot", "tk_nrm2", "tk_axpy", "tk_scale_into", "tk_rsub",
              "tk_gemv_t_add", "tk_arnoldi_mgs", "tk_copy_kernel", "tk_residual_restrict_jacobi0"}
+    # (eager cycles: the CUDA-graph replay hides the coarse levels' kernels)
+    from paper_2405_04808_b200 import graph as G
+    graph_on = G.ENABLED
+    G.ENABLED = False
+    eager_steps = 3
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    for _ in range(eager_steps):
+        prec(r_dev)
+    eb.record(stream)
+    torch.cuda.synchronize()
+    eager_ms = ea.elapsed_time(eb) / eager_steps
     dev.INSTR.timed, dev.INSTR.records = names, []
     prec(r_dev)
     torch.cuda.synchronize()
+    G.ENABLED = graph_on
     per = {}
     for nm, a, e0, e1 in dev.INSTR.records:
         ms = e0.elapsed_time(e1)
@@ -402,6 +415,10 @@ def run_ours(args, rank, world, local_rank):
                         "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}
                     for k, v in sorted(per.items(), key=lambda kv: -kv[1]["ms"])},
         "gpu_launches": launches,
+        "vcycle_graph": {"enabled": graph_on,
+                         "api": "levels 1..L-1 incl. the coarse SGS-GMRES (device WHILE loop) "
+                                "replayed as one CUDA graph per V-cycle",
+                         "eager_ms_per_step": eager_ms},
         "clocks": clocks,
         "cpu_baseline": cpu,
         "solve": solve,

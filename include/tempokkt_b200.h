@@ -235,6 +235,41 @@ int tk_host_device_ptr(void* host, void** dptr);
 int tk_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ld, double* w, double* h,
                    double* work, void* stream);
 
+/* --- CUDA-graph V-cycle with a device-side coarse GMRES ------------------- */
+/* Replaces the host-driven loop of multigrid.py:245-260 (coarse_solve ->
+ * krylov.py:77-191 gmres from x0 = 0, SGS right preconditioner) inside a
+ * captured V-cycle (multigrid.py:269-301) so that a cycle replays as ONE
+ * graph launch with no host round trip.  Capture runs on a non-default
+ * stream; the coarse Arnoldi loop is a WHILE conditional node whose
+ * condition the Givens kernel sets (cudaGraphSetConditional). */
+int tk_graph_capture_begin(void* stream);
+int tk_graph_cond_create(void* stream, uint64_t* handle);
+int tk_graph_while_begin(void* stream, void* body_stream, uint64_t handle);
+int tk_graph_while_end(void* body_stream);
+int tk_graph_capture_end(void* stream, void** exec);
+int tk_graph_launch(void* exec, void* stream);
+int tk_graph_destroy(void* exec);
+/* Device GMRES state for a basis of `cap` columns (header, H, g, cs, sn, y). */
+int64_t tk_gm_state_len(int32_t cap);
+/* beta = ||b||, target = rel_tol*beta, g_0 = beta, V_0 = vj = b/beta; the
+ * condition is set to 0 (skip the loop) when the host path must take over. */
+int tk_gm_begin(int64_t n, const double* b, double* V, int64_t ld, double* vj, double* state,
+                int32_t cap, double rel_tol, int32_t max_iters, uint64_t handle, double* work,
+                void* stream);
+/* MGS step j (j read from the state) with w = A M^{-1} v_j; V_{j+1} also to vj. */
+int tk_gm_arnoldi(int64_t n, double* V, int64_t ld, double* w, double* state, int32_t cap,
+                  double* vj, double* work, void* stream);
+/* Givens update + stopping tests of krylov.py; sets the loop condition. */
+int tk_gm_givens(double* state, int32_t cap, uint64_t handle, void* stream);
+/* y = H^{-1} g, vy = V^T y. */
+int tk_gm_combine(int64_t n, const double* V, int64_t ld, double* state, int32_t cap,
+                  double* vy, void* stream);
+/* r (= A x on entry) <- b - A x; ||r||, ||x||; res[0] = 1 when the host path
+ * must redo the solve (restart, breakdown, non-finite, basis overflow),
+ * res[1] = iterations.  res may be mapped host memory. */
+int tk_gm_finish(int64_t n, const double* b, double* r, const double* x, double* state,
+                 int32_t cap, int32_t* res, double* work, void* stream);
+
 /* --- setup: stage linearisation on the device (timedisc.py:133, kkt.py:100) - */
 /* van der Pol: K,C,B at (v_{i-1}, u_i, z_i), v_{-1} = u0.  n_controls in {1,2}. */
 int tk_stage_vanderpol(int32_t n_steps, double dt, double theta, double mu, int32_t n_controls,

@@ -83,6 +83,19 @@ _SIGS = {
     "tk_gemv_t_add": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _p]),
     "tk_arnoldi_mgs": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _p, _p]),
     "tk_copy_kernel": (C.c_int, [_i64, _p, _p, _p]),
+    "tk_graph_capture_begin": (C.c_int, [_p]),
+    "tk_graph_cond_create": (C.c_int, [_p, C.POINTER(C.c_uint64)]),
+    "tk_graph_while_begin": (C.c_int, [_p, _p, C.c_uint64]),
+    "tk_graph_while_end": (C.c_int, [_p]),
+    "tk_graph_capture_end": (C.c_int, [_p, C.POINTER(C.c_void_p)]),
+    "tk_graph_launch": (C.c_int, [_p, _p]),
+    "tk_graph_destroy": (C.c_int, [_p]),
+    "tk_gm_state_len": (_i64, [_i32]),
+    "tk_gm_begin": (C.c_int, [_i64, _p, _p, _i64, _p, _p, _i32, _d, _i32, C.c_uint64, _p, _p]),
+    "tk_gm_arnoldi": (C.c_int, [_i64, _p, _i64, _p, _p, _i32, _p, _p, _p]),
+    "tk_gm_givens": (C.c_int, [_p, _i32, C.c_uint64, _p]),
+    "tk_gm_combine": (C.c_int, [_i64, _p, _i64, _p, _i32, _p, _p]),
+    "tk_gm_finish": (C.c_int, [_i64, _p, _p, _p, _p, _i32, _p, _p, _p]),
     "tk_host_device_ptr": (C.c_int, [_p, C.POINTER(C.c_void_p)]),
     "tk_host_alloc_mapped": (C.c_int, [_i64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "tk_host_free": (C.c_int, [_p]),

@@ -125,8 +125,13 @@ __device__ __forceinline__ double reduce_partials(const double* __restrict__ par
 
 __global__ void __launch_bounds__(kReduceThreads, 4)
 arnoldi_mgs_kernel(int64_t n, int j, double* __restrict__ V, int64_t ld, double* __restrict__ w,
-                   double* __restrict__ h, double* __restrict__ part) {
+                   double* __restrict__ h, double* __restrict__ part, const int* __restrict__ jdev,
+                   int64_t hstride, double* __restrict__ vcopy) {
     namespace cg = cooperative_groups;
+    if (jdev) {          // graphed GMRES: the step index lives on the device
+        j = *jdev;
+        h += (int64_t)j * hstride;
+    }
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[kReduceThreads / 32 + 34];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -179,17 +184,42 @@ arnoldi_mgs_kernel(int64_t n, int j, double* __restrict__ V, int64_t ld, double*
     if (hp != 0.0) {
         const double inv = 1.0 / hp;
         double* Vn = V + (int64_t)(j + 1) * ld;
-        for (int64_t k = k0; k < n; k += stride) Vn[k] = inv * w[k];
+        if (vcopy) {
+            for (int64_t k = k0; k < n; k += stride) {
+                const double v = inv * w[k];
+                Vn[k] = v;
+                vcopy[k] = v;
+            }
+        } else {
+            for (int64_t k = k0; k < n; k += stride) Vn[k] = inv * w[k];
+        }
     }
 }
 
 int arnoldi_launch(int64_t n, int j, double* V, int64_t ld, double* w, double* h, double* work,
                    cudaStream_t s) {
-    void* args[] = {(void*)&n, (void*)&j, (void*)&V, (void*)&ld, (void*)&w, (void*)&h, (void*)&work};
+    const int* jdev = nullptr;
+    int64_t hstride = 0;
+    double* vcopy = nullptr;
+    void* args[] = {(void*)&n, (void*)&j,    (void*)&V,       (void*)&ld,   (void*)&w,
+                    (void*)&h, (void*)&work, (void*)&jdev, (void*)&hstride, (void*)&vcopy};
     const cudaError_t e = cudaLaunchCooperativeKernel((const void*)arnoldi_mgs_kernel,
                                                       dim3(kReduceBlocks), dim3(kReduceThreads),
                                                       args, 0, s);
     return cuda_status(e, "arnoldi_mgs_kernel");
+}
+
+// the step index j from device memory (*jdev), h = H + j*hstride, and the new
+// basis vector also copied to vcopy (the next step's preconditioner input)
+int arnoldi_dev_launch(int64_t n, const int* jdev, double* V, int64_t ld, double* w, double* H,
+                       int64_t hstride, double* vcopy, double* work, cudaStream_t s) {
+    int j = 0;
+    void* args[] = {(void*)&n, (void*)&j,    (void*)&V,    (void*)&ld,      (void*)&w,
+                    (void*)&H, (void*)&work, (void*)&jdev, (void*)&hstride, (void*)&vcopy};
+    const cudaError_t e = cudaLaunchCooperativeKernel((const void*)arnoldi_mgs_kernel,
+                                                      dim3(kReduceBlocks), dim3(kReduceThreads),
+                                                      args, 0, s);
+    return cuda_status(e, "arnoldi_mgs_kernel (device j)");
 }
 
 int64_t reduce_work_len() { return 2 * kReduceBlocks; }

@@ -19,6 +19,7 @@ def test_pipeline_matches_serial():
     dim = h.levels[0].kkt.dim
     rng = np.random.default_rng(5)
     rhs = [rng.standard_normal(dim) for _ in range(5)]
+    prec(rhs[0])        # the first cycle runs eagerly, the rest replay the CUDA graph
     ref = [prec(r) for r in rhs]                      # numpy in -> numpy out
     ins = [torch.from_numpy(r).pin_memory() for r in rhs]
     outs = [torch.empty(dim, dtype=torch.float64).pin_memory() for _ in rhs]
