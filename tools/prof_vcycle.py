@@ -22,9 +22,21 @@ def main():
                           cycle_kind=S["cycle"], coarse_tol=S["coarse_tol"])
     r = dev.to_device(s.rhs())
     prec = P.mg_preconditioner(h)
-    for _ in range(reps):
-        prec(r)
-    torch.cuda.synchronize()
+    if os.environ.get("PROF_GRAPH") == "1":
+        # eager warm-up cycle + graph capture, then ONE graphed cycle inside
+        # cudaProfilerStart/Stop (ncu --profile-from-start off)
+        for _ in range(2):
+            prec(r)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        for _ in range(reps):
+            prec(r)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+    else:
+        for _ in range(reps):
+            prec(r)
+        torch.cuda.synchronize()
     print("ok", s.describe(), h.stats.calls, h.stats.iters)
 
 
