@@ -69,8 +69,11 @@ def supported(h) -> bool:
 class VCycleGraph:
     """Levels 1..L-1 of a V-cycle from zero, captured once (see module doc)."""
 
-    def __init__(self, h, cap: int = DEFAULT_CAP):
+    def __init__(self, h, cap: int = DEFAULT_CAP, start: int = 1):
+        """start = 1: levels 1..L-1 of a V-cycle; start = L-1: the coarse
+        solve alone (used for the coarse level gathered on one GPU)."""
         self.h = h
+        self.start = start
         self.key = (h.sweeps, float(h.omega), float(h.coarse_tol), int(h.coarse_max_iters))
         self.cap = max(1, min(int(cap), int(h.coarse_max_iters)))
         lib = _lib.load()
@@ -80,7 +83,7 @@ class VCycleGraph:
         self.Y = [None] * L          # second sweep buffer (sweeps > 1)
         self.E = [None] * L          # level correction (E[1] is the graph output)
         self.W = [None] * L          # residual work (general residual-restrict)
-        for l in range(1, L):
+        for l in range(start, L):
             n = h.levels[l].kkt.dim
             self.B[l] = dev.empty(n)
             self.E[l] = dev.empty(n)
@@ -193,7 +196,7 @@ class VCycleGraph:
             s = dev.stream()
             _lib.check(lib.tk_graph_capture_begin(s), "tk_graph_capture_begin")
             try:
-                self._record_level(1, body_stream)
+                self._record_level(self.start, body_stream)
             except Exception:
                 g = ctypes.c_void_p()
                 lib.tk_graph_capture_end(s, ctypes.byref(g))
@@ -215,21 +218,21 @@ class VCycleGraph:
             1 + dev._launches("tk_backward_subst", (a.lref,)))
         self.per_coarse_iter = sgs + 1 + 1 + 1          # prec, apply, arnoldi, givens
         fixed = 0
-        for l in range(1, h.n_levels - 1):
+        for l in range(self.start, h.n_levels - 1):
             fixed += 2 * h.sweeps + 1 + 1                # sweeps, restrict, prolong
         fixed += 2 + 1 + 1 + 2 + sgs + 1 + 1 + 2 * 2 + 1  # begin, combine, prec, apply, finish
         return fixed
 
     # --- replay -------------------------------------------------------------
-    def run(self, stream=None) -> int:
-        """Launch the recorded levels (input B[1], output E[1]) on the current
-        stream; synchronise and return the coarse iteration count, or -1 when
-        the host path has to redo the cycle."""
+    def run(self, stream=None) -> None:
+        """Launch the recorded levels (input B[start], output E[start]) on the
+        current stream (asynchronous; see result())."""
         s = dev.stream() if stream is None else stream
         dev.call("tk_graph_launch", self.exec, s)
-        return s
 
     def result(self) -> int:
+        """Synchronise; the coarse iteration count, or -1 when the host path
+        has to redo the solve."""
         torch.cuda.current_stream().synchronize()
         if int(self.res.host[0]) != 0:
             return -1
@@ -278,3 +281,28 @@ def graphed_vcycle(h, b):
     h.stats.calls += 1
     h.stats.iters += its
     return x
+
+
+def graphed_coarse(h, r):
+    """SGS-GMRES coarse solve from zero (multigrid.py:245-260) as one graph
+    launch; None when the host-driven solver must run instead."""
+    L = h.n_levels
+    g = getattr(h, "_cgraph", None)
+    key = (h.sweeps, float(h.omega), float(h.coarse_tol), int(h.coarse_max_iters))
+    if g is None or g.key != key:
+        if not getattr(h, "_coarse_warm", False):
+            return None                  # first solve eager: kernel attributes
+        h._cgraph = None
+        g = h._cgraph = VCycleGraph(h, start=L - 1)
+    g.B[L - 1].copy_(r)
+    g.run()
+    if dev.INSTR.counting:
+        dev.INSTR.launches += g.launches
+    its = g.result()
+    if its < 0:
+        return None
+    if dev.INSTR.counting:
+        dev.INSTR.launches += its * g.per_coarse_iter
+    h.stats.calls += 1
+    h.stats.iters += its
+    return g.E[L - 1].clone()

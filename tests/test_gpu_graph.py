@@ -92,7 +92,8 @@ def test_graph_cycle_vs_oracle():
 
 def test_graph_fallback_on_basis_overflow():
     """cap = 1 coarse column: the device loop flags, the cycle re-runs eagerly
-    with the same result and iteration count."""
+    (its coarse solve through the coarse-only graph) with the same result and
+    iteration count."""
     import paper_2405_04808_b200 as P
     from paper_2405_04808_b200 import graph as G
     h, _ = _burgers()
@@ -103,7 +104,30 @@ def test_graph_fallback_on_basis_overflow():
     h._graph = G.VCycleGraph(h, cap=1)
     xg, cg, ig = _graphed(h, b)
     assert cg == ce and ig == ie
-    assert rel(xg, xe) == 0.0
+    assert rel(xg, xe) < 1e-13
+    assert getattr(h, "_cgraph", None) is not None
+
+
+def test_coarse_graph_matches_host_gmres():
+    """graphed_coarse (coarse-only graph, used for the level gathered on rank 0
+    of the time-slab path) against the host-driven coarse GMRES."""
+    import paper_2405_04808_b200 as P
+    from paper_2405_04808_b200 import graph as G
+    from paper_2405_04808_b200.multigrid import coarse_solve
+    h, _ = _burgers(nt=64, levels=2)
+    rng = np.random.default_rng(2)
+    r = rng.standard_normal(h.levels[-1].kkt.dim)
+    G.ENABLED = False
+    try:
+        xe = coarse_solve(h, r)
+    finally:
+        G.ENABLED = True
+    ie = h.stats.iters
+    xg = coarse_solve(h, r)            # eager (warm-up) -> sets _coarse_warm
+    xg = coarse_solve(h, r)            # graph
+    assert h._cgraph is not None
+    assert h.stats.iters == 3 * ie and h.stats.calls == 3
+    assert rel(xg, xe) < 1e-13
 
 
 def test_graph_fgmres_solve_matches_eager():
