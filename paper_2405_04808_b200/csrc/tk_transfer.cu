@@ -213,6 +213,69 @@ __global__ void restrict_jacobi0_kernel(Lay Lf, Lay Lc, int64_t fbase, int64_t c
     }
 }
 
+// Row-based variant: one CTA per coarse block row; each of its segments is one
+// (kind, coarse time) whose sources are located once, then streamed (16-byte
+// accesses when aligned).  Same arithmetic as restrict_jacobi0_kernel; with
+// omega == 1 the v, z, lam segments are zero and u, mu the negated couplings.
+__global__ void __launch_bounds__(256) restrict_jacobi0_rows(Lay Lf, Lay Lc, int64_t fbase, int64_t cbase,
+                                                             int c0, int c1, int r0, int r1,
+                                                             const double* __restrict__ b,
+                                                             const double* __restrict__ x,
+                                                             const double* __restrict__ hu,
+                                                             const double* __restrict__ hm, double omega,
+                                                             double* __restrict__ rc, bool vec) {
+    const double c1w = 1.0 - omega;
+    for (int c = c0 + blockIdx.x; c < c1; c += gridDim.x) {
+        int kinds[5], ts[5];
+        int64_t offs[5];
+        int ns = 0;
+        auto add = [&](int k, int t, int64_t o) { kinds[ns] = k; ts[ns] = t; offs[ns] = o; ++ns; };
+        if (c >= 1) add(KV, c, Lc.off_v(c));
+        if (c < Lc.N) { add(KU, c + 1, Lc.off_u(c)); add(KZ, c + 1, Lc.off_z(c)); }
+        if (c >= 1) add(KM, c, Lc.off_mu(c));
+        if (c < Lc.N) add(KL, c + 1, Lc.off_l(c));
+        for (int q = 0; q < ns; ++q) {
+            const int kind = kinds[q], t = ts[q], ft = 2 * t;
+            const int len = kind == KZ ? Lf.nz : Lf.nu;
+            double* dst = rc + (offs[q] - cbase);
+            const double* b1 = nullptr;   // c1w * b (z: average of fine 2t-1, 2t)
+            const double* b2 = nullptr;
+            if (c1w != 0.0) {
+                if (kind == KZ) {
+                    b1 = b + (kind_off(Lf, KZ, ft - 1) - fbase);
+                    b2 = b + (kind_off(Lf, KZ, ft) - fbase);
+                } else {
+                    b1 = b + (kind_off(Lf, kind, ft) - fbase);
+                }
+            }
+            const double* xs = nullptr;   // the continuity coupling
+            if (kind == KM) xs = (ft - 1 >= r0) ? x + (kind_off(Lf, KU, ft) - fbase) : hu;
+            else if (kind == KU) xs = (ft < r1) ? x + (kind_off(Lf, KM, ft) - fbase) : hm;
+            auto val = [&](int k) -> double {
+                double v = b1 == nullptr ? 0.0 : (b2 ? c1w * (0.5 * (b1[k] + b2[k])) : c1w * b1[k]);
+                if (xs) v -= xs[k];
+                return v;
+            };
+            if (vec) {
+                for (int k = 2 * threadIdx.x; k < len; k += 2 * blockDim.x) {
+                    double2 o;
+                    if (b1 == nullptr && xs) {
+                        const double2 u = *reinterpret_cast<const double2*>(xs + k);
+                        o.x = 0.0 - u.x;
+                        o.y = 0.0 - u.y;
+                    } else {
+                        o.x = val(k);
+                        o.y = val(k + 1);
+                    }
+                    *reinterpret_cast<double2*>(dst + k) = o;
+                }
+            } else {
+                for (int k = threadIdx.x; k < len; k += blockDim.x) dst[k] = val(k);
+            }
+        }
+    }
+}
+
 int restrict_jacobi0_launch(int n_fine, int nu, int nz, int r0, int r1, const double* b,
                             const double* x, const double* hu, const double* hm, double omega,
                             double* rc, cudaStream_t s) {
@@ -229,6 +292,16 @@ int restrict_jacobi0_launch(int n_fine, int nu, int nz, int r0, int r1, const do
     }
     int64_t fbase, flen, cbase, clen;
     slab_geom(Lf, Lc, r0, r1, fbase, flen, cbase, clen);
+    if (nu >= 32) {   // row-based (the element-wise kernel for tiny rows)
+        const int c0 = r0 / 2, c1 = (r1 == n_fine + 1) ? Lc.N + 1 : r1 / 2;
+        auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        const bool vec = (nu % 2 == 0) && (nz % 2 == 0) && (fbase % 2 == 0) && (cbase % 2 == 0) &&
+                         al(b) && al(x) && al(hu) && al(hm) && al(rc);
+        const int rows = c1 - c0;
+        restrict_jacobi0_rows<<<rows, nu >= 512 ? 256 : 128, 0, s>>>(Lf, Lc, fbase, cbase, c0, c1, r0, r1, b,
+                                                                    x, hu, hm, omega, rc, vec);
+        return check_launch("restrict_jacobi0_rows");
+    }
     restrict_jacobi0_kernel<<<grid_for(clen, 256, 148 * 32), 256, 0, s>>>(
         Lf, Lc, fbase, cbase, clen, r0, r1, b, x, hu, hm, omega, rc);
     return check_launch("restrict_jacobi0");
