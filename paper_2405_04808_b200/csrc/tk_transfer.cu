@@ -135,6 +135,58 @@ __global__ void __launch_bounds__(256) prolong_rows_kernel(Lay Lf, Lay Lc, int64
         if (i < Lf.N) { add(KU, i + 1, Lf.off_u(i)); add(KZ, i + 1, Lf.off_z(i)); }
         if (i >= 1) add(KM, i, Lf.off_mu(i));
         if (i < Lf.N) add(KL, i + 1, Lf.off_l(i));
+        if (vec && Lf.nu <= 2 * (int)blockDim.x && Lf.nz <= 2 * (int)blockDim.x) {
+            // one double2 per thread and segment: every load of the row is issued
+            // before the first store (the stores could alias later loads)
+            constexpr int qk[5] = {KV, KU, KZ, KM, KL};
+            double2 d[5], u[5], w[5];
+            double* dsts[5];
+            bool on[5], two[5];
+            const int k = 2 * threadIdx.x;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                const int kind = qk[q];
+                const bool vm = kind == KV || kind == KM;
+                const int t = vm ? i : i + 1;
+                on[q] = (vm ? i >= 1 : i < Lf.N) && k < (kind == KZ ? Lf.nz : Lf.nu);
+                two[q] = false;
+                dsts[q] = xf;
+                if (!on[q]) continue;
+                const int64_t off = kind == KV ? Lf.off_v(i) : kind == KU ? Lf.off_u(i) :
+                                    kind == KZ ? Lf.off_z(i) : kind == KM ? Lf.off_mu(i) : Lf.off_l(i);
+                dsts[q] = xf + (off - fbase) + k;
+                const double* a;
+                const double* b = nullptr;
+                if (kind == KZ) {
+                    a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, KZ, (t + 1) / 2);
+                } else if ((t & 1) == 0) {
+                    a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, t / 2);
+                } else if (t == 1) {
+                    a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, 1);
+                } else {
+                    a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, (t - 1) / 2);
+                    b = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, (t + 1) / 2);
+                }
+                two[q] = b != nullptr;
+                d[q] = *reinterpret_cast<const double2*>(dsts[q]);
+                u[q] = *reinterpret_cast<const double2*>(a + k);
+                if (b) w[q] = *reinterpret_cast<const double2*>(b + k);
+            }
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                if (!on[q]) continue;
+                double2 o = d[q];
+                if (two[q]) {
+                    o.x = o.x + 0.5 * (u[q].x + w[q].x);
+                    o.y = o.y + 0.5 * (u[q].y + w[q].y);
+                } else {
+                    o.x = o.x + u[q].x;
+                    o.y = o.y + u[q].y;
+                }
+                *reinterpret_cast<double2*>(dsts[q]) = o;
+            }
+            continue;
+        }
         for (int q = 0; q < ns; ++q) {
             const int kind = kinds[q], t = ts[q];
             const int len = kind == KZ ? Lf.nz : Lf.nu;
