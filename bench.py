@@ -46,7 +46,7 @@ _NCU_FULL = {
     "tk_residual_restrict": "tri_resrestrict",
     "tk_prolong_add": "prolong_rows_kernel",
     "tk_kkt_apply": "tri_apply<0",
-    "tk_residual_restrict_jacobi0": "restrict_jacobi0_kernel",
+    "tk_residual_restrict_jacobi0": "restrict_jacobi0",
 }
 
 
