@@ -2,12 +2,15 @@
 // states/multipliers (u, v, lam, mu) use injection down / linear interpolation
 // up; piecewise-constant controls use 2-interval averages down / copies up.
 //
-// Both kernels run over a time slab of FINE block rows [r0, r1) (the whole
-// level is the slab [0, N+1)).  One thread per element of the output slice:
-// the element's global offset gives (block row, variable kind, component,
-// time index), from which the source elements are located.  Restriction is
-// slab-local; prolongation reads two halo segments: the previous slab's last
-// coarse (u, lam) and the next slab's first coarse (v, mu).
+// The kernels run over a time slab of FINE block rows [r0, r1) (the whole
+// level is the slab [0, N+1)).  Restriction: one thread per element of the
+// output slice, whose global offset gives (block row, variable kind,
+// component, time index).  Prolongation and the restricted residual after a
+// zero-start sweep: one CTA per block row (n_u >= 32, 16-byte streams) or
+// one thread per block row (tiny rows); every segment of a row is one kind at
+// one time, so its sources are located once.  Restriction is slab-local;
+// prolongation reads two halo segments: the previous slab's last coarse
+// (u, lam) and the next slab's first coarse (v, mu).
 #include "tk_common.cuh"
 
 namespace tk {
@@ -53,16 +56,6 @@ __device__ __forceinline__ int64_t kind_off(const Lay& L, int kind, int t) {
     }
 }
 
-// coarse slice [cbase, cbase + clen) of layout Lc; element (kind, c, t) with halos
-__device__ __forceinline__ double coarse_val(const Lay& Lc, const double* xc, int64_t cbase,
-                                             int64_t clen, const double* hprev,
-                                             const double* hnext, int kind, int c, int t) {
-    const int64_t g = kind_off(Lc, kind, t) + c;
-    const int64_t l = g - cbase;
-    if (l >= 0 && l < clen) return xc[l];
-    if (l < 0) return hprev[(kind == KU ? 0 : Lc.nu) + c];   // previous slab: (u, lam)
-    return hnext[(kind == KV ? 0 : Lc.nu) + c];                // next slab: (v, mu)
-}
 
 __global__ void restrict_kernel(Lay Lf, Lay Lc, int64_t fbase, int64_t cbase, int64_t clen,
                                 const double* __restrict__ xf, double* __restrict__ xc) {
@@ -77,30 +70,6 @@ __global__ void restrict_kernel(Lay Lf, Lay Lc, int64_t fbase, int64_t cbase, in
         } else {
             xc[k] = xf[kind_off(Lf, kind, 2 * t) + c - fbase];
         }
-    }
-}
-
-__global__ void prolong_add_kernel(Lay Lf, Lay Lc, int64_t fbase, int64_t flen, int64_t cbase,
-                                   int64_t clen, const double* __restrict__ xc,
-                                   const double* __restrict__ hprev,
-                                   const double* __restrict__ hnext, double* __restrict__ xf) {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < flen;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        int kind, c, t;
-        decode(Lf, fbase + k, kind, c, t);
-        double val;
-        if (kind == KZ) {
-            val = coarse_val(Lc, xc, cbase, clen, hprev, hnext, KZ, c, (t + 1) / 2);
-        } else if ((t & 1) == 0) {
-            val = coarse_val(Lc, xc, cbase, clen, hprev, hnext, kind, c, t / 2);
-        } else if (t == 1) {
-            val = coarse_val(Lc, xc, cbase, clen, hprev, hnext, kind, c, 1);
-        } else {
-            const int j = (t - 1) / 2;
-            val = 0.5 * (coarse_val(Lc, xc, cbase, clen, hprev, hnext, kind, c, j) +
-                         coarse_val(Lc, xc, cbase, clen, hprev, hnext, kind, c, j + 1));
-        }
-        xf[k] = xf[k] + val;
     }
 }
 
@@ -226,6 +195,43 @@ __global__ void __launch_bounds__(256) prolong_rows_kernel(Lay Lf, Lay Lc, int64
     }
 }
 
+// Tiny rows (van der Pol, n_u < 32): one THREAD per fine block row (the
+// element-wise kernel spent its time in the 64-bit index decode); same
+// arithmetic as prolong_rows_kernel's scalar path.
+__global__ void prolong_small_kernel(Lay Lf, Lay Lc, int64_t fbase, int r0, int r1, int64_t cbase,
+                                     int64_t clen, const double* __restrict__ xc,
+                                     const double* __restrict__ hprev,
+                                     const double* __restrict__ hnext, double* __restrict__ xf) {
+    for (int i = r0 + blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += gridDim.x * blockDim.x) {
+        auto seg = [&](int kind, int t, int64_t off, int len) {
+            double* dst = xf + (off - fbase);
+            const double* a;
+            const double* b = nullptr;
+            if (kind == KZ) {
+                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, KZ, (t + 1) / 2);
+            } else if ((t & 1) == 0) {
+                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, t / 2);
+            } else if (t == 1) {
+                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, 1);
+            } else {
+                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, (t - 1) / 2);
+                b = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, (t + 1) / 2);
+            }
+            for (int k = 0; k < len; ++k) {
+                const double val = b ? 0.5 * (a[k] + b[k]) : a[k];
+                dst[k] = dst[k] + val;
+            }
+        };
+        if (i >= 1) seg(KV, i, Lf.off_v(i), Lf.nu);
+        if (i < Lf.N) {
+            seg(KU, i + 1, Lf.off_u(i), Lf.nu);
+            seg(KZ, i + 1, Lf.off_z(i), Lf.nz);
+        }
+        if (i >= 1) seg(KM, i, Lf.off_mu(i), Lf.nu);
+        if (i < Lf.N) seg(KL, i + 1, Lf.off_l(i), Lf.nu);
+    }
+}
+
 // rc = R (b - A x) for x = ONE block-Jacobi sweep from zero, x = omega D^{-1} b
 // (the pre-smoothing of every V-cycle level, multigrid.py:284-288).  Then
 // D x = omega b, so  b - A x = (1 - omega) b - (L + U) x: the only other
@@ -238,36 +244,9 @@ static void slab_geom(const Lay& Lf, const Lay& Lc, int r0, int r1, int64_t& fba
 
 // Time slab of fine rows [r0, r1): the coupling partners outside the slab are
 // the halo segments (u of row r0-1 = u_{r0}, mu of row r1 = mu_{r1}).
-__global__ void restrict_jacobi0_kernel(Lay Lf, Lay Lc, int64_t fbase, int64_t cbase, int64_t clen,
-                                        int r0, int r1, const double* __restrict__ b,
-                                        const double* __restrict__ x, const double* __restrict__ hu,
-                                        const double* __restrict__ hm, double omega,
-                                        double* __restrict__ rc) {
-    const double c1 = 1.0 - omega;
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < clen;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        int kind, c, t;
-        decode(Lc, cbase + k, kind, c, t);
-        double v;
-        if (kind == KZ) {
-            v = c1 == 0.0 ? 0.0
-                          : c1 * (0.5 * (b[kind_off(Lf, KZ, 2 * t - 1) + c - fbase] +
-                                         b[kind_off(Lf, KZ, 2 * t) + c - fbase]));
-        } else {
-            const int ft = 2 * t;
-            v = c1 == 0.0 ? 0.0 : c1 * b[kind_off(Lf, kind, ft) + c - fbase];
-            if (kind == KM)        // u_{2t} lives in fine row 2t-1
-                v -= (ft - 1 >= r0) ? x[kind_off(Lf, KU, ft) + c - fbase] : hu[c];
-            else if (kind == KU)   // mu_{2t} lives in fine row 2t
-                v -= (ft < r1) ? x[kind_off(Lf, KM, ft) + c - fbase] : hm[c];
-        }
-        rc[k] = v;
-    }
-}
-
 // Row-based variant: one CTA per coarse block row; each of its segments is one
 // (kind, coarse time) whose sources are located once, then streamed (16-byte
-// accesses when aligned).  Same arithmetic as restrict_jacobi0_kernel; with
+// accesses when aligned).  With
 // omega == 1 the v, z, lam segments are zero and u, mu the negated couplings.
 __global__ void __launch_bounds__(256) restrict_jacobi0_rows(Lay Lf, Lay Lc, int64_t fbase, int64_t cbase,
                                                              int c0, int c1, int r0, int r1,
@@ -328,6 +307,42 @@ __global__ void __launch_bounds__(256) restrict_jacobi0_rows(Lay Lf, Lay Lc, int
     }
 }
 
+// Tiny rows: one THREAD per coarse block row, same arithmetic as the kernels above.
+__global__ void restrict_jacobi0_small(Lay Lf, Lay Lc, int64_t fbase, int64_t cbase, int c0, int c1,
+                                       int r0, int r1, const double* __restrict__ b,
+                                       const double* __restrict__ x, const double* __restrict__ hu,
+                                       const double* __restrict__ hm, double omega,
+                                       double* __restrict__ rc) {
+    const double c1w = 1.0 - omega;
+    for (int c = c0 + blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += gridDim.x * blockDim.x) {
+        auto seg = [&](int kind, int t, int64_t off, int len) {
+            const int ft = 2 * t;
+            double* dst = rc + (off - cbase);
+            const double* xs = nullptr;
+            if (kind == KM) xs = (ft - 1 >= r0) ? x + (kind_off(Lf, KU, ft) - fbase) : hu;
+            else if (kind == KU) xs = (ft < r1) ? x + (kind_off(Lf, KM, ft) - fbase) : hm;
+            for (int k = 0; k < len; ++k) {
+                double v;
+                if (kind == KZ)
+                    v = c1w == 0.0 ? 0.0
+                                   : c1w * (0.5 * (b[kind_off(Lf, KZ, ft - 1) + k - fbase] +
+                                                    b[kind_off(Lf, KZ, ft) + k - fbase]));
+                else
+                    v = c1w == 0.0 ? 0.0 : c1w * b[kind_off(Lf, kind, ft) + k - fbase];
+                if (xs) v -= xs[k];
+                dst[k] = v;
+            }
+        };
+        if (c >= 1) seg(KV, c, Lc.off_v(c), Lc.nu);
+        if (c < Lc.N) {
+            seg(KU, c + 1, Lc.off_u(c), Lc.nu);
+            seg(KZ, c + 1, Lc.off_z(c), Lc.nz);
+        }
+        if (c >= 1) seg(KM, c, Lc.off_mu(c), Lc.nu);
+        if (c < Lc.N) seg(KL, c + 1, Lc.off_l(c), Lc.nu);
+    }
+}
+
 int restrict_jacobi0_launch(int n_fine, int nu, int nz, int r0, int r1, const double* b,
                             const double* x, const double* hu, const double* hm, double omega,
                             double* rc, cudaStream_t s) {
@@ -354,9 +369,13 @@ int restrict_jacobi0_launch(int n_fine, int nu, int nz, int r0, int r1, const do
                                                                     x, hu, hm, omega, rc, vec);
         return check_launch("restrict_jacobi0_rows");
     }
-    restrict_jacobi0_kernel<<<grid_for(clen, 256, 148 * 32), 256, 0, s>>>(
-        Lf, Lc, fbase, cbase, clen, r0, r1, b, x, hu, hm, omega, rc);
-    return check_launch("restrict_jacobi0");
+    {   // tiny rows: one thread per coarse block row
+        const int c0 = r0 / 2, c1 = (r1 == n_fine + 1) ? Lc.N + 1 : r1 / 2;
+        const int rows = c1 - c0;
+        restrict_jacobi0_small<<<(rows + 255) / 256, 256, 0, s>>>(Lf, Lc, fbase, cbase, c0, c1, r0, r1, b,
+                                                                  x, hu, hm, omega, rc);
+        return check_launch("restrict_jacobi0_small");
+    }
 }
 
 // fine rows [r0, r1) -> coarse rows [r0/2, r1/2) (through N/2 for the last slab)
@@ -394,9 +413,10 @@ int transfer_launch(int restrict_op, int n_fine, int nu, int nz, int r0, int r1,
         auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
         const bool vec = (nu % 2 == 0) && (nz % 2 == 0) && (fbase % 2 == 0) && (cbase % 2 == 0) &&
                          al(in) && al(out) && al(hprev) && al(hnext);
-        if (nu < 32) {   // tiny rows (van der Pol): one thread per fine element
-            prolong_add_kernel<<<grid_for(flen, th, 148 * 32), th, 0, s>>>(
-                Lf, Lc, fbase, flen, cbase, clen, in, hprev, hnext, out);
+        if (nu < 32) {   // tiny rows (van der Pol): one thread per fine block row
+            const int rows = r1 - r0;
+            prolong_small_kernel<<<(rows + th - 1) / th, th, 0, s>>>(Lf, Lc, fbase, r0, r1, cbase, clen,
+                                                                   in, hprev, hnext, out);
             return check_launch("transfer");
         }
         const int rows = r1 - r0;
