@@ -202,33 +202,50 @@ __global__ void prolong_small_kernel(Lay Lf, Lay Lc, int64_t fbase, int r0, int 
                                      int64_t clen, const double* __restrict__ xc,
                                      const double* __restrict__ hprev,
                                      const double* __restrict__ hnext, double* __restrict__ xf) {
-    for (int i = r0 + blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += gridDim.x * blockDim.x) {
-        auto seg = [&](int kind, int t, int64_t off, int len) {
-            double* dst = xf + (off - fbase);
-            const double* a;
-            const double* b = nullptr;
-            if (kind == KZ) {
-                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, KZ, (t + 1) / 2);
-            } else if ((t & 1) == 0) {
-                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, t / 2);
-            } else if (t == 1) {
-                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, 1);
-            } else {
-                a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, (t - 1) / 2);
-                b = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, (t + 1) / 2);
+    // a CTA owns blockDim.x consecutive fine rows: their contiguous slice of xf
+    // is staged through shared memory with coalesced loads/stores, and each
+    // thread updates its own row there
+    extern __shared__ double sx[];
+    const int rb = blockDim.x;
+    for (int i0 = r0 + blockIdx.x * rb; i0 < r1; i0 += gridDim.x * rb) {
+        const int i1 = min(i0 + rb, r1);
+        const int64_t g0 = Lf.start(i0), g1 = (i1 == Lf.N + 1) ? Lf.dim() : Lf.start(i1);
+        const int len = (int)(g1 - g0);
+        double* row0 = xf + (g0 - fbase);
+        for (int k = threadIdx.x; k < len; k += rb) sx[k] = row0[k];
+        __syncthreads();
+        const int i = i0 + threadIdx.x;
+        if (i < i1) {
+            auto seg = [&](int kind, int t, int64_t off, int ln) {
+                double* dst = sx + (off - g0);
+                const double* a;
+                const double* b = nullptr;
+                if (kind == KZ) {
+                    a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, KZ, (t + 1) / 2);
+                } else if ((t & 1) == 0) {
+                    a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, t / 2);
+                } else if (t == 1) {
+                    a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, 1);
+                } else {
+                    a = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, (t - 1) / 2);
+                    b = coarse_seg(Lc, xc, cbase, clen, hprev, hnext, kind, (t + 1) / 2);
+                }
+                for (int k = 0; k < ln; ++k) {
+                    const double val = b ? 0.5 * (a[k] + b[k]) : a[k];
+                    dst[k] = dst[k] + val;
+                }
+            };
+            if (i >= 1) seg(KV, i, Lf.off_v(i), Lf.nu);
+            if (i < Lf.N) {
+                seg(KU, i + 1, Lf.off_u(i), Lf.nu);
+                seg(KZ, i + 1, Lf.off_z(i), Lf.nz);
             }
-            for (int k = 0; k < len; ++k) {
-                const double val = b ? 0.5 * (a[k] + b[k]) : a[k];
-                dst[k] = dst[k] + val;
-            }
-        };
-        if (i >= 1) seg(KV, i, Lf.off_v(i), Lf.nu);
-        if (i < Lf.N) {
-            seg(KU, i + 1, Lf.off_u(i), Lf.nu);
-            seg(KZ, i + 1, Lf.off_z(i), Lf.nz);
+            if (i >= 1) seg(KM, i, Lf.off_mu(i), Lf.nu);
+            if (i < Lf.N) seg(KL, i + 1, Lf.off_l(i), Lf.nu);
         }
-        if (i >= 1) seg(KM, i, Lf.off_mu(i), Lf.nu);
-        if (i < Lf.N) seg(KL, i + 1, Lf.off_l(i), Lf.nu);
+        __syncthreads();
+        for (int k = threadIdx.x; k < len; k += rb) row0[k] = sx[k];
+        __syncthreads();
     }
 }
 
@@ -313,34 +330,56 @@ __global__ void restrict_jacobi0_small(Lay Lf, Lay Lc, int64_t fbase, int64_t cb
                                        const double* __restrict__ x, const double* __restrict__ hu,
                                        const double* __restrict__ hm, double omega,
                                        double* __restrict__ rc) {
+    // a CTA owns blockDim.x consecutive coarse rows; each thread writes its row
+    // into shared memory, the contiguous slice leaves with coalesced stores
+    extern __shared__ double sx[];
     const double c1w = 1.0 - omega;
-    for (int c = c0 + blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += gridDim.x * blockDim.x) {
-        auto seg = [&](int kind, int t, int64_t off, int len) {
-            const int ft = 2 * t;
-            double* dst = rc + (off - cbase);
-            const double* xs = nullptr;
-            if (kind == KM) xs = (ft - 1 >= r0) ? x + (kind_off(Lf, KU, ft) - fbase) : hu;
-            else if (kind == KU) xs = (ft < r1) ? x + (kind_off(Lf, KM, ft) - fbase) : hm;
-            for (int k = 0; k < len; ++k) {
-                double v;
-                if (kind == KZ)
-                    v = c1w == 0.0 ? 0.0
-                                   : c1w * (0.5 * (b[kind_off(Lf, KZ, ft - 1) + k - fbase] +
-                                                    b[kind_off(Lf, KZ, ft) + k - fbase]));
-                else
-                    v = c1w == 0.0 ? 0.0 : c1w * b[kind_off(Lf, kind, ft) + k - fbase];
-                if (xs) v -= xs[k];
-                dst[k] = v;
+    const int rb = blockDim.x;
+    for (int q0 = c0 + blockIdx.x * rb; q0 < c1; q0 += gridDim.x * rb) {
+        const int q1 = min(q0 + rb, c1);
+        const int64_t g0 = Lc.start(q0), g1 = (q1 == Lc.N + 1) ? Lc.dim() : Lc.start(q1);
+        const int len = (int)(g1 - g0);
+        const int c = q0 + threadIdx.x;
+        if (c < q1) {
+            auto seg = [&](int kind, int t, int64_t off, int ln) {
+                const int ft = 2 * t;
+                double* dst = sx + (off - g0);
+                const double* xs = nullptr;
+                if (kind == KM) xs = (ft - 1 >= r0) ? x + (kind_off(Lf, KU, ft) - fbase) : hu;
+                else if (kind == KU) xs = (ft < r1) ? x + (kind_off(Lf, KM, ft) - fbase) : hm;
+                for (int k = 0; k < ln; ++k) {
+                    double v;
+                    if (kind == KZ)
+                        v = c1w == 0.0 ? 0.0
+                                       : c1w * (0.5 * (b[kind_off(Lf, KZ, ft - 1) + k - fbase] +
+                                                        b[kind_off(Lf, KZ, ft) + k - fbase]));
+                    else
+                        v = c1w == 0.0 ? 0.0 : c1w * b[kind_off(Lf, kind, ft) + k - fbase];
+                    if (xs) v -= xs[k];
+                    dst[k] = v;
+                }
+            };
+            if (c >= 1) seg(KV, c, Lc.off_v(c), Lc.nu);
+            if (c < Lc.N) {
+                seg(KU, c + 1, Lc.off_u(c), Lc.nu);
+                seg(KZ, c + 1, Lc.off_z(c), Lc.nz);
             }
-        };
-        if (c >= 1) seg(KV, c, Lc.off_v(c), Lc.nu);
-        if (c < Lc.N) {
-            seg(KU, c + 1, Lc.off_u(c), Lc.nu);
-            seg(KZ, c + 1, Lc.off_z(c), Lc.nz);
+            if (c >= 1) seg(KM, c, Lc.off_mu(c), Lc.nu);
+            if (c < Lc.N) seg(KL, c + 1, Lc.off_l(c), Lc.nu);
         }
-        if (c >= 1) seg(KM, c, Lc.off_mu(c), Lc.nu);
-        if (c < Lc.N) seg(KL, c + 1, Lc.off_l(c), Lc.nu);
+        __syncthreads();
+        double* out = rc + (g0 - cbase);
+        for (int k = threadIdx.x; k < len; k += rb) out[k] = sx[k];
+        __syncthreads();
     }
+}
+
+// rows per CTA of the tiny-row kernels: a power of two, <= 256, with the
+// CTA's rows (rb * m doubles) within 48 KB of shared memory
+static int small_rows_per_cta(int m) {
+    int rb = 256;
+    while (rb > 32 && (int64_t)rb * m * 8 > 48 * 1024) rb >>= 1;
+    return rb;
 }
 
 int restrict_jacobi0_launch(int n_fine, int nu, int nz, int r0, int r1, const double* b,
@@ -372,8 +411,9 @@ int restrict_jacobi0_launch(int n_fine, int nu, int nz, int r0, int r1, const do
     {   // tiny rows: one thread per coarse block row
         const int c0 = r0 / 2, c1 = (r1 == n_fine + 1) ? Lc.N + 1 : r1 / 2;
         const int rows = c1 - c0;
-        restrict_jacobi0_small<<<(rows + 255) / 256, 256, 0, s>>>(Lf, Lc, fbase, cbase, c0, c1, r0, r1, b,
-                                                                  x, hu, hm, omega, rc);
+        const int rb = small_rows_per_cta(Lc.m);
+        restrict_jacobi0_small<<<grid_for(rows, rb, 148 * 8), rb, (size_t)rb * Lc.m * 8, s>>>(
+            Lf, Lc, fbase, cbase, c0, c1, r0, r1, b, x, hu, hm, omega, rc);
         return check_launch("restrict_jacobi0_small");
     }
 }
@@ -415,8 +455,9 @@ int transfer_launch(int restrict_op, int n_fine, int nu, int nz, int r0, int r1,
                          al(in) && al(out) && al(hprev) && al(hnext);
         if (nu < 32) {   // tiny rows (van der Pol): one thread per fine block row
             const int rows = r1 - r0;
-            prolong_small_kernel<<<(rows + th - 1) / th, th, 0, s>>>(Lf, Lc, fbase, r0, r1, cbase, clen,
-                                                                   in, hprev, hnext, out);
+            const int rb = small_rows_per_cta((int)Lf.m);
+            prolong_small_kernel<<<grid_for(rows, rb, 148 * 8), rb, (size_t)rb * Lf.m * 8, s>>>(
+                Lf, Lc, fbase, r0, r1, cbase, clen, in, hprev, hnext, out);
             return check_launch("transfer");
         }
         const int rows = r1 - r0;
