@@ -47,6 +47,7 @@ _NCU_FULL = {
     "tk_prolong_add": "prolong_rows_kernel",
     "tk_kkt_apply": "tri_apply<0",
     "tk_residual_restrict_jacobi0": "restrict_jacobi0",
+    "tk_jacobi0_restrict": "tri_rows_part",
 }
 
 
@@ -230,7 +231,8 @@ def run_ours(args, rank, world, local_rank):
     names = {"tk_jacobi_sweep", "tk_residual_restrict", "tk_prolong_add", "tk_forward_subst",
              "tk_backward_subst", "tk_sgs_back_half", "tk_kkt_apply", "tk_kkt_apply_diag",
              "tk_kkt_residual", "tk_dot", "tk_nrm2", "tk_axpy", "tk_scale_into", "tk_rsub",
-             "tk_gemv_t_add", "tk_arnoldi_mgs", "tk_copy_kernel", "tk_residual_restrict_jacobi0"}
+             "tk_gemv_t_add", "tk_arnoldi_mgs", "tk_copy_kernel", "tk_residual_restrict_jacobi0",
+             "tk_jacobi0_restrict"}
     # (eager cycles: the CUDA-graph replay hides the coarse levels' kernels)
     from paper_2405_04808_b200 import graph as G
     graph_on = G.ENABLED
@@ -256,7 +258,8 @@ def run_ours(args, rank, world, local_rank):
         d["bytes"] += roofline.algorithmic_bytes(nm, a)
     fine_recs = {}
     for nm, a, e0, e1 in dev.INSTR.records:   # fine-level launch of each HBM kernel
-        if nm in ("tk_jacobi_sweep", "tk_residual_restrict", "tk_residual_restrict_jacobi0"):
+        if nm in ("tk_jacobi_sweep", "tk_residual_restrict", "tk_residual_restrict_jacobi0",
+                  "tk_jacobi0_restrict"):
             lvl = roofline.dim_of(a[0]._obj)
         elif nm == "tk_prolong_add":
             lvl = int(a[0]) * (4 * int(a[1]) + int(a[2]))

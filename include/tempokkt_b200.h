@@ -197,6 +197,15 @@ int tk_prolong_add_slab(int32_t n_fine, int32_t n_u, int32_t n_z, int32_t row0, 
  * coupling partners outside the slab from L->halo_u / L->halo_mu. */
 int tk_residual_restrict_jacobi0(const tk_level* L, const double* b, const double* x,
                                  double omega, double* rc, void* stream);
+/* The V-cycle's zero-start pre-smoothing sweep and its restricted residual
+ * in ONE pass (multigrid.py:284-288 with one sweep from zero): x_out =
+ * D^{-1} b (tk_jacobi_sweep with x_in = NULL, omega = 1) and rc exactly as
+ * tk_residual_restrict_jacobi0(L, b, x_out, 1, rc).  TRI levels of the
+ * partitioned row solve, whole level, even N, omega == 1: check
+ * tk_jacobi0_restrict_ok(), else TK_ERR_UNSUPPORTED. */
+int32_t tk_jacobi0_restrict_ok(const tk_level* L, double omega);
+int tk_jacobi0_restrict(const tk_level* L, const double* b, double omega, double* x_out,
+                        double* rc, void* stream);
 int tk_residual_restrict(const tk_level* L, const double* b, const double* x, double* rc,
                          double* work, void* stream);
 

@@ -57,6 +57,8 @@ _SIGS = {
     "tk_kkt_apply_diag": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
     "tk_diag_solve": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
     "tk_jacobi_sweep": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _d, _p]),
+    "tk_jacobi0_restrict_ok": (_i32, [C.POINTER(TkLevel), _d]),
+    "tk_jacobi0_restrict": (C.c_int, [C.POINTER(TkLevel), _p, _d, _p, _p, _p]),
     "tk_forward_subst": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
     "tk_backward_subst": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
     "tk_sgs_back_half": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),

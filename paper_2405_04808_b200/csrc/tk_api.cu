@@ -27,6 +27,8 @@ int dense_launch(const tk_level*, int, const double*, const double*, double*, do
 int tri_launch(const tk_level*, int, const double*, const double*, double*, double, cudaStream_t);
 int64_t tri_smem_bytes(int n);
 int tri_resrestrict_launch(const tk_level*, const double*, const double*, double*, cudaStream_t);
+bool tri_jacobi0_restrict_ok(const tk_level*, double);
+int tri_jacobi0_restrict_launch(const tk_level*, const double*, double, double*, double*, cudaStream_t);
 int64_t tri_fac_len(const tk_level*);
 int64_t tri_scratch_len(const tk_level*);
 int64_t dense_fac_len(const tk_level*);
@@ -135,6 +137,19 @@ int tk_jacobi_sweep(const tk_level* L, const double* b, const double* x_in, doub
     TK_CHECK_ARG(b && x_out, "tk_jacobi_sweep: null vector");
     TK_CHECK_ARG(x_in != x_out, "tk_jacobi_sweep: x_out must not alias x_in");
     return level_op(L, 4, 4, b, x_in, x_out, omega, stream);
+}
+
+int32_t tk_jacobi0_restrict_ok(const tk_level* L, double omega) {
+    if (check_level(L)) return 0;
+    return tri_jacobi0_restrict_ok(L, omega) ? 1 : 0;
+}
+
+int tk_jacobi0_restrict(const tk_level* L, const double* b, double omega, double* x_out, double* rc,
+                        void* stream) {
+    TK_CHECK_ARG(b && x_out && rc, "tk_jacobi0_restrict: null vector");
+    const int e = check_level(L);
+    if (e) return e;
+    return tri_jacobi0_restrict_launch(L, b, omega, x_out, rc, as_stream(stream));
 }
 
 int tk_forward_subst(const tk_level* L, const double* r, double* delta, void* stream) {

@@ -1802,7 +1802,7 @@ static int carry_grid_launch(bool fwd, int n, int nc, const double* M, const dou
 
 int part_nodes_per_lane(int n);
 int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, double* y,
-                double omega, const double* chain, cudaStream_t s);
+                double omega, const double* chain, cudaStream_t s, double* rc = nullptr);
 
 // warp-per-row partitioned solves (tk_tri_part.cu) for 32 < n <= 512;
 // TK_PART=0 selects the CTA-wide cyclic-reduction kernels instead
@@ -2060,6 +2060,27 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
         default: set_error("tri: bad op %d", op); return TK_ERR_ARG;
     }
     return check_launch("tri_rows");
+}
+
+static bool use_part(int n);
+// y = D^{-1} b (zero-start sweep, omega = 1) and the restricted residual rc
+// of tk_residual_restrict_jacobi0 in one pass (tri_rows_part<..., RJ>)
+bool tri_jacobi0_restrict_ok(const tk_level* Lv, double omega) {
+    const int n = Lv->n_u;
+    const bool rec = Lv->fac != nullptr && !(Lv->flags & TK_FLAG_ONTHEFLY) &&
+                     (!use_part(n) || (Lv->flags & TK_FLAG_RECROWS));
+    const bool whole = Lv->row0 == 0 && (Lv->row1 == 0 || Lv->row1 == Lv->n_steps + 1);
+    return Lv->family == TK_FAMILY_TRI && omega == 1.0 && !rec && use_part(n) &&
+           part_nodes_per_lane(n) > 0 && whole && (Lv->n_steps % 2) == 0 && Lv->n_steps >= 2;
+}
+int tri_jacobi0_restrict_launch(const tk_level* Lv, const double* b, double omega, double* y,
+                                double* rc, cudaStream_t s) {
+    if (!tri_jacobi0_restrict_ok(Lv, omega)) {
+        set_error("tk_jacobi0_restrict: level not supported (TRI partitioned rows, whole level, "
+                  "even N, omega = 1)");
+        return TK_ERR_UNSUPPORTED;
+    }
+    return part_launch(Lv, 0, b, nullptr, y, omega, nullptr, s, rc);
 }
 
 int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, double* y,

@@ -277,10 +277,18 @@ extern "C" int tk_debug_part_prof(long long* out10) {
 // chunk's bottom-up results, the interface PCR partners, the left interface
 // value and the first lam of the right neighbour) read the peer's shared
 // memory (distributed shared memory) after cluster barriers.
-template <int W, int MODE, bool FULL, int CL>
+//
+// RJ (MODE 0, x == nullptr, omega == 1, whole level, even N): the zero-start
+// sweep also writes the restricted residual rc = R (b - A y) of
+// tk_residual_restrict_jacobi0 (D y = b, so b - A y is the continuity
+// coupling): row 2c-1 writes -u_{2c} as the coarse mu_c, row 2c writes
+// -mu_{2c} as the coarse u_c and the zero v_c, z_{c+1}, lam_{c+1} of coarse
+// row c -- the separate restriction kernel and its re-read of y disappear.
+template <int W, int MODE, bool FULL, int CL, bool RJ>
 __global__ void __launch_bounds__(32 * W, PartCta<W>::min_blocks())
 tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ x,
-              double* __restrict__ y, double omega, const double* __restrict__ chain) {
+              double* __restrict__ y, double omega, const double* __restrict__ chain,
+              double* __restrict__ rc) {
     using Cf = PartCta<W>;
     constexpr int T = Cf::T;
     constexpr int TT = CL * T;                // interface nodes of a row
@@ -524,12 +532,29 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             }
         }
         TKPP(1);
+        const Lay Lc(L.N / 2, n, L.nz);
+        if (RJ && (i & 1) == 0) {   // zeros of coarse row c = i/2: v_c, z_{c+1}, lam_{c+1}
+            const int c = i / 2;
+            double zr[NA];
+#pragma unroll
+            for (int k = 0; k < NA; ++k) zr[k] = 0.0;
+            if (c >= 1) st4<FULL>(rc, Lc.off_v(c), j0, n, zr);
+            if (c < Lc.N) {
+                st4<FULL>(rc, Lc.off_z(c), j0, n, zr);
+                st4<FULL>(rc, Lc.off_l(c), j0, n, zr);
+            }
+        }
         if (!has_uzl) {   // last block (v_N, mu_N): mu = Qv v - r_v
             double xm[NA], o[NA];
             ld4<FULL>(x, om, j0, n, hx, xm);
 #pragma unroll
             for (int k = 0; k < NA; ++k) o[k] = xm[k] + omega * pm[k];
             st4<FULL>(y, om, j0, n, o);
+            if (RJ) {   // coarse u_{N/2} (coarse row N/2 - 1) = -mu_N
+#pragma unroll
+                for (int k = 0; k < NA; ++k) o[k] = 0.0 - o[k];
+                st4<FULL>(rc, Lc.t_u(i / 2), j0, n, o);
+            }
             continue;
         }
 
@@ -830,6 +855,11 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
 #pragma unroll
             for (int k = 0; k < NA; ++k) o[k] = oxu[k] + omega * yu[k];
             st4<FULL>(y, ou, j0, n, o);
+            if (RJ && (i & 1)) {   // row 2c-1: coarse mu_c = -u_{2c}
+#pragma unroll
+                for (int k = 0; k < NA; ++k) o[k] = 0.0 - o[k];
+                st4<FULL>(rc, Lc.t_mu((i + 1) / 2), j0, n, o);
+            }
 #pragma unroll
             for (int k = 0; k < NA; ++k) o[k] = oxz[k] + omega * (yw[k] - kap * yl[k]);
             st4<FULL>(y, oz, j0, n, o);
@@ -851,6 +881,11 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                     o[k] = oxm[k] + omega * dm;
                 }
                 st4<FULL>(y, om, j0, n, o);
+                if (RJ && (i & 1) == 0) {   // row 2c: coarse u_c = -mu_{2c}
+#pragma unroll
+                    for (int k = 0; k < NA; ++k) o[k] = 0.0 - o[k];
+                    st4<FULL>(rc, Lc.t_u(i / 2), j0, n, o);
+                }
             }
         }
         TKPP(8);
@@ -875,14 +910,14 @@ static int part_cluster(int n) { return n > kChunk * 32 * 8 ? 2 : 1; }
 
 int part_nodes_per_lane(int n) { return part_warps(n) ? kChunk : 0; }
 
-template <int W, int MODE, bool FULL, int CL>
+template <int W, int MODE, bool FULL, int CL, bool RJ = false>
 static int part_launch_t(const tk_level* Lv, const double* b, const double* x, double* y,
-                         double omega, const double* chain, cudaStream_t s) {
+                         double omega, const double* chain, cudaStream_t s, double* rc = nullptr) {
     using Cf = PartCta<W>;
     static int per_sm = 0;
     static int nsm = 0;
     const int64_t smem = Cf::smem_bytes();
-    auto kern = tri_rows_part<W, MODE, FULL, CL>;
+    auto kern = tri_rows_part<W, MODE, FULL, CL, RJ>;
     if (!per_sm) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -906,7 +941,7 @@ static int part_launch_t(const tk_level* Lv, const double* b, const double* x, d
     const int cap = nsm * per_sm / CL;
     if (clusters > cap) clusters = cap;
     if (CL == 1) {
-        kern<<<clusters, 32 * W, smem, s>>>(V, b, x, y, omega, chain);
+        kern<<<clusters, 32 * W, smem, s>>>(V, b, x, y, omega, chain, rc);
         return check_launch("tri_rows_part");
     }
     cudaLaunchConfig_t cfg = {};
@@ -915,14 +950,19 @@ static int part_launch_t(const tk_level* Lv, const double* b, const double* x, d
     at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(clusters * CL); cfg.blockDim = dim3(32 * W); cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = s; cfg.attrs = at; cfg.numAttrs = 1;
-    return cuda_status(cudaLaunchKernelEx(&cfg, kern, V, b, x, y, omega, chain), "tri_rows_part (cluster)");
+    return cuda_status(cudaLaunchKernelEx(&cfg, kern, V, b, x, y, omega, chain, rc),
+                       "tri_rows_part (cluster)");
 }
 
 // mode 0: rows (jacobi / D^{-1} b), 1/2: substitution pass 3 forward/backward
 int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, double* y,
-                double omega, const double* chain, cudaStream_t s) {
+                double omega, const double* chain, cudaStream_t s, double* rc) {
 #define TK_PART_CASE(WW, CC)                                                                        \
     if (w == WW && cl == CC) {                                                                      \
+        if (rc) {                                                                                   \
+            if (full) return part_launch_t<WW, 0, true, CC, true>(Lv, b, x, y, omega, chain, s, rc); \
+            return part_launch_t<WW, 0, false, CC, true>(Lv, b, x, y, omega, chain, s, rc);         \
+        }                                                                                           \
         if (full) {                                                                                 \
             if (mode == 0) return part_launch_t<WW, 0, true, CC>(Lv, b, x, y, omega, chain, s);     \
             if (mode == 1) return part_launch_t<WW, 1, true, CC>(Lv, b, x, y, omega, chain, s);     \
@@ -935,8 +975,14 @@ int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, 
     // FULL: every chunk is complete and every segment 16-byte aligned
     const int w = part_warps(Lv->n_u), cl = part_cluster(Lv->n_u);
     auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (rc && (mode != 0 || x || omega != 1.0 || Lv->row0 != 0 ||
+               (Lv->row1 != 0 && Lv->row1 != Lv->n_steps + 1) || (Lv->n_steps & 1))) {
+        set_error("tri_rows_part: the fused restriction needs a zero-start sweep with omega = 1 "
+                  "on a whole level with even N");
+        return TK_ERR_UNSUPPORTED;
+    }
     const bool full = w > 0 && Lv->n_u == kChunk * 32 * w * cl && Lv->n_u % 2 == 0 && Lv->n_z % 2 == 0 &&
-                      al(b) && al(x) && al(y) && al(chain) && al(Lv->K) && al(Lv->C) &&
+                      al(b) && al(x) && al(y) && al(chain) && al(rc) && al(Lv->K) && al(Lv->C) &&
                       al(Lv->Qm) && al(Lv->Ql) && al(Lv->Qz) && al(Lv->halo_u) && al(Lv->halo_mu);
     TK_PART_CASE(1, 1)
     TK_PART_CASE(2, 1)

@@ -134,7 +134,7 @@ class VCycleGraph:
         return cur
 
     def _record_level(self, l, body_stream):
-        from .multigrid import JACOBI0_RESIDUAL
+        from .multigrid import JACOBI0_RESIDUAL, fused_jacobi0_ok
         h = self.h
         L = h.n_levels
         a = h.levels[l].kkt
@@ -144,8 +144,15 @@ class VCycleGraph:
             return
         # pre-smoothing from zero: X (sweeps 1) or X/Y ping-pong ending in X
         bufs = [self.X[l]] if h.sweeps == 1 else [self.X[l], self.Y[l]]
-        x = self._sweeps(a, self.B[l], None, bufs, h.sweeps)
-        if h.sweeps == 1 and JACOBI0_RESIDUAL:
+        if h.sweeps == 1 and JACOBI0_RESIDUAL and fused_jacobi0_ok(a, h.omega):
+            x = self.X[l]
+            dev.call("tk_jacobi0_restrict", a.lref, dev.P(self.B[l]), float(h.omega), dev.P(x),
+                     dev.P(self.B[l + 1]), s)
+        else:
+            x = self._sweeps(a, self.B[l], None, bufs, h.sweeps)
+        if h.sweeps == 1 and JACOBI0_RESIDUAL and fused_jacobi0_ok(a, h.omega):
+            pass
+        elif h.sweeps == 1 and JACOBI0_RESIDUAL:
             dev.call("tk_residual_restrict_jacobi0", a.lref, dev.P(self.B[l]), dev.P(x),
                      float(h.omega), dev.P(self.B[l + 1]), s)
         else:
@@ -217,9 +224,11 @@ class VCycleGraph:
             dev._launches("tk_sgs_back_half", (a.lref,)) if self._fused_back_half(a) else
             1 + dev._launches("tk_backward_subst", (a.lref,)))
         self.per_coarse_iter = sgs + 1 + 1 + 1          # prec, apply, arnoldi, givens
+        from .multigrid import fused_jacobi0_ok
         fixed = 0
-        for l in range(self.start, h.n_levels - 1):
-            fixed += 2 * h.sweeps + 1 + 1                # sweeps, restrict, prolong
+        for l in range(self.start, h.n_levels - 1):     # sweeps, restrict, prolong
+            fused = h.sweeps == 1 and fused_jacobi0_ok(h.levels[l].kkt, h.omega)
+            fixed += 2 * h.sweeps + (0 if fused else 1) + 1
         fixed += 2 + 1 + 1 + 2 + sgs + 1 + 1 + 2 * 2 + 1  # begin, combine, prec, apply, finish
         return fixed
 
@@ -249,7 +258,7 @@ class VCycleGraph:
 def graphed_vcycle(h, b):
     """One V-cycle from zero on device tensor b through the graph; returns
     the fine-level result, or None when the eager path must run instead."""
-    from .multigrid import JACOBI0_RESIDUAL
+    from .multigrid import JACOBI0_RESIDUAL, fused_jacobi0_ok
     from .smoothers import jacobi_sweeps
     g = getattr(h, "_graph", None)
     key = (h.sweeps, float(h.omega), float(h.coarse_tol), int(h.coarse_max_iters))
@@ -259,11 +268,16 @@ def graphed_vcycle(h, b):
         h._graph = None
         g = h._graph = VCycleGraph(h)
     a = h.levels[0].kkt
-    x = jacobi_sweeps(a, b, None, h.sweeps, h.omega)
-    if h.sweeps == 1 and JACOBI0_RESIDUAL:
+    if h.sweeps == 1 and JACOBI0_RESIDUAL and fused_jacobi0_ok(a, h.omega):
+        x = dev.empty(a.dim)
+        dev.call("tk_jacobi0_restrict", a.lref, dev.P(b), float(h.omega), dev.P(x),
+                 dev.P(g.B[1]), dev.stream())
+    elif h.sweeps == 1 and JACOBI0_RESIDUAL:
+        x = jacobi_sweeps(a, b, None, h.sweeps, h.omega)
         dev.call("tk_residual_restrict_jacobi0", a.lref, dev.P(b), dev.P(x), float(h.omega),
                  dev.P(g.B[1]), dev.stream())
     else:
+        x = jacobi_sweeps(a, b, None, h.sweeps, h.omega)
         work = dev.empty(a.dim)
         dev.call("tk_residual_restrict", a.lref, dev.P(b), dev.P(x), dev.P(g.B[1]),
                  dev.P(work), dev.stream())

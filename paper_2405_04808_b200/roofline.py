@@ -14,6 +14,7 @@ constant weights counted as cache hits (0 bytes).  ``dim = N*(4nu+nz)``.
                            + 3/4 of the stage data (C of even rows, K and C of odd rows)
   restrict                 8*(coarse_dim + Nc*nz) read + 8*coarse_dim write
   prolong_add              8*(2*fine_dim + coarse_dim)
+  jacobi0_restrict         8*dim*2 + 8*coarse_dim + stage (zero-start sweep + restricted residual)
   dot 16n, nrm2 8n, axpy 24n, scale_into 16n, rsub 24n, gemv_t_add 8n(k+2)
 """
 
@@ -40,6 +41,10 @@ def algorithmic_bytes(name: str, args) -> int:
         L = _lvl(args[0])
         nvec = 2 + (1 if args[2] else 0)
         return 8 * dim_of(L) * nvec + stage_bytes(L)
+    if name == "tk_jacobi0_restrict":   # b read, x and the coarse rhs written, stage data
+        L = _lvl(args[0])
+        cdim = (L.n_steps // 2) * (4 * L.n_u + L.n_z)
+        return 8 * dim_of(L) * 2 + 8 * cdim + stage_bytes(L)
     if name in ("tk_diag_solve", "tk_forward_subst", "tk_backward_subst", "tk_sgs_back_half",
                 "tk_kkt_apply", "tk_kkt_apply_diag"):
         L = _lvl(args[0])

@@ -122,3 +122,36 @@ def test_large_n_identities(n_u):
     y = P.jacobi_apply(a, None, b, x, 1)
     r = a.residual(b, x)
     assert rel(a.apply_diag(y - x).cpu().numpy(), r.cpu().numpy()) < 1e-11
+
+
+@pytest.mark.parametrize("n_u", [33, 64, 100, 128, 300, 512, 1536])
+@pytest.mark.parametrize("n", [16, 64])
+def test_fused_jacobi0_restrict_bitwise(n_u, n):
+    """tk_jacobi0_restrict == zero-start tk_jacobi_sweep + tk_residual_restrict_jacobi0,
+    bit for bit (output and restricted residual), and against the oracle's
+    restricted residual of that sweep."""
+    import torch
+    from paper_2405_04808_b200 import device as dev
+    from paper_2405_04808_b200.multigrid import fused_jacobi0_ok
+    from paper_2405_04808_b200.smoothers import jacobi_sweeps
+    P, O, p, op, grid, u, v, z, rng = _case(n_u, n=n)
+    st = P.build_stage_blocks(p, grid.dt, u, v, z)
+    a = P.assemble_kkt(st)
+    assert fused_jacobi0_ok(a, 1.0) and not fused_jacobi0_ok(a, 0.8)
+    cdim = (n // 2) * 5 * n_u
+    b = dev.to_device(rng.standard_normal(a.dim))
+    x = dev.empty(a.dim)
+    rc = dev.to_device(np.full(cdim, np.nan))
+    dev.call("tk_jacobi0_restrict", a.lref, dev.P(b), 1.0, dev.P(x), dev.P(rc), dev.stream())
+    x2 = jacobi_sweeps(a, b, None, 1, 1.0)
+    rc2 = dev.empty(cdim)
+    dev.call("tk_residual_restrict_jacobi0", a.lref, dev.P(b), dev.P(x2), 1.0, dev.P(rc2),
+             dev.stream())
+    torch.cuda.synchronize()
+    assert torch.equal(x, x2)
+    assert torch.equal(rc, rc2)
+    ost = O.build_stages(op, grid.dt, u, v, z)
+    oa = O.Kkt(ost)
+    bh, xh = b.cpu().numpy(), x.cpu().numpy()
+    ro = O.restrict_kkt(O.Layout(n, n_u, n_u), O.Layout(n // 2, n_u, n_u), bh - oa.apply(xh))
+    assert rel(rc.cpu().numpy(), ro) < 1e-10
