@@ -200,9 +200,9 @@ int tk_residual_restrict_jacobi0(const tk_level* L, const double* b, const doubl
 /* The V-cycle's zero-start pre-smoothing sweep and its restricted residual
  * in ONE pass (multigrid.py:284-288 with one sweep from zero): x_out =
  * D^{-1} b (tk_jacobi_sweep with x_in = NULL, omega = 1) and rc exactly as
- * tk_residual_restrict_jacobi0(L, b, x_out, 1, rc).  TRI levels of the
- * partitioned row solve, whole level, even N, omega == 1: check
- * tk_jacobi0_restrict_ok(), else TK_ERR_UNSUPPORTED. */
+ * tk_residual_restrict_jacobi0(L, b, x_out, 1, rc).  DENSE levels and TRI
+ * levels of the partitioned row solve; whole level, even N, omega == 1:
+ * check tk_jacobi0_restrict_ok(), else TK_ERR_UNSUPPORTED. */
 int32_t tk_jacobi0_restrict_ok(const tk_level* L, double omega);
 int tk_jacobi0_restrict(const tk_level* L, const double* b, double omega, double* x_out,
                         double* rc, void* stream);

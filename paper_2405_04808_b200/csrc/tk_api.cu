@@ -29,6 +29,7 @@ int64_t tri_smem_bytes(int n);
 int tri_resrestrict_launch(const tk_level*, const double*, const double*, double*, cudaStream_t);
 bool tri_jacobi0_restrict_ok(const tk_level*, double);
 int tri_jacobi0_restrict_launch(const tk_level*, const double*, double, double*, double*, cudaStream_t);
+int dense_jacobi0_restrict(const tk_level*, const double*, double*, double*, cudaStream_t);
 int64_t tri_fac_len(const tk_level*);
 int64_t tri_scratch_len(const tk_level*);
 int64_t dense_fac_len(const tk_level*);
@@ -139,8 +140,16 @@ int tk_jacobi_sweep(const tk_level* L, const double* b, const double* x_in, doub
     return level_op(L, 4, 4, b, x_in, x_out, omega, stream);
 }
 
+static bool dense_jacobi0_restrict_ok(const tk_level* L, double omega) {
+    const bool whole = L->row0 == 0 && (L->row1 == 0 || L->row1 == L->n_steps + 1);
+    return L->family == TK_FAMILY_DENSE && omega == 1.0 && whole && (L->n_steps % 2) == 0 &&
+           L->n_steps >= 2 && L->n_u >= 1 && L->n_u <= TK_MAX_DENSE && L->n_z >= 1 &&
+           L->n_z <= TK_MAX_DENSE;
+}
+
 int32_t tk_jacobi0_restrict_ok(const tk_level* L, double omega) {
     if (check_level(L)) return 0;
+    if (L->family == TK_FAMILY_DENSE) return dense_jacobi0_restrict_ok(L, omega) ? 1 : 0;
     return tri_jacobi0_restrict_ok(L, omega) ? 1 : 0;
 }
 
@@ -149,6 +158,13 @@ int tk_jacobi0_restrict(const tk_level* L, const double* b, double omega, double
     TK_CHECK_ARG(b && x_out && rc, "tk_jacobi0_restrict: null vector");
     const int e = check_level(L);
     if (e) return e;
+    if (L->family == TK_FAMILY_DENSE) {
+        if (!dense_jacobi0_restrict_ok(L, omega)) {
+            set_error("tk_jacobi0_restrict: level not supported (whole level, even N, omega = 1)");
+            return TK_ERR_UNSUPPORTED;
+        }
+        return dense_jacobi0_restrict(L, b, x_out, rc, as_stream(stream));
+    }
     return tri_jacobi0_restrict_launch(L, b, omega, x_out, rc, as_stream(stream));
 }
 

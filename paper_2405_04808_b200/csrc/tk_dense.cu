@@ -306,10 +306,15 @@ __device__ __forceinline__ void solve_row(const DView<NU, NZ>& V, int i, const S
 
 enum DenseMode { D_APPLY = 0, D_APPLY_DIAG = 1, D_RESIDUAL = 2, D_SOLVE = 3, D_JACOBI = 4 };
 
+// rc != nullptr (D_JACOBI, x == nullptr, omega == 1, whole level, even N): the
+// zero-start sweep also writes the restricted residual of
+// tk_residual_restrict_jacobi0 (row 2c-1: coarse mu_c = -u_{2c}; row 2c:
+// coarse u_c = -mu_{2c} and the zero v_c, z_{c+1}, lam_{c+1} of coarse row c).
 template <int NU, int NZ, int MODE>
 __global__ void __launch_bounds__(128) dense_rows(DView<NU, NZ> V, const double* __restrict__ b,
                                                   const double* __restrict__ x,
-                                                  double* __restrict__ y, double omega) {
+                                                  double* __restrict__ y, double omega,
+                                                  double* __restrict__ rc = nullptr) {
     const Lay& L = V.lay;
     const Slab& S = V.sl;
     const int64_t bs0 = S.base;
@@ -353,7 +358,44 @@ __global__ void __launch_bounds__(128) dense_rows(DView<NU, NZ> V, const double*
 #pragma unroll
         for (int e = 0; e < NZ; ++e) xs.z[e] += omega * ys.z[e];
         store_seg<NU, NZ>(L, i, y, xs, bs0);
+        if (MODE == D_JACOBI && rc) {
+            const Lay Lc(L.N / 2, NU, NZ);
+            if (i & 1) {
+                double* p = rc + Lc.t_mu((i + 1) / 2);
+#pragma unroll
+                for (int e = 0; e < NU; ++e) p[e] = 0.0 - xs.u[e];
+            } else {
+                const int c = i / 2;
+                if (i >= 2) {
+                    double* p = rc + Lc.t_u(c);
+#pragma unroll
+                    for (int e = 0; e < NU; ++e) p[e] = 0.0 - xs.m[e];
+                }
+                if (c >= 1) {
+                    double* p = rc + Lc.off_v(c);
+#pragma unroll
+                    for (int e = 0; e < NU; ++e) p[e] = 0.0;
+                }
+                if (c < Lc.N) {
+                    double* pz = rc + Lc.off_z(c);
+                    double* pl = rc + Lc.off_l(c);
+#pragma unroll
+                    for (int e = 0; e < NZ; ++e) pz[e] = 0.0;
+#pragma unroll
+                    for (int e = 0; e < NU; ++e) pl[e] = 0.0;
+                }
+            }
+        }
     }
+}
+
+template <int NU, int NZ>
+static int dense_jacobi0_restrict_t(const tk_level* Lv, const double* b, double* y, double* rc,
+                                    cudaStream_t s) {
+    DView<NU, NZ> V(Lv);
+    const int rows = V.sl.r1 - V.sl.r0;
+    dense_rows<NU, NZ, D_JACOBI><<<grid_for(rows, 128, 1 << 20), 128, 0, s>>>(V, b, nullptr, y, 1.0, rc);
+    return check_launch("dense_rows (jacobi0 + restrict)");
 }
 
 // Serial block substitution (smoothers.py:79-109): one thread walks the time axis.
@@ -605,6 +647,19 @@ static int dense_launch_t(const tk_level* Lv, int op, const double* b, const dou
         case 4: return dense_launch_t<NU, 4>(Lv, op, b, x, y, omega, s);              \
         default: break;                                                               \
     }
+
+int dense_jacobi0_restrict(const tk_level* Lv, const double* b, double* y, double* rc,
+                           cudaStream_t s) {
+#define TK_DJR(NU, NZ) \
+    if (Lv->n_u == NU && Lv->n_z == NZ) return dense_jacobi0_restrict_t<NU, NZ>(Lv, b, y, rc, s);
+    TK_DJR(1, 1) TK_DJR(1, 2) TK_DJR(1, 3) TK_DJR(1, 4)
+    TK_DJR(2, 1) TK_DJR(2, 2) TK_DJR(2, 3) TK_DJR(2, 4)
+    TK_DJR(3, 1) TK_DJR(3, 2) TK_DJR(3, 3) TK_DJR(3, 4)
+    TK_DJR(4, 1) TK_DJR(4, 2) TK_DJR(4, 3) TK_DJR(4, 4)
+#undef TK_DJR
+    set_error("dense family supports 1<=n_u,n_z<=4 (got n_u=%d n_z=%d)", Lv->n_u, Lv->n_z);
+    return TK_ERR_UNSUPPORTED;
+}
 
 int dense_launch(const tk_level* Lv, int op, const double* b, const double* x, double* y,
                  double omega, cudaStream_t s) {

@@ -155,3 +155,34 @@ def test_fused_jacobi0_restrict_bitwise(n_u, n):
     bh, xh = b.cpu().numpy(), x.cpu().numpy()
     ro = O.restrict_kkt(O.Layout(n, n_u, n_u), O.Layout(n // 2, n_u, n_u), bh - oa.apply(xh))
     assert rel(rc.cpu().numpy(), ro) < 1e-10
+
+
+@pytest.mark.parametrize("n_controls", [1, 2])
+def test_fused_jacobi0_restrict_dense_bitwise(n_controls):
+    """DENSE (van der Pol) tk_jacobi0_restrict == zero-start sweep + restriction."""
+    import torch
+    import paper_2405_04808_b200 as P
+    from paper_2405_04808_b200 import device as dev
+    from paper_2405_04808_b200.multigrid import fused_jacobi0_ok
+    from paper_2405_04808_b200.smoothers import jacobi_sweeps
+    n = 64
+    grid = P.TimeGrid(5.0, n)
+    vp = P.build_vanderpol(P.VanDerPolConfig(n_controls=n_controls, u_init=(1.0, 0.0)), grid,
+                           with_targets=False)
+    rng = np.random.default_rng(4)
+    zc = 0.3 * rng.standard_normal((n, n_controls))
+    uv = P.forward_solve(vp, zc, grid).states
+    a = P.assemble_kkt(P.build_stage_blocks(vp, grid.dt, uv, uv, zc))
+    assert fused_jacobi0_ok(a, 1.0)
+    cdim = (n // 2) * (4 * 2 + n_controls)
+    b = dev.to_device(rng.standard_normal(a.dim))
+    x = dev.empty(a.dim)
+    rc = dev.to_device(np.full(cdim, np.nan))
+    dev.call("tk_jacobi0_restrict", a.lref, dev.P(b), 1.0, dev.P(x), dev.P(rc), dev.stream())
+    x2 = jacobi_sweeps(a, b, None, 1, 1.0)
+    rc2 = dev.empty(cdim)
+    dev.call("tk_residual_restrict_jacobi0", a.lref, dev.P(b), dev.P(x2), 1.0, dev.P(rc2),
+             dev.stream())
+    torch.cuda.synchronize()
+    assert torch.equal(x, x2)
+    assert torch.equal(rc, rc2)
