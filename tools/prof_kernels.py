@@ -28,6 +28,9 @@ work = dev.empty(a.dim)
 dev.call("tk_residual_restrict", a.lref, dev.P(b), dev.P(x1), dev.P(rc), dev.P(work), dev.stream())
 t.prolong_add(rc, x1)                             # prolong_rows_kernel
 dev.call("tk_residual_restrict_jacobi0", a.lref, dev.P(b), dev.P(x0), 1.0, dev.P(rc),
-         dev.stream())                            # restrict_jacobi0_kernel (x0 = D^-1 b)
+         dev.stream())                            # restrict_jacobi0_rows (x0 = D^-1 b)
+x2 = dev.empty(a.dim)
+dev.call("tk_jacobi0_restrict", a.lref, dev.P(b), 1.0, dev.P(x2), dev.P(rc),
+         dev.stream())                            # tri_rows_part<..., RJ>: sweep + restriction
 torch.cuda.synchronize()
 print("ok", s.describe())

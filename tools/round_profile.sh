@@ -11,7 +11,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   python tools/prof_vcycle.py 2 1 > gpurun_out/${tag}_launches.csv 2> gpurun_out/${tag}_launches.err; echo "ncu list rc=$?"
 PROF_GRAPH=1 timeout 600 ncu --profile-from-start off --graph-profiling graph --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   python tools/prof_vcycle.py 2 1 > gpurun_out/${tag}_launches_graph.csv 2> gpurun_out/${tag}_launches_graph.err; echo "ncu graph list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tri_apply|tri_rows_part|tri_resrestrict|prolong_rows|restrict_jacobi0" -s 1 -c 5 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tri_apply|tri_rows_part|tri_resrestrict|prolong_rows|restrict_jacobi0" -s 1 -c 6 \
   -o gpurun_out/${tag}_full python tools/prof_kernels.py 2 > gpurun_out/${tag}_full.log 2>&1; echo "ncu full rc=$?"
 python tools/ncu_summary.py gpurun_out/${tag}_launches.csv gpurun_out/${tag}_full.ncu-rep gpurun_out/${tag}_ncu > /dev/null 2>&1; echo "summary rc=$?"
 python tools/ncu_summary.py gpurun_out/${tag}_launches_graph.csv gpurun_out/${tag}_full.ncu-rep gpurun_out/${tag}_ncu_graph > /dev/null 2>&1; echo "graph summary rc=$?"
