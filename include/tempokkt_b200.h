@@ -111,6 +111,11 @@ typedef struct tk_level {
 
 #define TK_FLAG_ONTHEFLY 1
 #define TK_FLAG_RECROWS 2
+/* TK_FLAG_TOEPLITZ_W: the TRI weights Qm, Ql, Qz have constant diagonals
+ * (sub[1:] == sup[:-1] == s, diag == d; uniform P1 mass matrices), set by the
+ * host after checking; the partitioned row kernels then read one scalar per
+ * diagonal instead of per-node values (same values, bitwise same results). */
+#define TK_FLAG_TOEPLITZ_W 4
 
 /* --- library ------------------------------------------------------------ */
 const char* tk_version(void);

@@ -30,6 +30,7 @@ _i64 = C.c_int64
 
 TK_FLAG_ONTHEFLY = 1
 TK_FLAG_RECROWS = 2
+TK_FLAG_TOEPLITZ_W = 4
 
 
 class TkLevel(C.Structure):

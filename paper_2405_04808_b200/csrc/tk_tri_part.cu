@@ -284,7 +284,11 @@ extern "C" int tk_debug_part_prof(long long* out10) {
 // coupling): row 2c-1 writes -u_{2c} as the coarse mu_c, row 2c writes
 // -mu_{2c} as the coarse u_c and the zero v_c, z_{c+1}, lam_{c+1} of coarse
 // row c -- the separate restriction kernel and its re-read of y disappear.
-template <int W, int MODE, bool FULL, int CL, bool RJ>
+//
+// TOE (TK_FLAG_TOEPLITZ_W): the weights Qm, Ql, Qz have constant diagonals
+// (uniform P1 mass matrices), so each diagonal is one scalar per row instead
+// of per-node loads -- same values, same arithmetic, fewer loads/registers.
+template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE>
 __global__ void __launch_bounds__(32 * W, PartCta<W>::min_blocks())
 tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ x,
               double* __restrict__ y, double omega, const double* __restrict__ chain,
@@ -328,11 +332,26 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
 #endif
     const int64_t bs = V.sl.base;
     // constant weights at the chunk nodes (diagonal, super-diagonal)
+    // weight diagonal `part` (0 sub, 1 diag, 2 sup) at the chunk nodes
+    auto tw = [&](const double* Q, int part, bool on, double (&r)[NA]) {
+        if (TOE) {
+            const double v = on ? Q[part == 0 ? 1 : part * n] : 0.0;
+#pragma unroll
+            for (int k = 0; k < NA; ++k) r[k] = v;
+        } else {
+            ld4<FULL>(Q, part * n, j0, n, on, r);
+        }
+    };
+    // single node j of diagonal `part` (zero outside [0, n))
+    auto tw1 = [&](const double* Q, int part, int j) -> double {
+        if (TOE) return (j >= 0 && j < n) ? Q[part == 0 ? 1 : part * n] : 0.0;
+        return ld1(Q, part * n, j, n, true);
+    };
     double qzd[NA], qzs[NA], qzb[NA];
-    ld4<FULL>(Qz, n, j0, n, true, qzd);
-    ld4<FULL>(Qz, 2 * n, j0, n, true, qzs);
-    ld4<FULL>(Qz, 0, j0, n, true, qzb);
-    const double qzsL = ld1(Qz, 2 * n, jL, n, true), qzbR = ld1(Qz, 0, jR, n, true);
+    tw(Qz, 1, true, qzd);
+    tw(Qz, 2, true, qzs);
+    tw(Qz, 0, true, qzb);
+    const double qzsL = tw1(Qz, 2, jL), qzbR = tw1(Qz, 0, jR);
 
     if (kStage && V.sl.r0 + cid < V.sl.r1)
         stage_row<FULL, T>(SG, row_src<MODE>(V, x, chain, V.sl.r0 + cid), b, x,
@@ -461,12 +480,12 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 ld4<FULL>(C, 2 * n, j0, n, hc, cs);
                 ld4<FULL>(C, 0, j0, n, hc, cb);
                 const double csL = ld1(C, 2 * n, jL, n, hc), cbR = ld1(C, 0, jR, n, hc);
-                ld4<FULL>(Qv, n, j0, n, true, qvd);
-                ld4<FULL>(Qv, 2 * n, j0, n, true, qvs);
-                ld4<FULL>(Qv, 0, j0, n, true, qvb);
-                ld4<FULL>(Qu, n, j0, n, true, qud);
-                ld4<FULL>(Qu, 2 * n, j0, n, true, qus);
-                ld4<FULL>(Qu, 0, j0, n, true, qub);
+                tw(Qv, 1, true, qvd);
+                tw(Qv, 2, true, qvs);
+                tw(Qv, 0, true, qvb);
+                tw(Qu, 1, true, qud);
+                tw(Qu, 2, true, qus);
+                tw(Qu, 0, true, qub);
 #pragma unroll
                 for (int k = 0; k < NA; ++k) {
                     const int j = j0 + k;
@@ -502,9 +521,9 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             }
             // v, the mu part without C^T lam, C v into the lam row
             double qvd[NA], qvs[NA], qvb[NA], cd[NA], cs[NA], cb[NA];
-            ld4<FULL>(Qv, n, j0, n, has_vm, qvd);
-            ld4<FULL>(Qv, 2 * n, j0, n, has_vm, qvs);
-            ld4<FULL>(Qv, 0, j0, n, has_vm, qvb);
+            tw(Qv, 1, has_vm, qvd);
+            tw(Qv, 2, has_vm, qvs);
+            tw(Qv, 0, has_vm, qvb);
             ld4<FULL>(C, n, j0, n, hc, cd);
             ld4<FULL>(C, 2 * n, j0, n, hc, cs);
             ld4<FULL>(C, 0, j0, n, hc, cb);
@@ -562,9 +581,9 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         // U_k = [[Qu_{k,k+1}, K_{k+1,k}], [K_{k,k+1}, -k^2 Qz_{k,k+1}]]; the
         // scalar system has diagonal Qz_kk and coupling Qz_{k,k+1}.
         double qud[NA], qus[NA];
-        ld4<FULL>(Qu, n, j0, n, true, qud);
-        ld4<FULL>(Qu, 2 * n, j0, n, true, qus);
-        const double qusL = ld1(Qu, 2 * n, jL, n, true);
+        tw(Qu, 1, true, qud);
+        tw(Qu, 2, true, qus);
+        const double qusL = tw1(Qu, 2, jL);
         auto Dk = [&](int k, double& a, double& bb, double& c) {
             const bool in = j0 + k < n;
             a = in ? qud[k] : 1.0;
@@ -912,12 +931,15 @@ int part_nodes_per_lane(int n) { return part_warps(n) ? kChunk : 0; }
 
 template <int W, int MODE, bool FULL, int CL, bool RJ = false>
 static int part_launch_t(const tk_level* Lv, const double* b, const double* x, double* y,
-                         double omega, const double* chain, cudaStream_t s, double* rc = nullptr) {
+                         double omega, const double* chain, cudaStream_t s, double* rc = nullptr);
+template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE>
+static int part_launch_tt(const tk_level* Lv, const double* b, const double* x, double* y,
+                          double omega, const double* chain, cudaStream_t s, double* rc) {
     using Cf = PartCta<W>;
     static int per_sm = 0;
     static int nsm = 0;
     const int64_t smem = Cf::smem_bytes();
-    auto kern = tri_rows_part<W, MODE, FULL, CL, RJ>;
+    auto kern = tri_rows_part<W, MODE, FULL, CL, RJ, TOE>;
     if (!per_sm) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -952,6 +974,16 @@ static int part_launch_t(const tk_level* Lv, const double* b, const double* x, d
     cfg.stream = s; cfg.attrs = at; cfg.numAttrs = 1;
     return cuda_status(cudaLaunchKernelEx(&cfg, kern, V, b, x, y, omega, chain, rc),
                        "tri_rows_part (cluster)");
+}
+
+// TOE only for FULL rows (every chunk inside the level, so the masked
+// boundary entries of the stored diagonals are never needed)
+template <int W, int MODE, bool FULL, int CL, bool RJ>
+static int part_launch_t(const tk_level* Lv, const double* b, const double* x, double* y,
+                         double omega, const double* chain, cudaStream_t s, double* rc) {
+    if (FULL && (Lv->flags & TK_FLAG_TOEPLITZ_W))
+        return part_launch_tt<W, MODE, FULL, CL, RJ, FULL>(Lv, b, x, y, omega, chain, s, rc);
+    return part_launch_tt<W, MODE, FULL, CL, RJ, false>(Lv, b, x, y, omega, chain, s, rc);
 }
 
 // mode 0: rows (jacobi / D^{-1} b), 1/2: substitution pass 3 forward/backward

@@ -298,6 +298,16 @@ def stage_blocks_from_arrays(k, c, b, q_u, q_v, q_z) -> StageBlocks:
     return StageBlocks(fam, n, nu, nz, dev.to_device(kd), dev.to_device(cd), None, **w)
 
 
+def _toeplitz(q) -> bool:
+    """TRI weight [3][n] (sub, diag, sup) with constant diagonals."""
+    w = (q.detach().cpu().numpy() if isinstance(q, torch.Tensor) else np.asarray(q)).reshape(3, -1)
+    if w.shape[1] < 2:
+        return False
+    sub, d, sup = w
+    s = sup[0]
+    return bool((d == d[0]).all() and (sup[:-1] == s).all() and (sub[1:] == s).all())
+
+
 class BlockTriKKT:
     """Symmetric block-tridiagonal augmented operator on the device
     (kkt.py:194-276).  ``apply``/``residual``/``apply_diag`` launch the
@@ -320,6 +330,10 @@ class BlockTriKKT:
             Qz_inv=dev.P(s.Qz_inv), kappa=s.kappa, qz_cr=dev.P(s.qz_cr),
             row0=self.row0, row1=0 if not self.is_slab else self.row1,
             halo_u=dev.P(self.halo_u), halo_mu=dev.P(self.halo_mu), qz_w=dev.P(s.qz_w))
+        if s.family == FAMILY_TRI and os.environ.get("TK_TOEPLITZ", "1") != "0" and \
+                all(_toeplitz(q) for q in (s.Qm, s.Ql, s.Qz)):
+            # uniform-mesh mass matrices: one scalar per weight diagonal in the row kernels
+            self.level.flags |= _lib.TK_FLAG_TOEPLITZ_W
         self.lref = C.byref(self.level)
         self._fac = None
         self._scratch = None

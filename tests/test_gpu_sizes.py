@@ -186,3 +186,36 @@ def test_fused_jacobi0_restrict_dense_bitwise(n_controls):
     torch.cuda.synchronize()
     assert torch.equal(x, x2)
     assert torch.equal(rc, rc2)
+
+
+@pytest.mark.parametrize("n_u", [64, 128, 512, 1024, 1536])
+def test_toeplitz_weights_bitwise(n_u):
+    """TK_FLAG_TOEPLITZ_W (scalar weight diagonals in the partitioned row
+    kernels) gives the same sweeps / solves / fused pre-smoothing as the
+    per-node weight loads (same values; the compiler may contract the
+    products into FMAs differently, so agreement is to rounding, 1e-14); the
+    uniform Burgers mesh sets the flag."""
+    import torch
+    from paper_2405_04808_b200 import _lib, device as dev
+    from paper_2405_04808_b200.smoothers import jacobi_sweeps
+    P, O, p, op, grid, u, v, z, rng = _case(n_u, n=16)
+    st = P.build_stage_blocks(p, grid.dt, u, v, z)
+    a = P.assemble_kkt(st)
+    assert a.level.flags & _lib.TK_FLAG_TOEPLITZ_W
+    b = dev.to_device(rng.standard_normal(a.dim))
+    x = dev.to_device(rng.standard_normal(a.dim))
+    rc = dev.empty((16 // 2) * 5 * n_u)
+
+    def run():
+        y1 = jacobi_sweeps(a, b, x, 1, 1.0)
+        y2 = P.DiagonalSolver(a).solve_all(b)
+        y3 = dev.empty(a.dim)
+        dev.call("tk_jacobi0_restrict", a.lref, dev.P(b), 1.0, dev.P(y3), dev.P(rc), dev.stream())
+        torch.cuda.synchronize()
+        return y1.clone(), y2.clone(), y3.clone(), rc.clone()
+
+    t = run()
+    a.level.flags &= ~_lib.TK_FLAG_TOEPLITZ_W
+    g = run()
+    for p_, q_ in zip(t, g):
+        assert rel(p_.cpu().numpy(), q_.cpu().numpy()) < 1e-14
