@@ -42,12 +42,12 @@ _NCU_KERNELS = {
                          "tri_rows_rec_sgsb"),
 }
 _NCU_FULL = {
-    "tk_jacobi_sweep": "tri_rows_part",
+    "tk_jacobi_sweep": "tri_rows_part<4, 0, 1, 1, 0",
     "tk_residual_restrict": "tri_resrestrict",
     "tk_prolong_add": "prolong_rows_kernel",
     "tk_kkt_apply": "tri_apply<0",
     "tk_residual_restrict_jacobi0": "restrict_jacobi0",
-    "tk_jacobi0_restrict": "tri_rows_part",
+    "tk_jacobi0_restrict": "tri_rows_part<4, 0, 1, 1, 1",
 }
 
 
