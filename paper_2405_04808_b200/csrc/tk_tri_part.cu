@@ -45,7 +45,7 @@ constexpr int kChunk = TK_PART_CHUNK;
 #endif
 constexpr bool kStage = TK_PART_STAGE != 0;
 #ifndef TK_PART_EARLY
-#define TK_PART_EARLY 1          // issue the output's loads before the interface solve
+#define TK_PART_EARLY 0          // 1: issue the output's loads before the interface solve (better while the kernel spilled)
 #endif
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kPX = 19;          // symmetric PCR: published doubles per row
