@@ -38,7 +38,7 @@ namespace {
 #endif
 constexpr int kChunk = TK_PART_CHUNK;
 #ifndef TK_PART_STAGE
-#define TK_PART_STAGE 1          // cp.async staging of the next row's vectors
+#define TK_PART_STAGE 0          // 1: cp.async staging of the next row's vectors (0: L2 bulk prefetch + a large L1)
 #endif
 #ifndef TK_PART_MINB
 #define TK_PART_MINB 2           // CTAs per SM the W=4 build is register-limited to
@@ -942,8 +942,16 @@ static int part_launch_tt(const tk_level* Lv, const double* b, const double* x, 
     auto kern = tri_rows_part<W, MODE, FULL, CL, RJ, TOE>;
     if (!per_sm) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared);
+        // shared memory only as large as the resident CTAs need: the rest of the
+        // 256 KB unified array stays L1 (stage data, weights and vectors are
+        // read through it)
+        int carve = cudaSharedmemCarveoutMaxShared;
+        if (!kStage) {
+            const int64_t need = (int64_t)Cf::min_blocks() * (smem + 1024);
+            carve = (int)((100 * need + 228 * 1024 - 1) / (228 * 1024)) + 1;
+            if (carve > 100) carve = 100;
+        }
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
