@@ -44,6 +44,9 @@ constexpr int kChunk = TK_PART_CHUNK;
 #define TK_PART_MINB 2           // CTAs per SM the W=4 build is register-limited to
 #endif
 constexpr bool kStage = TK_PART_STAGE != 0;
+#ifndef TK_PART_PFD
+#define TK_PART_PFD 1            // L2 bulk prefetch distance (rows of this CTA ahead)
+#endif
 #ifndef TK_PART_EARLY
 #define TK_PART_EARLY 0          // 1: issue the output's loads before the interface solve (better while the kernel spilled)
 #endif
@@ -359,8 +362,8 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
     for (int i = V.sl.r0 + cid; i < V.sl.r1; i += ncl) {
         if (kStage) cpa_wait();
         const bool has_vm = i >= 1, has_uzl = i < L.N;
-        if (gt == 0 && i + ncl < V.sl.r1) {   // next row's stage data -> L2
-            const int i2 = i + ncl;
+        if (gt == 0 && i + TK_PART_PFD * ncl < V.sl.r1) {   // a later row's data -> L2
+            const int i2 = i + TK_PART_PFD * ncl;
             if (!kStage) {
                 const int64_t q0 = L.start(i2) - bs;
                 const int64_t q1 = (i2 == L.N ? L.dim() : L.start(i2 + 1)) - bs;
