@@ -248,6 +248,11 @@ int tk_host_device_ptr(void* host, void** dptr);
  * the tk_dot / tk_axpy / tk_nrm2 / tk_scale_into sequence. */
 int tk_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ld, double* w, double* h,
                    double* work, void* stream);
+/* For n*8 >= 16 MB, tk_arnoldi_mgs marks w L2-persisting (access-policy
+ * window, persisting carve-out set to the device maximum on first use;
+ * TK_ARNOLDI_PERSIST=0 disables it).  tk_l2_persist_reset() returns those
+ * lines to normal status; call it after synchronising, at the end of a solve. */
+int tk_l2_persist_reset(void);
 
 /* --- CUDA-graph V-cycle with a device-side coarse GMRES ------------------- */
 /* Replaces the host-driven loop of multigrid.py:245-260 (coarse_solve ->

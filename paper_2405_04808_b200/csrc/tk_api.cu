@@ -45,6 +45,7 @@ int dot_launch(int64_t, const double*, const double*, double*, double*, int, cud
 int vec_launch(int, int64_t, double, const double*, double*, cudaStream_t);
 int gemv_t_add_launch(int64_t, int, const double*, int64_t, const double*, double*, cudaStream_t);
 int arnoldi_launch(int64_t, int, double*, int64_t, double*, double*, double*, cudaStream_t);
+int l2_persist_reset();
 int copy_small_launch(int64_t, const double*, double*, cudaStream_t);
 int restrict_jacobi0_launch(int, int, int, int, int, const double*, const double*, const double*,
                             const double*, double, double*, cudaStream_t);
@@ -347,6 +348,8 @@ int tk_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ld, double* w, doubl
                  "tk_arnoldi_mgs: bad arguments");
     return arnoldi_launch(n, j, V, ld, w, h, work, as_stream(stream));
 }
+
+int tk_l2_persist_reset(void) { return l2_persist_reset(); }
 
 int tk_gemv_t_add(int64_t n, int32_t k, const double* V, int64_t ld, const double* c, double* x,
                   void* stream) {

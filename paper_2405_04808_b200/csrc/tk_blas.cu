@@ -3,6 +3,7 @@
 // summing a fixed grid-stride slice, then one CTA summing the partials in a
 // fixed tree order, so repeated solves are bitwise reproducible.
 #include <cooperative_groups.h>
+#include <stdlib.h>
 
 #include "tk_common.cuh"
 
@@ -196,11 +197,67 @@ arnoldi_mgs_kernel(int64_t n, int j, double* __restrict__ V, int64_t ld, double*
     }
 }
 
+// w is re-read and re-written by every MGS pass while each basis vector is
+// streamed once or twice: when w is too large to stay in L2 by itself next to
+// the streamed basis (tens of MB), the launch marks it L2-persisting
+// (access-policy window; the persisting carve-out is set once to the device
+// maximum).  TK_ARNOLDI_PERSIST=0 disables it.
+static bool g_persist_used = false;
+
+// return the persisting lines to normal status (host-synchronous: call after
+// the stream that used the window has been synchronised, e.g. at the end of
+// a Krylov solve) so later kernels see the whole L2
+int l2_persist_reset() {
+    if (!g_persist_used) return TK_OK;
+    g_persist_used = false;
+    return cuda_status(cudaCtxResetPersistingL2Cache(), "cudaCtxResetPersistingL2Cache");
+}
+
+static size_t persist_bytes() {
+    static int64_t cap = -1;
+    if (cap < 0) {
+        cap = 0;
+        const char* e = getenv("TK_ARNOLDI_PERSIST");
+        if (e && e[0] == '0') return 0;
+        int dev = 0, mx = 0, win = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        if (mx > 0 && win > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mx) == cudaSuccess)
+            cap = mx < win ? mx : win;
+        cudaGetLastError();
+    }
+    return (size_t)cap;
+}
+
 int arnoldi_launch(int64_t n, int j, double* V, int64_t ld, double* w, double* h, double* work,
                    cudaStream_t s) {
     const int* jdev = nullptr;
     int64_t hstride = 0;
     double* vcopy = nullptr;
+    const size_t wb = (size_t)n * 8;
+    const size_t cap = wb >= ((size_t)16 << 20) ? persist_bytes() : 0;
+    if (cap > 0) {
+        g_persist_used = true;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[1].val.accessPolicyWindow.base_ptr = (void*)w;
+        at[1].val.accessPolicyWindow.num_bytes = wb < cap ? wb : cap;
+        at[1].val.accessPolicyWindow.hitRatio = wb <= cap ? 1.0f : (float)cap / (float)wb;
+        at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.gridDim = dim3(kReduceBlocks);
+        cfg.blockDim = dim3(kReduceThreads);
+        cfg.stream = s;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        return cuda_status(cudaLaunchKernelEx(&cfg, arnoldi_mgs_kernel, n, j, V, ld, w, h, work, jdev,
+                                              hstride, vcopy),
+                           "arnoldi_mgs_kernel (persisting w)");
+    }
     void* args[] = {(void*)&n, (void*)&j,    (void*)&V,       (void*)&ld,   (void*)&w,
                     (void*)&h, (void*)&work, (void*)&jdev, (void*)&hstride, (void*)&vcopy};
     const cudaError_t e = cudaLaunchCooperativeKernel((const void*)arnoldi_mgs_kernel,

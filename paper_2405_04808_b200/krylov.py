@@ -321,6 +321,9 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
     if x_norm is None:                    # no cycle ran (max_iters == 0)
         x_norm = ops.nrm2(x)
         true_norm = ops.nrm2(_residual(op, b, x))
+    # the Arnoldi steps of a large basis held w L2-persisting (tk_arnoldi_mgs):
+    # give the lines back now that the solve has synchronised
+    _lib.check(_lib.load().tk_l2_persist_reset(), "tk_l2_persist_reset")
     if not math.isfinite(x_norm):
         raise NonFiniteValue("non-finite solution vector")
     # ||b - A x|| of the final x: the deterministic kernels give the bits the
