@@ -225,6 +225,15 @@ int tk_axpy(int64_t n, double a, const double* x, double* y, void* stream);
 int tk_scale_into(int64_t n, double a, const double* x, double* y, void* stream);
 /* y = b - y  (used for r = b - A x when A x is already in y) */
 int tk_rsub(int64_t n, const double* b, double* y, void* stream);
+/* y += sign * a[0] * x with the scalar a in device memory (the sharded MGS:
+ * `w -= h_i V_i` with h_i an allreduced dot that stays on the device). */
+int tk_axpy_dev(int64_t n, const double* a, double sign, const double* x, double* y,
+                void* stream);
+/* nrm[0] = sqrt(sq[0]) (nrm may be NULL) and, when it is nonzero and y is
+ * given, y = x / nrm[0] (krylov.py:150-163 `hj1 = norm2(w)`, `V[j+1] = w / hj1`
+ * with the squared norm allreduced on the device). */
+int tk_sqrt_div(int64_t n, const double* sq, double* nrm, const double* x, double* y,
+                void* stream);
 /* x += V^T c: V is k rows of length n with leading dimension ld; c on device */
 int tk_gemv_t_add(int64_t n, int32_t k, const double* V, int64_t ld, const double* c,
                   double* x, void* stream);
@@ -253,6 +262,12 @@ int tk_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ld, double* w, doubl
  * TK_ARNOLDI_PERSIST=0 disables it).  tk_l2_persist_reset() returns those
  * lines to normal status; call it after synchronising, at the end of a solve. */
 int tk_l2_persist_reset(void);
+/* 1 when tk_arnoldi_mgs / tk_gm_arnoldi can run on the current device: their
+ * fixed cooperative grid (592 CTAs of 256 threads) must be co-resident, which
+ * a MIG slice or an SM-limited MPS client may not allow.  When 0 they return
+ * TK_ERR_UNSUPPORTED and the host runs the unfused tk_dot / tk_axpy / tk_nrm2
+ * / tk_scale_into sequence (same reductions, bitwise equal). */
+int32_t tk_arnoldi_supported(void);
 
 /* --- CUDA-graph V-cycle with a device-side coarse GMRES ------------------- */
 /* Replaces the host-driven loop of multigrid.py:245-260 (coarse_solve ->
@@ -298,6 +313,21 @@ int tk_stage_vanderpol(int32_t n_steps, double dt, double theta, double mu, int3
 int tk_stage_burgers(int32_t n_steps, int32_t n_u, double dt, double theta, double nu,
                      const double* u0, const double* u, const double* v, double* K, double* C,
                      void* stream);
+
+/* --- setup: singularity checks (kkt.py:323-389, 496-543) ------------------- */
+/* bad[s] = 1 when stage K_s fails the K half of Theorem 1 (check_theorem1
+ * kkt.py:530-543): partial-pivoting LU (linalg.lu_factor linalg.py:75-103)
+ * meets a pivot below pivot_floor*max|K_s| (reference PIVOT_FLOOR = 1e-14,
+ * linalg.py:38) or K_s holds a non-finite entry.  One flag per local stage
+ * of the level (slab: stages [row0, min(row1, N))).  The weight (SPD) half of
+ * the theorem is checked by the host on the time-constant weights. */
+int tk_check_k(const tk_level* L, double pivot_floor, int32_t* bad, void* stream);
+/* bad[i] = 1 (i = 0..N) when the diagonal block of block row i, assembled as
+ * assemble_kkt (kkt.py:279-320), fails the same partial-pivoting LU test --
+ * where DiagonalSolver (kkt.py:347-368) raises SingularBlock(i).  Whole DENSE
+ * levels (TRI blocks are quasi-definite once the weights are SPD, which the
+ * host checks); TK_ERR_UNSUPPORTED otherwise. */
+int tk_check_blocks(const tk_level* L, double pivot_floor, int32_t* bad, void* stream);
 
 /* --- setup: host routines (CPU) ------------------------------------------- */
 /* theta-method forward march with Newton (timedisc.py:152-191), host memory. */

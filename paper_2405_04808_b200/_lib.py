@@ -83,10 +83,13 @@ _SIGS = {
     "tk_axpy": (C.c_int, [_i64, _d, _p, _p, _p]),
     "tk_scale_into": (C.c_int, [_i64, _d, _p, _p, _p]),
     "tk_rsub": (C.c_int, [_i64, _p, _p, _p]),
+    "tk_axpy_dev": (C.c_int, [_i64, _p, _d, _p, _p, _p]),
+    "tk_sqrt_div": (C.c_int, [_i64, _p, _p, _p, _p, _p]),
     "tk_gemv_t_add": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _p]),
     "tk_arnoldi_mgs": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _p, _p]),
     "tk_copy_kernel": (C.c_int, [_i64, _p, _p, _p]),
     "tk_l2_persist_reset": (C.c_int, []),
+    "tk_arnoldi_supported": (_i32, []),
     "tk_graph_capture_begin": (C.c_int, [_p]),
     "tk_graph_cond_create": (C.c_int, [_p, C.POINTER(C.c_uint64)]),
     "tk_graph_while_begin": (C.c_int, [_p, _p, C.c_uint64]),
@@ -107,6 +110,8 @@ _SIGS = {
     "tk_stage_burgers": (C.c_int, [_i32, _i32, _d, _d, _d, _p, _p, _p, _p, _p, _p]),
     "tk_forward_vanderpol_host": (C.c_int, [_i32, _d, _d, _d, _i32, _p, _p, _d, _p]),
     "tk_forward_burgers_host": (C.c_int, [_i32, _i32, _d, _d, _d, _p, _p, _d, _p]),
+    "tk_check_k": (C.c_int, [C.POINTER(TkLevel), _d, _p, _p]),
+    "tk_check_blocks": (C.c_int, [C.POINTER(TkLevel), _d, _p, _p]),
     "tk_cr_scalar_factor": (C.c_int, [_i32, _p, _p]),
     "tk_cr_scalar_solve_host": (C.c_int, [_i32, _p, _p, _p]),
 }

@@ -44,8 +44,11 @@ int64_t reduce_work_len();
 int dot_launch(int64_t, const double*, const double*, double*, double*, int, cudaStream_t);
 int vec_launch(int, int64_t, double, const double*, double*, cudaStream_t);
 int gemv_t_add_launch(int64_t, int, const double*, int64_t, const double*, double*, cudaStream_t);
+int axpy_dev_launch(int64_t, const double*, double, const double*, double*, cudaStream_t);
+int sqrt_div_launch(int64_t, const double*, double*, const double*, double*, cudaStream_t);
 int arnoldi_launch(int64_t, int, double*, int64_t, double*, double*, double*, cudaStream_t);
 int l2_persist_reset();
+int arnoldi_supported();
 int copy_small_launch(int64_t, const double*, double*, cudaStream_t);
 int restrict_jacobi0_launch(int, int, int, int, int, const double*, const double*, const double*,
                             const double*, double, double*, cudaStream_t);
@@ -53,6 +56,8 @@ int stage_vdp_launch(int, double, double, double, int, const double*, const doub
                      const double*, const double*, double*, double*, double*, cudaStream_t);
 int stage_burgers_launch(int, int, double, double, double, const double*, const double*,
                          const double*, double*, double*, cudaStream_t);
+int check_k_launch(const tk_level*, double, int32_t*, cudaStream_t);
+int check_blocks_launch(const tk_level*, double, int32_t*, cudaStream_t);
 
 static int check_level(const tk_level* L) {
     if (!L) { set_error("null level"); return TK_ERR_ARG; }
@@ -316,6 +321,18 @@ int tk_scale_into(int64_t n, double a, const double* x, double* y, void* stream)
     return vec_launch(1, n, a, x, y, as_stream(stream));
 }
 
+int tk_axpy_dev(int64_t n, const double* a, double sign, const double* x, double* y,
+                void* stream) {
+    TK_CHECK_ARG(a && x && y && n >= 0, "tk_axpy_dev: bad arguments");
+    return axpy_dev_launch(n, a, sign, x, y, as_stream(stream));
+}
+
+int tk_sqrt_div(int64_t n, const double* sq, double* nrm, const double* x, double* y,
+                void* stream) {
+    TK_CHECK_ARG(sq && n >= 0 && (!y || x), "tk_sqrt_div: bad arguments");
+    return sqrt_div_launch(n, sq, nrm, x, y, as_stream(stream));
+}
+
 int tk_rsub(int64_t n, const double* b, double* y, void* stream) {
     TK_CHECK_ARG(b && y, "tk_rsub: null vector");
     return vec_launch(2, n, 0.0, b, y, as_stream(stream));
@@ -349,6 +366,8 @@ int tk_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ld, double* w, doubl
     return arnoldi_launch(n, j, V, ld, w, h, work, as_stream(stream));
 }
 
+int32_t tk_arnoldi_supported(void) { return arnoldi_supported() ? 1 : 0; }
+
 int tk_l2_persist_reset(void) { return l2_persist_reset(); }
 
 int tk_gemv_t_add(int64_t n, int32_t k, const double* V, int64_t ld, const double* c, double* x,
@@ -374,6 +393,24 @@ int tk_stage_burgers(int32_t n_steps, int32_t n_u, double dt, double theta, doub
     TK_CHECK_ARG(n_steps >= 1 && n_u >= 2 && u0 && u && v && K && C,
                  "tk_stage_burgers: bad arguments");
     return stage_burgers_launch(n_steps, n_u, dt, theta, nu, u0, u, v, K, C, as_stream(stream));
+}
+
+int tk_check_k(const tk_level* L, double pivot_floor, int32_t* bad, void* stream) {
+    int rc = check_level(L);
+    if (rc != TK_OK) return rc;
+    TK_CHECK_ARG(bad && pivot_floor >= 0.0, "tk_check_k: bad arguments");
+    return check_k_launch(L, pivot_floor, bad, as_stream(stream));
+}
+
+int tk_check_blocks(const tk_level* L, double pivot_floor, int32_t* bad, void* stream) {
+    int rc = check_level(L);
+    if (rc != TK_OK) return rc;
+    TK_CHECK_ARG(bad && pivot_floor >= 0.0, "tk_check_blocks: bad arguments");
+    if (L->family != TK_FAMILY_DENSE || L->row0 != 0 || L->row1 != 0) {
+        set_error("tk_check_blocks: whole DENSE levels only");
+        return TK_ERR_UNSUPPORTED;
+    }
+    return check_blocks_launch(L, pivot_floor, bad, as_stream(stream));
 }
 
 }  // extern "C"

@@ -73,6 +73,26 @@ __global__ void rsub_kernel(int64_t n, const double* __restrict__ b, double* __r
         y[k] = b[k] - y[k];
 }
 
+// Krylov updates whose scalar lives in device memory (the sharded (F)GMRES:
+// the scalar is an NCCL-allreduced dot that never visits the host).
+__global__ void axpy_dev_kernel(int64_t n, const double* __restrict__ a, double sign,
+                                const double* __restrict__ x, double* __restrict__ y) {
+    const double c = sign * a[0];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += stride)
+        y[k] = fma(c, x[k], y[k]);
+}
+
+__global__ void sqrt_div_kernel(int64_t n, const double* __restrict__ sq, double* __restrict__ nrm,
+                                const double* __restrict__ x, double* __restrict__ y) {
+    const double s = sqrt(sq[0]);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && nrm) nrm[0] = s;
+    if (s == 0.0 || !y) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += stride)
+        y[k] = x[k] / s;
+}
+
 __global__ void gemv_t_add_kernel(int64_t n, int kk, const double* __restrict__ V, int64_t ld,
                                   const double* __restrict__ c, double* __restrict__ x) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -213,21 +233,51 @@ int l2_persist_reset() {
     return cuda_status(cudaCtxResetPersistingL2Cache(), "cudaCtxResetPersistingL2Cache");
 }
 
-static size_t persist_bytes() {
-    static int64_t cap = -1;
-    if (cap < 0) {
-        cap = 0;
+// Persisting-L2 budget of the current device: the window size and the
+// persisting carve-out (set to the device maximum on first use), per device.
+struct PersistCap {
+    int64_t carve = -1;   // bytes of persisting L2 (0: unavailable / disabled)
+    int64_t window = 0;   // max access-policy window
+};
+static PersistCap g_persist[64];
+
+static PersistCap persist_cap() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    PersistCap& c = g_persist[dev & 63];
+    if (c.carve < 0) {
+        c.carve = 0;
         const char* e = getenv("TK_ARNOLDI_PERSIST");
-        if (e && e[0] == '0') return 0;
-        int dev = 0, mx = 0, win = 0;
-        cudaGetDevice(&dev);
+        if (e && e[0] == '0') return c;
+        int mx = 0, win = 0;
         cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
         cudaDeviceGetAttribute(&win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-        if (mx > 0 && win > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mx) == cudaSuccess)
-            cap = mx < win ? mx : win;
+        if (mx > 0 && win > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mx) == cudaSuccess) {
+            c.carve = mx;
+            c.window = win;
+        }
         cudaGetLastError();
     }
-    return (size_t)cap;
+    return c;
+}
+
+// Whether the fixed cooperative grid of the Arnoldi kernel is co-resident on
+// the current device (not on a MIG slice / SM-limited MPS client / smaller
+// part): checked once per device; the host falls back to the unfused kernels.
+static int g_coop_ok[64];
+int arnoldi_supported() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& ok = g_coop_ok[dev & 63];
+    if (ok == 0) {
+        int sms = 0, per = 0, coop = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, arnoldi_mgs_kernel, kReduceThreads, 0);
+        cudaGetLastError();
+        ok = (coop && (int64_t)per * sms >= kReduceBlocks) ? 1 : -1;
+    }
+    return ok > 0;
 }
 
 int arnoldi_launch(int64_t n, int j, double* V, int64_t ld, double* w, double* h, double* work,
@@ -235,9 +285,18 @@ int arnoldi_launch(int64_t n, int j, double* V, int64_t ld, double* w, double* h
     const int* jdev = nullptr;
     int64_t hstride = 0;
     double* vcopy = nullptr;
+    if (!arnoldi_supported()) {
+        set_error("tk_arnoldi_mgs: the cooperative grid of %d CTAs is not co-resident on this device",
+                  kReduceBlocks);
+        return TK_ERR_UNSUPPORTED;
+    }
     const size_t wb = (size_t)n * 8;
-    const size_t cap = wb >= ((size_t)16 << 20) ? persist_bytes() : 0;
-    if (cap > 0) {
+    const PersistCap pc = wb >= ((size_t)16 << 20) ? persist_cap() : PersistCap{0, 0};
+    if (pc.carve > 0) {
+        // window over (the first window-size bytes of) w; the persisting
+        // carve-out holds carve bytes of it
+        const size_t nb = wb < (size_t)pc.window ? wb : (size_t)pc.window;
+        const float hit = nb <= (size_t)pc.carve ? 1.0f : (float)pc.carve / (float)nb;
         g_persist_used = true;
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[2];
@@ -245,8 +304,8 @@ int arnoldi_launch(int64_t n, int j, double* V, int64_t ld, double* w, double* h
         at[0].val.cooperative = 1;
         at[1].id = cudaLaunchAttributeAccessPolicyWindow;
         at[1].val.accessPolicyWindow.base_ptr = (void*)w;
-        at[1].val.accessPolicyWindow.num_bytes = wb < cap ? wb : cap;
-        at[1].val.accessPolicyWindow.hitRatio = wb <= cap ? 1.0f : (float)cap / (float)wb;
+        at[1].val.accessPolicyWindow.num_bytes = nb;
+        at[1].val.accessPolicyWindow.hitRatio = hit;
         at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cfg.gridDim = dim3(kReduceBlocks);
@@ -270,6 +329,10 @@ int arnoldi_launch(int64_t n, int j, double* V, int64_t ld, double* w, double* h
 // basis vector also copied to vcopy (the next step's preconditioner input)
 int arnoldi_dev_launch(int64_t n, const int* jdev, double* V, int64_t ld, double* w, double* H,
                        int64_t hstride, double* vcopy, double* work, cudaStream_t s) {
+    if (!arnoldi_supported()) {
+        set_error("tk_gm_arnoldi: the cooperative grid is not co-resident on this device");
+        return TK_ERR_UNSUPPORTED;
+    }
     int j = 0;
     void* args[] = {(void*)&n, (void*)&j,    (void*)&V,    (void*)&ld,      (void*)&w,
                     (void*)&H, (void*)&work, (void*)&jdev, (void*)&hstride, (void*)&vcopy};
@@ -311,6 +374,20 @@ int vec_launch(int op, int64_t n, double a, const double* x, double* y, cudaStre
         default: return TK_ERR_ARG;
     }
     return check_launch("vec");
+}
+
+int axpy_dev_launch(int64_t n, const double* a, double sign, const double* x, double* y,
+                    cudaStream_t s) {
+    const int th = 256;
+    axpy_dev_kernel<<<grid_for(n, th, 148 * 16), th, 0, s>>>(n, a, sign, x, y);
+    return check_launch("axpy_dev");
+}
+
+int sqrt_div_launch(int64_t n, const double* sq, double* nrm, const double* x, double* y,
+                    cudaStream_t s) {
+    const int th = 256;
+    sqrt_div_kernel<<<grid_for(n > 0 ? n : 1, th, 148 * 16), th, 0, s>>>(n, sq, nrm, x, y);
+    return check_launch("sqrt_div");
 }
 
 int gemv_t_add_launch(int64_t n, int k, const double* V, int64_t ld, const double* c, double* x,

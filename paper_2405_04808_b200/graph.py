@@ -63,6 +63,9 @@ def supported(h) -> bool:
     """Graph replay covers single-GPU V-cycles with at least two levels."""
     if not ENABLED or h.n_levels < 2 or h.cycle_kind != "v":
         return False
+    from .krylov import fused_arnoldi_ok
+    if not fused_arnoldi_ok():         # the device GMRES uses the cooperative Arnoldi step
+        return False
     return not any(lv.kkt.is_slab for lv in h.levels)
 
 

@@ -20,6 +20,7 @@ Anything else raises :class:`UnsupportedStructure` -- there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import os
 from dataclasses import dataclass, field
 from typing import Optional
@@ -29,12 +30,13 @@ import torch
 
 from . import _lib
 from . import device as dev
-from .errors import DimensionMismatch, UnsupportedStructure
+from .errors import DimensionMismatch, SingularBlock, UnsupportedStructure
 from .timedisc import ProblemSpec, stage_jacobians, stage_weights
 
 FAMILY_DENSE = _lib.FAMILY_DENSE
 FAMILY_TRI = _lib.FAMILY_TRI
 MAX_DENSE = 4
+PIVOT_FLOOR = 1e-14            # linalg.py:38
 
 
 class KktLayout:
@@ -97,6 +99,17 @@ def _tri_diags(a: np.ndarray) -> np.ndarray:
     return out
 
 
+def _tri_dense(d: np.ndarray) -> np.ndarray:
+    """(N, 3, n) (sub, diag, sup) diagonals -> (N, n, n) dense matrices."""
+    N, _, n = d.shape
+    out = np.zeros((N, n, n))
+    i = np.arange(n)
+    out[:, i, i] = d[:, 1]
+    out[:, i[1:], i[:-1]] = d[:, 0, 1:]
+    out[:, i[:-1], i[1:]] = d[:, 2, :-1]
+    return out
+
+
 def _is_tridiagonal(a: np.ndarray) -> bool:
     return not (np.triu(a, 2).any() or np.tril(a, -2).any())
 
@@ -133,9 +146,76 @@ class StageBlocks:
     row0: int = 0
     row1: int = 0
 
+    # reference-layout host arrays of the stored stages (kkt.py:63-68), when the
+    # stages came from host arrays; otherwise built lazily from the device data
+    host_arrays: Optional[dict] = field(default=None, repr=False)
+    # B_i of a TRI family built natively (reference formula, stage-constant)
+    b_const: Optional[np.ndarray] = field(default=None, repr=False)
+
     def __post_init__(self):
         if self.n_global == 0:
             self.n_global = self.n_steps
+
+    # --- the reference's StageBlocks fields (kkt.py:53-80), host numpy ------
+    # Callers of the reference (sqp.py:252-313 apply_cx / apply_cx_t /
+    # hessian_operator) read k, c, b, q_u, q_v, q_z as (N, ., .) arrays.  They
+    # are materialised on first access (dense: N n_u^2 doubles each), so they
+    # are meant for desk-size instances; the device path never reads them.
+    def _stage_host(self, name):
+        if self.host_arrays is not None:
+            return self.host_arrays[name]
+        return None
+
+    @functools.cached_property
+    def k(self) -> np.ndarray:
+        a = self._stage_host("k")
+        return a if a is not None else self._dense_stage(self.K)
+
+    @functools.cached_property
+    def c(self) -> np.ndarray:
+        a = self._stage_host("c")
+        return a if a is not None else self._dense_stage(self.C)
+
+    @functools.cached_property
+    def b(self) -> np.ndarray:
+        a = self._stage_host("b")
+        if a is not None:
+            return a
+        if self.family == FAMILY_DENSE:
+            return dev.to_host(self.B[:self.n_steps]).copy()
+        bc = self.b_const if self.b_const is not None else \
+            self.kappa * self.host_weights["q_z"]
+        return np.broadcast_to(bc, (self.n_steps,) + bc.shape).copy()
+
+    def _weight_seq(self, name):
+        a = self._stage_host(name)
+        if a is not None:
+            return a
+        hw = self.host_weights
+        if name == "q_z":
+            return np.broadcast_to(hw["q_z"], (self.n_steps,) + hw["q_z"].shape).copy()
+        out = np.broadcast_to(hw["q_mid"], (self.n_steps,) + hw["q_mid"].shape).copy()
+        if self.row0 + self.n_steps >= self.n_global and self.n_steps > 0:
+            out[-1] = hw["q_last"]           # the terminal stage N-1 is stored
+        return out
+
+    @functools.cached_property
+    def q_u(self) -> np.ndarray:
+        return self._weight_seq("q_u")
+
+    @functools.cached_property
+    def q_v(self) -> np.ndarray:
+        return self._weight_seq("q_v")
+
+    @functools.cached_property
+    def q_z(self) -> np.ndarray:
+        return self._weight_seq("q_z")
+
+    def _dense_stage(self, t) -> np.ndarray:
+        a = dev.to_host(t[:self.n_steps])
+        if self.family == FAMILY_DENSE:
+            return a.copy()
+        return _tri_dense(a)
 
     @property
     def rows(self):
@@ -212,7 +292,8 @@ def build_stage_blocks(p: ProblemSpec, dt: float, u_seq, v_seq, z_seq,
     n = int(np.shape(u_seq)[0])
     nu, nz = p.n_u, p.n_z
     q_mid, q_last, q_z = _problem_weights(p, dt, n)
-    nat = p.native
+    # reference-built ProblemSpecs (timedisc.py:61-94) carry no `native` tag
+    nat = getattr(p, "native", None)
     r0, r1 = (0, n + 1) if rows is None else (int(rows[0]), int(rows[1]))
     slab = dict(n_global=n, row0=r0, row1=0 if rows is None else r1)
     s0, s1 = r0, min(r1, n)           # stages of the slab
@@ -244,7 +325,9 @@ def build_stage_blocks(p: ProblemSpec, dt: float, u_seq, v_seq, z_seq,
             dev.call("tk_stage_burgers", ns, nu, dt, p.theta, nat["nu"], dev.P(u0), dev.P(u),
                      dev.P(v), dev.P(K), dev.P(Cm), dev.stream())
         w = _weights(FAMILY_TRI, q_mid, q_last, q_z, kappa)
-        return StageBlocks(FAMILY_TRI, ns, nu, nz, K, Cm, None, **w, **slab)
+        fz = p.mass      # F_z of the P1 Burgers semi-discretisation (problems.py:149-197)
+        b_const = dt * p.theta * fz + dt * (1.0 - p.theta) * fz      # timedisc.py:148
+        return StageBlocks(FAMILY_TRI, ns, nu, nz, K, Cm, None, **w, **slab, b_const=b_const)
     # generic ProblemSpec: evaluate the callables once on the host
     u_seq, v_seq, z_seq = (np.asarray(a, dtype=np.float64) for a in (u_seq, v_seq, z_seq))
     k = np.empty((n, nu, nu)); c = np.empty((n, nu, nu)); b = np.empty((n, nu, nz))
@@ -255,9 +338,10 @@ def build_stage_blocks(p: ProblemSpec, dt: float, u_seq, v_seq, z_seq,
     qu = np.empty((n, nu, nu)); qz = np.empty((n, nz, nz))
     for i in range(n):
         qu[i], _, qz[i] = stage_weights(p, dt, i, n)
-    st = stage_blocks_from_arrays(k, c, b, qu, qu, qz)
+    st = stage_blocks_from_arrays(k, c, b, qu, qu.copy(), qz)
     if rows is None:
         return st
+    st.host_arrays = {nm: a[s0:max(s1, s0 + 1)] for nm, a in st.host_arrays.items()}
     st.K = st.K[s0:max(s1, s0 + 1)].contiguous()
     st.C = st.C[s0:max(s1, s0 + 1)].contiguous()
     if st.B is not None:
@@ -285,17 +369,19 @@ def stage_blocks_from_arrays(k, c, b, q_u, q_v, q_z) -> StageBlocks:
         kappa_ok = bool(np.allclose(b, kappa * qz[None], rtol=0.0,
                                     atol=1e-13 * max(np.abs(b).max(), 1e-300)))
     fam = _choose_family(nu, nz, q_mid, qz, kappa_ok)
+    ha = dict(k=k, c=c, b=b, q_u=q_u, q_v=q_v, q_z=q_z)
     if fam == FAMILY_DENSE:
         w = _weights(fam, q_mid, q_last, qz, 0.0)
         return StageBlocks(fam, n, nu, nz, dev.to_device(k), dev.to_device(c),
-                           dev.to_device(b), **w)
+                           dev.to_device(b), **w, host_arrays=ha)
     if not all(_is_tridiagonal(a) for a in (k[i] for i in range(n))) or \
             not all(_is_tridiagonal(a) for a in (c[i] for i in range(n))):
         raise UnsupportedStructure("K_i / C_i are not tridiagonal")
     kd = np.stack([_tri_diags(k[i]) for i in range(n)])
     cd = np.stack([_tri_diags(c[i]) for i in range(n)])
     w = _weights(fam, q_mid, q_last, qz, kappa)
-    return StageBlocks(fam, n, nu, nz, dev.to_device(kd), dev.to_device(cd), None, **w)
+    return StageBlocks(fam, n, nu, nz, dev.to_device(kd), dev.to_device(cd), None, **w,
+                       host_arrays=ha)
 
 
 def _toeplitz(q) -> bool:
@@ -481,12 +567,21 @@ def assemble_kkt(s: StageBlocks, nu: Optional[int] = None,
 
 class DiagonalSolver:
     """D^{-1} over all block rows (kkt.py:338-389), one exact local KKT solve
-    per time interval on the device (no explicit inverses are formed)."""
+    per time interval on the device (no explicit inverses are formed).
 
-    def __init__(self, a: BlockTriKKT):
+    Construction verifies the blocks like the reference's factorisation
+    (kkt.py:347-368): a block whose partial-pivoting LU meets a pivot below
+    ``pivot_floor * max|block|`` raises :class:`SingularBlock` with its block
+    index.  DENSE levels run exactly that test on every assembled block
+    (tk_check_blocks); TRI blocks are symmetric quasi-definite, hence
+    nonsingular, once the weights are SPD, which is what is checked there.
+    """
+
+    def __init__(self, a: BlockTriKKT, pivot_floor: float = PIVOT_FLOOR):
         self.a = a
         self.layout = a.layout if a.dim <= 1 << 22 else None
         self.n_steps = a.n_steps
+        _check_blocks(a, pivot_floor)
 
     def solve_all(self, r, out=None):
         host = dev.is_host(r)
@@ -504,3 +599,97 @@ class DiagonalSolver:
         full[s:s + w] = np.asarray(dev.to_host(r_block) if isinstance(r_block, torch.Tensor)
                                    else r_block)
         return dev.to_host(self.solve_all(dev.to_device(full)))[s:s + w]
+
+
+# ---------------------------------------------------------------------------
+# Theorem 1 verification (kkt.py:496-543) and the block singularity test
+# ---------------------------------------------------------------------------
+@dataclass
+class Theorem1Report:
+    """Per-condition, per-stage verification of the diagonal-block
+    nonsingularity hypotheses (kkt.py:496-517): Q blocks SPD, K nonsingular."""
+
+    q_u_ok: np.ndarray
+    q_v_ok: np.ndarray
+    q_z_ok: np.ndarray
+    k_ok: np.ndarray
+
+    @property
+    def passed(self) -> bool:
+        return bool(self.q_u_ok.all() and self.q_v_ok.all()
+                    and self.q_z_ok.all() and self.k_ok.all())
+
+    def failures(self):
+        out = []
+        for name, arr in (("q_u", self.q_u_ok), ("q_v", self.q_v_ok),
+                          ("q_z", self.q_z_ok), ("k", self.k_ok)):
+            for i in np.nonzero(~arr)[0]:
+                out.append((name, int(i)))
+        return out
+
+
+def _is_spd(m: np.ndarray) -> bool:
+    """Symmetric to 1e-12 relative and Cholesky-factorable (kkt.py:520-527)."""
+    import scipy.linalg
+    m = np.asarray(m, dtype=np.float64)
+    if not np.allclose(m, m.T, rtol=0.0, atol=1e-12 * max(1.0, np.abs(m).max())):
+        return False
+    try:
+        scipy.linalg.cholesky(m, lower=True, check_finite=False)
+    except (scipy.linalg.LinAlgError, ValueError):
+        return False
+    return True
+
+
+def _stage_flags(s: StageBlocks, pivot_floor: float) -> np.ndarray:
+    """k_ok per stored stage from tk_check_k (one thread per stage on the device)."""
+    ns = s.n_steps
+    if ns == 0:
+        return np.ones(0, dtype=bool)
+    bad = torch.zeros(ns, dtype=torch.int32, device=dev.device())
+    a = BlockTriKKT(s)
+    dev.call("tk_check_k", a.lref, float(pivot_floor), bad.data_ptr(), dev.stream())
+    return bad.cpu().numpy() == 0
+
+
+def check_theorem1(s: StageBlocks, pivot_floor: float = PIVOT_FLOOR) -> Theorem1Report:
+    """Report-only verification of Theorem 1's hypotheses (kkt.py:530-543).
+
+    The weights are time-constant apart from the terminal stage, so the SPD
+    tests run once per distinct weight on the host; the K_i test is the
+    partial-pivoting LU pivot floor of linalg.lu_factor (linalg.py:75-103),
+    evaluated per stage on the device (tk_check_k).
+    """
+    n = s.n_steps
+    hw = s.host_weights
+    if not hw:
+        raise UnsupportedStructure("stage blocks carry no host copy of their weights")
+    term = s.row0 + n >= s.n_global        # the terminal stage N-1 is stored here
+    mid_ok, last_ok, z_ok = _is_spd(hw["q_mid"]), _is_spd(hw["q_last"]), _is_spd(hw["q_z"])
+    q_ok = np.full(n, mid_ok)
+    if term and n > 0:
+        q_ok[-1] = last_ok
+    return Theorem1Report(q_u_ok=q_ok, q_v_ok=q_ok.copy(), q_z_ok=np.full(n, z_ok),
+                          k_ok=_stage_flags(s, pivot_floor))
+
+
+def _check_blocks(a: BlockTriKKT, pivot_floor: float) -> None:
+    """Raise SingularBlock(i) for the first diagonal block the reference's
+    DiagonalSolver could not factor (kkt.py:347-368)."""
+    s = a.stage
+    if s.family == FAMILY_DENSE and not a.is_slab:
+        bad = torch.zeros(a.n_steps + 1, dtype=torch.int32, device=dev.device())
+        dev.call("tk_check_blocks", a.lref, float(pivot_floor), bad.data_ptr(), dev.stream())
+        idx = np.nonzero(bad.cpu().numpy())[0]
+        if idx.size:
+            i = int(idx[0])
+            raise SingularBlock(i, f"diagonal block {i}: pivot below floor "
+                                   f"{pivot_floor:.1e} * max|block|")
+        return
+    hw = s.host_weights
+    if s.family == FAMILY_TRI and hw:
+        for name in ("q_mid", "q_last", "q_z"):
+            if not _is_spd(hw[name]):
+                raise UnsupportedStructure(
+                    f"TRI local solves need SPD weights ({name} is not); the reference "
+                    "would factor these blocks by pivoted LU")

@@ -162,6 +162,16 @@ class VecOps:
 
 
 _OPS = None
+_FUSED_OK = {}
+
+
+def fused_arnoldi_ok() -> bool:
+    """The cooperative Arnoldi grid fits the current device (else the unfused
+    kernels run: same reductions, same bits)."""
+    d = torch.cuda.current_device()
+    if d not in _FUSED_OK:
+        _FUSED_OK[d] = bool(_lib.load().tk_arnoldi_supported())
+    return _FUSED_OK[d]
 
 
 def vec_ops() -> VecOps:
@@ -184,15 +194,80 @@ def _residual(op, b, x):
     return y
 
 
-def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
+class DeviceSpace:
+    """The vector space of a single-GPU solve: every operation a
+    libtempokkt_b200.so kernel on whole vectors (VecOps)."""
+
+    def __init__(self):
+        self.ops = vec_ops()
+
+    def nrm2(self, x) -> float:
+        return self.ops.nrm2(x)
+
+    def nrm2_pair(self, x, r):
+        """(||x||, ||r||) with one synchronisation."""
+        self.ops.nrm2_async(x, 2)        # the finiteness check rides on the next sync
+        rn = self.ops.nrm2(r)
+        return float(self.ops.ms.host[2]), rn
+
+    def scale_into(self, a, x, y):
+        self.ops.scale_into(a, x, y)
+
+    def axpy(self, a, x, y):
+        self.ops.axpy(a, x, y)
+
+    def arnoldi(self, V, j, w):
+        if FUSED_ARNOLDI and fused_arnoldi_ok():   # one launch + one copy per step
+            return self.ops.arnoldi(V, j, w)
+        hcol = np.empty(j + 2)
+        for i in range(j + 1):
+            hij = self.ops.dot(V[i], w)
+            hcol[i] = hij
+            self.ops.axpy(-hij, V[i], w)
+        hcol[j + 1] = self.ops.nrm2(w)
+        if hcol[j + 1] != 0.0:
+            self.ops.scale_into(1.0 / hcol[j + 1], w, V[j + 1])
+        return hcol
+
+    def gemv_t_add(self, V, c, x):
+        self.ops.gemv_t_add(V, c, x)
+
+    def residual(self, op, b, x):
+        return _residual(op, b, x)
+
+    def finish(self):
+        # the Arnoldi steps of a large basis held w L2-persisting (tk_arnoldi_mgs):
+        # give the lines back once the solve has synchronised
+        _lib.check(_lib.load().tk_l2_persist_reset(), "tk_l2_persist_reset")
+
+
+_DEPTH = [0]          # nesting of solves (the coarse GMRES runs inside the outer one)
+
+
+def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible, space=None):
+    """Right-preconditioned (F)GMRES with restarts (krylov.py:77-191): same
+    modified Gram-Schmidt Arnoldi, Givens rotations, stopping and breakdown
+    rules and reports as the reference.  ``space`` supplies the vector
+    operations (DeviceSpace: one GPU; slabs.SlabSpace: time slabs over ranks
+    with allreduced dots)."""
+    space = DeviceSpace() if space is None else space
+    _DEPTH[0] += 1
+    try:
+        return _gmres_body(op, prec, b, x0, rel_tol, max_iters, restart, flexible, space)
+    finally:
+        _DEPTH[0] -= 1
+        if _DEPTH[0] == 0:          # outermost solve only (also on an exception)
+            space.finish()
+
+
+def _gmres_body(op, prec, b, x0, rel_tol, max_iters, restart, flexible, space):
     if not (0.0 < rel_tol < 1.0):
         raise ValueError(f"rel_tol must lie in (0,1), got {rel_tol}")
     n = op.dim
     host = dev.is_host(b)
-    b = dev.to_device(b)
+    b = dev.to_device(b) if not hasattr(space, "to_local") else space.to_local(b)
     if b.shape != (n,):
         raise DimensionMismatch(f"rhs shape {tuple(b.shape)} != operator dim {n}")
-    ops = vec_ops()
     prec = _as_prec(prec)
     if restart is None:
         restart = max_iters
@@ -201,13 +276,13 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
     if x0 is None:
         r = b.clone()                      # b - A*0, bitwise
         x = torch.empty_like(b)
-        ops.scale_into(0.0, r, x)          # x = 0 (signed zeros add exactly)
+        space.scale_into(0.0, r, x)        # x = 0 (signed zeros add exactly)
     else:
-        x = dev.to_device(x0).clone()
+        x = (dev.to_device(x0) if not hasattr(space, "to_local") else space.to_local(x0)).clone()
         if x.shape != (n,):
             raise DimensionMismatch(f"x0 shape {tuple(x.shape)} != operator dim {n}")
-        r = _residual(op, b, x)
-    beta0 = ops.nrm2(r)
+        r = space.residual(op, b, x)
+    beta0 = space.nrm2(r)
     if not math.isfinite(beta0):
         raise NonFiniteValue("non-finite initial residual")
     history = [beta0]
@@ -227,23 +302,23 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
         # bases grow on demand (doubling): a coarse solve that stops after a
         # few iterations does not hold max_iters+1 vectors of HBM
         cap = min(m, 16)
-        V = torch.empty((cap + 1, n), dtype=dev.F64, device=b.device)
-        Z = torch.empty((cap, n), dtype=dev.F64, device=b.device) \
+        V = torch.empty((cap + 1, n), dtype=b.dtype, device=b.device)
+        Z = torch.empty((cap, n), dtype=b.dtype, device=b.device) \
             if (flexible and prec is not None) else None
         H = np.zeros((m + 1, m)); cs = [0.0] * m; sn = [0.0] * m
         g = [0.0] * (m + 1)
         g[0] = beta
-        ops.scale_into(1.0 / beta, r, V[0])
+        space.scale_into(1.0 / beta, r, V[0])
         jd = 0
         broke = False
         for j in range(m):
             if j + 1 > cap:
                 cap = min(m, 2 * cap)
-                V2 = torch.empty((cap + 1, n), dtype=dev.F64, device=b.device)
+                V2 = torch.empty((cap + 1, n), dtype=b.dtype, device=b.device)
                 V2[:j + 1].copy_(V[:j + 1])
                 V = V2
                 if Z is not None:
-                    Z2 = torch.empty((cap, n), dtype=dev.F64, device=b.device)
+                    Z2 = torch.empty((cap, n), dtype=b.dtype, device=b.device)
                     Z2[:j].copy_(Z[:j])
                     Z = Z2
                 V2 = Z2 = None
@@ -254,16 +329,9 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
                 if Z is not None:
                     Z[j].copy_(zj)
                     zj = Z[j]
-            w = dev.to_device(op(zj))
-            if FUSED_ARNOLDI:     # one launch + one copy per step (V[j+1] written too)
-                hcol = ops.arnoldi(V, j, w)
-            else:
-                hcol = np.empty(j + 2)
-                for i in range(j + 1):
-                    hij = ops.dot(V[i], w)
-                    hcol[i] = hij
-                    ops.axpy(-hij, V[i], w)
-                hcol[j + 1] = ops.nrm2(w)
+            w = op(zj)
+            w = dev.to_device(w) if not hasattr(space, "to_local") else space.to_local(w)
+            hcol = space.arnoldi(V, j, w)       # MGS; V[j+1] = w / h_{j+1} written too
             hj1 = float(hcol[j + 1])
             if not np.isfinite(hcol).all():
                 raise NonFiniteValue("non-finite Hessenberg entry in Arnoldi")
@@ -293,37 +361,34 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible):
                 break
             if est <= target or total >= max_iters:
                 break
-            if not FUSED_ARNOLDI:
-                ops.scale_into(1.0 / hj1, w, V[j + 1])
         if jd > 0:
             y = np.zeros(jd)
             for i in range(jd - 1, -1, -1):
                 y[i] = (np.float64(g[i]) - H[i, i + 1:jd] @ y[i + 1:jd]) / H[i, i]
             yt = y
             if Z is not None:
-                ops.gemv_t_add(Z, yt, x)
+                space.gemv_t_add(Z, yt, x)
             else:
                 vy = torch.empty_like(b)
-                ops.scale_into(0.0, V[0], vy)
-                ops.gemv_t_add(V, yt, vy)
-                ops.axpy(1.0, vy if prec is None else dev.to_device(prec(vy)), x)
+                space.scale_into(0.0, V[0], vy)
+                space.gemv_t_add(V, yt, vy)
+                if prec is not None:
+                    pv = prec(vy)
+                    vy = dev.to_device(pv) if not hasattr(space, "to_local") else \
+                        space.to_local(pv)
+                space.axpy(1.0, vy, x)
         zj = w = None        # views of Z / V: drop them so the bases are freed before a restart
         del V, Z
-        r = _residual(op, b, x)
-        ops.nrm2_async(x, 2)              # the finiteness check rides on the next sync
-        true_norm = ops.nrm2(r)
-        x_norm = float(ops.ms.host[2])
+        r = space.residual(op, b, x)
+        x_norm, true_norm = space.nrm2_pair(x, r)
         beta = true_norm
         if broke and true_norm > max(target, 10 * BREAKDOWN_TOL * beta0):
             raise Breakdown("zero Arnoldi norm with nonzero residual")
         if true_norm <= target or total >= max_iters or broke:
             break
     if x_norm is None:                    # no cycle ran (max_iters == 0)
-        x_norm = ops.nrm2(x)
-        true_norm = ops.nrm2(_residual(op, b, x))
-    # the Arnoldi steps of a large basis held w L2-persisting (tk_arnoldi_mgs):
-    # give the lines back now that the solve has synchronised
-    _lib.check(_lib.load().tk_l2_persist_reset(), "tk_l2_persist_reset")
+        x_norm = space.nrm2(x)
+        true_norm = space.nrm2(space.residual(op, b, x))
     if not math.isfinite(x_norm):
         raise NonFiniteValue("non-finite solution vector")
     # ||b - A x|| of the final x: the deterministic kernels give the bits the

@@ -119,7 +119,7 @@ def stage_weights(p: ProblemSpec, dt: float, i: int, n_steps: int):
 
 
 def _native_forward(p: ProblemSpec, controls: np.ndarray, grid: TimeGrid, tol: float):
-    nat = p.native
+    nat = getattr(p, "native", None)
     n = grid.n_steps
     lib = _lib.load()
     states = np.empty((n, p.n_u))
@@ -148,7 +148,7 @@ def forward_solve(p: ProblemSpec, controls, grid: TimeGrid,
     n = grid.n_steps
     if controls.shape != (n, p.n_z):
         raise DimensionMismatch(f"controls shape {controls.shape} != ({n}, {p.n_z})")
-    if p.native is not None:
+    if getattr(p, "native", None) is not None:       # reference specs have no tag
         return Trajectory(states=_native_forward(p, controls, grid, newton_tol),
                           controls=controls.copy())
     # generic specs: per-step Newton with the callables (setup path only)

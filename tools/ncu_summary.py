@@ -25,14 +25,17 @@ def launches(path):
             continue
         unit = r.get("Metric Unit", "")
         if m == "gpu__time_duration.sum":
-            per[k]["ns"] += v * (1000.0 if unit == "us" else 1.0e6 if unit == "ms" else 1.0)
+            per[k]["ns"] += v * {"us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6,
+                                 "s": 1e9, "second": 1e9}.get(unit, 1.0)
             per[k]["n"] += 1
         elif m.startswith("dram__bytes"):
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+                     "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
             per[k]["bytes"] += v * scale
     # one-off hierarchy setup (stage linearisation, factor records, chunk and
     # group propagators) is listed but excluded from the V-cycle shares
-    setup = ("tri_chain_kernel<1, 0, 1,", "tri_factor_kernel", "stage_", "tri_transpose")
+    setup = ("tri_chain_kernel<1, 0, 1,", "tri_factor_kernel", "stage_", "tri_transpose",
+             "check_k_kernel", "check_blocks_kernel", "FillFunctor")
     is_setup = {k: any(s in k for s in setup) for k in per}
     tot = sum(d["ns"] for k, d in per.items() if not is_setup[k])
     out = []
@@ -68,7 +71,9 @@ def full(path):
                 return float("nan")
             u = units.get(key, "")
             scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3,
-                     "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
+                     "B": 1e-6, "KB": 1e-3, "MB": 1.0, "GB": 1e3,
+                     "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
+                     "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}.get(u, 1.0)
             return v * scale
         dur_us = f("gpu__time_duration.sum")
         rd, wr = f("dram__bytes_read.sum"), f("dram__bytes_write.sum")
