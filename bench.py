@@ -235,10 +235,10 @@ def solve_once(P, h, b, setup):
     wall time with a device synchronisation on both sides."""
     import torch
     S = setup.solver
+    torch.cuda.empty_cache()                      # cached blocks back to the driver
     free, _ = torch.cuda.mem_get_info()
-    free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
     per_it = 2 * setup.dim * 8                    # V and Z columns
-    m_fit = int(0.85 * free // per_it) - 2
+    m_fit = int(0.9 * free // per_it) - 4         # (+ x, r, w and V-cycle temporaries)
     restart = None if m_fit >= S["max_iters"] + 1 else max(2, m_fit)
     h.stats = type(h.stats)()
     torch.cuda.synchronize()

@@ -28,6 +28,8 @@ BREAKDOWN_TOL = 1e-14
 # MGS Arnoldi step as one cooperative launch (tk_arnoldi_mgs) instead of
 # j+1 dot/axpy pairs with a host round trip each; bitwise identical
 FUSED_ARNOLDI = True
+# Krylov bases above this size are allocated at their full length at once
+GROW_LIMIT_BYTES = 2 << 30
 
 
 @dataclass
@@ -300,8 +302,12 @@ def _gmres_body(op, prec, b, x0, rel_tol, max_iters, restart, flexible, space):
         if m <= 0:
             break
         # bases grow on demand (doubling): a coarse solve that stops after a
-        # few iterations does not hold max_iters+1 vectors of HBM
-        cap = min(m, 16)
+        # few iterations does not hold max_iters+1 vectors of HBM; bases whose
+        # full size exceeds GROW_LIMIT_BYTES (outer solves of the large
+        # configurations, restart sized to the free HBM) are allocated once,
+        # since growing would hold the old and the new basis side by side
+        nb = 2 if (flexible and prec is not None) else 1
+        cap = m if (m + 1) * n * 8 * nb > GROW_LIMIT_BYTES else min(m, 16)
         V = torch.empty((cap + 1, n), dtype=b.dtype, device=b.device)
         Z = torch.empty((cap, n), dtype=b.dtype, device=b.device) \
             if (flexible and prec is not None) else None

@@ -140,26 +140,39 @@ class TorchComm(Comm):
         return float(t.item())
 
     def gather(self, t, sizes):
+        """Every rank's slab of the coarse vector onto rank 0: ONE grouped
+        P2P batch (ncclGroupStart/End: the receives land side by side in the
+        full vector, all in flight at once), no staging copies."""
         d = self.dist
+        if self.size == 1:
+            return t
         if self.rank == 0:
-            parts = [t]
-            for r in range(1, self.size):
-                buf = torch.empty(sizes[r], dtype=t.dtype, device=t.device)
-                d.recv(buf, r, group=self.group)
-                parts.append(buf)
-            return torch.cat(parts)
-        d.send(t.contiguous(), 0, group=self.group)
+            offs = np.concatenate([[0], np.cumsum(sizes)])
+            full = torch.empty(int(offs[-1]), dtype=t.dtype, device=t.device)
+            full[:sizes[0]].copy_(t)
+            ops = [d.P2POp(d.irecv, full[offs[r]:offs[r + 1]], r, self.group)
+                   for r in range(1, self.size)]
+            for q in d.batch_isend_irecv(ops):
+                q.wait()
+            return full
+        for q in d.batch_isend_irecv([d.P2POp(d.isend, t.contiguous(), 0, self.group)]):
+            q.wait()
         return None
 
     def scatter(self, full, sizes, like):
         d = self.dist
+        if self.size == 1:
+            return full
         if self.rank == 0:
             offs = np.concatenate([[0], np.cumsum(sizes)])
-            for r in range(1, self.size):
-                d.send(full[offs[r]:offs[r + 1]].contiguous(), r, group=self.group)
-            return full[:sizes[0]].clone()
+            ops = [d.P2POp(d.isend, full[offs[r]:offs[r + 1]], r, self.group)
+                   for r in range(1, self.size)]
+            for q in d.batch_isend_irecv(ops):
+                q.wait()
+            return full[:sizes[0]]
         buf = torch.empty(sizes[self.rank], dtype=like.dtype, device=like.device)
-        d.recv(buf, 0, group=self.group)
+        for q in d.batch_isend_irecv([d.P2POp(d.irecv, buf, 0, self.group)]):
+            q.wait()
         return buf
 
 
@@ -345,6 +358,52 @@ class CudaBackend:
     def local_dot(self, x, y):
         return self.ops.dot_dev(x, y).reshape(1).clone()
 
+    # Krylov vector operations on slab vectors (SlabSpace) ---------------------
+    def scale_into(self, a, x, y):
+        self.ops.scale_into(a, x, y)
+
+    def axpy(self, a, x, y):
+        self.ops.axpy(a, x, y)
+
+    def rsub(self, b, y):
+        self.dev.call("tk_rsub", y.numel(), self.dev.P(b), self.dev.P(y), self.dev.stream())
+
+    def gemv_t_add(self, V, c, x):
+        self.ops.gemv_t_add(V, c, x)
+
+    def sq_norms(self, vecs):
+        """Local squared norms of `vecs` side by side in one device tensor."""
+        out = self.dev.empty(len(vecs))
+        for k, v in enumerate(vecs):
+            self.dev.call("tk_dot", v.numel(), self.dev.P(v), self.dev.P(v),
+                          out[k:].data_ptr(), self.dev.P(self.ops.work), self.dev.stream())
+        return out
+
+    def mgs(self, comm, V, j, w):
+        """One modified Gram-Schmidt Arnoldi step on slab vectors (krylov.py:
+        141-163): every h_i = <V_i, w> is a local partial dot + an allreduce
+        that stays on the device and feeds `w -= h_i V_i` (tk_axpy_dev), the
+        norm likewise (tk_sqrt_div writes V_{j+1} = w / h_{j+1}); the host
+        reads the column once, after the whole step has been enqueued."""
+        d = self.dev
+        n = w.numel()
+        if getattr(self, "_h", None) is None or self._h.numel() < j + 2:
+            self._h = d.empty(max(64, 2 * (j + 2)))
+        h = self._h
+        for i in range(j + 1):
+            d.call("tk_dot", n, d.P(V[i]), d.P(w), h[i:].data_ptr(), d.P(self.ops.work),
+                   d.stream())
+            comm.allreduce_sum(h[i:i + 1])
+            d.call("tk_axpy_dev", n, h[i:].data_ptr(), -1.0, d.P(V[i]), d.P(w), d.stream())
+        d.call("tk_dot", n, d.P(w), d.P(w), h[j + 1:].data_ptr(), d.P(self.ops.work), d.stream())
+        comm.allreduce_sum(h[j + 1:j + 2])
+        d.call("tk_sqrt_div", n, h[j + 1:].data_ptr(), h[j + 1:].data_ptr(), d.P(w),
+               d.P(V[j + 1]), d.stream())
+        return h[:j + 2].cpu().numpy()
+
+    def finish(self):
+        pass
+
 
 # --------------------------------------------------------------------------- hierarchy
 class SlabHierarchy:
@@ -466,6 +525,81 @@ class SlabHierarchy:
         return float(self.comm.allreduce_sum(t).item())
 
 
+# --------------------------------------------------------------------------- Krylov
+class SlabSpace:
+    """Vector space of a time-sharded (F)GMRES (the ``space`` of
+    krylov._gmres_engine): vectors are per-rank slabs, axpy-type operations are
+    local, every inner product is a local partial sum + one allreduce, so all
+    ranks see the same Hessenberg column and take the same branches
+    (reference krylov.py:77-191 run on vectors that happen to be sharded)."""
+
+    def __init__(self, hier: "SlabHierarchy"):
+        self.h, self.be, self.comm = hier, hier.be, hier.comm
+
+    def to_local(self, x):
+        return self.be.to_local(x)
+
+    def _norms(self, vecs):
+        sq = self.comm.allreduce_sum(self.be.sq_norms(vecs))
+        return [math.sqrt(v) for v in sq.tolist()]
+
+    def nrm2(self, x) -> float:
+        return self._norms([x])[0]
+
+    def nrm2_pair(self, x, r):
+        a, b = self._norms([x, r])
+        return a, b
+
+    def scale_into(self, a, x, y):
+        self.be.scale_into(a, x, y)
+
+    def axpy(self, a, x, y):
+        self.be.axpy(a, x, y)
+
+    def arnoldi(self, V, j, w):
+        return self.be.mgs(self.comm, V, j, w)
+
+    def gemv_t_add(self, V, c, x):
+        self.be.gemv_t_add(V, c, x)
+
+    def residual(self, op, b, x):
+        y = self.be.to_local(op(x))
+        self.be.rsub(b, y)
+        return y
+
+    def finish(self):
+        self.be.finish()
+
+
+def slab_operator(h: SlabHierarchy):
+    """The time-sharded augmented operator as a krylov.LinearOperator on slab
+    vectors (BlockTriKKT.as_operator, kkt.py:249-250, with the halo exchange)."""
+    from .krylov import LinearOperator
+    return LinearOperator(dim=h.local_dim, apply=h.apply)
+
+
+def slab_preconditioner(h: SlabHierarchy):
+    """One sharded V-cycle from zero (mg_preconditioner, multigrid.py:304-311)."""
+    from .krylov import Preconditioner
+    return Preconditioner(apply=h.vcycle, is_flexible=True)
+
+
+def fgmres(h: SlabHierarchy, b_local, x0=None, rel_tol=1e-10, max_iters=401, restart=None):
+    """Flexible GMRES (krylov.py:204-210) over time slabs: this rank's part of
+    the solution and the (rank-identical) SolveReport."""
+    from .krylov import _gmres_engine
+    return _gmres_engine(slab_operator(h), slab_preconditioner(h), b_local, x0, rel_tol,
+                         max_iters, restart, flexible=True, space=SlabSpace(h))
+
+
+def gmres(h: SlabHierarchy, prec, b_local, x0=None, rel_tol=1e-10, max_iters=401, restart=None):
+    """Restarted right-preconditioned GMRES (krylov.py:194-201) over time
+    slabs with a fixed (linear) slab preconditioner, or None."""
+    from .krylov import _gmres_engine
+    return _gmres_engine(slab_operator(h), prec, b_local, x0, rel_tol, max_iters, restart,
+                         flexible=False, space=SlabSpace(h))
+
+
 # --------------------------------------------------------------------------- bench
 def bench_rank(args, rank, world, local_rank):
     """bench.py --gpus N (N > 1): strong scaling of the V-cycle on configs[idx]."""
@@ -552,6 +686,33 @@ def bench_rank(args, rank, world, local_rank):
     dist.barrier()
     e2e_ms = comm.allreduce_max(e0.elapsed_time(e1)) / e2e_steps
     unknowns = s.grid.n_steps * s.dof_per_step
+    # the full sharded MG-FGMRES solve (tol / iteration cap of the config), wall
+    # clock between barriers with device synchronisation, slowest rank; the
+    # restart length is sized to the smallest free HBM over the ranks (V and Z
+    # hold two slab vectors per iteration) so that every rank restarts alike
+    solve = None
+    if getattr(args, "solve_config", 0) >= 0:
+        torch.cuda.empty_cache()
+        free, _ = torch.cuda.mem_get_info()
+        m_fit = int(0.9 * free // (2 * ln * 8)) - 4
+        m_fit = -int(comm.allreduce_max(-float(m_fit)))
+        restart = None if m_fit >= S["max_iters"] + 1 else max(2, m_fit)
+        if rank == 0:
+            h.coarse.stats = type(h.coarse.stats)()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        xs, rep = fgmres(h, r_loc, rel_tol=S["rel_tol"], max_iters=S["max_iters"],
+                         restart=restart)
+        torch.cuda.synchronize()
+        dist.barrier()
+        secs = comm.allreduce_max(time.perf_counter() - t0)
+        del xs
+        solve = {"config": f"configs[{args.config}] {s.describe()}", "seconds": round(secs, 4),
+                 "outer": "fgmres over time slabs (distributed MGS, allreduced dots)",
+                 "restart": restart, "iterations": rep.iterations,
+                 "final_rel_residual": rep.final_relative_residual,
+                 "coarse_iters_avg": h.coarse.stats.average if rank == 0 else None}
     if rank != 0:
         return None
     return {
@@ -573,4 +734,5 @@ def bench_rank(args, rank, world, local_rank):
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": None,
+        "solve": solve,
     }

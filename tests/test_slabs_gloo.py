@@ -127,6 +127,41 @@ class OracleBackend:
     def local_dot(self, x, y):
         return torch.tensor([float(np.dot(x.numpy(), y.numpy()))], dtype=torch.float64)
 
+    # Krylov vector operations on slab vectors (slabs.SlabSpace) -- host torch
+    # here; the CUDA backend runs the libtempokkt_b200.so kernels
+    def scale_into(self, a, x, y):
+        torch.mul(x, a, out=y)
+
+    def axpy(self, a, x, y):
+        y.add_(x, alpha=a)
+
+    def rsub(self, b, y):
+        torch.sub(b, y, out=y)
+
+    def gemv_t_add(self, V, c, x):
+        c = torch.as_tensor(np.asarray(c, dtype=np.float64))
+        x.add_(V[:c.numel()].T @ c)
+
+    def sq_norms(self, vecs):
+        return torch.tensor([float(np.dot(v.numpy(), v.numpy())) for v in vecs],
+                            dtype=torch.float64)
+
+    def mgs(self, comm, V, j, w):
+        h = torch.zeros(j + 2, dtype=torch.float64)
+        for i in range(j + 1):
+            h[i] = float(np.dot(V[i].numpy(), w.numpy()))
+            comm.allreduce_sum(h[i:i + 1])
+            w.sub_(V[i], alpha=float(h[i]))
+        h[j + 1] = float(np.dot(w.numpy(), w.numpy()))
+        comm.allreduce_sum(h[j + 1:j + 2])
+        h[j + 1] = np.sqrt(float(h[j + 1]))
+        if float(h[j + 1]) != 0.0:
+            torch.div(w, float(h[j + 1]), out=V[j + 1])
+        return h.numpy().copy()
+
+    def finish(self):
+        pass
+
 
 def _worker(rank, world, port, name, levels, out):
     import sys
@@ -149,7 +184,14 @@ def _worker(rank, world, port, name, levels, out):
     e = sh.vcycle(b)
     ax = sh.apply(x)
     d = sh.dot(x, b)
-    np.savez(os.path.join(out, f"r{rank}.npz"), off=off, e=e.numpy(), ax=ax.numpy(), d=d)
+    # the sharded outer solve (row 13): FGMRES around the slab V-cycle
+    xs, rep = slabs.fgmres(sh, b, rel_tol=1e-8, max_iters=40)
+    # plain GMRES without a preconditioner, restarted, from a nonzero guess
+    xg, repg = slabs.gmres(sh, None, b, x0=x, rel_tol=1e-3, max_iters=12, restart=5)
+    np.savez(os.path.join(out, f"r{rank}.npz"), off=off, e=e.numpy(), ax=ax.numpy(), d=d,
+             xs=np.asarray(xs), its=rep.iterations, hist=np.asarray(rep.residual_history),
+             rel=rep.final_relative_residual, xg=np.asarray(xg), gits=repg.iterations,
+             ghist=np.asarray(repg.residual_history))
     dist.destroy_process_group()
 
 
@@ -181,3 +223,18 @@ def test_gloo_two_ranks_match_oracle(tmp_path, name, levels):
     assert np.abs(e - ref).max() <= 1e-12 * np.abs(ref).max()
     assert np.abs(ax - h.levels[0].kkt.apply(g["x"])).max() <= 1e-13 * np.abs(ax).max()
     assert abs(float(parts[0]["d"]) - float(np.dot(g["x"], g["b"]))) < 1e-9
+    # sharded FGMRES == the oracle's single-process FGMRES: identical iteration
+    # counts on every rank, residual history and solution within 1e-10
+    xo, orep = O.fgmres(h.levels[0].kkt.apply, O.mg_prec(h), g["b"], rel_tol=1e-8, max_iters=40)
+    xs = np.concatenate([q["xs"] for q in parts])
+    for q in parts:
+        assert int(q["its"]) == orep.iterations
+        assert np.allclose(q["hist"], orep.history, rtol=1e-10, atol=0)
+        assert np.array_equal(q["hist"], parts[0]["hist"])
+    assert np.linalg.norm(xs - xo) <= 1e-10 * np.linalg.norm(xo)
+    xgo, grep_ = O.gmres(h.levels[0].kkt.apply, None, g["b"], x0=g["x"], rel_tol=1e-3,
+                         max_iters=12, restart=5)
+    xg = np.concatenate([q["xg"] for q in parts])
+    assert int(parts[0]["gits"]) == int(parts[1]["gits"]) == grep_.iterations
+    assert np.allclose(parts[0]["ghist"], grep_.history, rtol=1e-10, atol=0)
+    assert np.linalg.norm(xg - xgo) <= 1e-10 * np.linalg.norm(xgo)

@@ -54,6 +54,47 @@ def test_virtual_ranks_match_single(name, R, levels):
     assert abs(d - float(np.dot(g["x"], b))) <= 1e-12 * abs(np.dot(np.abs(g["x"]), np.abs(b)))
 
 
+@pytest.mark.parametrize("name,R,levels", [("cfg1_burgers", 2, 4), ("cfg0_vdp", 4, 3)])
+def test_sharded_fgmres_matches_single_and_oracle(name, R, levels):
+    """The outer MG-FGMRES over time slabs (slabs.fgmres: distributed MGS with
+    device-resident allreduced dots) against the single-GPU solve and the
+    oracle: identical iteration counts, history and solution within 1e-10."""
+    import torch
+
+    import paper_2405_04808_b200 as P
+    from conftest import oracle_problem
+    from oracle import tk_oracle as O
+    from paper_2405_04808_b200 import slabs
+    g, p, grid = _setup(name)
+    u, v, z, b = g["u"], g["v"], g["z"], g["b"]
+    its = 30
+    h = P.build_hierarchy(p, u, v, z, grid, levels, sweeps=int(g["sweeps"]), coarse_tol=1e-2)
+    x1, rep1 = P.fgmres(h.levels[0].kkt.as_operator(), P.mg_preconditioner(h), b,
+                        rel_tol=1e-8, max_iters=its)
+    oh = O.build_hierarchy(oracle_problem(g), u, v, z, int(g["n"]), float(g["dt"]), levels,
+                           sweeps=int(g["sweeps"]), coarse_tol=1e-2)
+    xo, orep = O.fgmres(oh.levels[0].kkt.apply, O.mg_prec(oh), b, rel_tol=1e-8, max_iters=its)
+    comms = slabs.ThreadComm.group(R)
+
+    def body(c):
+        sh = slabs.SlabHierarchy(p, u, v, z, grid, levels, c, sweeps=int(g["sweeps"]),
+                                 coarse_tol=1e-2)
+        off, ln = sh.local_span()
+        bl = torch.from_numpy(np.ascontiguousarray(b[off:off + ln])).cuda()
+        xs, rep = slabs.fgmres(sh, bl, rel_tol=1e-8, max_iters=its)
+        torch.cuda.synchronize()
+        return off, xs.cpu().numpy(), rep
+
+    res = sorted(slabs.run_threads(comms, body), key=lambda t: t[0])
+    xs = np.concatenate([r[1] for r in res])
+    for _, _, rep in res:
+        assert rep.iterations == rep1.iterations == orep.iterations
+        assert rep.residual_history == res[0][2].residual_history
+        assert np.allclose(rep.residual_history, orep.history, rtol=1e-10, atol=0)
+    assert np.linalg.norm(xs - x1) <= 1e-10 * np.linalg.norm(x1)
+    assert np.linalg.norm(xs - xo) <= 1e-10 * np.linalg.norm(xo)
+
+
 def test_slab_transfers_and_halo_checks():
     import torch
 
