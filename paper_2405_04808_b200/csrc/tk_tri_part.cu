@@ -43,6 +43,9 @@ constexpr int kChunk = TK_PART_CHUNK;
 #ifndef TK_PART_MINB
 #define TK_PART_MINB 2           // CTAs per SM the W=4 build is register-limited to
 #endif
+#ifndef TK_PART_MINB3
+#define TK_PART_MINB3 3          // the same for the x-free rows (MODE 3: ~180 registers)
+#endif
 constexpr bool kStage = TK_PART_STAGE != 0;
 #ifndef TK_PART_PFD
 #define TK_PART_PFD 1            // L2 bulk prefetch distance (rows of this CTA ahead)
@@ -66,7 +69,10 @@ struct PartCta {
     static constexpr int64_t smem_bytes() {
         return ((int64_t)(2 * kPX + (kStage ? kChunk * kSgC + kSgN : 0)) * T) * 8;
     }
-    static constexpr int min_blocks() { return (TK_PART_MINB * 4) / W > 1 ? (TK_PART_MINB * 4) / W : 1; }
+    static constexpr int min_blocks(int mode = 0) {
+        return ((mode == 3 ? TK_PART_MINB3 : TK_PART_MINB) * 4) / W > 1
+                   ? ((mode == 3 ? TK_PART_MINB3 : TK_PART_MINB) * 4) / W : 1;
+    }
 };
 
 // NA consecutive nodes [j0, j0+NA) of segment p + o (zero beyond n), NA even.
@@ -192,7 +198,7 @@ __device__ __forceinline__ RowSrc row_src(const TView& V, const double* x, const
     r.om = L.off_mu(i) - bs; r.ol = L.off_l(i) - bs;
     r.uprev = nullptr;
     r.munext = nullptr;
-    if (MODE == 0) {
+    if (MODE == 0 || MODE == 3) {
         if (x) { r.uprev = V.sl.uprev(L, x, i); r.munext = V.sl.munext(L, x, i); }
     } else if (MODE == 1) {
         if (i >= 1) r.uprev = chain + (size_t)(i - 1) * V.n;
@@ -265,7 +271,9 @@ extern "C" int tk_debug_part_prof(long long* out10) {
     } while (0)
 #endif
 
-// MODE 0: Jacobi / D^{-1} b (couplings from x through the slab);
+// MODE 0: Jacobi x + omega D^{-1}(b - A x) (couplings from x through the slab);
+// MODE 3: Jacobi with omega = 1, D^{-1}(b + (L + U) x): x enters through the
+// coupling segments u_{i-1}, mu_{i+1} only (x == nullptr: D^{-1} b, scaled by omega);
 // MODE 1 / 2: pass 3 of the forward / backward substitution (coupling from
 // the chain vector, no update).
 //
@@ -281,7 +289,7 @@ extern "C" int tk_debug_part_prof(long long* out10) {
 // value and the first lam of the right neighbour) read the peer's shared
 // memory (distributed shared memory) after cluster barriers.
 //
-// RJ (MODE 0, x == nullptr, omega == 1, whole level, even N): the zero-start
+// RJ (MODE 3, x == nullptr, omega == 1, whole level, even N): the zero-start
 // sweep also writes the restricted residual rc = R (b - A y) of
 // tk_residual_restrict_jacobi0 (D y = b, so b - A y is the continuity
 // coupling): row 2c-1 writes -u_{2c} as the coarse mu_c, row 2c writes
@@ -292,7 +300,7 @@ extern "C" int tk_debug_part_prof(long long* out10) {
 // (uniform P1 mass matrices), so each diagonal is one scalar per row instead
 // of per-node loads -- same values, same arithmetic, fewer loads/registers.
 template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE>
-__global__ void __launch_bounds__(32 * W, PartCta<W>::min_blocks())
+__global__ void __launch_bounds__(32 * W, PartCta<W>::min_blocks(MODE))
 tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ x,
               double* __restrict__ y, double omega, const double* __restrict__ chain,
               double* __restrict__ rc) {
@@ -369,6 +377,10 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 const int64_t q1 = (i2 == L.N ? L.dim() : L.start(i2 + 1)) - bs;
                 pf_l2(b + q0, q1 - q0);
                 if (MODE == 0 && x) pf_l2(x + q0, q1 - q0);
+                if (MODE == 3 && x) {   // only the two coupling segments of x
+                    pf_l2(V.sl.uprev(L, x, i2), n);
+                    pf_l2(V.sl.munext(L, x, i2), n);
+                }
             }
             if (i2 < L.N) {
                 pf_l2(V.Ki(i2, n), 3 * n);
@@ -383,7 +395,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                       om = L.off_mu(i) - bs, ol = L.off_l(i) - bs;
         const double* uprev = nullptr;
         const double* munext = nullptr;
-        if (MODE == 0) {
+        if (MODE == 0 || MODE == 3) {
             if (x) { uprev = V.sl.uprev(L, x, i); munext = V.sl.munext(L, x, i); }
         } else if (MODE == 1) {
             if (i >= 1) uprev = chain + (size_t)(i - 1) * n;
@@ -950,7 +962,7 @@ static int part_launch_tt(const tk_level* Lv, const double* b, const double* x, 
         // read through it)
         int carve = cudaSharedmemCarveoutMaxShared;
         if (!kStage) {
-            const int64_t need = (int64_t)Cf::min_blocks() * (smem + 1024);
+            const int64_t need = (int64_t)Cf::min_blocks(MODE) * (smem + 1024);
             carve = (int)((100 * need + 228 * 1024 - 1) / (228 * 1024)) + 1;
             if (carve > 100) carve = 100;
         }
@@ -1003,22 +1015,34 @@ int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, 
 #define TK_PART_CASE(WW, CC)                                                                        \
     if (w == WW && cl == CC) {                                                                      \
         if (rc) {                                                                                   \
-            if (full) return part_launch_t<WW, 0, true, CC, true>(Lv, b, x, y, omega, chain, s, rc); \
-            return part_launch_t<WW, 0, false, CC, true>(Lv, b, x, y, omega, chain, s, rc);         \
+            if (full) return part_launch_t<WW, 3, true, CC, true>(Lv, b, x, y, omega, chain, s, rc); \
+            return part_launch_t<WW, 3, false, CC, true>(Lv, b, x, y, omega, chain, s, rc);         \
         }                                                                                           \
         if (full) {                                                                                 \
             if (mode == 0) return part_launch_t<WW, 0, true, CC>(Lv, b, x, y, omega, chain, s);     \
+            if (mode == 3) return part_launch_t<WW, 3, true, CC>(Lv, b, x, y, omega, chain, s);     \
             if (mode == 1) return part_launch_t<WW, 1, true, CC>(Lv, b, x, y, omega, chain, s);     \
             return part_launch_t<WW, 2, true, CC>(Lv, b, x, y, omega, chain, s);                    \
         }                                                                                           \
         if (mode == 0) return part_launch_t<WW, 0, false, CC>(Lv, b, x, y, omega, chain, s);        \
+        if (mode == 3) return part_launch_t<WW, 3, false, CC>(Lv, b, x, y, omega, chain, s);        \
         if (mode == 1) return part_launch_t<WW, 1, false, CC>(Lv, b, x, y, omega, chain, s);        \
         return part_launch_t<WW, 2, false, CC>(Lv, b, x, y, omega, chain, s);                       \
     }
+    // Jacobi with omega == 1 or from zero needs x only through the two
+    // continuity couplings: x + D^{-1}(b - A x) = D^{-1}(b + (L + U) x), the
+    // local solve of b with u_{i-1} / mu_{i+1} moved to the right-hand side
+    // (MODE 3: no D x products, no second read of x; 180 instead of 232
+    // registers).  TK_JACOBI_RESIDUAL_FORM=1 keeps the residual form.
+    static const bool resid_form = [] {
+        const char* e = getenv("TK_JACOBI_RESIDUAL_FORM");
+        return e && e[0] == '1';
+    }();
+    if (mode == 0 && (x == nullptr || (omega == 1.0 && !resid_form))) mode = 3;
     // FULL: every chunk is complete and every segment 16-byte aligned
     const int w = part_warps(Lv->n_u), cl = part_cluster(Lv->n_u);
     auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    if (rc && (mode != 0 || x || omega != 1.0 || Lv->row0 != 0 ||
+    if (rc && (mode != 3 || x || omega != 1.0 || Lv->row0 != 0 ||
                (Lv->row1 != 0 && Lv->row1 != Lv->n_steps + 1) || (Lv->n_steps & 1))) {
         set_error("tri_rows_part: the fused restriction needs a zero-start sweep with omega = 1 "
                   "on a whole level with even N");

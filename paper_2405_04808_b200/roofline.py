@@ -5,7 +5,8 @@ element read or written once, stage data read once, halo re-reads and the
 constant weights counted as cache hits (0 bytes).  ``dim = N*(4nu+nz)``.
 
   stage bytes / interval   DENSE: 8*(2*nu*nu + nu*nz)   TRI: 8*6*nu
-  jacobi sweep             8*dim*(b + out [+ x_in]) + stage
+  jacobi sweep             8*dim*(b + out [+ x_in]) + stage; omega = 1: x enters only
+                           through the couplings u_{i-1}, mu_{i+1}: 8*dim*2 + 16*N*nu + stage
   diag solve / subst       8*dim*2 + stage
   apply / apply_diag       8*dim*2 + stage ;  residual 8*dim*3 + stage
   residual_restrict        DENSE: residual + restrict as separate passes;
@@ -39,6 +40,8 @@ def dim_of(L) -> int:
 def algorithmic_bytes(name: str, args) -> int:
     if name == "tk_jacobi_sweep":
         L = _lvl(args[0])
+        if args[2] and float(args[4]) == 1.0:   # D^{-1}(b + (L+U) x): two coupling segments of x
+            return 8 * dim_of(L) * 2 + 16 * L.n_steps * L.n_u + stage_bytes(L)
         nvec = 2 + (1 if args[2] else 0)
         return 8 * dim_of(L) * nvec + stage_bytes(L)
     if name == "tk_jacobi0_restrict":   # b read, x and the coarse rhs written, stage data

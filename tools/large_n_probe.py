@@ -32,5 +32,5 @@ for _ in range(10):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
-byts = roofline.algorithmic_bytes("tk_jacobi_sweep", (a.lref, 0, 1, 0))
+byts = roofline.algorithmic_bytes("tk_jacobi_sweep", (a.lref, 0, 1, 0, 1.0))
 print(f"n_u={nu} nt={nt}: identity err {float(e):.2e}  jacobi {ms:.3f} ms  {byts / ms / 1e6:.0f} GB/s")

@@ -32,6 +32,6 @@ for _ in range(K):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / K
-byts = roofline.algorithmic_bytes("tk_jacobi_sweep", (a.lref, 0, 1, 0))
+byts = roofline.algorithmic_bytes("tk_jacobi_sweep", (a.lref, 0, 1, 0, 1.0))
 print(f"{tag}: {ms:.4f} ms/sweep  {byts / ms / 1e6:.0f} GB/s")
 np.save(f"/tmp/jac_{tag}.npy", y.cpu().numpy()[:: 997])
