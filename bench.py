@@ -47,25 +47,38 @@ def _targs(kernel: str):
     return [t.strip() for t in k[k.index("<") + 1:k.rindex(">")].split(",")]
 
 
+def _t(kernel: str, i: int):
+    a = _targs(kernel)
+    return a[i] if i < len(a) else "0"
+
+
 # call -> (TRI predicate, DENSE predicate) on the kernel name;
 # tri_rows_part<W, MODE, FULL, CL, RJ, TOE>, dense_rows<NU, NZ, MODE>
 _NCU_FULL = {
-    "tk_jacobi_sweep": (lambda k: "tri_rows_part<" in k and _targs(k)[1] == "0"
-                        and _targs(k)[4] == "0",
-                        lambda k: "dense_rows<" in k and _targs(k)[2] == "4"),
-    "tk_jacobi0_restrict": (lambda k: "tri_rows_part<" in k and _targs(k)[1] == "0"
-                            and _targs(k)[4] == "1",
-                            lambda k: "dense_rows<" in k and _targs(k)[2] == "4"),
+    "tk_jacobi_sweep": (lambda k: "tri_rows_part<" in k and _t(k, 1) in ("0", "3")
+                        and _t(k, 4) == "0" and _t(k, 6) == "0",
+                        lambda k: "dense_rows<" in k and _t(k, 2) == "4"),
+    "tk_jacobi0_restrict": (lambda k: "tri_rows_part<" in k and _t(k, 1) == "3"
+                            and _t(k, 4) == "1",
+                            lambda k: "dense_rows<" in k and _t(k, 2) == "4"),
+    "tk_jacobi0_restrict_um": (lambda k: "tri_rows_part<" in k and _t(k, 1) == "3"
+                               and _t(k, 4) == "1",
+                               lambda k: False),
+    "tk_jacobi_prolong": (lambda k: "tri_rows_part<" in k and _t(k, 1) == "3"
+                          and _t(k, 6) == "1",
+                          lambda k: False),
     "tk_residual_restrict": (lambda k: "tri_resrestrict" in k,
-                             lambda k: "dense_rows<" in k and _targs(k)[2] == "2"),
+                             lambda k: "dense_rows<" in k and _t(k, 2) == "2"),
     "tk_prolong_add": (lambda k: "prolong_rows_kernel" in k, lambda k: "prolong_small_kernel" in k),
     "tk_kkt_apply": (lambda k: "tri_apply<0" in k,
-                     lambda k: "dense_rows<" in k and _targs(k)[2] == "0"),
+                     lambda k: "dense_rows<" in k and _t(k, 2) == "0"),
     "tk_residual_restrict_jacobi0": (lambda k: "restrict_jacobi0_rows" in k,
                                      lambda k: "restrict_jacobi0_small" in k),
 }
-_NCU_NAMES = {"tk_jacobi_sweep": ("tri_rows_part<W, 0, ., CL, 0, .>", "dense_rows<NU, NZ, 4>"),
-              "tk_jacobi0_restrict": ("tri_rows_part<W, 0, ., CL, 1, .>", "dense_rows<NU, NZ, 4>"),
+_NCU_NAMES = {"tk_jacobi_sweep": ("tri_rows_part<W, 3, ., CL, 0, .>", "dense_rows<NU, NZ, 4>"),
+              "tk_jacobi0_restrict": ("tri_rows_part<W, 3, ., CL, 1, .>", "dense_rows<NU, NZ, 4>"),
+              "tk_jacobi0_restrict_um": ("tri_rows_part<W, 3, ., CL, 1, ., 0>", None),
+              "tk_jacobi_prolong": ("tri_rows_part<W, 3, ., CL, 0, ., 1>", None),
               "tk_residual_restrict": ("tri_resrestrict", "dense_rows<NU, NZ, 2>"),
               "tk_prolong_add": ("prolong_rows_kernel", "prolong_small_kernel"),
               "tk_kkt_apply": ("tri_apply<0>", "dense_rows<NU, NZ, 0>"),
@@ -289,7 +302,7 @@ def run_ours(args, rank, world, local_rank):
              "tk_backward_subst", "tk_sgs_back_half", "tk_kkt_apply", "tk_kkt_apply_diag",
              "tk_kkt_residual", "tk_dot", "tk_nrm2", "tk_axpy", "tk_scale_into", "tk_rsub",
              "tk_gemv_t_add", "tk_arnoldi_mgs", "tk_copy_kernel", "tk_residual_restrict_jacobi0",
-             "tk_jacobi0_restrict"}
+             "tk_jacobi0_restrict", "tk_jacobi0_restrict_um", "tk_jacobi_prolong"}
     # (eager cycles: the CUDA-graph replay hides the coarse levels' kernels)
     from paper_2405_04808_b200 import graph as G
     graph_on = G.ENABLED
@@ -316,7 +329,7 @@ def run_ours(args, rank, world, local_rank):
     fine_recs = {}
     for nm, a, e0, e1 in dev.INSTR.records:   # fine-level launch of each HBM kernel
         if nm in ("tk_jacobi_sweep", "tk_residual_restrict", "tk_residual_restrict_jacobi0",
-                  "tk_jacobi0_restrict"):
+                  "tk_jacobi0_restrict", "tk_jacobi0_restrict_um", "tk_jacobi_prolong"):
             lvl = roofline.dim_of(a[0]._obj)
         elif nm == "tk_prolong_add":
             lvl = int(a[0]) * (4 * int(a[1]) + int(a[2]))
@@ -344,7 +357,7 @@ def run_ours(args, rank, world, local_rank):
                            "on the coarsest level (SGS-GMRES: substitutions, operator, "
                            "Krylov vector kernels) over all calls"}
     dev.INSTR.timed, dev.INSTR.records = None, []
-    dominant = max(per, key=lambda k: per[k]["ms"])
+    dominant_eager = max(per, key=lambda k: per[k]["ms"])
     # the fine-level KKT mat-vec (the outer Krylov operator), timed on its own
     a0 = h.levels[0].kkt
     y0 = dev.empty(a0.dim)
@@ -360,7 +373,7 @@ def run_ours(args, rank, world, local_rank):
     clk = ClockSampler(local_rank)
     clk.start()
     time.sleep(0.3)
-    dev.INSTR.timed, dev.INSTR.records = {dominant, "tk_jacobi_sweep"}, []
+    dev.INSTR.timed, dev.INSTR.records = set(names), []
     dev.INSTR.counting, dev.INSTR.launches = True, 0
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -380,7 +393,9 @@ def run_ours(args, rank, world, local_rank):
 
     def kernel_stats(nm, fine_only=False):
         rs = [(a, s.elapsed_time(t)) for n_, a, s, t in recs if n_ == nm]
-        if fine_only and nm == "tk_jacobi_sweep":
+        if not rs:
+            return 0.0, float("nan"), 0
+        if fine_only:
             top = max(roofline.dim_of(a[0]._obj) for a, _ in rs)
             rs = [(a, ms) for a, ms in rs if roofline.dim_of(a[0]._obj) == top]
         byts = sum(roofline.algorithmic_bytes(nm, a) for a, _ in rs)
@@ -401,9 +416,19 @@ def run_ours(args, rank, world, local_rank):
                            "ncu_kernel": _NCU_NAMES[nm][0 if fam == 1 else 1]
                            if nm in _NCU_NAMES else None,
                            "traffic": tr, "traffic_source": tsrc}
+    # dominant kernel = the C-ABI call with the most device time among those
+    # launched in the timed region (the graphed coarse levels replay as one
+    # launch; their share is reported in `coarse_share`)
+    tot_by = {}
+    for n_, a, s_, t_ in recs:
+        tot_by[n_] = tot_by.get(n_, 0.0) + s_.elapsed_time(t_)
+    dominant = max(tot_by, key=tot_by.get)
     b_dom, ms_dom, n_dom = kernel_stats(dominant)
     ach = b_dom / (ms_dom * 1e-3) / 1e9
-    b_j, ms_j, n_j = kernel_stats("tk_jacobi_sweep", fine_only=True)
+    # the fine-level post-smoothing sweep (with the prolongation inside on V(1,1) levels)
+    jac_name = "tk_jacobi_prolong" if any(n_ == "tk_jacobi_prolong" for n_, *_ in recs) \
+        else "tk_jacobi_sweep"
+    b_j, ms_j, n_j = kernel_stats(jac_name, fine_only=True)
     ach_j = b_j / (ms_j * 1e-3) / 1e9
 
     # e2e through the public API with pinned host buffers: every step copies its
@@ -492,9 +517,9 @@ def run_ours(args, rank, world, local_rank):
                      "note": ("the Gauss-Seidel substitutions are serial in time (one CTA walks "
                               "the coarse intervals): latency-bound, not HBM-bound"
                               if "subst" in dominant else ""),
-                     "fine_jacobi": {"achieved": ach_j, "frac": ach_j / hbm,
+                     "fine_jacobi": {"call": jac_name, "achieved": ach_j, "frac": ach_j / hbm,
                                      "bytes_per_launch": b_j, "ms_per_launch": ms_j,
-                                     "traffic": ncu_traffic("tk_jacobi_sweep", args.config,
+                                     "traffic": ncu_traffic(jac_name, args.config,
                                                             fam)[0]}},
         "hbm_kernels": hbm_kernels,
         "kernels": {k: {"calls": v["calls"], "ms": round(v["ms"], 4),

@@ -213,6 +213,24 @@ int tk_jacobi0_restrict(const tk_level* L, const double* b, double omega, double
                         double* rc, void* stream);
 int tk_residual_restrict(const tk_level* L, const double* b, const double* x, double* rc,
                          double* work, void* stream);
+/* V(1,1) with omega = 1 (multigrid.py:284-299, one sweep each side): the
+ * post-smoothing sweep x + D^{-1}(b - A x) equals D^{-1}(b + (L + U) x), and
+ * (L + U) x reads only the continuity couplings u_{i-1}, mu_{i+1} of x.  So
+ * the prolongation x + P ec (multigrid.py:115-132, :297) folds into the sweep:
+ *   x_out = D^{-1}(b + (L + U)(x + P ec))
+ * reads the u and mu segments of x and of the coarse correction ec and never
+ * forms x + P ec in HBM (same arithmetic per element as tk_prolong_add then
+ * tk_jacobi_sweep with omega = 1).  tk_jacobi0_restrict_um is the matching
+ * pre-smoothing: tk_jacobi0_restrict storing ONLY the u and mu segments of
+ * its x (the other segments of x_um are left untouched), which is all the
+ * fused post-smoothing reads.  TRI levels with full partitioned rows (n_u a
+ * power-of-two multiple of 128 up to 2048), whole level, even N: check
+ * tk_jacobi_prolong_ok(), else TK_ERR_UNSUPPORTED. */
+int32_t tk_jacobi_prolong_ok(const tk_level* L, double omega);
+int tk_jacobi0_restrict_um(const tk_level* L, const double* b, double* x_um, double* rc,
+                           void* stream);
+int tk_jacobi_prolong(const tk_level* L, const double* b, const double* x, const double* ec,
+                      double* x_out, void* stream);
 
 /* --- Krylov vector kernels (krylov.py:77-191) ----------------------------- */
 /* Deterministic reductions: fixed grid, fixed order.  `out` is a device scalar.

@@ -28,7 +28,11 @@ int tri_launch(const tk_level*, int, const double*, const double*, double*, doub
 int64_t tri_smem_bytes(int n);
 int tri_resrestrict_launch(const tk_level*, const double*, const double*, double*, cudaStream_t);
 bool tri_jacobi0_restrict_ok(const tk_level*, double);
-int tri_jacobi0_restrict_launch(const tk_level*, const double*, double, double*, double*, cudaStream_t);
+int tri_jacobi0_restrict_launch(const tk_level*, const double*, double, double*, double*, cudaStream_t,
+                                int partial = 0);
+bool tri_jacobi_prolong_ok(const tk_level*, double);
+int tri_jacobi_prolong_launch(const tk_level*, const double*, const double*, const double*, double*,
+                              cudaStream_t);
 int dense_jacobi0_restrict(const tk_level*, const double*, double*, double*, cudaStream_t);
 int64_t tri_fac_len(const tk_level*);
 int64_t tri_scratch_len(const tk_level*);
@@ -172,6 +176,36 @@ int tk_jacobi0_restrict(const tk_level* L, const double* b, double omega, double
         return dense_jacobi0_restrict(L, b, x_out, rc, as_stream(stream));
     }
     return tri_jacobi0_restrict_launch(L, b, omega, x_out, rc, as_stream(stream));
+}
+
+int32_t tk_jacobi_prolong_ok(const tk_level* L, double omega) {
+    if (check_level(L)) return 0;
+    if (L->family != TK_FAMILY_TRI) return 0;
+    return tri_jacobi_prolong_ok(L, omega) ? 1 : 0;
+}
+
+int tk_jacobi0_restrict_um(const tk_level* L, const double* b, double* x_um, double* rc,
+                           void* stream) {
+    TK_CHECK_ARG(b && x_um && rc, "tk_jacobi0_restrict_um: null vector");
+    const int e = check_level(L);
+    if (e) return e;
+    if (L->family != TK_FAMILY_TRI || !tri_jacobi_prolong_ok(L, 1.0)) {
+        set_error("tk_jacobi0_restrict_um: level not supported (see tk_jacobi_prolong_ok)");
+        return TK_ERR_UNSUPPORTED;
+    }
+    return tri_jacobi0_restrict_launch(L, b, 1.0, x_um, rc, as_stream(stream), 1);
+}
+
+int tk_jacobi_prolong(const tk_level* L, const double* b, const double* x, const double* ec,
+                      double* x_out, void* stream) {
+    TK_CHECK_ARG(b && x && ec && x_out && x != x_out && b != x_out, "tk_jacobi_prolong: bad vectors");
+    const int e = check_level(L);
+    if (e) return e;
+    if (L->family != TK_FAMILY_TRI) {
+        set_error("tk_jacobi_prolong: TRI levels only");
+        return TK_ERR_UNSUPPORTED;
+    }
+    return tri_jacobi_prolong_launch(L, b, x, ec, x_out, as_stream(stream));
 }
 
 int tk_forward_subst(const tk_level* L, const double* r, double* delta, void* stream) {

@@ -1802,7 +1802,9 @@ static int carry_grid_launch(bool fwd, int n, int nc, const double* M, const dou
 
 int part_nodes_per_lane(int n);
 int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, double* y,
-                double omega, const double* chain, cudaStream_t s, double* rc = nullptr);
+                double omega, const double* chain, cudaStream_t s, double* rc = nullptr,
+                const double* ec = nullptr, int opt = 0);
+bool part_full_rows(const tk_level* Lv);
 
 // warp-per-row partitioned solves (tk_tri_part.cu) for 32 < n <= 512;
 // TK_PART=0 selects the CTA-wide cyclic-reduction kernels instead
@@ -2074,13 +2076,29 @@ bool tri_jacobi0_restrict_ok(const tk_level* Lv, double omega) {
            part_nodes_per_lane(n) > 0 && whole && (Lv->n_steps % 2) == 0 && Lv->n_steps >= 2;
 }
 int tri_jacobi0_restrict_launch(const tk_level* Lv, const double* b, double omega, double* y,
-                                double* rc, cudaStream_t s) {
+                                double* rc, cudaStream_t s, int partial) {
     if (!tri_jacobi0_restrict_ok(Lv, omega)) {
         set_error("tk_jacobi0_restrict: level not supported (TRI partitioned rows, whole level, "
                   "even N, omega = 1)");
         return TK_ERR_UNSUPPORTED;
     }
-    return part_launch(Lv, 0, b, nullptr, y, omega, nullptr, s, rc);
+    return part_launch(Lv, 0, b, nullptr, y, omega, nullptr, s, rc, nullptr, partial ? 1 : 0);
+}
+
+// y = D^{-1}(b + (L + U)(x + P ec)): the V-cycle's prolongation fused into
+// the omega = 1 post-smoothing sweep (tri_rows_part<..., PR>); only the u and
+// mu segments of x are read
+bool tri_jacobi_prolong_ok(const tk_level* Lv, double omega) {
+    return tri_jacobi0_restrict_ok(Lv, omega) && part_full_rows(Lv);
+}
+int tri_jacobi_prolong_launch(const tk_level* Lv, const double* b, const double* x,
+                              const double* ec, double* y, cudaStream_t s) {
+    if (!tri_jacobi_prolong_ok(Lv, 1.0)) {
+        set_error("tk_jacobi_prolong: level not supported (TRI partitioned full rows, whole "
+                  "level, even N)");
+        return TK_ERR_UNSUPPORTED;
+    }
+    return part_launch(Lv, 0, b, x, y, 1.0, nullptr, s, nullptr, ec, 0);
 }
 
 int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, double* y,

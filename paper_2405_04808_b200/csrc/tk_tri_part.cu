@@ -44,7 +44,7 @@ constexpr int kChunk = TK_PART_CHUNK;
 #define TK_PART_MINB 2           // CTAs per SM the W=4 build is register-limited to
 #endif
 #ifndef TK_PART_MINB3
-#define TK_PART_MINB3 3          // the same for the x-free rows (MODE 3: ~180 registers)
+#define TK_PART_MINB3 3          // the same for the x-free rows (MODE 1/2/3) up to W = 4
 #endif
 constexpr bool kStage = TK_PART_STAGE != 0;
 #ifndef TK_PART_PFD
@@ -69,9 +69,14 @@ struct PartCta {
     static constexpr int64_t smem_bytes() {
         return ((int64_t)(2 * kPX + (kStage ? kChunk * kSgC + kSgN : 0)) * T) * 8;
     }
+    // resident CTAs per SM the build is register-limited to.  The residual
+    // form (MODE 0, ~232 registers): 8 warps per SM.  The x-free rows (MODE
+    // 1/2/3): 164 registers for 12 warps per SM up to W = 4 and 128
+    // registers for 16 warps per SM at W = 8 / 16 (no spills).
     static constexpr int min_blocks(int mode = 0) {
-        return ((mode == 3 ? TK_PART_MINB3 : TK_PART_MINB) * 4) / W > 1
-                   ? ((mode == 3 ? TK_PART_MINB3 : TK_PART_MINB) * 4) / W : 1;
+        if (mode == 0) return (TK_PART_MINB * 4) / W > 1 ? (TK_PART_MINB * 4) / W : 1;
+        if (W >= 8) return 16 / W;
+        return (TK_PART_MINB3 * 4) / W;
     }
 };
 
@@ -299,11 +304,11 @@ extern "C" int tk_debug_part_prof(long long* out10) {
 // TOE (TK_FLAG_TOEPLITZ_W): the weights Qm, Ql, Qz have constant diagonals
 // (uniform P1 mass matrices), so each diagonal is one scalar per row instead
 // of per-node loads -- same values, same arithmetic, fewer loads/registers.
-template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE>
+template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE, bool PR>
 __global__ void __launch_bounds__(32 * W, PartCta<W>::min_blocks(MODE))
 tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ x,
               double* __restrict__ y, double omega, const double* __restrict__ chain,
-              double* __restrict__ rc) {
+              double* __restrict__ rc, int opt) {
     using Cf = PartCta<W>;
     constexpr int T = Cf::T;
     constexpr int TT = CL * T;                // interface nodes of a row
@@ -330,6 +335,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
     };
     const double kap = V.kappa, k2 = kap * kap;
     const double* Qz = V.Qz;
+    const bool px = RJ && (opt & 1);   // partial x: only the u and mu segments are stored
     double* PX[2] = {sm, sm + kPX * T};    // PCR ping-pong slots
     double* XB[1] = {PX[1]};               // exchange 1 (12 per thread; PX[1] is first written at step 2)
     double* SG = sm + 2 * kPX * T;         // staged vector data of the next row [kSgC*4 + kSgN][T]
@@ -380,6 +386,11 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 if (MODE == 3 && x) {   // only the two coupling segments of x
                     pf_l2(V.sl.uprev(L, x, i2), n);
                     pf_l2(V.sl.munext(L, x, i2), n);
+                    if (PR && (i2 & 1) == 0) {   // their coarse sources (even rows: new ones)
+                        const Lay Lp(L.N / 2, n, L.nz);
+                        if (i2 >= 2) pf_l2(chain + Lp.t_u(i2 / 2), n);
+                        if (i2 / 2 + 1 <= Lp.N) pf_l2(chain + Lp.t_mu(i2 / 2 + 1), n);
+                    }
                 }
             }
             if (i2 < L.N) {
@@ -404,6 +415,44 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         }
         const bool hx = MODE == 0 && x != nullptr;
         const bool hc = C != nullptr;
+        const Lay Lc(L.N / 2, n, L.nz);
+        // PR: the couplings are those of x + P e (e = chain, the coarse
+        // correction; multigrid.py:115-132): for the fine time t of the segment,
+        // even t adds coarse t/2, t = 1 coarse 1, odd t >= 3 the mean of coarse
+        // (t-1)/2 and (t+1)/2 -- the arithmetic of tk_prolong_add
+        const double *upa = nullptr, *upb = nullptr, *mna = nullptr, *mnb = nullptr;
+        if (PR) {
+            static_assert(!PR || (MODE == 3 && !kStage && !RJ), "PR: MODE 3 rows only");
+            if (uprev) {          // u_t, t = i
+                const int t = i;
+                if ((t & 1) == 0 || t == 1) upa = chain + Lc.t_u(t == 1 ? 1 : t / 2);
+                else { upa = chain + Lc.t_u((t - 1) / 2); upb = chain + Lc.t_u((t + 1) / 2); }
+            }
+            if (munext) {         // mu_t, t = i + 1
+                const int t = i + 1;
+                if ((t & 1) == 0 || t == 1) mna = chain + Lc.t_mu(t == 1 ? 1 : t / 2);
+                else { mna = chain + Lc.t_mu((t - 1) / 2); mnb = chain + Lc.t_mu((t + 1) / 2); }
+            }
+        }
+        // x' = x + P e on the chunk nodes / one node of a coupling segment
+        auto pr4 = [&](const double* ca, const double* cb, double (&r)[NA]) {
+            if (!PR || !ca) return;
+            double a4[NA];
+            ld4<FULL>(ca, 0, j0, n, true, a4);
+            if (cb) {
+                double b4[NA];
+                ld4<FULL>(cb, 0, j0, n, true, b4);
+#pragma unroll
+                for (int k = 0; k < NA; ++k) r[k] = r[k] + 0.5 * (a4[k] + b4[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NA; ++k) r[k] = r[k] + a4[k];
+            }
+        };
+        auto pr1 = [&](const double* ca, const double* cb, int j, double v) -> double {
+            if (!PR || !ca || j < 0 || j >= n) return v;
+            return cb ? v + 0.5 * (ca[j] + cb[j]) : v + ca[j];
+        };
         TKPP(0);
 
         // ---- phase 1: residual of the chunk in registers
@@ -472,11 +521,12 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 for (int k = 0; k < NA; ++k) xv[k] = 0.0;
             }
             g4(10, up);
+            pr4(upa, upb, up);
             // v at the chunk and its two neighbours
             double vv[NA];
             const double bmL = g1(0), bmR = g1(1);
             const double xvL = hx ? g1(2) : 0.0, xvR = hx ? g1(3) : 0.0;
-            const double upL = g1(4), upR = g1(5);
+            const double upL = pr1(upa, upb, jL, g1(4)), upR = pr1(upa, upb, jR, g1(5));
 #pragma unroll
             for (int k = 0; k < NA; ++k) vv[k] = -((rm[k] + xv[k]) - up[k]);
             const double vL = -((bmL + xvL) - upL), vR = -((bmR + xvR) - upR);
@@ -531,6 +581,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             } else if (has_uzl && munext) {
                 double mn[NA];
                 g4(11, mn);
+                pr4(mna, mnb, mn);
 #pragma unroll
                 for (int k = 0; k < NA; ++k) f0[k] -= mn[k];
             }
@@ -553,7 +604,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 if (hc) f1[k] -= cd[k] * vv[k] + cb[k] * vm + cs[k] * vp;
                 if (!in) { f0[k] = f1[k] = fw[k] = pm[k] = vv[k] = 0.0; }
             }
-            if (has_vm) {
+            if (has_vm && !px) {
                 double o[NA];
                 if (hx) {
 #pragma unroll
@@ -566,7 +617,6 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             }
         }
         TKPP(1);
-        const Lay Lc(L.N / 2, n, L.nz);
         if (RJ && (i & 1) == 0) {   // zeros of coarse row c = i/2: v_c, z_{c+1}, lam_{c+1}
             const int c = i / 2;
             double zr[NA];
@@ -894,12 +944,14 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 for (int k = 0; k < NA; ++k) o[k] = 0.0 - o[k];
                 st4<FULL>(rc, Lc.t_mu((i + 1) / 2), j0, n, o);
             }
+            if (!px) {
 #pragma unroll
-            for (int k = 0; k < NA; ++k) o[k] = oxz[k] + omega * (yw[k] - kap * yl[k]);
-            st4<FULL>(y, oz, j0, n, o);
+                for (int k = 0; k < NA; ++k) o[k] = oxz[k] + omega * (yw[k] - kap * yl[k]);
+                st4<FULL>(y, oz, j0, n, o);
 #pragma unroll
-            for (int k = 0; k < NA; ++k) o[k] = oxl[k] + omega * yl[k];
-            st4<FULL>(y, ol, j0, n, o);
+                for (int k = 0; k < NA; ++k) o[k] = oxl[k] + omega * yl[k];
+                st4<FULL>(y, ol, j0, n, o);
+            }
             if (has_vm) {
 #pragma unroll
                 for (int k = 0; k < NA; ++k) {
@@ -931,30 +983,29 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
 // ---------------------------------------------------------------------------
 // host dispatch
 // ---------------------------------------------------------------------------
-// warps per CTA and CTAs per row (cluster size): up to 8 warps (n_u <= 1024)
-// one CTA per row; 1024 < n_u <= 2048 a 2-CTA cluster of 8 warps each (one
-// CTA of 16 warps would need 512 threads x 255 registers)
-static int part_warps(int n) {
+// warps per CTA and CTAs per row (cluster size).  The x-free rows (modes
+// 1/2/3, 128 registers at W >= 8) take up to 16 warps, so n_u <= 2048 is one
+// CTA per row; the residual form (mode 0, ~232 registers) takes up to 8 warps
+// and splits 1024 < n_u <= 2048 over a 2-CTA cluster.
+static int part_wmax(int mode) { return mode == 0 ? 8 : 16; }
+static int part_warps(int n, int mode) {
     if (n <= 4 || n > 2 * kChunk * 32 * 8) return 0;
     int w = 1;
-    while (kChunk * 32 * w < n && w < 8) w <<= 1;
+    while (kChunk * 32 * w < n && w < part_wmax(mode)) w <<= 1;
     return w;
 }
-static int part_cluster(int n) { return n > kChunk * 32 * 8 ? 2 : 1; }
+static int part_cluster(int n, int mode) { return n > kChunk * 32 * part_wmax(mode) ? 2 : 1; }
 
-int part_nodes_per_lane(int n) { return part_warps(n) ? kChunk : 0; }
+int part_nodes_per_lane(int n) { return part_warps(n, 0) ? kChunk : 0; }
 
-template <int W, int MODE, bool FULL, int CL, bool RJ = false>
-static int part_launch_t(const tk_level* Lv, const double* b, const double* x, double* y,
-                         double omega, const double* chain, cudaStream_t s, double* rc = nullptr);
-template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE>
+template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE, bool PR>
 static int part_launch_tt(const tk_level* Lv, const double* b, const double* x, double* y,
-                          double omega, const double* chain, cudaStream_t s, double* rc) {
+                          double omega, const double* chain, cudaStream_t s, double* rc, int opt) {
     using Cf = PartCta<W>;
     static int per_sm = 0;
     static int nsm = 0;
     const int64_t smem = Cf::smem_bytes();
-    auto kern = tri_rows_part<W, MODE, FULL, CL, RJ, TOE>;
+    auto kern = tri_rows_part<W, MODE, FULL, CL, RJ, TOE, PR>;
     if (!per_sm) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // shared memory only as large as the resident CTAs need: the rest of the
@@ -986,7 +1037,7 @@ static int part_launch_tt(const tk_level* Lv, const double* b, const double* x, 
     const int cap = nsm * per_sm / CL;
     if (clusters > cap) clusters = cap;
     if (CL == 1) {
-        kern<<<clusters, 32 * W, smem, s>>>(V, b, x, y, omega, chain, rc);
+        kern<<<clusters, 32 * W, smem, s>>>(V, b, x, y, omega, chain, rc, opt);
         return check_launch("tri_rows_part");
     }
     cudaLaunchConfig_t cfg = {};
@@ -995,44 +1046,55 @@ static int part_launch_tt(const tk_level* Lv, const double* b, const double* x, 
     at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(clusters * CL); cfg.blockDim = dim3(32 * W); cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = s; cfg.attrs = at; cfg.numAttrs = 1;
-    return cuda_status(cudaLaunchKernelEx(&cfg, kern, V, b, x, y, omega, chain, rc),
+    return cuda_status(cudaLaunchKernelEx(&cfg, kern, V, b, x, y, omega, chain, rc, opt),
                        "tri_rows_part (cluster)");
 }
 
 // TOE only for FULL rows (every chunk inside the level, so the masked
 // boundary entries of the stored diagonals are never needed)
-template <int W, int MODE, bool FULL, int CL, bool RJ>
+template <int W, int MODE, bool FULL, int CL, bool RJ = false, bool PR = false>
 static int part_launch_t(const tk_level* Lv, const double* b, const double* x, double* y,
-                         double omega, const double* chain, cudaStream_t s, double* rc) {
+                         double omega, const double* chain, cudaStream_t s, double* rc = nullptr,
+                         int opt = 0) {
     if (FULL && (Lv->flags & TK_FLAG_TOEPLITZ_W))
-        return part_launch_tt<W, MODE, FULL, CL, RJ, FULL>(Lv, b, x, y, omega, chain, s, rc);
-    return part_launch_tt<W, MODE, FULL, CL, RJ, false>(Lv, b, x, y, omega, chain, s, rc);
+        return part_launch_tt<W, MODE, FULL, CL, RJ, FULL, PR>(Lv, b, x, y, omega, chain, s, rc, opt);
+    return part_launch_tt<W, MODE, FULL, CL, RJ, false, PR>(Lv, b, x, y, omega, chain, s, rc, opt);
 }
 
-// mode 0: rows (jacobi / D^{-1} b), 1/2: substitution pass 3 forward/backward
+// mode 0: rows (jacobi / D^{-1} b), 1/2: substitution pass 3 forward/backward;
+// rc: the zero-start sweep also writes its restricted residual (opt bit 0:
+// only the u and mu segments of y are stored); ec (mode 0, omega == 1): the
+// couplings are those of x + P ec (the V-cycle's prolongation fused into the
+// post-smoothing sweep)
 int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, double* y,
-                double omega, const double* chain, cudaStream_t s, double* rc) {
-#define TK_PART_CASE(WW, CC)                                                                        \
+                double omega, const double* chain, cudaStream_t s, double* rc, const double* ec,
+                int opt) {
+#define TK_PART_X(WW, CC)                                                                           \
     if (w == WW && cl == CC) {                                                                      \
         if (rc) {                                                                                   \
-            if (full) return part_launch_t<WW, 3, true, CC, true>(Lv, b, x, y, omega, chain, s, rc); \
-            return part_launch_t<WW, 3, false, CC, true>(Lv, b, x, y, omega, chain, s, rc);         \
+            if (full) return part_launch_t<WW, 3, true, CC, true>(Lv, b, x, y, omega, chain, s, rc, opt); \
+            return part_launch_t<WW, 3, false, CC, true>(Lv, b, x, y, omega, chain, s, rc, opt);    \
         }                                                                                           \
+        if (ec) return part_launch_t<WW, 3, true, CC, false, true>(Lv, b, x, y, omega, ec, s);      \
         if (full) {                                                                                 \
-            if (mode == 0) return part_launch_t<WW, 0, true, CC>(Lv, b, x, y, omega, chain, s);     \
             if (mode == 3) return part_launch_t<WW, 3, true, CC>(Lv, b, x, y, omega, chain, s);     \
             if (mode == 1) return part_launch_t<WW, 1, true, CC>(Lv, b, x, y, omega, chain, s);     \
-            return part_launch_t<WW, 2, true, CC>(Lv, b, x, y, omega, chain, s);                    \
+            if (mode == 2) return part_launch_t<WW, 2, true, CC>(Lv, b, x, y, omega, chain, s);     \
+        } else {                                                                                    \
+            if (mode == 3) return part_launch_t<WW, 3, false, CC>(Lv, b, x, y, omega, chain, s);    \
+            if (mode == 1) return part_launch_t<WW, 1, false, CC>(Lv, b, x, y, omega, chain, s);    \
+            if (mode == 2) return part_launch_t<WW, 2, false, CC>(Lv, b, x, y, omega, chain, s);    \
         }                                                                                           \
-        if (mode == 0) return part_launch_t<WW, 0, false, CC>(Lv, b, x, y, omega, chain, s);        \
-        if (mode == 3) return part_launch_t<WW, 3, false, CC>(Lv, b, x, y, omega, chain, s);        \
-        if (mode == 1) return part_launch_t<WW, 1, false, CC>(Lv, b, x, y, omega, chain, s);        \
-        return part_launch_t<WW, 2, false, CC>(Lv, b, x, y, omega, chain, s);                       \
+    }
+#define TK_PART_R(WW, CC)                                                                           \
+    if (mode == 0 && w == WW && cl == CC) {                                                         \
+        if (full) return part_launch_t<WW, 0, true, CC>(Lv, b, x, y, omega, chain, s);              \
+        return part_launch_t<WW, 0, false, CC>(Lv, b, x, y, omega, chain, s);                       \
     }
     // Jacobi with omega == 1 or from zero needs x only through the two
     // continuity couplings: x + D^{-1}(b - A x) = D^{-1}(b + (L + U) x), the
     // local solve of b with u_{i-1} / mu_{i+1} moved to the right-hand side
-    // (MODE 3: no D x products, no second read of x; 180 instead of 232
+    // (MODE 3: no D x products, no second read of x; 164 / 128 instead of 232
     // registers).  TK_JACOBI_RESIDUAL_FORM=1 keeps the residual form.
     static const bool resid_form = [] {
         const char* e = getenv("TK_JACOBI_RESIDUAL_FORM");
@@ -1040,25 +1102,46 @@ int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, 
     }();
     if (mode == 0 && (x == nullptr || (omega == 1.0 && !resid_form))) mode = 3;
     // FULL: every chunk is complete and every segment 16-byte aligned
-    const int w = part_warps(Lv->n_u), cl = part_cluster(Lv->n_u);
+    const int w = part_warps(Lv->n_u, mode), cl = part_cluster(Lv->n_u, mode);
     auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    if (rc && (mode != 3 || x || omega != 1.0 || Lv->row0 != 0 ||
-               (Lv->row1 != 0 && Lv->row1 != Lv->n_steps + 1) || (Lv->n_steps & 1))) {
+    const bool whole_even = Lv->row0 == 0 && (Lv->row1 == 0 || Lv->row1 == Lv->n_steps + 1) &&
+                            (Lv->n_steps & 1) == 0;
+    if (rc && (mode != 3 || x || omega != 1.0 || !whole_even)) {
         set_error("tri_rows_part: the fused restriction needs a zero-start sweep with omega = 1 "
                   "on a whole level with even N");
         return TK_ERR_UNSUPPORTED;
     }
     const bool full = w > 0 && Lv->n_u == kChunk * 32 * w * cl && Lv->n_u % 2 == 0 && Lv->n_z % 2 == 0 &&
-                      al(b) && al(x) && al(y) && al(chain) && al(rc) && al(Lv->K) && al(Lv->C) &&
-                      al(Lv->Qm) && al(Lv->Ql) && al(Lv->Qz) && al(Lv->halo_u) && al(Lv->halo_mu);
-    TK_PART_CASE(1, 1)
-    TK_PART_CASE(2, 1)
-    TK_PART_CASE(4, 1)
-    TK_PART_CASE(8, 1)
-    TK_PART_CASE(8, 2)
-#undef TK_PART_CASE
+                      al(b) && al(x) && al(y) && al(chain) && al(rc) && al(ec) && al(Lv->K) &&
+                      al(Lv->C) && al(Lv->Qm) && al(Lv->Ql) && al(Lv->Qz) && al(Lv->halo_u) &&
+                      al(Lv->halo_mu);
+    if (ec && (mode != 3 || !x || rc || !whole_even || !full)) {
+        set_error("tri_rows_part: the fused prolongation needs omega = 1, x, a whole level with "
+                  "even N and full 16-byte aligned rows");
+        return TK_ERR_UNSUPPORTED;
+    }
+    TK_PART_X(1, 1)
+    TK_PART_X(2, 1)
+    TK_PART_X(4, 1)
+    TK_PART_X(8, 1)
+    TK_PART_X(16, 1)
+    TK_PART_R(1, 1)
+    TK_PART_R(2, 1)
+    TK_PART_R(4, 1)
+    TK_PART_R(8, 1)
+    TK_PART_R(8, 2)
+#undef TK_PART_X
+#undef TK_PART_R
     set_error("tri_rows_part: unsupported n_u=%d", Lv->n_u);
     return TK_ERR_UNSUPPORTED;
+}
+
+// whether tk_jacobi_prolong's fused rows cover the level (full rows: n_u a
+// power-of-two multiple of 128 up to 2048, TOEPLITZ or not)
+bool part_full_rows(const tk_level* Lv) {
+    const int w = part_warps(Lv->n_u, 3);
+    return w > 0 && part_cluster(Lv->n_u, 3) == 1 && Lv->n_u == kChunk * 32 * w &&
+           Lv->n_z % 2 == 0;
 }
 
 }  // namespace tk

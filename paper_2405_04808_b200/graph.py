@@ -137,13 +137,22 @@ class VCycleGraph:
         return cur
 
     def _record_level(self, l, body_stream):
-        from .multigrid import JACOBI0_RESIDUAL, fused_jacobi0_ok
+        from .multigrid import JACOBI0_RESIDUAL, fused_jacobi0_ok, fused_v11_ok
         h = self.h
         L = h.n_levels
         a = h.levels[l].kkt
         s = dev.stream()
         if l == L - 1:
             self._record_coarse(a, self.B[l], self.E[l], body_stream)
+            return
+        if fused_v11_ok(h, a) and fused_jacobi0_ok(a, h.omega):
+            # V(1,1), omega = 1: pre-smoothing storing u / mu only, prolongation
+            # inside the post-smoothing sweep
+            dev.call("tk_jacobi0_restrict_um", a.lref, dev.P(self.B[l]), dev.P(self.X[l]),
+                     dev.P(self.B[l + 1]), s)
+            self._record_level(l + 1, body_stream)
+            dev.call("tk_jacobi_prolong", a.lref, dev.P(self.B[l]), dev.P(self.X[l]),
+                     dev.P(self.E[l + 1]), dev.P(self.E[l]), s)
             return
         # pre-smoothing from zero: X (sweeps 1) or X/Y ping-pong ending in X
         bufs = [self.X[l]] if h.sweeps == 1 else [self.X[l], self.Y[l]]
@@ -229,8 +238,12 @@ class VCycleGraph:
         self.per_coarse_iter = sgs + 1 + 1 + 1          # prec, apply, arnoldi, givens
         from .multigrid import fused_jacobi0_ok
         fixed = 0
+        from .multigrid import fused_v11_ok
         for l in range(self.start, h.n_levels - 1):     # sweeps, restrict, prolong
             fused = h.sweeps == 1 and fused_jacobi0_ok(h.levels[l].kkt, h.omega)
+            if fused and fused_v11_ok(h, h.levels[l].kkt):
+                fixed += 2
+                continue
             fixed += 2 * h.sweeps + (0 if fused else 1) + 1
         fixed += 2 + 1 + 1 + 2 + sgs + 1 + 1 + 2 * 2 + 1  # begin, combine, prec, apply, finish
         return fixed
@@ -271,7 +284,13 @@ def graphed_vcycle(h, b):
         h._graph = None
         g = h._graph = VCycleGraph(h)
     a = h.levels[0].kkt
-    if h.sweeps == 1 and JACOBI0_RESIDUAL and fused_jacobi0_ok(a, h.omega):
+    from .multigrid import fused_v11_ok
+    v11 = fused_v11_ok(h, a) and fused_jacobi0_ok(a, h.omega)
+    if v11:
+        x = dev.empty(a.dim)
+        dev.call("tk_jacobi0_restrict_um", a.lref, dev.P(b), dev.P(x), dev.P(g.B[1]),
+                 dev.stream())
+    elif h.sweeps == 1 and JACOBI0_RESIDUAL and fused_jacobi0_ok(a, h.omega):
         x = dev.empty(a.dim)
         dev.call("tk_jacobi0_restrict", a.lref, dev.P(b), float(h.omega), dev.P(x),
                  dev.P(g.B[1]), dev.stream())
@@ -288,8 +307,14 @@ def graphed_vcycle(h, b):
     g.run()
     if dev.INSTR.counting:
         dev.INSTR.launches += g.launches
-    h.transfers[0].prolong_add(g.E[1], x)
-    x = jacobi_sweeps(a, b, x, h.sweeps, h.omega)
+    if v11:
+        y = dev.empty(a.dim)
+        dev.call("tk_jacobi_prolong", a.lref, dev.P(b), dev.P(x), dev.P(g.E[1]), dev.P(y),
+                 dev.stream())
+        x = y
+    else:
+        h.transfers[0].prolong_add(g.E[1], x)
+        x = jacobi_sweeps(a, b, x, h.sweeps, h.omega)
     its = g.result()
     if its < 0:
         return None

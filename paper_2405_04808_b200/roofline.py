@@ -16,6 +16,9 @@ constant weights counted as cache hits (0 bytes).  ``dim = N*(4nu+nz)``.
   restrict                 8*(coarse_dim + Nc*nz) read + 8*coarse_dim write
   prolong_add              8*(2*fine_dim + coarse_dim)
   jacobi0_restrict         8*dim*2 + 8*coarse_dim + stage (zero-start sweep + restricted residual)
+  jacobi0_restrict_um      8*dim + 16*N*nu (u, mu of x) + 8*coarse_dim + stage
+  jacobi_prolong           8*dim*2 + 16*N*nu (u, mu of x) + 8*N*nu (u, mu of the coarse
+                           correction: 2 segments per coarse row) + stage
   dot 16n, nrm2 8n, axpy 24n, scale_into 16n, rsub 24n, gemv_t_add 8n(k+2)
 """
 
@@ -48,6 +51,13 @@ def algorithmic_bytes(name: str, args) -> int:
         L = _lvl(args[0])
         cdim = (L.n_steps // 2) * (4 * L.n_u + L.n_z)
         return 8 * dim_of(L) * 2 + 8 * cdim + stage_bytes(L)
+    if name == "tk_jacobi0_restrict_um":   # b read; u, mu of x and the coarse rhs written
+        L = _lvl(args[0])
+        cdim = (L.n_steps // 2) * (4 * L.n_u + L.n_z)
+        return 8 * dim_of(L) + 16 * L.n_steps * L.n_u + 8 * cdim + stage_bytes(L)
+    if name == "tk_jacobi_prolong":        # b, u/mu of x and of ec read; x_out written
+        L = _lvl(args[0])
+        return 8 * dim_of(L) * 2 + 16 * L.n_steps * L.n_u + 8 * L.n_steps * L.n_u + stage_bytes(L)
     if name in ("tk_diag_solve", "tk_forward_subst", "tk_backward_subst", "tk_sgs_back_half",
                 "tk_kkt_apply", "tk_kkt_apply_diag"):
         L = _lvl(args[0])
