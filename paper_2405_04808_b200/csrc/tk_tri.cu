@@ -1413,12 +1413,29 @@ static int chain_nc(int N, int Lc) {
     if (Lc <= 0 || K <= 0) return 1;
     return (K + Lc - 1) / Lc;
 }
-int64_t tri_chain_prod_len(const tk_level* Lv) {
-    if (Lv->chain_chunk <= 0) return 0;
+// warp-per-chunk chain with precomputed partition factors (tk_tri_chainw.cu)
+int chainw_nodes(int n);
+int64_t chainw_len(const tk_level* Lv);
+int chainw_factor(const tk_level* Lv, double* facw, cudaStream_t s);
+int chainw_launch(const tk_level* Lv, bool fwd, const double* a, const double* facw, double* chain,
+                  int Lc, int grid, int cbase, const double* st, double* en, cudaStream_t s);
+
+// P, P^T, ends, starts, U_t, counters | Phi, Phi^T, group ends, group starts
+static int64_t chain_prod_base_len(const tk_level* Lv) {
     const int64_t n = Lv->n_u, nc = chain_nc(Lv->n_steps, Lv->chain_chunk);
     const int64_t ng = chain_ng((int)nc, carry_group((int)n, (int)nc));
-    // P, P^T, ends, starts, U_t, counters | Phi, Phi^T, group ends, group starts
-    return 2 * nc * n * n + 3 * nc * n + 4 + 2 * ng * n * n + 2 * ng * n;
+    const int64_t len = 2 * nc * n * n + 3 * nc * n + 4 + 2 * ng * n * n + 2 * ng * n;
+    return (len + 1) & ~(int64_t)1;   // the warp-chain records that follow are TMA sources (16 B)
+}
+int64_t tri_chain_prod_len(const tk_level* Lv) {
+    if (Lv->chain_chunk <= 0) return 0;
+    return chain_prod_base_len(Lv) + chainw_len(Lv);
+}
+// the level's warp-chain records (null: tri_chain_kernel runs the chain)
+static double* chainw_records(const tk_level* Lv) {
+    if (!Lv->chain_prod || Lv->chain_chunk <= 0 || chainw_len(Lv) == 0) return nullptr;
+    if (reinterpret_cast<uintptr_t>(Lv->chain_prod) & 15) return nullptr;
+    return Lv->chain_prod + chain_prod_base_len(Lv);
 }
 
 // ---------------------------------------------------------------------------
@@ -1952,8 +1969,15 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             double* E = chunked ? PT + (size_t)nc * n * n : nullptr;
             double* S = chunked ? E + (size_t)nc * n : nullptr;
             const double* av = sgsb ? b : y;   // D^{-1} r of pass 1 (or w itself)
+            const double* facw = chainw_records(Lv);
+            int cw_rc = TK_OK;
             auto chain_launch = [&](int grid, int cbase, const double* st, double* en) {
                 if (grid <= 0) return;
+                if (facw) {   // one warp per chunk, precomputed partition factors
+                    const int e = chainw_launch(Lv, fwd, av, facw, chn, Lc, grid, cbase, st, en, s);
+                    if (e) cw_rc = e;
+                    return;
+                }
                 if (stg) {
                     if (fwd) tri_chain_kernel<true, true, false, NT><<<grid, cth, csm, s>>>(V, av, fac, chn, Lc, cbase, st, en);
                     else tri_chain_kernel<false, true, false, NT><<<grid, cth, csm, s>>>(V, av, fac, chn, Lc, cbase, st, en);
@@ -1987,6 +2011,7 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                 if (rc) return rc;
                 chain_launch(nc - 1, fwd ? 1 : 0, S, nullptr);   // non-seed chunks again
             }
+            if (cw_rc) return cw_rc;
             // pass 3: parallel solves with the chain coupling
             if (sgsb) {
                 tri_rows_rec_sgsb<NT><<<rows, rth, rsm, s>>>(V, b, chn, y);
@@ -2033,6 +2058,10 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                 return TK_ERR_ARG;
             }
             const int N = Lv->n_steps, Lc = Lv->chain_chunk, nc = chain_nc(N, Lc);
+            if (double* fw = chainw_records(Lv)) {
+                const int e = chainw_factor(Lv, fw, s);
+                if (e) return e;
+            }
             {
                 double* cntp = Lv->chain_prod + 2 * (size_t)nc * n * n + 3 * (size_t)nc * n;
                 const cudaError_t e = cudaMemsetAsync(cntp, 0, 4 * sizeof(double), s);
