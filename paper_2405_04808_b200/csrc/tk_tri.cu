@@ -2013,7 +2013,10 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
             }
             if (cw_rc) return cw_rc;
             // pass 3: parallel solves with the chain coupling
-            if (sgsb) {
+            if (sgsb && !rec && use_part(n) && y != b) {   // y = w - D^{-1} U y_{+1}: partitioned rows
+                const int rc = part_launch(Lv, 4, nullptr, b, y, 1.0, chn, s);
+                if (rc) return rc;
+            } else if (sgsb) {
                 tri_rows_rec_sgsb<NT><<<rows, rth, rsm, s>>>(V, b, chn, y);
             } else if (rec) {
                 if (fwd) tri_rows_rec_cpl<true, NT><<<rows, rth, rsm, s>>>(V, b, chn, y);

@@ -73,7 +73,8 @@ struct PartCta {
     // form (MODE 0, ~232 registers): 8 warps per SM.  The x-free rows (MODE
     // 1/2/3): 164 registers for 12 warps per SM up to W = 4 and 128
     // registers for 16 warps per SM at W = 8 / 16 (no spills).
-    static constexpr int min_blocks(int mode = 0) {
+    static constexpr int min_blocks(int mode = 0, int mb = 0) {
+        if (mb > 0) return mb;
         if (mode == 0) return (TK_PART_MINB * 4) / W > 1 ? (TK_PART_MINB * 4) / W : 1;
         if (W >= 8) return 16 / W;
         return (TK_PART_MINB3 * 4) / W;
@@ -280,7 +281,12 @@ extern "C" int tk_debug_part_prof(long long* out10) {
 // MODE 3: Jacobi with omega = 1, D^{-1}(b + (L + U) x): x enters through the
 // coupling segments u_{i-1}, mu_{i+1} only (x == nullptr: D^{-1} b, scaled by omega);
 // MODE 1 / 2: pass 3 of the forward / backward substitution (coupling from
-// the chain vector, no update).
+// the chain vector, no update);
+// MODE 4: pass 3 of the SGS back half (D - U)^{-1} D w (smoothers.py:130-152):
+// y_i = w_i - D_i^{-1} U_i y_{i+1}, i.e. MODE 2 with a zero right-hand side
+// (b == nullptr) on top of the base vector x = w;
+// MB > 0: resident CTAs per SM forced (4: 128 registers) so that a level of
+// at most 4 x 148 rows runs as ONE wave instead of two.
 //
 // Every phase works in chunk order: thread t owns nodes [4t, 4t+4) of every
 // segment, loaded with two 16-byte loads per segment (all of a block row's
@@ -304,8 +310,8 @@ extern "C" int tk_debug_part_prof(long long* out10) {
 // TOE (TK_FLAG_TOEPLITZ_W): the weights Qm, Ql, Qz have constant diagonals
 // (uniform P1 mass matrices), so each diagonal is one scalar per row instead
 // of per-node loads -- same values, same arithmetic, fewer loads/registers.
-template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE, bool PR>
-__global__ void __launch_bounds__(32 * W, PartCta<W>::min_blocks(MODE))
+template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE, bool PR, int MB>
+__global__ void __launch_bounds__(32 * W, PartCta<W>::min_blocks(MODE, MB))
 tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ x,
               double* __restrict__ y, double omega, const double* __restrict__ chain,
               double* __restrict__ rc, int opt) {
@@ -381,8 +387,8 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             if (!kStage) {
                 const int64_t q0 = L.start(i2) - bs;
                 const int64_t q1 = (i2 == L.N ? L.dim() : L.start(i2 + 1)) - bs;
-                pf_l2(b + q0, q1 - q0);
-                if (MODE == 0 && x) pf_l2(x + q0, q1 - q0);
+                if (b) pf_l2(b + q0, q1 - q0);
+                if ((MODE == 0 || MODE == 4) && x) pf_l2(x + q0, q1 - q0);
                 if (MODE == 3 && x) {   // only the two coupling segments of x
                     pf_l2(V.sl.uprev(L, x, i2), n);
                     pf_l2(V.sl.munext(L, x, i2), n);
@@ -472,11 +478,11 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 }
                 const bool up = has_vm && uprev != nullptr, mnx = has_uzl && munext != nullptr;
                 switch (a) {
-                    case 0: ld4<FULL>(b, ov, j0, n, has_vm, r); break;
-                    case 1: ld4<FULL>(b, om, j0, n, has_vm, r); break;
-                    case 2: ld4<FULL>(b, ou, j0, n, has_uzl, r); break;
-                    case 3: ld4<FULL>(b, oz, j0, n, has_uzl, r); break;
-                    case 4: ld4<FULL>(b, ol, j0, n, has_uzl, r); break;
+                    case 0: ld4<FULL>(b, ov, j0, n, has_vm && MODE != 4, r); break;
+                    case 1: ld4<FULL>(b, om, j0, n, has_vm && MODE != 4, r); break;
+                    case 2: ld4<FULL>(b, ou, j0, n, has_uzl && MODE != 4, r); break;
+                    case 3: ld4<FULL>(b, oz, j0, n, has_uzl && MODE != 4, r); break;
+                    case 4: ld4<FULL>(b, ol, j0, n, has_uzl && MODE != 4, r); break;
                     case 5: ld4<FULL>(x, ov, j0, n, has_vm, r); break;
                     case 6: ld4<FULL>(x, ou, j0, n, has_uzl, r); break;
                     case 7: ld4<FULL>(x, oz, j0, n, has_uzl, r); break;
@@ -490,8 +496,8 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 if (kStage) return sgn[a * T];
                 const bool up = has_vm && uprev != nullptr;
                 switch (a) {
-                    case 0: return ld1(b, om, jL, n, has_vm);
-                    case 1: return ld1(b, om, jR, n, has_vm);
+                    case 0: return ld1(b, om, jL, n, has_vm && MODE != 4);
+                    case 1: return ld1(b, om, jR, n, has_vm && MODE != 4);
                     case 2: return ld1(x, ov, jL, n, has_vm);
                     case 3: return ld1(x, ov, jR, n, has_vm);
                     case 4: return ld1(uprev, 0, jL, n, up);
@@ -609,6 +615,10 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 if (hx) {
 #pragma unroll
                     for (int k = 0; k < NA; ++k) o[k] = xv[k] + omega * vv[k];
+                } else if (MODE == 4) {   // base w (v itself is zero: no rhs, no u coupling)
+                    ld4<FULL>(x, ov, j0, n, true, o);
+#pragma unroll
+                    for (int k = 0; k < NA; ++k) o[k] = o[k] + omega * vv[k];
                 } else {
 #pragma unroll
                     for (int k = 0; k < NA; ++k) o[k] = omega * vv[k];
@@ -630,7 +640,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         }
         if (!has_uzl) {   // last block (v_N, mu_N): mu = Qv v - r_v
             double xm[NA], o[NA];
-            ld4<FULL>(x, om, j0, n, hx, xm);
+            ld4<FULL>(x, om, j0, n, hx || MODE == 4, xm);
 #pragma unroll
             for (int k = 0; k < NA; ++k) o[k] = xm[k] + omega * pm[k];
             st4<FULL>(y, om, j0, n, o);
@@ -797,7 +807,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         }
 #if TK_PART_EARLY
         // the output's loads, issued early: their latency overlaps the interface solve
-        const bool hxu = MODE == 0 && x != nullptr;
+        const bool hxu = (MODE == 0 || MODE == 4) && x != nullptr;
         double oxu[NA], oxz[NA], oxl[NA], oxm[NA], ocd[NA], ocs[NA], ocb[NA];
         ld4<FULL>(x, ou, j0, n, hxu, oxu);
         ld4<FULL>(x, oz, j0, n, hxu, oxz);
@@ -921,7 +931,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         TKPP(7);
 #if !TK_PART_EARLY
         // the output's loads, issued early: their latency overlaps the interface solve
-        const bool hxu = MODE == 0 && x != nullptr;
+        const bool hxu = (MODE == 0 || MODE == 4) && x != nullptr;
         double oxu[NA], oxz[NA], oxl[NA], oxm[NA], ocd[NA], ocs[NA], ocb[NA];
         ld4<FULL>(x, ou, j0, n, hxu, oxu);
         ld4<FULL>(x, oz, j0, n, hxu, oxz);
@@ -998,14 +1008,14 @@ static int part_cluster(int n, int mode) { return n > kChunk * 32 * part_wmax(mo
 
 int part_nodes_per_lane(int n) { return part_warps(n, 0) ? kChunk : 0; }
 
-template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE, bool PR>
+template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE, bool PR, int MB = 0>
 static int part_launch_tt(const tk_level* Lv, const double* b, const double* x, double* y,
                           double omega, const double* chain, cudaStream_t s, double* rc, int opt) {
     using Cf = PartCta<W>;
     static int per_sm = 0;
     static int nsm = 0;
     const int64_t smem = Cf::smem_bytes();
-    auto kern = tri_rows_part<W, MODE, FULL, CL, RJ, TOE, PR>;
+    auto kern = tri_rows_part<W, MODE, FULL, CL, RJ, TOE, PR, MB>;
     if (!per_sm) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // shared memory only as large as the resident CTAs need: the rest of the
@@ -1013,7 +1023,7 @@ static int part_launch_tt(const tk_level* Lv, const double* b, const double* x, 
         // read through it)
         int carve = cudaSharedmemCarveoutMaxShared;
         if (!kStage) {
-            const int64_t need = (int64_t)Cf::min_blocks(MODE) * (smem + 1024);
+            const int64_t need = (int64_t)Cf::min_blocks(MODE, MB) * (smem + 1024);
             carve = (int)((100 * need + 228 * 1024 - 1) / (228 * 1024)) + 1;
             if (carve > 100) carve = 100;
         }
@@ -1056,8 +1066,24 @@ template <int W, int MODE, bool FULL, int CL, bool RJ = false, bool PR = false>
 static int part_launch_t(const tk_level* Lv, const double* b, const double* x, double* y,
                          double omega, const double* chain, cudaStream_t s, double* rc = nullptr,
                          int opt = 0) {
-    if (FULL && (Lv->flags & TK_FLAG_TOEPLITZ_W))
+    if (FULL && (Lv->flags & TK_FLAG_TOEPLITZ_W)) {
+        if (W == 4 && MODE != 0 && !RJ && !PR) {
+            // a short level (the coarsest one: 513 rows at configs[2]): 4 CTAs per SM
+            // hold every row at once; 3 per SM would run 444 rows, then 69
+            static int nsm = 0;
+            if (!nsm) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            }
+            const int r1 = Lv->row1 > 0 ? Lv->row1 : Lv->n_steps + 1;
+            const int rows = r1 - Lv->row0;
+            if (rows > 3 * nsm && rows <= 4 * nsm)
+                return part_launch_tt<W, MODE, FULL, CL, RJ, FULL, PR, (W == 4 && MODE != 0 && !RJ && !PR) ? 4 : 0>(
+                    Lv, b, x, y, omega, chain, s, rc, opt);
+        }
         return part_launch_tt<W, MODE, FULL, CL, RJ, FULL, PR>(Lv, b, x, y, omega, chain, s, rc, opt);
+    }
     return part_launch_tt<W, MODE, FULL, CL, RJ, false, PR>(Lv, b, x, y, omega, chain, s, rc, opt);
 }
 
@@ -1080,10 +1106,12 @@ int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, 
             if (mode == 3) return part_launch_t<WW, 3, true, CC>(Lv, b, x, y, omega, chain, s);     \
             if (mode == 1) return part_launch_t<WW, 1, true, CC>(Lv, b, x, y, omega, chain, s);     \
             if (mode == 2) return part_launch_t<WW, 2, true, CC>(Lv, b, x, y, omega, chain, s);     \
+            if (mode == 4) return part_launch_t<WW, 4, true, CC>(Lv, b, x, y, omega, chain, s);     \
         } else {                                                                                    \
             if (mode == 3) return part_launch_t<WW, 3, false, CC>(Lv, b, x, y, omega, chain, s);    \
             if (mode == 1) return part_launch_t<WW, 1, false, CC>(Lv, b, x, y, omega, chain, s);    \
             if (mode == 2) return part_launch_t<WW, 2, false, CC>(Lv, b, x, y, omega, chain, s);    \
+            if (mode == 4) return part_launch_t<WW, 4, false, CC>(Lv, b, x, y, omega, chain, s);    \
         }                                                                                           \
     }
 #define TK_PART_R(WW, CC)                                                                           \
