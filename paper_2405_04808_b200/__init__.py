@@ -17,7 +17,9 @@ from .errors import (Breakdown, ConfigError, DimensionMismatch, IndivisibleSteps
 from .timedisc import ProblemSpec, TimeGrid, Trajectory, forward_solve
 from .problems import BurgersConfig, VanDerPolConfig, build_burgers, build_vanderpol
 from .kkt import (BlockTriKKT, DiagonalSolver, KktLayout, StageBlocks, assemble_kkt,
-                  build_stage_blocks, stage_blocks_from_arrays)
+                  assemble_rhs, build_stage_blocks, check_theorem1, clustered_permutation,
+                  dump_matrix_market, factor_diagonal, from_clustered, split_parts,
+                  stage_blocks_from_arrays, to_clustered)
 from .krylov import LinearOperator, Preconditioner, SolveReport, fgmres, gmres
 from .smoothers import (bgs_apply, fgs_apply, jacobi_apply, sgs_apply,
                         smoother_preconditioner)
@@ -32,7 +34,9 @@ __all__ = [
     "ProblemSpec", "TimeGrid", "Trajectory", "forward_solve",
     "BurgersConfig", "VanDerPolConfig", "build_burgers", "build_vanderpol",
     "BlockTriKKT", "DiagonalSolver", "KktLayout", "StageBlocks", "assemble_kkt",
-    "build_stage_blocks", "stage_blocks_from_arrays",
+    "build_stage_blocks", "stage_blocks_from_arrays", "assemble_rhs", "check_theorem1",
+    "clustered_permutation", "dump_matrix_market", "factor_diagonal", "from_clustered",
+    "split_parts", "to_clustered",
     "LinearOperator", "Preconditioner", "SolveReport", "fgmres", "gmres",
     "bgs_apply", "fgs_apply", "jacobi_apply", "sgs_apply", "smoother_preconditioner",
     "MgHierarchy", "TransferOps", "build_hierarchy", "coarse_solve", "cycle",

@@ -693,3 +693,123 @@ def _check_blocks(a: BlockTriKKT, pivot_floor: float) -> None:
                 raise UnsupportedStructure(
                     f"TRI local solves need SPD weights ({name} is not); the reference "
                     "would factor these blocks by pivoted LU")
+
+
+# ---------------------------------------------------------------------------
+# Splitting views, orderings, right-hand side assembly, debugging dump
+# (kkt.py:323-335, 392-493, 546-560): callers of the path, host-side helpers
+# ---------------------------------------------------------------------------
+KINDS = ("u", "v", "z", "lam", "mu")
+
+
+def factor_diagonal(a: BlockTriKKT, pivot_floor: float = PIVOT_FLOOR) -> "DiagonalSolver":
+    """Verified block-diagonal solver of ``a`` (kkt.py:323-335).  The
+    reference returns per-block pivoted LU factors; here the local KKT solves
+    are refactored on the device at every application, so the "factors" are
+    the checked :class:`DiagonalSolver` (``solve_block(i, r)`` /
+    ``solve_all(r)``).  Raises :class:`SingularBlock` with the offending block
+    index exactly when the reference's factorisation does."""
+    return DiagonalSolver(a, pivot_floor)
+
+
+def split_parts(a: BlockTriKKT):
+    """Operator views (D, L, U) of A = D - L - U (kkt.py:392-425): D is the
+    block diagonal (tk_kkt_apply_diag), L and U the negated strictly lower /
+    upper parts, i.e. the continuity couplings (L x)_mu = -x_u, (U x)_u = -x_mu."""
+    from .krylov import LinearOperator
+    lay = a.layout
+    iu = torch.from_numpy(lay.rows("u").reshape(-1)).to(dev.device())
+    im = torch.from_numpy(lay.rows("mu").reshape(-1)).to(dev.device())
+
+    def _wrap(fn):
+        def apply(x):
+            host = dev.is_host(x)
+            xd = dev.to_device(x)
+            a._chk(xd)
+            y = fn(xd)
+            return dev.to_host(y) if host else y
+        return apply
+
+    def lower_neg(x):
+        y = torch.zeros_like(x)
+        y[im] = -x[iu]
+        return y
+
+    def upper_neg(x):
+        y = torch.zeros_like(x)
+        y[iu] = -x[im]
+        return y
+
+    return (LinearOperator(dim=lay.dim, apply=_wrap(a.apply_diag)),
+            LinearOperator(dim=lay.dim, apply=_wrap(lower_neg)),
+            LinearOperator(dim=lay.dim, apply=_wrap(upper_neg)))
+
+
+def _clustered_rows(n: int, nu: int, nz: int) -> dict:
+    """Index arrays of the variable-clustered ordering (kkt.py:428-440):
+    (u_t, v_t) pairs over time, then every z_t, then (lam_t, mu_t) pairs."""
+    t = np.arange(n)[:, None]
+    ku, kz = np.arange(nu)[None, :], np.arange(nz)[None, :]
+    mult = 2 * n * nu + n * nz
+    return {"u": 2 * nu * t + ku, "v": 2 * nu * t + nu + ku, "z": 2 * n * nu + nz * t + kz,
+            "lam": mult + 2 * nu * t + ku, "mu": mult + 2 * nu * t + nu + ku}
+
+
+def clustered_permutation(nu: int, nz: int, n: int) -> np.ndarray:
+    """``perm`` with ``x_time_clustered = x_variable_clustered[perm]`` (kkt.py:443-450)."""
+    lay = KktLayout(n, nu, nz)
+    src = _clustered_rows(n, nu, nz)
+    perm = np.empty(lay.dim, dtype=np.intp)
+    for kind in KINDS:
+        perm[lay.rows(kind).ravel()] = src[kind].ravel()
+    return perm
+
+
+def _check_len(x, nu, nz, n):
+    x = np.asarray(x)
+    dim = n * (4 * nu + nz)
+    if x.shape != (dim,):
+        raise DimensionMismatch(f"vector shape {x.shape} != ({dim},)")
+    return x
+
+
+def from_clustered(x_clustered, nu: int, nz: int, n: int) -> np.ndarray:
+    """Variable-clustered -> time-clustered ordering (kkt.py:453-459)."""
+    return _check_len(x_clustered, nu, nz, n)[clustered_permutation(nu, nz, n)]
+
+
+def to_clustered(x_ordered, nu: int, nz: int, n: int) -> np.ndarray:
+    """Inverse of :func:`from_clustered` (kkt.py:462-470)."""
+    x = _check_len(x_ordered, nu, nz, n)
+    out = np.empty_like(x)
+    out[clustered_permutation(nu, nz, n)] = x
+    return out
+
+
+def assemble_rhs(s: StageBlocks, b1, b1v, b2, b3, b4) -> np.ndarray:
+    """Right-hand side in the time-clustered ordering (kkt.py:473-493): the
+    targets b1, b1v, b2 enter weighted by Q_u, Q_v, Q_z on the u, v, z rows,
+    the dynamics and continuity residuals b3, b4 fill the lam and mu rows."""
+    n, nu, nz = s.n_steps, s.n_u, s.n_z
+    lay = KktLayout(n, nu, nz)
+    rhs = np.empty(lay.dim)
+    for kind, q, t, w in (("u", s.q_u, b1, nu), ("v", s.q_v, b1v, nu), ("z", s.q_z, b2, nz)):
+        t = np.asarray(t, dtype=np.float64).reshape(n, w)
+        rhs[lay.rows(kind)] = np.einsum("tij,tj->ti", q, t)
+    rhs[lay.rows("lam")] = np.asarray(b3, dtype=np.float64).reshape(n, nu)
+    rhs[lay.rows("mu")] = np.asarray(b4, dtype=np.float64).reshape(n, nu)
+    return rhs
+
+
+def dump_matrix_market(a: BlockTriKKT, path: str) -> None:
+    """Coordinate-format text dump of the dense materialisation, for small N
+    (kkt.py:546-560): MatrixMarket header, ``rows cols nnz``, 1-based entries."""
+    dense = a.materialize()
+    ii, jj = np.nonzero(dense)
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write("%%MatrixMarket matrix coordinate real general\n")
+        fh.write(f"% block-tridiagonal augmented system, N={a.n_steps} "
+                 f"n_u={a.n_u} n_z={a.n_z}\n")
+        fh.write(f"{dense.shape[0]} {dense.shape[1]} {ii.size}\n")
+        for i, j in zip(ii, jj):
+            fh.write(f"{i + 1} {j + 1} {dense[i, j]:.17g}\n")

@@ -35,7 +35,7 @@ def launches(path):
     # one-off hierarchy setup (stage linearisation, factor records, chunk and
     # group propagators) is listed but excluded from the V-cycle shares
     setup = ("tri_chain_kernel<1, 0, 1,", "tri_factor_kernel", "stage_", "tri_transpose",
-             "check_k_kernel", "check_blocks_kernel", "FillFunctor")
+             "check_k_kernel", "check_blocks_kernel", "FillFunctor", "tri_chainw_factor")
     is_setup = {k: any(s in k for s in setup) for k in per}
     tot = sum(d["ns"] for k, d in per.items() if not is_setup[k])
     out = []

@@ -32,5 +32,14 @@ dev.call("tk_residual_restrict_jacobi0", a.lref, dev.P(b), dev.P(x0), 1.0, dev.P
 x2 = dev.empty(a.dim)
 dev.call("tk_jacobi0_restrict", a.lref, dev.P(b), 1.0, dev.P(x2), dev.P(rc),
          dev.stream())                            # tri_rows_part<..., RJ>: sweep + restriction
+from paper_2405_04808_b200 import _lib  # noqa: E402
+if a.family == 1 and _lib.load().tk_jacobi_prolong_ok(a.lref, 1.0):
+    x3 = dev.empty(a.dim)
+    dev.call("tk_jacobi0_restrict_um", a.lref, dev.P(b), dev.P(x3), dev.P(rc),
+             dev.stream())                        # ... storing only u / mu (V(1,1) pre-smoothing)
+    ec = dev.to_device(__import__("numpy").random.default_rng(5).standard_normal(t.coarse_dim))
+    x4 = dev.empty(a.dim)
+    dev.call("tk_jacobi_prolong", a.lref, dev.P(b), dev.P(x3), dev.P(ec), dev.P(x4),
+             dev.stream())                        # tri_rows_part<..., PR>: prolongation + post-smoothing
 torch.cuda.synchronize()
 print("ok", s.describe())
