@@ -247,7 +247,7 @@ int tk_rsub(int64_t n, const double* b, double* y, void* stream);
  * `w -= h_i V_i` with h_i an allreduced dot that stays on the device). */
 int tk_axpy_dev(int64_t n, const double* a, double sign, const double* x, double* y,
                 void* stream);
-/* nrm[0] = sqrt(sq[0]) (nrm may be NULL) and, when it is nonzero and y is
+/* nrm[0] = sqrt(sq[0]) (nrm may be NULL, must not alias sq) and, when it is nonzero and y is
  * given, y = x / nrm[0] (krylov.py:150-163 `hj1 = norm2(w)`, `V[j+1] = w / hj1`
  * with the squared norm allreduced on the device). */
 int tk_sqrt_div(int64_t n, const double* sq, double* nrm, const double* x, double* y,
@@ -275,11 +275,16 @@ int tk_host_device_ptr(void* host, void** dptr);
  * the tk_dot / tk_axpy / tk_nrm2 / tk_scale_into sequence. */
 int tk_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ld, double* w, double* h,
                    double* work, void* stream);
-/* For n*8 >= 16 MB, tk_arnoldi_mgs marks w L2-persisting (access-policy
- * window, persisting carve-out set to the device maximum on first use;
+/* For 16 MB <= n*8 <= 192 MB (and at most twice the device's persisting
+ * carve-out), tk_arnoldi_mgs marks w L2-persisting (access-policy window;
+ * the carve-out is set to the device maximum on first use;
  * TK_ARNOLDI_PERSIST=0 disables it).  tk_l2_persist_reset() returns those
- * lines to normal status; call it after synchronising, at the end of a solve. */
+ * lines to normal status and gives the carve-out back (while it is set every
+ * other kernel runs in the remaining L2 only); call it after synchronising,
+ * at the end of a solve.  tk_l2_persist_allow(0) keeps nested solves (the
+ * coarse GMRES inside an outer FGMRES) from claiming the window. */
 int tk_l2_persist_reset(void);
+int tk_l2_persist_allow(int32_t on);
 /* 1 when tk_arnoldi_mgs / tk_gm_arnoldi can run on the current device: their
  * fixed cooperative grid (592 CTAs of 256 threads) must be co-resident, which
  * a MIG slice or an SM-limited MPS client may not allow.  When 0 they return

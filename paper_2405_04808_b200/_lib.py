@@ -92,6 +92,7 @@ _SIGS = {
     "tk_arnoldi_mgs": (C.c_int, [_i64, _i32, _p, _i64, _p, _p, _p, _p]),
     "tk_copy_kernel": (C.c_int, [_i64, _p, _p, _p]),
     "tk_l2_persist_reset": (C.c_int, []),
+    "tk_l2_persist_allow": (C.c_int, [_i32]),
     "tk_arnoldi_supported": (_i32, []),
     "tk_graph_capture_begin": (C.c_int, [_p]),
     "tk_graph_cond_create": (C.c_int, [_p, C.POINTER(C.c_uint64)]),

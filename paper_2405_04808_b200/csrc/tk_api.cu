@@ -52,6 +52,7 @@ int axpy_dev_launch(int64_t, const double*, double, const double*, double*, cuda
 int sqrt_div_launch(int64_t, const double*, double*, const double*, double*, cudaStream_t);
 int arnoldi_launch(int64_t, int, double*, int64_t, double*, double*, double*, cudaStream_t);
 int l2_persist_reset();
+int l2_persist_allow(int);
 int arnoldi_supported();
 int copy_small_launch(int64_t, const double*, double*, cudaStream_t);
 int restrict_jacobi0_launch(int, int, int, int, int, const double*, const double*, const double*,
@@ -364,6 +365,8 @@ int tk_axpy_dev(int64_t n, const double* a, double sign, const double* x, double
 int tk_sqrt_div(int64_t n, const double* sq, double* nrm, const double* x, double* y,
                 void* stream) {
     TK_CHECK_ARG(sq && n >= 0 && (!y || x), "tk_sqrt_div: bad arguments");
+    // every CTA reads sq[0] while one thread writes nrm[0]: in place would race
+    TK_CHECK_ARG(nrm != sq, "tk_sqrt_div: nrm must not alias sq");
     return sqrt_div_launch(n, sq, nrm, x, y, as_stream(stream));
 }
 
@@ -403,6 +406,7 @@ int tk_arnoldi_mgs(int64_t n, int32_t j, double* V, int64_t ld, double* w, doubl
 int32_t tk_arnoldi_supported(void) { return arnoldi_supported() ? 1 : 0; }
 
 int tk_l2_persist_reset(void) { return l2_persist_reset(); }
+int tk_l2_persist_allow(int32_t on) { return l2_persist_allow(on); }
 
 int tk_gemv_t_add(int64_t n, int32_t k, const double* V, int64_t ld, const double* c, double* x,
                   void* stream) {

@@ -224,13 +224,30 @@ arnoldi_mgs_kernel(int64_t n, int j, double* __restrict__ V, int64_t ld, double*
 // maximum).  TK_ARNOLDI_PERSIST=0 disables it.
 static bool g_persist_used = false;
 
-// return the persisting lines to normal status (host-synchronous: call after
-// the stream that used the window has been synchronised, e.g. at the end of
-// a Krylov solve) so later kernels see the whole L2
+struct PersistCap;
+static void persist_release();
+// nested solves: only the outermost one may hold w L2-persisting (the coarse
+// GMRES inside a V-cycle inside an outer FGMRES would otherwise claim the
+// carve-out for the whole outer solve)
+static bool g_persist_allowed = true;
+int l2_persist_allow(int on) {
+    g_persist_allowed = on != 0;
+    return TK_OK;
+}
+
+// return the persisting lines to normal status AND give the persisting
+// carve-out back (host-synchronous: call after the stream that used the
+// window has been synchronised, e.g. at the end of a Krylov solve).  The
+// carve-out must not outlive the solve: while cudaLimitPersistingL2CacheSize
+// is set, every later kernel runs in the remaining L2 only -- the n_u = 2048
+// KKT apply of configs[4] took 5.96 ms instead of 3.32 ms after one coarse
+// solve had left it set.
 int l2_persist_reset() {
     if (!g_persist_used) return TK_OK;
     g_persist_used = false;
-    return cuda_status(cudaCtxResetPersistingL2Cache(), "cudaCtxResetPersistingL2Cache");
+    const int e = cuda_status(cudaCtxResetPersistingL2Cache(), "cudaCtxResetPersistingL2Cache");
+    persist_release();
+    return e;
 }
 
 // Persisting-L2 budget of the current device: the window size and the
@@ -259,6 +276,17 @@ static PersistCap persist_cap() {
         cudaGetLastError();
     }
     return c;
+}
+
+static void persist_release() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    PersistCap& c = g_persist[dev & 63];
+    if (c.carve > 0) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        cudaGetLastError();
+        c.carve = -1;   // re-established by the next solve that wants it
+    }
 }
 
 // Whether the fixed cooperative grid of the Arnoldi kernel is co-resident on
@@ -291,7 +319,11 @@ int arnoldi_launch(int64_t n, int j, double* V, int64_t ld, double* w, double* h
         return TK_ERR_UNSUPPORTED;
     }
     const size_t wb = (size_t)n * 8;
-    const PersistCap pc = wb >= ((size_t)16 << 20) ? persist_cap() : PersistCap{0, 0};
+    // w persisting only where most of it fits the carve-out (configs[3]: 75 MB);
+    // far larger vectors (configs[2]: 335 MB) gain nothing and would only lose L2
+    PersistCap pc = g_persist_allowed && wb >= ((size_t)16 << 20) && wb <= ((size_t)192 << 20) ? persist_cap()
+                                                                           : PersistCap{0, 0};
+    if (pc.carve > 0 && wb > 2 * (size_t)pc.carve) pc.carve = 0;
     if (pc.carve > 0) {
         // window over (the first window-size bytes of) w; the persisting
         // carve-out holds carve bytes of it

@@ -2147,7 +2147,9 @@ int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, dou
     }
     const int rows = V.sl.r1 - V.sl.r0;
     if (op == T_APPLY || op == T_APPLY_DIAG || op == T_RESIDUAL) {
-        const int th = n >= 256 ? 256 : 128;
+        // TK_APPLY_THREADS overrides (experiments)
+        static const int th_env = getenv("TK_APPLY_THREADS") ? atoi(getenv("TK_APPLY_THREADS")) : 0;
+        const int th = th_env >= 32 ? th_env : (n >= 256 ? 256 : 128);
         const int grid = rows < (1 << 30) ? rows : (1 << 30);
         if (op == T_APPLY) tri_apply<T_APPLY><<<grid, th, 0, s>>>(V, b, x, y);
         else if (op == T_APPLY_DIAG) tri_apply<T_APPLY_DIAG><<<grid, th, 0, s>>>(V, b, x, y);

@@ -4,6 +4,8 @@ host<->device copies; every computation goes through libtempokkt_b200.so."""
 from __future__ import annotations
 
 import numpy as np
+import os
+
 import torch
 
 from . import _lib
@@ -22,8 +24,15 @@ def stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+# TK_POISON=1 (debugging): uninitialised buffers start as NaN, so a kernel that
+# reads memory it should not depend on shows up as a NaN instead of a heisenbug
+_POISON = os.environ.get("TK_POISON") == "1"
+
+
 def empty(n, *shape) -> torch.Tensor:
     dims = (n,) + shape if shape else (n,)
+    if _POISON:
+        return torch.full(dims, float("nan"), dtype=F64, device=device())
     return torch.empty(dims, dtype=F64, device=device())
 
 

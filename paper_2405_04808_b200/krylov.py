@@ -17,6 +17,8 @@ import math
 from dataclasses import dataclass, field
 from typing import Callable
 
+import os
+
 import numpy as np
 import torch
 
@@ -253,13 +255,16 @@ def _gmres_engine(op, prec, b, x0, rel_tol, max_iters, restart, flexible, space=
     operations (DeviceSpace: one GPU; slabs.SlabSpace: time slabs over ranks
     with allreduced dots)."""
     space = DeviceSpace() if space is None else space
+    lib = _lib.load()
     _DEPTH[0] += 1
+    lib.tk_l2_persist_allow(1 if _DEPTH[0] == 1 else 0)   # only the outermost solve's w persists
     try:
         return _gmres_body(op, prec, b, x0, rel_tol, max_iters, restart, flexible, space)
     finally:
         _DEPTH[0] -= 1
         if _DEPTH[0] == 0:          # outermost solve only (also on an exception)
             space.finish()
+        lib.tk_l2_persist_allow(1 if _DEPTH[0] <= 1 else 0)
 
 
 def _gmres_body(op, prec, b, x0, rel_tol, max_iters, restart, flexible, space):

@@ -387,17 +387,20 @@ class CudaBackend:
         reads the column once, after the whole step has been enqueued."""
         d = self.dev
         n = w.numel()
-        if getattr(self, "_h", None) is None or self._h.numel() < j + 2:
-            self._h = d.empty(max(64, 2 * (j + 2)))
+        if getattr(self, "_h", None) is None or self._h.numel() < j + 3:
+            self._h = d.empty(max(64, 2 * (j + 3)))   # h_0..h_{j+1} + the squared-norm slot
         h = self._h
         for i in range(j + 1):
             d.call("tk_dot", n, d.P(V[i]), d.P(w), h[i:].data_ptr(), d.P(self.ops.work),
                    d.stream())
             comm.allreduce_sum(h[i:i + 1])
             d.call("tk_axpy_dev", n, h[i:].data_ptr(), -1.0, d.P(V[i]), d.P(w), d.stream())
-        d.call("tk_dot", n, d.P(w), d.P(w), h[j + 1:].data_ptr(), d.P(self.ops.work), d.stream())
-        comm.allreduce_sum(h[j + 1:j + 2])
-        d.call("tk_sqrt_div", n, h[j + 1:].data_ptr(), h[j + 1:].data_ptr(), d.P(w),
+        # the squared norm in a scratch slot: tk_sqrt_div reads sq[0] in every CTA
+        # while one thread stores the root, so the two must not alias
+        sq = h[h.numel() - 1:]
+        d.call("tk_dot", n, d.P(w), d.P(w), sq.data_ptr(), d.P(self.ops.work), d.stream())
+        comm.allreduce_sum(sq)
+        d.call("tk_sqrt_div", n, sq.data_ptr(), h[j + 1:].data_ptr(), d.P(w),
                d.P(V[j + 1]), d.stream())
         return h[:j + 2].cpu().numpy()
 
