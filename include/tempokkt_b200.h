@@ -316,6 +316,14 @@ int tk_gm_begin(int64_t n, const double* b, double* V, int64_t ld, double* vj, d
 /* MGS step j (j read from the state) with w = A M^{-1} v_j; V_{j+1} also to vj. */
 int tk_gm_arnoldi(int64_t n, double* V, int64_t ld, double* w, double* state, int32_t cap,
                   double* vj, double* work, void* stream);
+/* Z[j] = z with j read from the state (before tk_gm_arnoldi advances it): the
+ * preconditioned directions z_j = M^{-1} v_j of the loop are kept, so that the
+ * solution of the cycle is x = Z y (tk_gm_combine on Z) instead of
+ * M^{-1}(V y) -- the same vector for the fixed linear M^{-1} of the coarse
+ * solve (SGS), without the extra preconditioner application of
+ * krylov.py:165-176. */
+int tk_gm_storez(int64_t n, const double* z, double* Z, int64_t ldz, const double* state,
+                 int32_t cap, void* stream);
 /* Givens update + stopping tests of krylov.py; sets the loop condition. */
 int tk_gm_givens(double* state, int32_t cap, uint64_t handle, void* stream);
 /* y = H^{-1} g, vy = V^T y. */

@@ -105,6 +105,7 @@ _SIGS = {
     "tk_gm_begin": (C.c_int, [_i64, _p, _p, _i64, _p, _p, _i32, _d, _i32, C.c_uint64, _p, _p]),
     "tk_gm_arnoldi": (C.c_int, [_i64, _p, _i64, _p, _p, _i32, _p, _p, _p]),
     "tk_gm_givens": (C.c_int, [_p, _i32, C.c_uint64, _p]),
+    "tk_gm_storez": (C.c_int, [_i64, _p, _p, _i64, _p, _i32, _p]),
     "tk_gm_combine": (C.c_int, [_i64, _p, _i64, _p, _i32, _p, _p]),
     "tk_gm_finish": (C.c_int, [_i64, _p, _p, _p, _p, _i32, _p, _p, _p]),
     "tk_host_device_ptr": (C.c_int, [_p, C.POINTER(C.c_void_p)]),

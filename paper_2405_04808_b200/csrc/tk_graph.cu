@@ -180,6 +180,17 @@ __global__ void gm_gemv_kernel(int64_t n, const double* __restrict__ V, int64_t 
     }
 }
 
+// Z[j] = z (j = the Arnoldi step about to run, read from the state)
+__global__ void gm_storez_kernel(int64_t n, const double* __restrict__ z, double* __restrict__ Z,
+                                 int64_t ldz, const double* __restrict__ st, int cap) {
+    GmView s(const_cast<double*>(st), cap);
+    const int j = s.hd->j;
+    if (j < 0 || j >= cap) return;
+    double* dst = Z + (int64_t)j * ldz;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += stride) dst[k] = z[k];
+}
+
 __global__ void gm_finish_kernel(double* st, int cap, int* res) {
     if (threadIdx.x != 0) return;
     GmView s(st, cap);
@@ -318,6 +329,13 @@ int tk_gm_arnoldi(int64_t n, double* V, int64_t ld, double* w, double* state, in
                  "tk_gm_arnoldi: bad arguments");
     GmView v(state, cap);
     return arnoldi_dev_launch(n, &v.hd->j, V, ld, w, v.H, cap + 1, vj, work, as_stream(stream));
+}
+
+int tk_gm_storez(int64_t n, const double* z, double* Z, int64_t ldz, const double* state,
+                 int32_t cap, void* stream) {
+    TK_CHECK_ARG(z && Z && state && n > 0 && ldz >= n && cap >= 1, "tk_gm_storez: bad arguments");
+    gm_storez_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, as_stream(stream)>>>(n, z, Z, ldz, state, cap);
+    return check_launch("gm_storez_kernel");
 }
 
 int tk_gm_givens(double* state, int32_t cap, uint64_t handle, void* stream) {

@@ -38,6 +38,10 @@ from .kkt import FAMILY_TRI
 
 # environment switch: TK_GRAPH=0 keeps every cycle eager
 ENABLED = os.environ.get("TK_GRAPH", "1") != "0"
+# the device coarse GMRES keeps z_j = M^{-1} v_j and forms x = Z y: one SGS
+# application fewer per coarse solve than M^{-1}(V y) (the same vector for the
+# fixed linear SGS preconditioner); TK_COARSE_ZBASIS=0 keeps the reference form
+ZBASIS = os.environ.get("TK_COARSE_ZBASIS", "1") != "0"
 DEFAULT_CAP = 64
 
 
@@ -99,6 +103,7 @@ class VCycleGraph:
         nc = ac.dim
         self.nc = nc
         self.V = dev.empty(self.cap + 1, nc)
+        self.Z = dev.empty(self.cap, nc) if ZBASIS else None
         self.vj, self.zj, self.w, self.w1, self.vy, self.r = (dev.empty(nc) for _ in range(6))
         self.w2 = dev.empty(nc) if not self._fused_back_half(ac) else None
         self.state = dev.empty(int(lib.tk_gm_state_len(self.cap)))
@@ -191,14 +196,21 @@ class VCycleGraph:
         with torch.cuda.stream(body_stream):
             bs = dev.stream()
             self._sgs(a, self.vj, self.zj)
+            if self.Z is not None:
+                dev.call("tk_gm_storez", nc, dev.P(self.zj), dev.P(self.Z), self.Z.stride(0),
+                         dev.P(self.state), cap, bs)
             dev.call("tk_kkt_apply", a.lref, dev.P(self.zj), dev.P(self.w), bs)
             dev.call("tk_gm_arnoldi", nc, dev.P(self.V), ld, dev.P(self.w), dev.P(self.state),
                      cap, dev.P(self.vj), dev.P(self.work), bs)
             dev.call("tk_gm_givens", dev.P(self.state), cap, handle.value, bs)
         _lib.check(lib.tk_graph_while_end(body_stream.cuda_stream), "tk_graph_while_end")
-        dev.call("tk_gm_combine", nc, dev.P(self.V), ld, dev.P(self.state), cap,
-                 dev.P(self.vy), s)
-        self._sgs(a, self.vy, x)
+        if self.Z is not None:       # x = Z y
+            dev.call("tk_gm_combine", nc, dev.P(self.Z), self.Z.stride(0), dev.P(self.state), cap,
+                     dev.P(x), s)
+        else:                        # x = M^{-1} (V y)
+            dev.call("tk_gm_combine", nc, dev.P(self.V), ld, dev.P(self.state), cap,
+                     dev.P(self.vy), s)
+            self._sgs(a, self.vy, x)
         dev.call("tk_kkt_apply", a.lref, dev.P(x), dev.P(self.r), s)
         dev.call("tk_gm_finish", nc, dev.P(b), dev.P(self.r), dev.P(x), dev.P(self.state), cap,
                  self.res.dev_ptr, dev.P(self.work), s)
@@ -235,7 +247,8 @@ class VCycleGraph:
         sgs = dev._launches("tk_forward_subst", (a.lref,)) + (
             dev._launches("tk_sgs_back_half", (a.lref,)) if self._fused_back_half(a) else
             1 + dev._launches("tk_backward_subst", (a.lref,)))
-        self.per_coarse_iter = sgs + 1 + 1 + 1          # prec, apply, arnoldi, givens
+        zb = 1 if self.Z is not None else 0
+        self.per_coarse_iter = sgs + zb + 1 + 1 + 1     # prec, (store z), apply, arnoldi, givens
         from .multigrid import fused_jacobi0_ok
         fixed = 0
         from .multigrid import fused_v11_ok
@@ -245,7 +258,7 @@ class VCycleGraph:
                 fixed += 2
                 continue
             fixed += 2 * h.sweeps + (0 if fused else 1) + 1
-        fixed += 2 + 1 + 1 + 2 + sgs + 1 + 1 + 2 * 2 + 1  # begin, combine, prec, apply, finish
+        fixed += 2 + 1 + 1 + 2 + (0 if zb else sgs) + 1 + 1 + 2 * 2 + 1  # begin, combine, (prec), apply, finish
         return fixed
 
     # --- replay -------------------------------------------------------------
