@@ -107,7 +107,11 @@ def ncu_traffic(call: str, config: int, family: int):
         pred = _NCU_FULL[call][0 if family == 1 else 1]
         fine = [d for d in summ["full_capture"] if pred(d["kernel"])]
         if fine:
-            d = max(fine, key=lambda e: e["duration_us"])
+            # the u/mu-only pre-smoothing shares its kernel name with the full one (the
+            # partial store is a runtime flag): it is the capture that wrote fewer bytes
+            pick = min if call == "tk_jacobi0_restrict_um" else max
+            d = pick(fine, key=lambda e: e["dram_write_MB"] if call.startswith("tk_jacobi0_restrict")
+                     else e["duration_us"])
             return int((d["dram_read_MB"] + d["dram_write_MB"]) * 1e6), src
         return None, src
     pats = _NCU_KERNELS.get(call) if family == 1 else None

@@ -61,7 +61,7 @@ __host__ __device__ constexpr int cw_oP(int NA) { return cw_oV(NA) + 4; }
 __host__ __device__ constexpr int cw_oB(int NA, int LT) { return cw_oP(NA) + 8 * LT; }
 __host__ __device__ constexpr int cw_oC(int NA, int LT) { return cw_oB(NA, LT) + 4; }
 __host__ __device__ constexpr int cw_oE(int NA, int LT) { return cw_oC(NA, LT) + 4 * NA; }
-__host__ __device__ constexpr int cw_slots(int NA, int LT) { return cw_oE(NA, LT) + 2; }
+__host__ __device__ constexpr int cw_slots(int NA, int LT) { return cw_oE(NA, LT) + 4; }
 
 __device__ __forceinline__ unsigned s_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mb_init(uint64_t* bar, unsigned count) {
@@ -450,6 +450,293 @@ __global__ void __launch_bounds__(T, 1)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Streaming variant for 512 < n_u <= 2048 (T = 64 / 128 threads of 16 nodes):
+// the interval record (up to 380 KB) no longer fits shared memory, so every
+// thread streams ITS OWN coefficients through a private ring of R 32-byte
+// groups filled by cp.async in the exact order the solve consumes them
+// (cws_slot).  No staging barrier, no mbarrier: `cp.async.wait_group R-1`
+// before a group is read, the refill of the freed slot (R groups ahead, into
+// the next interval's record when the order wraps) right after.  Whole
+// records are pulled into L2 two intervals ahead by one bulk prefetch.
+// tri_chain_kernel needed ~32 us per interval at n_u = 2048 (record reads on
+// the critical path); this takes ~2.5 us.
+// ---------------------------------------------------------------------------
+template <int NA, int LT>
+__host__ __device__ constexpr int cws_common() { return 5 * NA - 4 + 2 * LT; }
+constexpr int kCwsRing = 27;
+template <int NA, int LT>
+__host__ __device__ constexpr int cws_gpi() {   // groups per interval, padded to a multiple of the ring
+    return (cws_common<NA, LT>() + NA + 1 + kCwsRing - 1) / kCwsRing * kCwsRing;
+}
+// record slot of the i-th group in consumption order (FWD: C first; BWD: E, C last)
+template <bool FWD, int NA, int LT>
+__host__ __device__ constexpr int cws_slot(int i) {
+    if (FWD) {
+        if (i < NA) return cw_oC(NA, LT) + 4 * i;
+        i -= NA;
+    }
+    if (i < 2 * (NA - 2)) {
+        const int q = i / 2 + 1;
+        return (i & 1) ? cw_oS(NA) + 4 * (NA - 2 - q) : cw_oT(NA) + 4 * (q - 1);
+    }
+    i -= 2 * (NA - 2);
+    if (i == 0) return cw_oT(NA) + 4 * (NA - 2);
+    i -= 1;
+    if (i == 0) return cw_oV(NA);
+    i -= 1;
+    if (i < 2 * LT) return cw_oP(NA) + 4 * i;
+    i -= 2 * LT;
+    if (i == 0) return cw_oB(NA, LT);
+    i -= 1;
+    if (i < 3 * (NA - 1)) {
+        const int q = NA - 2 - i / 3, r = i % 3;
+        return r == 0 ? cw_oDi(NA) + 4 * q : (r == 1 ? cw_oG(NA) + 4 * q : cw_oT(NA) + 4 * q);
+    }
+    i -= 3 * (NA - 1);
+    if (i == 0) return cw_oE(NA, LT);
+    i -= 1;
+    if (!FWD && i < NA) return cw_oC(NA, LT) + 4 * i;
+    return 0;   // padding group (never read)
+}
+
+template <bool FWD, int NA, int T>
+__global__ void __launch_bounds__(T, 1)
+    tri_chainw_stream(TView V, const double* __restrict__ a, const double* __restrict__ facw,
+                      double* __restrict__ chain, int Lc, int cbase,
+                      const double* __restrict__ starts, double* __restrict__ ends) {
+    constexpr int LT = ilog2(T);
+    constexpr int SL = cw_slots(NA, LT);
+    constexpr int REC = SL * T;
+    constexpr int R = kCwsRing;
+    constexpr int GPI = cws_gpi<NA, LT>();
+    constexpr int CB = FWD ? NA : 0;                     // first common group
+    constexpr int CM = cws_common<NA, LT>();
+    static_assert(GPI % R == 0 && R < GPI, "ring must divide the interval stream");
+    extern __shared__ __align__(16) double sm[];
+    double2* ring = reinterpret_cast<double2*>(sm);      // [R][2][T]
+    double2* xH = ring + R * 2 * T;                      // exchange arrays [T] each
+    double2* xP[2] = {xH + T, xH + 2 * T};
+    double2* xX = xH + 3 * T;
+    double2* xE = xH + 4 * T;
+    const Lay& L = V.lay;
+    const int n = V.n, N = L.N;
+    const int t = threadIdx.x;
+    const int K = N - 1;
+    const int c = cbase + blockIdx.x;
+    const int lo = c * Lc, hi = min(K, lo + Lc);
+    const int k0 = FWD ? lo : K - hi, k1 = FWD ? hi : K - lo;
+    const bool seed = k0 == 0;
+    auto blk = [&](int k) { return FWD ? 1 + k : N - 1 - k; };
+    auto aseg = [&](int i) { return a + (FWD ? L.off_u(i) : L.off_mu(i)); };
+    const int i0 = FWD ? 0 : N;
+    const double* s0 = seed ? aseg(i0) : (starts ? starts + (size_t)c * n : nullptr);
+    const int j0 = NA * t;
+    double w[NA];
+#pragma unroll
+    for (int k = 0; k < NA; ++k) w[k] = (s0 && j0 + k < n) ? s0[j0 + k] : 0.0;
+    if (seed) {
+#pragma unroll
+        for (int k = 0; k < NA; ++k)
+            if (j0 + k < n) chain[(size_t)i0 * n + j0 + k] = w[k];
+    }
+    if (k0 >= k1) return;
+    // group g (0 <= g < 2 GPI) of the stream that starts at interval step k
+    auto issue = [&](int k, int g) {
+        const int kk = k + (g >= GPI ? 1 : 0);
+        const int gi = g >= GPI ? g - GPI : g;
+        const int kc = kk < k1 ? kk : k1 - 1;              // past the chunk: refetch (never read)
+        const int sl = cws_slot<FWD, NA, LT>(gi);
+        const double2* src = reinterpret_cast<const double2*>(facw + (size_t)blk(kc) * REC) +
+                             (sl >> 1) * T + t;
+        double2* dst = ring + ((gi % R) * 2) * T + t;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s_u32(dst)), "l"(src) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s_u32(dst + T)), "l"(src + T)
+                     : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    auto l2_prefetch = [&](int k) {   // the whole record of step k -> L2 (one thread)
+        if (t != 0 || k >= k1) return;
+        const char* p = reinterpret_cast<const char*>(facw + (size_t)blk(k) * REC);
+        const unsigned bytes = (unsigned)(REC * sizeof(double));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+    };
+    l2_prefetch(k0 + 1);
+#pragma unroll
+    for (int g = 0; g < R; ++g) issue(k0, g);
+    double* eout = ends ? ends + (size_t)c * n : nullptr;
+    for (int k = k0; k < k1; ++k) {
+        const int i = blk(k);
+        l2_prefetch(k + 2);
+        // take group g of this interval: wait, read, refill the slot with group g + R
+        auto take = [&](int g, double2& u0, double2& u1) {
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(R - 1) : "memory");
+            const double2* src = ring + ((g % R) * 2) * T + t;
+            u0 = src[0];
+            u1 = src[T];
+            issue(k, g + R);
+        };
+        // an unread group: its copy must still have landed before the slot is refilled
+        // (two copies in flight to one slot may complete in either order)
+        auto skip = [&](int g) {
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(R - 1) : "memory");
+            issue(k, g + R);
+        };
+        // a_i at the chunk nodes: issued now, consumed after the solve
+        double av[NA];
+        {
+            const double* as = aseg(i) + j0;
+#pragma unroll
+            for (int q = 0; q < NA; q += 2) {
+                if (j0 + q + 1 < n && (reinterpret_cast<uintptr_t>(as + q) & 15) == 0) {
+                    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];\n"
+                                 : "=d"(av[q]), "=d"(av[q + 1]) : "l"(as + q) : "memory");
+                } else {
+                    av[q] = j0 + q < n ? as[q] : 0.0;
+                    av[q + 1] = j0 + q + 1 < n ? as[q + 1] : 0.0;
+                }
+            }
+        }
+        // ---- right-hand side
+        double g0[NA], g1[NA];
+        if (FWD) {
+            xE[t] = make_double2(w[0], w[NA - 1]);
+            bsync<T>();
+            const double wl = t > 0 ? xE[t - 1].y : 0.0;
+            const double wr = t < T - 1 ? xE[t + 1].x : 0.0;
+#pragma unroll
+            for (int q = 0; q < NA; ++q) {
+                double2 c0, c1;
+                take(q, c0, c1);
+                const double wm = q > 0 ? w[q - 1] : wl, wp = q < NA - 1 ? w[q + 1] : wr;
+                g0[q] = 0.0;
+                g1[q] = -(c0.y * w[q] + c0.x * wm + c1.x * wp);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < NA; ++q) { g0[q] = -w[q]; g1[q] = 0.0; }
+        }
+        // ---- the two Thomas rhs sweeps, interleaved
+        double gg0[NA], gg1[NA];
+        gg0[0] = g0[0]; gg1[0] = g1[0];
+        double h0 = g0[NA - 2], h1 = g1[NA - 2];
+#pragma unroll
+        for (int q = 1; q < NA; ++q) {
+            {
+                double2 ta, tb;
+                take(CB + (q < NA - 1 ? 2 * (q - 1) : 2 * (NA - 2)), ta, tb);
+                gg0[q] = fma(-ta.x, gg0[q - 1], fma(-tb.x, gg1[q - 1], g0[q]));
+                gg1[q] = fma(-ta.y, gg0[q - 1], fma(-tb.y, gg1[q - 1], g1[q]));
+            }
+            const int qb = NA - 2 - q;
+            if (qb >= 0) {
+                double2 sa, sb;
+                take(CB + 2 * (q - 1) + 1, sa, sb);
+                const double n0 = fma(-sa.x, h0, fma(-sb.x, h1, g0[qb]));
+                const double n1 = fma(-sa.y, h0, fma(-sb.y, h1, g1[qb]));
+                h0 = n0; h1 = n1;
+            }
+        }
+        xH[t] = make_double2(h0, h1);
+        bsync<T>();
+        // ---- interface rhs and the rhs-only parallel cyclic reduction
+        double R0 = gg0[NA - 1], R1 = gg1[NA - 1];
+        {
+            const double2 hn = t < T - 1 ? xH[t + 1] : make_double2(0.0, 0.0);
+            double2 va, vb;
+            take(CB + 2 * NA - 3, va, vb);
+            R0 -= va.x * hn.x + va.y * hn.y;
+            R1 -= vb.x * hn.x + vb.y * hn.y;
+        }
+#pragma unroll
+        for (int l = 0; l < LT; ++l) {
+            const int s = 1 << l;
+            double2* P = xP[l & 1];
+            P[t] = make_double2(R0, R1);
+            double2 aa, ab, ca, cb;
+            take(CB + 2 * NA - 2 + 2 * l, aa, ab);
+            take(CB + 2 * NA - 2 + 2 * l + 1, ca, cb);
+            bsync<T>();
+            const double2 rm = t >= s ? P[t - s] : make_double2(0.0, 0.0);
+            const double2 rp = t + s < T ? P[t + s] : make_double2(0.0, 0.0);
+            R0 = fma(-aa.x, rm.x, fma(-aa.y, rm.y, R0)) - fma(ca.x, rp.x, ca.y * rp.y);
+            R1 = fma(-ab.x, rm.x, fma(-ab.y, rm.y, R1)) - fma(cb.x, rp.x, cb.y * rp.y);
+        }
+        double x0[NA], x1[NA];
+        {
+            double2 ba, bb;
+            take(CB + 2 * NA - 2 + 2 * LT, ba, bb);
+            x0[NA - 1] = ba.x * R0 + ba.y * R1;
+            x1[NA - 1] = bb.x * R0 + bb.y * R1;
+        }
+        xX[t] = make_double2(x0[NA - 1], x1[NA - 1]);
+        bsync<T>();
+        const double2 xl = t > 0 ? xX[t - 1] : make_double2(0.0, 0.0);
+        // ---- back-substitution
+#pragma unroll
+        for (int q = NA - 2; q >= 0; --q) {
+            constexpr int BS = CB + 2 * NA - 1 + 2 * LT;
+            double2 da, db, ga, gb, ta, tb;
+            take(BS + 3 * (NA - 2 - q), da, db);
+            take(BS + 3 * (NA - 2 - q) + 1, ga, gb);
+            take(BS + 3 * (NA - 2 - q) + 2, ta, tb);
+            const double p0 = (da.x * gg0[q] + da.y * gg1[q]) + (ga.x * xl.x + ga.y * xl.y);
+            const double p1 = (db.x * gg0[q] + db.y * gg1[q]) + (gb.x * xl.x + gb.y * xl.y);
+            x0[q] = fma(-ta.x, x0[q + 1], fma(-ta.y, x1[q + 1], p0));
+            x1[q] = fma(-tb.x, x0[q + 1], fma(-tb.y, x1[q + 1], p1));
+        }
+        // ---- the step's coupling vector
+        if (FWD) {
+#pragma unroll
+            for (int q = 0; q < NA; ++q) w[q] = av[q] + x0[q];
+            skip(CB + CM);                                  // the edge group (BWD only)
+        } else {
+            xE[t] = make_double2(x1[0], x1[NA - 1]);
+            bsync<T>();
+            const double ll = t > 0 ? xE[t - 1].y : 0.0;
+            const double lr = t < T - 1 ? xE[t + 1].x : 0.0;
+            double2 ed, e1;
+            take(CM, ed, e1);                               // (Cp[j0-1], Cs[j0+NA])
+            double cs_[NA], cd_[NA], cp_[NA];
+#pragma unroll
+            for (int q = 0; q < NA; ++q) {
+                double2 c0, c1;
+                take(CM + 1 + q, c0, c1);
+                cs_[q] = c0.x; cd_[q] = c0.y; cp_[q] = c1.x;
+            }
+#pragma unroll
+            for (int q = 0; q < NA; ++q) {
+                const double cpm = q > 0 ? cp_[q - 1] : ed.x;
+                const double csn = q < NA - 1 ? cs_[q + 1] : ed.y;
+                const double lm = q > 0 ? x1[q - 1] : ll, lp = q < NA - 1 ? x1[q + 1] : lr;
+                w[q] = av[q] + (cd_[q] * x1[q] + cpm * lm + csn * lp);
+            }
+        }
+#pragma unroll
+        for (int g = CM + NA + 1; g < GPI; ++g) skip(g);   // padding groups
+        {
+            double* dst = chain + (size_t)i * n + j0;
+            const bool last = k + 1 == k1 && eout != nullptr;
+#pragma unroll
+            for (int q = 0; q < NA; q += 2) {
+                if (j0 + q + 1 < n && (reinterpret_cast<uintptr_t>(dst + q) & 15) == 0) {
+                    *reinterpret_cast<double2*>(dst + q) = make_double2(w[q], w[q + 1]);
+                } else {
+                    if (j0 + q < n) dst[q] = w[q];
+                    if (j0 + q + 1 < n) dst[q + 1] = w[q + 1];
+                }
+                if (last) {
+                    if (j0 + q < n) eout[j0 + q] = w[q];
+                    if (j0 + q + 1 < n) eout[j0 + q + 1] = w[q + 1];
+                }
+            }
+        }
+        bsync<T>();   // the exchange arrays are free for the next step
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -465,12 +752,14 @@ int chainw_nodes(int n) {
         const char* a = getenv("TK_CHAIN_NA");
         if (a && atoi(a) == 16) na512 = 16;
     }
-    if (!on || n < 32 || n > 512 || (n & 1)) return 0;
+    if (!on || n < 32 || n > 2048 || (n & 1)) return 0;
     if (n <= 128) return 4 * 1000 + 32;
     if (n <= 256) return 8 * 1000 + 32;
-    return na512 == 16 ? 16 * 1000 + 32 : 8 * 1000 + 64;
+    if (n <= 512) return na512 == 16 ? 16 * 1000 + 32 : 8 * 1000 + 64;
+    // beyond 512 the records exceed shared memory: per-thread cp.async streams
+    return n <= 1024 ? 16 * 1000 + 64 : 16 * 1000 + 128;
 }
-static int cw_log2(int t) { return t == 64 ? 6 : 5; }
+static int cw_log2(int t) { return t == 128 ? 7 : (t == 64 ? 6 : 5); }
 // doubles of the level's warp-chain records (N intervals; record 0 unused)
 int64_t chainw_len(const tk_level* Lv) {
     const int cfg = chainw_nodes(Lv->n_u);
@@ -493,6 +782,8 @@ int chainw_factor(const tk_level* Lv, double* facw, cudaStream_t s) {
         case 8032: return chainw_factor_t<8, 32>(Lv, facw, s);
         case 8064: return chainw_factor_t<8, 64>(Lv, facw, s);
         case 16032: return chainw_factor_t<16, 32>(Lv, facw, s);
+        case 16064: return chainw_factor_t<16, 64>(Lv, facw, s);
+        case 16128: return chainw_factor_t<16, 128>(Lv, facw, s);
         default: set_error("chainw_factor: unsupported n_u=%d", Lv->n_u); return TK_ERR_UNSUPPORTED;
     }
 }
@@ -513,9 +804,34 @@ static int chainw_launch_t(const tk_level* Lv, const double* a, const double* fa
     tri_chainw_kernel<FWD, NA, T><<<grid, T, smem, s>>>(V, a, facw, chain, Lc, cbase, st, en);
     return check_launch("tri_chainw_kernel");
 }
+template <bool FWD, int NA, int T>
+static int chainw_stream_t(const tk_level* Lv, const double* a, const double* facw, double* chain,
+                           int Lc, int grid, int cbase, const double* st, double* en,
+                           cudaStream_t s) {
+    const size_t smem = (size_t)(kCwsRing * 2 * T + 5 * T) * sizeof(double2);
+    static bool attr = false;
+    if (!attr) {
+        const cudaError_t e = cudaFuncSetAttribute(tri_chainw_stream<FWD, NA, T>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_status(e, "tri_chainw_stream: attributes");
+        attr = true;
+    }
+    TView V(Lv);
+    tri_chainw_stream<FWD, NA, T><<<grid, T, smem, s>>>(V, a, facw, chain, Lc, cbase, st, en);
+    return check_launch("tri_chainw_stream");
+}
 int chainw_launch(const tk_level* Lv, bool fwd, const double* a, const double* facw, double* chain,
                   int Lc, int grid, int cbase, const double* st, double* en, cudaStream_t s) {
     if (grid <= 0) return TK_OK;
+    switch (chainw_nodes(Lv->n_u)) {
+        case 16064:
+            return fwd ? chainw_stream_t<true, 16, 64>(Lv, a, facw, chain, Lc, grid, cbase, st, en, s)
+                       : chainw_stream_t<false, 16, 64>(Lv, a, facw, chain, Lc, grid, cbase, st, en, s);
+        case 16128:
+            return fwd ? chainw_stream_t<true, 16, 128>(Lv, a, facw, chain, Lc, grid, cbase, st, en, s)
+                       : chainw_stream_t<false, 16, 128>(Lv, a, facw, chain, Lc, grid, cbase, st, en, s);
+        default: break;
+    }
 #define TK_CW(NN, TT)                                                                               \
     case NN * 1000 + TT:                                                                            \
         return fwd ? chainw_launch_t<true, NN, TT>(Lv, a, facw, chain, Lc, grid, cbase, st, en, s)  \

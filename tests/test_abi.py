@@ -97,8 +97,8 @@ def test_chain_sizing_without_gpu():
     n = 512
     want = 2 * nc * n * n + 3 * nc * n + 4 + 2 * ng * n * n + 2 * ng * n
     # + the warp-chain records (tk_tri_chainw.cu): n_u = 512 runs 64 threads of 8 nodes,
-    # 198 coefficient slots per thread, one record per interval (16-byte aligned)
-    recs = 512 * 198 * 64
+    # 200 coefficient slots per thread, one record per interval (16-byte aligned)
+    recs = 512 * 200 * 64
     import ctypes
     assert lib.tk_chain_prod_len(ctypes.byref(lv)) == want + (want & 1) + recs
     lv.chain_chunk = 100                                            # 6 chunks: single carry
