@@ -57,16 +57,16 @@ def _t(kernel: str, i: int):
 _NCU_FULL = {
     "tk_jacobi_sweep": (lambda k: "tri_rows_part<" in k and _t(k, 1) in ("0", "3")
                         and _t(k, 4) == "0" and _t(k, 6) == "0",
-                        lambda k: "dense_rows<" in k and _t(k, 2) == "4"),
+                        lambda k: "dense_rows_split<" in k or ("dense_rows<" in k and _t(k, 2) == "4")),
     "tk_jacobi0_restrict": (lambda k: "tri_rows_part<" in k and _t(k, 1) == "3"
                             and _t(k, 4) == "1",
                             lambda k: "dense_rows<" in k and _t(k, 2) == "4"),
     "tk_jacobi0_restrict_um": (lambda k: "tri_rows_part<" in k and _t(k, 1) == "3"
                                and _t(k, 4) == "1",
-                               lambda k: False),
+                               lambda k: "dense_rows_split<" in k),
     "tk_jacobi_prolong": (lambda k: "tri_rows_part<" in k and _t(k, 1) == "3"
                           and _t(k, 6) == "1",
-                          lambda k: False),
+                          lambda k: "dense_rows_split<" in k),
     "tk_residual_restrict": (lambda k: "tri_resrestrict" in k,
                              lambda k: "dense_rows<" in k and _t(k, 2) == "2"),
     "tk_prolong_add": (lambda k: "prolong_rows_kernel" in k, lambda k: "prolong_small_kernel" in k),
@@ -77,8 +77,8 @@ _NCU_FULL = {
 }
 _NCU_NAMES = {"tk_jacobi_sweep": ("tri_rows_part<W, 3, ., CL, 0, .>", "dense_rows<NU, NZ, 4>"),
               "tk_jacobi0_restrict": ("tri_rows_part<W, 3, ., CL, 1, .>", "dense_rows<NU, NZ, 4>"),
-              "tk_jacobi0_restrict_um": ("tri_rows_part<W, 3, ., CL, 1, ., 0>", None),
-              "tk_jacobi_prolong": ("tri_rows_part<W, 3, ., CL, 0, ., 1>", None),
+              "tk_jacobi0_restrict_um": ("tri_rows_part<W, 3, ., CL, 1, ., 0>", "dense_rows_split<NU, NZ>"),
+              "tk_jacobi_prolong": ("tri_rows_part<W, 3, ., CL, 0, ., 1>", "dense_rows_split<NU, NZ>"),
               "tk_residual_restrict": ("tri_resrestrict", "dense_rows<NU, NZ, 2>"),
               "tk_prolong_add": ("prolong_rows_kernel", "prolong_small_kernel"),
               "tk_kkt_apply": ("tri_apply<0>", "dense_rows<NU, NZ, 0>"),

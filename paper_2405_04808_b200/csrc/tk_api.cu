@@ -34,6 +34,8 @@ bool tri_jacobi_prolong_ok(const tk_level*, double);
 int tri_jacobi_prolong_launch(const tk_level*, const double*, const double*, const double*, double*,
                               cudaStream_t);
 int dense_jacobi0_restrict(const tk_level*, const double*, double*, double*, cudaStream_t);
+int dense_split(const tk_level*, const double*, const double*, double*, const double*, double*, int,
+                cudaStream_t);
 int64_t tri_fac_len(const tk_level*);
 int64_t tri_scratch_len(const tk_level*);
 int64_t dense_fac_len(const tk_level*);
@@ -181,7 +183,7 @@ int tk_jacobi0_restrict(const tk_level* L, const double* b, double omega, double
 
 int32_t tk_jacobi_prolong_ok(const tk_level* L, double omega) {
     if (check_level(L)) return 0;
-    if (L->family != TK_FAMILY_TRI) return 0;
+    if (L->family == TK_FAMILY_DENSE) return dense_jacobi0_restrict_ok(L, omega) ? 1 : 0;
     return tri_jacobi_prolong_ok(L, omega) ? 1 : 0;
 }
 
@@ -190,10 +192,12 @@ int tk_jacobi0_restrict_um(const tk_level* L, const double* b, double* x_um, dou
     TK_CHECK_ARG(b && x_um && rc, "tk_jacobi0_restrict_um: null vector");
     const int e = check_level(L);
     if (e) return e;
-    if (L->family != TK_FAMILY_TRI || !tri_jacobi_prolong_ok(L, 1.0)) {
+    if (!tk_jacobi_prolong_ok(L, 1.0)) {
         set_error("tk_jacobi0_restrict_um: level not supported (see tk_jacobi_prolong_ok)");
         return TK_ERR_UNSUPPORTED;
     }
+    if (L->family == TK_FAMILY_DENSE)
+        return dense_split(L, b, nullptr, x_um, nullptr, rc, 1, as_stream(stream));
     return tri_jacobi0_restrict_launch(L, b, 1.0, x_um, rc, as_stream(stream), 1);
 }
 
@@ -202,9 +206,12 @@ int tk_jacobi_prolong(const tk_level* L, const double* b, const double* x, const
     TK_CHECK_ARG(b && x && ec && x_out && x != x_out && b != x_out, "tk_jacobi_prolong: bad vectors");
     const int e = check_level(L);
     if (e) return e;
-    if (L->family != TK_FAMILY_TRI) {
-        set_error("tk_jacobi_prolong: TRI levels only");
-        return TK_ERR_UNSUPPORTED;
+    if (L->family == TK_FAMILY_DENSE) {
+        if (!dense_jacobi0_restrict_ok(L, 1.0)) {
+            set_error("tk_jacobi_prolong: level not supported (whole level, even N)");
+            return TK_ERR_UNSUPPORTED;
+        }
+        return dense_split(L, b, x, x_out, ec, nullptr, 0, as_stream(stream));
     }
     return tri_jacobi_prolong_launch(L, b, x, ec, x_out, as_stream(stream));
 }

@@ -8,6 +8,8 @@
 // for the dynamics multiplier.  This is D_i^{-1} of DiagonalSolver
 // (kkt.py:338-389) without forming the (4nu+nz)^2 inverse: the HBM stream
 // per interval is the vectors plus K_i, C_i, B_i only.
+#include <stdlib.h>
+
 #include "tk_common.cuh"
 
 namespace tk {
@@ -389,6 +391,125 @@ __global__ void __launch_bounds__(128) dense_rows(DView<NU, NZ> V, const double*
     }
 }
 
+
+// Splitting-form rows (omega = 1 or from zero; the DENSE twin of
+// tri_rows_part<.., 3, ..>): y = D^{-1}(b + (L + U) x) -- the local solve of b
+// with the continuity couplings u_{i-1}, mu_{i+1} of x moved to the
+// right-hand side, so x is read at those two segments only.
+//   ec != nullptr: the couplings are those of x + P ec (the V-cycle's
+//     prolongation folded into the post-smoothing sweep, multigrid.py:115-132,
+//     :297-299; the arithmetic of tk_prolong_add);
+//   rc != nullptr (x == nullptr, whole level, even N): the zero-start sweep
+//     also writes its restricted residual (as dense_rows<.., D_JACOBI> does);
+//     partial: only the u and mu segments of y are stored.
+template <int NU, int NZ>
+__global__ void __launch_bounds__(128) dense_rows_split(DView<NU, NZ> V, const double* __restrict__ b,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ y, double omega,
+                                                        const double* __restrict__ ec,
+                                                        double* __restrict__ rc, int partial) {
+    const Lay& L = V.lay;
+    const Slab& S = V.sl;
+    const int64_t bs0 = S.base;
+    const Lay Lc(L.N / 2, NU, NZ);
+    for (int i = S.r0 + blockIdx.x * blockDim.x + threadIdx.x; i < S.r1;
+         i += gridDim.x * blockDim.x) {
+        Seg<NU, NZ> bs, ys;
+        load_seg<NU, NZ>(L, i, b, bs, bs0);
+        const double* uprev = x ? S.uprev(L, x, i) : nullptr;
+        const double* munext = x ? S.munext(L, x, i) : nullptr;
+        if (uprev) {          // u_t, t = i
+            const int t = i;
+            const double* ca = nullptr;
+            const double* cb = nullptr;
+            if (ec) {
+                if ((t & 1) == 0 || t == 1) ca = ec + Lc.t_u(t == 1 ? 1 : t / 2);
+                else { ca = ec + Lc.t_u((t - 1) / 2); cb = ec + Lc.t_u((t + 1) / 2); }
+            }
+#pragma unroll
+            for (int e = 0; e < NU; ++e) {
+                double up = uprev[e];
+                if (ca) up = cb ? up + 0.5 * (ca[e] + cb[e]) : up + ca[e];
+                bs.m[e] -= up;
+            }
+        }
+        if (munext) {         // mu_t, t = i + 1
+            const int t = i + 1;
+            const double* ca = nullptr;
+            const double* cb = nullptr;
+            if (ec) {
+                if ((t & 1) == 0 || t == 1) ca = ec + Lc.t_mu(t == 1 ? 1 : t / 2);
+                else { ca = ec + Lc.t_mu((t - 1) / 2); cb = ec + Lc.t_mu((t + 1) / 2); }
+            }
+#pragma unroll
+            for (int e = 0; e < NU; ++e) {
+                double mn = munext[e];
+                if (ca) mn = cb ? mn + 0.5 * (ca[e] + cb[e]) : mn + ca[e];
+                bs.u[e] -= mn;
+            }
+        }
+        solve_row<NU, NZ>(V, i, bs, ys);
+#pragma unroll
+        for (int e = 0; e < NU; ++e) {
+            ys.v[e] = 0.0 + omega * ys.v[e]; ys.u[e] = 0.0 + omega * ys.u[e];
+            ys.m[e] = 0.0 + omega * ys.m[e]; ys.l[e] = 0.0 + omega * ys.l[e];
+        }
+#pragma unroll
+        for (int e = 0; e < NZ; ++e) ys.z[e] = 0.0 + omega * ys.z[e];
+        if (partial) {
+            if (i >= 1) {
+                double* pm = y + (L.off_mu(i) - bs0);
+#pragma unroll
+                for (int e = 0; e < NU; ++e) pm[e] = ys.m[e];
+            }
+            if (i < L.N) {
+                double* pu = y + (L.off_u(i) - bs0);
+#pragma unroll
+                for (int e = 0; e < NU; ++e) pu[e] = ys.u[e];
+            }
+        } else {
+            store_seg<NU, NZ>(L, i, y, ys, bs0);
+        }
+        if (rc) {
+            if (i & 1) {
+                double* p = rc + Lc.t_mu((i + 1) / 2);
+#pragma unroll
+                for (int e = 0; e < NU; ++e) p[e] = 0.0 - ys.u[e];
+            } else {
+                const int c = i / 2;
+                if (i >= 2) {
+                    double* p = rc + Lc.t_u(c);
+#pragma unroll
+                    for (int e = 0; e < NU; ++e) p[e] = 0.0 - ys.m[e];
+                }
+                if (c >= 1) {
+                    double* p = rc + Lc.off_v(c);
+#pragma unroll
+                    for (int e = 0; e < NU; ++e) p[e] = 0.0;
+                }
+                if (c < Lc.N) {
+                    double* pz = rc + Lc.off_z(c);
+                    double* pl = rc + Lc.off_l(c);
+#pragma unroll
+                    for (int e = 0; e < NZ; ++e) pz[e] = 0.0;
+#pragma unroll
+                    for (int e = 0; e < NU; ++e) pl[e] = 0.0;
+                }
+            }
+        }
+    }
+}
+
+template <int NU, int NZ>
+static int dense_split_t(const tk_level* Lv, const double* b, const double* x, double* y,
+                         double omega, const double* ec, double* rc, int partial, cudaStream_t s) {
+    DView<NU, NZ> V(Lv);
+    const int rows = V.sl.r1 - V.sl.r0;
+    dense_rows_split<NU, NZ><<<grid_for(rows, 128, 1 << 20), 128, 0, s>>>(V, b, x, y, omega, ec, rc,
+                                                                           partial);
+    return check_launch("dense_rows_split");
+}
+
 template <int NU, int NZ>
 static int dense_jacobi0_restrict_t(const tk_level* Lv, const double* b, double* y, double* rc,
                                     cudaStream_t s) {
@@ -594,6 +715,14 @@ int64_t dense_fac_len(const tk_level* Lv) {
 }
 int64_t dense_scratch_len(const tk_level* Lv) { return (int64_t)(Lv->n_steps + 1) * Lv->n_u; }
 
+static bool dense_resid_form() {
+    static const bool on = [] {
+        const char* e = getenv("TK_JACOBI_RESIDUAL_FORM");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 template <int NU, int NZ>
 static int dense_launch_t(const tk_level* Lv, int op, const double* b, const double* x, double* y,
                           double omega, cudaStream_t s) {
@@ -611,7 +740,13 @@ static int dense_launch_t(const tk_level* Lv, int op, const double* b, const dou
             dense_rows<NU, NZ, D_APPLY_DIAG><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
         case D_RESIDUAL: dense_rows<NU, NZ, D_RESIDUAL><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
         case D_SOLVE: dense_rows<NU, NZ, D_SOLVE><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
-        case D_JACOBI: dense_rows<NU, NZ, D_JACOBI><<<grid, th, 0, s>>>(V, b, x, y, omega); break;
+        case D_JACOBI:
+            // omega = 1 or from zero: x enters through the two couplings only
+            // (TK_JACOBI_RESIDUAL_FORM=1 keeps x + omega D^{-1}(b - A x))
+            if ((x == nullptr || omega == 1.0) && !dense_resid_form())
+                return dense_split_t<NU, NZ>(Lv, b, x, y, omega, nullptr, nullptr, 0, s);
+            dense_rows<NU, NZ, D_JACOBI><<<grid, th, 0, s>>>(V, b, x, y, omega);
+            break;
         case 10:
         case 11: {
             const bool fwd = op == 10;
@@ -657,6 +792,20 @@ int dense_jacobi0_restrict(const tk_level* Lv, const double* b, double* y, doubl
     TK_DJR(3, 1) TK_DJR(3, 2) TK_DJR(3, 3) TK_DJR(3, 4)
     TK_DJR(4, 1) TK_DJR(4, 2) TK_DJR(4, 3) TK_DJR(4, 4)
 #undef TK_DJR
+    set_error("dense family supports 1<=n_u,n_z<=4 (got n_u=%d n_z=%d)", Lv->n_u, Lv->n_z);
+    return TK_ERR_UNSUPPORTED;
+}
+
+// tk_jacobi0_restrict_um (x == nullptr, rc, partial) / tk_jacobi_prolong (x, ec) on DENSE levels
+int dense_split(const tk_level* Lv, const double* b, const double* x, double* y, const double* ec,
+                double* rc, int partial, cudaStream_t s) {
+#define TK_DSP(NU, NZ) \
+    if (Lv->n_u == NU && Lv->n_z == NZ) return dense_split_t<NU, NZ>(Lv, b, x, y, 1.0, ec, rc, partial, s);
+    TK_DSP(1, 1) TK_DSP(1, 2) TK_DSP(1, 3) TK_DSP(1, 4)
+    TK_DSP(2, 1) TK_DSP(2, 2) TK_DSP(2, 3) TK_DSP(2, 4)
+    TK_DSP(3, 1) TK_DSP(3, 2) TK_DSP(3, 3) TK_DSP(3, 4)
+    TK_DSP(4, 1) TK_DSP(4, 2) TK_DSP(4, 3) TK_DSP(4, 4)
+#undef TK_DSP
     set_error("dense family supports 1<=n_u,n_z<=4 (got n_u=%d n_z=%d)", Lv->n_u, Lv->n_z);
     return TK_ERR_UNSUPPORTED;
 }

@@ -102,3 +102,51 @@ def test_fused_cycle_vs_oracle_and_unfused(n_u, levels, monkeypatch):
     x_unf = P.cycle(h2, 0, b)
     assert rel(x_eager, x_unf) < 1e-12
     assert h2.stats.iters == its
+
+
+@pytest.mark.parametrize("kind", ["w", "f"])
+def test_fused_levels_inside_w_and_f_cycles(kind):
+    """W / F cycles (multigrid.py:290-296) revisit a level with a non-zero
+    iterate: only the visits from zero take the fused pair, the others the
+    general kernels; both against the oracle."""
+    from paper_2405_04808_b200 import multigrid as M
+    P, O, p, op, grid, u, v, z, rng = _case(128, n=32)
+    h = P.build_hierarchy(p, u, v, z, grid, 3, sweeps=1, coarse_tol=1e-2, cycle_kind=kind)
+    assert M.fused_v11_ok(h, h.levels[0].kkt)
+    oh = O.build_hierarchy(op, u, v, z, 32, grid.dt, 3, sweeps=1, coarse_tol=1e-2, cycle_kind=kind)
+    b = rng.standard_normal(h.levels[0].kkt.dim)
+    assert rel(P.cycle(h, 0, b), O.cycle(oh, 0, b)) < 1e-10
+    assert h.stats.iters == oh.coarse_iters
+
+
+@pytest.mark.parametrize("n_controls", [1, 2])
+def test_dense_fused_cycle_vs_oracle_and_unfused(n_controls, monkeypatch):
+    """van der Pol (DENSE family): the splitting-form rows with the folded
+    prolongation (dense_rows_split) against the oracle and the unfused kernels."""
+    import paper_2405_04808_b200 as P
+    from oracle import tk_oracle as O
+    from paper_2405_04808_b200 import multigrid as M
+    n = 64
+    grid = P.TimeGrid(5.0, n)
+    vp = P.build_vanderpol(P.VanDerPolConfig(n_controls=n_controls, u_init=(1.0, 0.0)), grid,
+                           with_targets=False)
+    rng = np.random.default_rng(3)
+    zc = 0.3 * rng.standard_normal((n, n_controls))
+    uv = P.forward_solve(vp, zc, grid).states
+    vv = uv + 0.01 * rng.standard_normal(uv.shape)
+    h = P.build_hierarchy(vp, uv, vv, zc, grid, 4, sweeps=1)
+    assert M.fused_v11_ok(h, h.levels[0].kkt)
+    ov = O.vanderpol(n_controls=n_controls, u0=(1.0, 0.0))
+    oh = O.build_hierarchy(ov, uv, vv, zc, n, grid.dt, 4, sweeps=1)
+    b = rng.standard_normal(h.levels[0].kkt.dim)
+    xo = O.cycle(oh, 0, b)
+    x_eager = P.cycle(h, 0, b)
+    assert rel(x_eager, xo) < 1e-10
+    assert h.stats.iters == oh.coarse_iters
+    assert rel(P.cycle(h, 0, b), xo) < 1e-10           # graph replay
+    x = rng.standard_normal(h.levels[0].kkt.dim)
+    a, oa = h.levels[0].kkt, oh.levels[0].kkt
+    assert rel(P.jacobi_apply(a, None, b, x, 2, 1.0), O.jacobi(oa, O.DiagSolve(oa), b, x, 2, 1.0)) < 1e-11
+    monkeypatch.setattr(M, "FUSED_PROLONG", False)
+    h2 = P.build_hierarchy(vp, uv, vv, zc, grid, 4, sweeps=1)
+    assert rel(P.cycle(h2, 0, b), x_eager) < 1e-12
