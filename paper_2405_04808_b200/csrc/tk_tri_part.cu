@@ -50,6 +50,9 @@ constexpr bool kStage = TK_PART_STAGE != 0;
 #ifndef TK_PART_PFD
 #define TK_PART_PFD 1            // L2 bulk prefetch distance (rows of this CTA ahead)
 #endif
+#ifndef TK_PART_SINGLE
+#define TK_PART_SINGLE 0         // 1: single PCR exchange buffer for W >= 8 (measured: no gain at n_u = 2048)
+#endif
 #ifndef TK_PART_EARLY
 #define TK_PART_EARLY 0          // 1: issue the output's loads before the interface solve (better while the kernel spilled)
 #endif
@@ -66,8 +69,12 @@ template <int W>
 struct PartCta {
     static constexpr int T = 32 * W;          // threads = chunks = interface nodes
     static constexpr int P = kChunk * T;      // padded system size
+    // TK_PART_SINGLE=1 (W >= 8): ONE exchange buffer with a second barrier per PCR
+    // step instead of a ping-pong pair (frees 78 KB for L1 at W = 16; measured
+    // equal at n_u = 2048: 6.16 vs 6.14 ms per sweep, so the pair stays)
+    static constexpr bool kSingle = TK_PART_SINGLE != 0 && W >= 8 && !kStage;
     static constexpr int64_t smem_bytes() {
-        return ((int64_t)(2 * kPX + (kStage ? kChunk * kSgC + kSgN : 0)) * T) * 8;
+        return ((int64_t)((kSingle ? 1 : 2) * kPX + (kStage ? kChunk * kSgC + kSgN : 0)) * T) * 8;
     }
     // resident CTAs per SM the build is register-limited to.  The residual
     // form (MODE 0, ~232 registers): 8 warps per SM.  The x-free rows (MODE
@@ -342,9 +349,9 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
     const double kap = V.kappa, k2 = kap * kap;
     const double* Qz = V.Qz;
     const bool px = RJ && (opt & 1);   // partial x: only the u and mu segments are stored
-    double* PX[2] = {sm, sm + kPX * T};    // PCR ping-pong slots
+    double* PX[2] = {sm, Cf::kSingle ? sm : sm + kPX * T};   // PCR ping-pong slots (or one)
     double* XB[1] = {PX[1]};               // exchange 1 (12 per thread; PX[1] is first written at step 2)
-    double* SG = sm + 2 * kPX * T;         // staged vector data of the next row [kSgC*4 + kSgN][T]
+    double* SG = sm + (Cf::kSingle ? 1 : 2) * kPX * T;   // staged vector data of the next row [kSgC*4 + kSgN][T]
     double* XO = nullptr;                  // interface solution (a PCR slot)
     double* LAM = nullptr;                 // first lam of every chunk (the other PCR slot)
 
@@ -819,6 +826,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         const double ocsL = ld1(C, 2 * n, jL, n, hc), ocbR = ld1(C, 0, jR, n, hc);
         TKPP(4);
 #endif
+        if (Cf::kSingle) csync();   // exchange 1 has been read: the buffer is free for the PCR
         // symmetric parallel cyclic reduction (ping-pong slots, one barrier per step).
         // Row l publishes G = C^T B^{-1} C, g = C^T B^{-1} R (for row l+s) and
         // B^{-1}, q = B^{-1} R, P = B^{-1} C (for row l-s).
@@ -881,6 +889,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                     sC = 0.0;
                 }
                 slot ^= 1;
+                if (Cf::kSingle) csync();   // every partner has read this step's values
             }
             const S2 iv = inv_s2f(B00, B01, B11);
             double* E = PX[slot];
@@ -889,7 +898,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             E[2 * T + tid] = sR * frcp(sB);
             csync();
             XO = E;
-            LAM = PX[slot ^ 1];
+            LAM = Cf::kSingle ? E + 4 * T : PX[slot ^ 1];
         }
         TKPP(5);
         const double X0 = XO[tid], X1 = XO[T + tid], sX = XO[2 * T + tid];
