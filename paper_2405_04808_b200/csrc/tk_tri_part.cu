@@ -48,7 +48,11 @@ constexpr int kChunk = TK_PART_CHUNK;
 #endif
 constexpr bool kStage = TK_PART_STAGE != 0;
 #ifndef TK_PART_PFD
-#define TK_PART_PFD 1            // L2 bulk prefetch distance (rows of this CTA ahead)
+#define TK_PART_PFD 0            // L2 bulk prefetch distance in rows of this CTA: 0 = the row itself, as
+                                 // one burst at its start (with 3 CTAs per SM the other rows hide the
+                                 // latency; a row ahead measured equal for the plain sweeps and slower
+                                 // for the fused prolongation: 0.352 vs 0.345 ms at n_u = 512, 8.30 vs
+                                 // 6.74 ms at n_u = 2048)
 #endif
 #ifndef TK_PART_SINGLE
 #define TK_PART_SINGLE 0         // 1: single PCR exchange buffer for W >= 8 (measured: no gain at n_u = 2048)
