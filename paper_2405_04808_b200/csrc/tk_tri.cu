@@ -900,6 +900,11 @@ __device__ __forceinline__ void tma_g2s(void* dst, const void* src, unsigned byt
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// L2 bulk prefetch of [p, p + bytes) (bytes a multiple of 16, p 16-byte aligned)
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, unsigned bytes) {
+    if (bytes == 0) return;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     asm volatile(
         "{\n .reg .pred P1;\n WAIT_%=:\n"
@@ -1101,6 +1106,11 @@ __global__ void __launch_bounds__(1024, 1)
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_expect_tx(&tbar, bytes);
         tma_g2s(blk, M + (size_t)chunk_at(t) * n * n + (size_t)r0 * n, bytes, &tbar);
+        // the single staging buffer exposes this copy's latency every transition: pull the
+        // next two row blocks into L2 now, so that their copies are L2 hits
+        for (int a = 1; a <= 2; ++a)
+            if (t + a < nc - 1)
+                l2_prefetch_bulk(M + (size_t)chunk_at(t + a) * n * n + (size_t)r0 * n, bytes);
     };
     if (tid == 0) {
         mbar_init(&tbar, 1);
@@ -1201,6 +1211,9 @@ __global__ void __launch_bounds__(1024, 1)
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_expect_tx(&tbar, bytes);
         tma_g2s(blk, M + (size_t)chunk_of(t) * n * n + (size_t)r0 * n, bytes, &tbar);
+        for (int a = 1; a <= 2; ++a)   // the next two row blocks -> L2 (see tri_chain_carry)
+            if (t + a < L)
+                l2_prefetch_bulk(M + (size_t)chunk_of(t + a) * n * n + (size_t)r0 * n, bytes);
     };
     if (tid == 0) {
         mbar_init(&tbar, 1);
