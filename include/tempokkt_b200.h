@@ -35,6 +35,13 @@ extern "C" {
 #define TK_FAMILY_TRI 1       /* tridiagonal-in-space stage blocks (1D FE Burgers), nz==nu  */
 
 #define TK_MAX_DENSE 4
+/* DENSE levels beyond TK_MAX_DENSE (general dense stage blocks, e.g. the
+ * reference's heat-Neumann problem): one warp per block row, the local saddle
+ * system by pivoted elimination in shared memory; n_u <= 40, n_z <= 8.  The
+ * fused V(1,1) kernels and the substitution factor records cover the small
+ * sizes only (tk_jacobi0_restrict_ok / tk_jacobi_prolong_ok return 0; no
+ * tk_subst_factor: the substitutions run as one serial kernel). */
+#define TK_MAX_DENSE_GENERAL 40
 
 /*
  * One level of the operator ladder (replaces BlockTriKKT + DiagonalSolver,

@@ -15,7 +15,8 @@ from .errors import (Breakdown, ConfigError, DimensionMismatch, IndivisibleSteps
                      NativeLibraryError, NewtonDivergence, NonFiniteValue, SingularBlock,
                      SingularMatrix, TempoKktError, UnsupportedStructure)
 from .timedisc import ProblemSpec, TimeGrid, Trajectory, forward_solve
-from .problems import BurgersConfig, VanDerPolConfig, build_burgers, build_vanderpol
+from .problems import (BurgersConfig, HeatNeumannConfig, VanDerPolConfig, build_burgers,
+                       build_heat_neumann, build_vanderpol)
 from .kkt import (BlockTriKKT, DiagonalSolver, KktLayout, StageBlocks, assemble_kkt,
                   assemble_rhs, build_stage_blocks, check_theorem1, clustered_permutation,
                   dump_matrix_market, factor_diagonal, from_clustered, split_parts,
@@ -32,7 +33,8 @@ __all__ = [
     "NewtonDivergence", "NonFiniteValue", "SingularBlock", "SingularMatrix", "TempoKktError",
     "UnsupportedStructure",
     "ProblemSpec", "TimeGrid", "Trajectory", "forward_solve",
-    "BurgersConfig", "VanDerPolConfig", "build_burgers", "build_vanderpol",
+    "BurgersConfig", "HeatNeumannConfig", "VanDerPolConfig", "build_burgers",
+    "build_heat_neumann", "build_vanderpol",
     "BlockTriKKT", "DiagonalSolver", "KktLayout", "StageBlocks", "assemble_kkt",
     "build_stage_blocks", "stage_blocks_from_arrays", "assemble_rhs", "check_theorem1",
     "clustered_permutation", "dump_matrix_market", "factor_diagonal", "from_clustered",

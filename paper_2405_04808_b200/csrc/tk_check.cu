@@ -185,15 +185,58 @@ __global__ void check_blocks_kernel(tk_level L, double pivot_floor, int32_t* bad
     }
 }
 
+// General DENSE sizes (n_u, n_z beyond TK_MAX_DENSE): the same getrf tests with
+// the work matrix in shared memory, one CTA per stage / block row (setup only).
+__global__ void check_k_big_kernel(tk_level L, int ns, double pivot_floor, int32_t* bad) {
+    extern __shared__ double csm[];
+    const int nu = L.n_u;
+    for (int s = blockIdx.x; s < ns; s += gridDim.x) {
+        if (threadIdx.x == 0) {
+            for (int e = 0; e < nu * nu; ++e) csm[e] = L.K[(size_t)s * nu * nu + e];
+            bad[s] = getrf_singular<0>(csm, nu, pivot_floor) ? 1 : 0;
+        }
+    }
+}
+__global__ void check_blocks_big_kernel(tk_level L, double pivot_floor, int32_t* bad) {
+    extern __shared__ double csm[];
+    for (int i = blockIdx.x; i <= L.n_steps; i += gridDim.x) {
+        if (threadIdx.x == 0) {
+            const int m = dense_block(L, i, csm);
+            bad[i] = getrf_singular<0>(csm, m, pivot_floor) ? 1 : 0;
+        }
+    }
+}
+static bool dense_big(const tk_level* L) {
+    return L->family == TK_FAMILY_DENSE && (L->n_u > TK_MAX_DENSE || L->n_z > TK_MAX_DENSE);
+}
+
 int check_k_launch(const tk_level* L, double pivot_floor, int32_t* bad, cudaStream_t s) {
     const int r1 = L->row1 > 0 ? L->row1 : L->n_steps + 1;
     const int ns = (r1 < L->n_steps ? r1 : L->n_steps) - L->row0;
     if (ns <= 0) return TK_OK;
+    if (dense_big(L)) {
+        const size_t sm = (size_t)L->n_u * L->n_u * sizeof(double);
+        check_k_big_kernel<<<ns < 2048 ? ns : 2048, 32, sm, s>>>(*L, ns, pivot_floor, bad);
+        return check_launch("check_k (general dense)");
+    }
     check_k_kernel<<<grid_for(ns, 64, 148 * 32), 64, 0, s>>>(*L, ns, pivot_floor, bad);
     return check_launch("check_k");
 }
 
 int check_blocks_launch(const tk_level* L, double pivot_floor, int32_t* bad, cudaStream_t s) {
+    if (dense_big(L)) {
+        const int m = 4 * L->n_u + L->n_z;
+        const size_t sm = (size_t)m * m * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(check_blocks_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 220 * 1024);
+            attr = true;
+        }
+        const int rows = L->n_steps + 1;
+        check_blocks_big_kernel<<<rows < 2048 ? rows : 2048, 32, sm, s>>>(*L, pivot_floor, bad);
+        return check_launch("check_blocks (general dense)");
+    }
     check_blocks_kernel<<<grid_for(L->n_steps + 1, 32, 148 * 64), 32, 0, s>>>(*L, pivot_floor,
                                                                              bad);
     return check_launch("check_blocks");

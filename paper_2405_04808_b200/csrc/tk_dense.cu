@@ -810,8 +810,13 @@ int dense_split(const tk_level* Lv, const double* b, const double* x, double* y,
     return TK_ERR_UNSUPPORTED;
 }
 
+int denseg_launch(const tk_level* Lv, int op, const double* b, const double* x, double* y,
+                  double omega, cudaStream_t s);
+
 int dense_launch(const tk_level* Lv, int op, const double* b, const double* x, double* y,
                  double omega, cudaStream_t s) {
+    if (Lv->n_u > TK_MAX_DENSE || Lv->n_z > TK_MAX_DENSE)   // general sizes: tk_denseg.cu
+        return denseg_launch(Lv, op, b, x, y, omega, s);
     switch (Lv->n_u) {
         case 1: TK_DENSE_NZ(1); break;
         case 2: TK_DENSE_NZ(2); break;

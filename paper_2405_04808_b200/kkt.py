@@ -36,6 +36,7 @@ from .timedisc import ProblemSpec, stage_jacobians, stage_weights
 FAMILY_DENSE = _lib.FAMILY_DENSE
 FAMILY_TRI = _lib.FAMILY_TRI
 MAX_DENSE = 4
+MAX_DENSE_GENERAL, MAX_DENSE_GENERAL_NZ = 40, 8     # warp-per-row dense kernels (tk_denseg.cu)
 PIVOT_FLOOR = 1e-14            # linalg.py:38
 
 
@@ -275,9 +276,12 @@ def _choose_family(n_u, n_z, q_mid, q_z, kappa_ok):
         return FAMILY_DENSE
     if n_z == n_u and _is_tridiagonal(q_mid) and _is_tridiagonal(q_z) and kappa_ok:
         return FAMILY_TRI
+    if n_u <= MAX_DENSE_GENERAL and n_z <= MAX_DENSE_GENERAL_NZ:
+        return FAMILY_DENSE        # general dense blocks (e.g. heat-Neumann, problems.py:218-266)
     raise UnsupportedStructure(
-        f"stage blocks with n_u={n_u}, n_z={n_z} are neither small dense (<= {MAX_DENSE}) "
-        "nor tridiagonal with B = kappa*Qz")
+        f"stage blocks with n_u={n_u}, n_z={n_z} are neither dense of moderate size "
+        f"(n_u <= {MAX_DENSE_GENERAL}, n_z <= {MAX_DENSE_GENERAL_NZ}) nor tridiagonal with "
+        "B = kappa*Qz")
 
 
 def build_stage_blocks(p: ProblemSpec, dt: float, u_seq, v_seq, z_seq,
@@ -454,6 +458,8 @@ class BlockTriKKT:
     def _ensure_fac(self) -> None:
         if self._fac is not None or os.environ.get("TK_SERIAL_SUBST") == "1":
             return
+        if self.family == FAMILY_DENSE and (self.n_u > MAX_DENSE or self.n_z > MAX_DENSE):
+            return          # general dense sizes: the substitutions run as one serial kernel
         lib = _lib.load()
         nf = int(lib.tk_subst_factor_len(self.lref))
         ns = int(lib.tk_subst_scratch_len(self.lref))

@@ -1,5 +1,6 @@
-"""Problem builders: van der Pol (problems.py:24-97) and 1D viscous Burgers
-with P1 finite elements (problems.py:100-197).
+"""Problem builders: van der Pol (problems.py:24-97), 1D viscous Burgers with
+P1 finite elements (problems.py:100-197) and Neumann boundary control of the
+1D heat equation (problems.py:200-266; general dense stage blocks).
 
 Each returns a :class:`ProblemSpec` with the reference's Python callables
 (so generic code paths and tests can evaluate F) plus a ``native`` tag that
@@ -159,3 +160,53 @@ def build_burgers(cfg: BurgersConfig, g: TimeGrid) -> ProblemSpec:
                        z_target=np.broadcast_to(np.zeros(n), (g.n_steps, n)), w_state=mass,
                        w_control=cfg.alpha * mass, f_hess_vec=f_hess_vec, name="burgers",
                        native={"kind": "burgers", "nu": nu})
+
+
+@dataclass
+class HeatNeumannConfig:
+    """Left-flux boundary control of the 1D heat equation (problems.py:200-215):
+    tracking weights alpha1 (running) and alpha2 (terminal), n_cells P1 cells."""
+
+    alpha1: float = 1e3
+    alpha2: float = 0.0
+    n_cells: int = 16
+    t_final: float = 1.0
+
+    def __post_init__(self):
+        if self.alpha1 < 0.0 or self.alpha2 < 0.0:
+            raise ValueError("tracking weights must be nonnegative")
+        if self.alpha1 == 0.0 and self.alpha2 == 0.0:
+            raise ValueError("alpha1 and alpha2 cannot both be zero")
+
+
+def build_heat_neumann(cfg: HeatNeumannConfig, g: TimeGrid, theta: float = 1.0) -> ProblemSpec:
+    """P1 FE heat operator on [0, 1] with flux boundary data, every node an
+    unknown (problems.py:218-266): F(u, z) = -A u - z e_first with the Neumann
+    mass / stiffness matrices, u0 = cos(pi x), zero targets, w_state =
+    alpha1 M, scalar control weight 1.  N_z = 1, N_u = n_cells + 1: general
+    dense stage blocks (the warp-per-row kernels of tk_denseg.cu)."""
+    nn = cfg.n_cells + 1
+    h = 1.0 / cfg.n_cells
+    mass = tridiag(nn, h / 6.0, 4.0 * h / 6.0, h / 6.0)
+    stiff = tridiag(nn, -1.0 / h, 2.0 / h, -1.0 / h)
+    for a, corner in ((mass, h / 3.0), (stiff, 1.0 / h)):
+        a[0, 0] = corner
+        a[-1, -1] = corner
+    fz = np.zeros((nn, 1))
+    fz[0, 0] = -1.0                       # -z * e_first
+
+    def f_eval(u, z):
+        return -stiff @ u + fz[:, 0] * z[0]
+
+    def f_jac_u(u, z):
+        return -stiff
+
+    def f_jac_z(u, z):
+        return fz
+
+    return ProblemSpec(
+        n_u=nn, n_z=1, mass=mass, f_eval=f_eval, f_jac_u=f_jac_u, f_jac_z=f_jac_z,
+        u0=np.cos(np.pi * h * np.arange(nn)), theta=theta, dt=g.dt,
+        u_target=np.zeros((g.n_steps, nn)), z_target=np.zeros((g.n_steps, 1)),
+        w_state=cfg.alpha1 * mass, w_control=np.array([[1.0]]),
+        w_terminal=(cfg.alpha2 * mass) if cfg.alpha2 > 0.0 else None, name="heat-neumann")
