@@ -27,8 +27,12 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE
 
 
 def sources():
-    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
-                  if f.endswith((".cu", ".cpp")))
+    """Every csrc/*.cu / *.cpp; the heavy template instantiation units (the
+    partitioned row kernels, one unit per row width) first so that the
+    parallel build starts them at once."""
+    srcs = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
+    heavy = [s for s in srcs if os.path.basename(s).startswith("tk_tri_part_w")]
+    return heavy + [s for s in srcs if s not in heavy]
 
 
 def _stale(srcs):

@@ -2173,13 +2173,12 @@ int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, dou
         set_error("tri family kernels support 2 <= n_u <= 4096 (got %d)", n);
         return TK_ERR_UNSUPPORTED;
     }
+    // compile-time n_u only for the headline size: the kernels behind tri_launch_t
+    // (CTA-wide cyclic reduction, record-based rows, the homogeneous chain runs of the
+    // set-up) are off the hot path since the partitioned rows and the partition-factor
+    // chain took over, and every further size costs ~25 s of build time
     switch (n) {
-        case 64: return tri_launch_t<64>(Lv, op, b, x, y, omega, s);
-        case 128: return tri_launch_t<128>(Lv, op, b, x, y, omega, s);
-        case 256: return tri_launch_t<256>(Lv, op, b, x, y, omega, s);
         case 512: return tri_launch_t<512>(Lv, op, b, x, y, omega, s);
-        case 1024: return tri_launch_t<1024>(Lv, op, b, x, y, omega, s);
-        case 2048: return tri_launch_t<2048>(Lv, op, b, x, y, omega, s);
         default: return tri_launch_t<0>(Lv, op, b, x, y, omega, s);
     }
 }
