@@ -662,10 +662,11 @@ def bench_rank(args, rank, world, local_rank):
     e1.record()
     torch.cuda.synchronize()
     jms = comm.allreduce_max(e0.elapsed_time(e1) / 5)
-    # algorithmic bytes of the slab: b, x in, x out + this slab's stage data
+    # algorithmic bytes of the slab (omega = 1: the splitting-form sweep reads b, the
+    # two coupling segments of x per row and this slab's stage data, writes x out)
     rows = min(a0.row1, a0.n_steps) - a0.row0
     sb = roofline.stage_bytes(a0) * rows // a0.n_steps
-    jbytes = 8 * a0.dim * 3 + sb
+    jbytes = 8 * a0.dim * 2 + 16 * rows * a0.n_u + sb
     try:
         import json as _json
         import os as _os
