@@ -465,10 +465,13 @@ __global__ void __launch_bounds__(T, 1)
 // ---------------------------------------------------------------------------
 template <int NA, int LT>
 __host__ __device__ constexpr int cws_common() { return 5 * NA - 4 + 2 * LT; }
-constexpr int kCwsRing = 27;
+// ring length (groups in flight per thread): 27 for 16 nodes per thread (108 groups per
+// interval), the whole interval (35 groups) for 4 nodes per thread
+template <int NA>
+__host__ __device__ constexpr int cws_ring() { return NA >= 16 ? 27 : 35; }
 template <int NA, int LT>
 __host__ __device__ constexpr int cws_gpi() {   // groups per interval, padded to a multiple of the ring
-    return (cws_common<NA, LT>() + NA + 1 + kCwsRing - 1) / kCwsRing * kCwsRing;
+    return (cws_common<NA, LT>() + NA + 1 + cws_ring<NA>() - 1) / cws_ring<NA>() * cws_ring<NA>();
 }
 // record slot of the i-th group in consumption order (FWD: C first; BWD: E, C last)
 template <bool FWD, int NA, int LT>
@@ -509,11 +512,11 @@ __global__ void __launch_bounds__(T, 1)
     constexpr int LT = ilog2(T);
     constexpr int SL = cw_slots(NA, LT);
     constexpr int REC = SL * T;
-    constexpr int R = kCwsRing;
+    constexpr int R = cws_ring<NA>();
     constexpr int GPI = cws_gpi<NA, LT>();
     constexpr int CB = FWD ? NA : 0;                     // first common group
     constexpr int CM = cws_common<NA, LT>();
-    static_assert(GPI % R == 0 && R < GPI, "ring must divide the interval stream");
+    static_assert(GPI % R == 0 && R <= GPI, "ring must divide the interval stream");
     extern __shared__ __align__(16) double sm[];
     double2* ring = reinterpret_cast<double2*>(sm);      // [R][2][T]
     double2* xH = ring + R * 2 * T;                      // exchange arrays [T] each
@@ -742,7 +745,9 @@ __global__ void __launch_bounds__(T, 1)
 // ---------------------------------------------------------------------------
 // (nodes per thread) * 1000 + threads of the warp chain for n_u (0: unsupported ->
 // tri_chain_kernel).  n_u <= 256: one warp; 256 < n_u <= 512: two warps of 8
-// nodes per thread (TK_CHAIN_NA=16: one warp of 16) -- the double-buffered
+// nodes per thread (TK_CHAIN_NA=16: one warp of 16, 4200 cycles per interval;
+// TK_CHAIN_NA=4: four warps of 4 through the streaming variant, measured
+// slower: 183 vs 171 us per forward substitution) -- the double-buffered
 // records (101 KB each at n_u = 512) bound the sizes covered.
 int chainw_nodes(int n) {
     static int on = -1, na512 = 8;
@@ -751,11 +756,12 @@ int chainw_nodes(int n) {
         on = (e && e[0] == '0') ? 0 : 1;
         const char* a = getenv("TK_CHAIN_NA");
         if (a && atoi(a) == 16) na512 = 16;
+        if (a && atoi(a) == 4) na512 = 4;
     }
     if (!on || n < 32 || n > 2048 || (n & 1)) return 0;
     if (n <= 128) return 4 * 1000 + 32;
     if (n <= 256) return 8 * 1000 + 32;
-    if (n <= 512) return na512 == 16 ? 16 * 1000 + 32 : 8 * 1000 + 64;
+    if (n <= 512) return na512 == 16 ? 16 * 1000 + 32 : (na512 == 4 ? 4 * 1000 + 128 : 8 * 1000 + 64);
     // beyond 512 the records exceed shared memory: per-thread cp.async streams
     return n <= 1024 ? 16 * 1000 + 64 : 16 * 1000 + 128;
 }
@@ -782,6 +788,7 @@ int chainw_factor(const tk_level* Lv, double* facw, cudaStream_t s) {
         case 8032: return chainw_factor_t<8, 32>(Lv, facw, s);
         case 8064: return chainw_factor_t<8, 64>(Lv, facw, s);
         case 16032: return chainw_factor_t<16, 32>(Lv, facw, s);
+        case 4128: return chainw_factor_t<4, 128>(Lv, facw, s);
         case 16064: return chainw_factor_t<16, 64>(Lv, facw, s);
         case 16128: return chainw_factor_t<16, 128>(Lv, facw, s);
         default: set_error("chainw_factor: unsupported n_u=%d", Lv->n_u); return TK_ERR_UNSUPPORTED;
@@ -808,7 +815,7 @@ template <bool FWD, int NA, int T>
 static int chainw_stream_t(const tk_level* Lv, const double* a, const double* facw, double* chain,
                            int Lc, int grid, int cbase, const double* st, double* en,
                            cudaStream_t s) {
-    const size_t smem = (size_t)(kCwsRing * 2 * T + 5 * T) * sizeof(double2);
+    const size_t smem = (size_t)(cws_ring<NA>() * 2 * T + 5 * T) * sizeof(double2);
     static bool attr = false;
     if (!attr) {
         const cudaError_t e = cudaFuncSetAttribute(tri_chainw_stream<FWD, NA, T>,
@@ -824,6 +831,9 @@ int chainw_launch(const tk_level* Lv, bool fwd, const double* a, const double* f
                   int Lc, int grid, int cbase, const double* st, double* en, cudaStream_t s) {
     if (grid <= 0) return TK_OK;
     switch (chainw_nodes(Lv->n_u)) {
+        case 4128:
+            return fwd ? chainw_stream_t<true, 4, 128>(Lv, a, facw, chain, Lc, grid, cbase, st, en, s)
+                       : chainw_stream_t<false, 4, 128>(Lv, a, facw, chain, Lc, grid, cbase, st, en, s);
         case 16064:
             return fwd ? chainw_stream_t<true, 16, 64>(Lv, a, facw, chain, Lc, grid, cbase, st, en, s)
                        : chainw_stream_t<false, 16, 64>(Lv, a, facw, chain, Lc, grid, cbase, st, en, s);
