@@ -117,6 +117,25 @@ def burgers(n_u=127, nu=1e-2, alpha=0.1, theta=0.5, u0_kind="step") -> Problem:
         w_state=mass, w_control=alpha * mass)
 
 
+def heat_neumann(n_cells=16, alpha1=1e3, alpha2=0.0, theta=1.0) -> Problem:
+    """Neumann boundary control of the 1D heat equation (problems.py:200-266):
+    P1 finite elements on n_cells cells, every node an unknown, the scalar
+    control is the left boundary flux, F(u, z) = -A u - z e_first."""
+    nn = n_cells + 1
+    h = 1.0 / n_cells
+    mass = _tridiag(nn, h / 6.0, 4.0 * h / 6.0, h / 6.0)
+    mass[0, 0] = mass[-1, -1] = h / 3.0
+    stiff = _tridiag(nn, -1.0 / h, 2.0 / h, -1.0 / h)
+    stiff[0, 0] = stiff[-1, -1] = 1.0 / h
+    e0 = np.zeros(nn)
+    e0[0] = 1.0
+    return Problem(
+        n_u=nn, n_z=1, mass=mass, f=lambda u, z: -stiff @ u - z[0] * e0,
+        f_u=lambda u, z: -stiff, f_z=lambda u, z: -e0.reshape(nn, 1),
+        u0=np.cos(np.pi * h * np.arange(nn)), theta=theta, w_state=alpha1 * mass,
+        w_control=np.array([[1.0]]), w_terminal=(alpha2 * mass) if alpha2 > 0.0 else None)
+
+
 # --------------------------------------------------------------------------
 # time discretisation (timedisc.py)
 # --------------------------------------------------------------------------

@@ -100,3 +100,33 @@ def test_full_solve(golden_case, outer):
     assert hist.shape == g[f"{outer}_hist"].shape
     assert rel(hist, g[f"{outer}_hist"]) < 1e-8
     assert rel(x, g[f"{outer}_x"]) < 1e-8
+
+
+def test_heat_neumann_oracle_vs_reference():
+    """The oracle on the reference's heat-Neumann problem (general dense
+    blocks, N_z = 1) against the reference-generated golden
+    (tests/golden/make_golden_heat.py): operator, local solves, smoothers,
+    transfers, one V-cycle and the FGMRES iteration count / history."""
+    from conftest import load_golden
+    g = load_golden("heat_ref")
+    n, levels = int(g["n"]), int(g["levels"])
+    p = O.heat_neumann(n_cells=int(g["n_cells"]))
+    dt = 1.0 / n
+    st = O.build_stages(p, dt, g["u"], g["v"], g["z"])
+    assert rel(st.k[0], g["k0"]) < 1e-15 and rel(st.c[1], g["c1"]) < 1e-15
+    assert rel(st.b[0], g["b0"]) < 1e-15 and rel(st.q_u[0], g["q_u0"]) < 1e-15
+    a = O.Kkt(st)
+    d = O.DiagSolve(a)
+    x, b = g["x"], g["b"]
+    assert rel(a.apply(x), g["apply"]) < 1e-14
+    assert rel(d.all(b), g["solve_all"]) < 1e-12
+    assert rel(O.jacobi(a, d, b, x, 2, 1.0), g["jacobi2"]) < 1e-12
+    assert rel(O.jacobi(a, d, b, x, 1, 0.7), g["jacobi_w"]) < 1e-12
+    assert rel(O.fgs(a, d, b, x), g["fgs"]) < 1e-12
+    assert rel(O.sgs(a, d, b, x), g["sgs"]) < 1e-12
+    h = O.build_hierarchy(p, g["u"], g["v"], g["z"], n, dt, levels, sweeps=1, coarse_tol=1e-2)
+    assert rel(O.cycle(h, 0, b), g["cycle"]) < 1e-11
+    xs, rep = O.fgmres(h.levels[0].kkt.apply, O.mg_prec(h), b, rel_tol=1e-8, max_iters=40)
+    assert rep.iterations == int(g["fgmres_iters"])
+    assert np.allclose(rep.history, g["fgmres_hist"], rtol=1e-10, atol=0)
+    assert rel(xs, g["fgmres_x"]) < 1e-10
