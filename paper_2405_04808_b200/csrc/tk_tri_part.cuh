@@ -406,10 +406,18 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 if (MODE == 3 && x) {   // only the two coupling segments of x
                     pf_l2(V.sl.uprev(L, x, i2), n);
                     pf_l2(V.sl.munext(L, x, i2), n);
-                    if (PR && (i2 & 1) == 0) {   // their coarse sources (even rows: new ones)
+                    if (PR) {   // and the coarse segments this row's couplings interpolate
                         const Lay Lp(L.N / 2, n, L.nz);
-                        if (i2 >= 2) pf_l2(chain + Lp.t_u(i2 / 2), n);
-                        if (i2 / 2 + 1 <= Lp.N) pf_l2(chain + Lp.t_mu(i2 / 2 + 1), n);
+                        if (i2 >= 1) {                      // u_t, t = i2
+                            const int t = i2;
+                            if ((t & 1) == 0 || t == 1) pf_l2(chain + Lp.t_u(t == 1 ? 1 : t / 2), n);
+                            else { pf_l2(chain + Lp.t_u((t - 1) / 2), n); pf_l2(chain + Lp.t_u((t + 1) / 2), n); }
+                        }
+                        if (i2 < L.N) {                     // mu_t, t = i2 + 1
+                            const int t = i2 + 1;
+                            if ((t & 1) == 0 || t == 1) pf_l2(chain + Lp.t_mu(t == 1 ? 1 : t / 2), n);
+                            else { pf_l2(chain + Lp.t_mu((t - 1) / 2), n); pf_l2(chain + Lp.t_mu((t + 1) / 2), n); }
+                        }
                     }
                 }
             }
