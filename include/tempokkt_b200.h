@@ -230,9 +230,9 @@ int tk_residual_restrict(const tk_level* L, const double* b, const double* x, do
  * tk_jacobi_sweep with omega = 1).  tk_jacobi0_restrict_um is the matching
  * pre-smoothing: tk_jacobi0_restrict storing ONLY the u and mu segments of
  * its x (the other segments of x_um are left untouched), which is all the
- * fused post-smoothing reads.  DENSE levels and TRI levels with full
- * partitioned rows (n_u a power-of-two multiple of 128 up to 2048); whole
- * level, even N: check tk_jacobi_prolong_ok(), else TK_ERR_UNSUPPORTED. */
+ * fused post-smoothing reads.  DENSE levels (n_u, n_z <= 4) and TRI levels of
+ * the partitioned rows (4 < n_u <= 2048); whole level, even N: check
+ * tk_jacobi_prolong_ok(), else TK_ERR_UNSUPPORTED. */
 int32_t tk_jacobi_prolong_ok(const tk_level* L, double omega);
 int tk_jacobi0_restrict_um(const tk_level* L, const double* b, double* x_um, double* rc,
                            void* stream);

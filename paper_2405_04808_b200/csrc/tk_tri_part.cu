@@ -56,9 +56,9 @@ int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, 
                       al(b) && al(x) && al(y) && al(chain) && al(rc) && al(ec) && al(Lv->K) &&
                       al(Lv->C) && al(Lv->Qm) && al(Lv->Ql) && al(Lv->Qz) && al(Lv->halo_u) &&
                       al(Lv->halo_mu);
-    if (ec && (mode != 3 || !x || rc || !whole_even || !full)) {
-        set_error("tri_rows_part: the fused prolongation needs omega = 1, x, a whole level with "
-                  "even N and full 16-byte aligned rows");
+    if (ec && (mode != 3 || !x || rc || !whole_even || w == 0 || cl != 1)) {
+        set_error("tri_rows_part: the fused prolongation needs omega = 1, x and a whole level with "
+                  "even N");
         return TK_ERR_UNSUPPORTED;
     }
     TK_PART_X(1, 1)
@@ -77,12 +77,10 @@ int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, 
     return TK_ERR_UNSUPPORTED;
 }
 
-// whether tk_jacobi_prolong's fused rows cover the level (full rows: n_u a
-// power-of-two multiple of 128 up to 2048, TOEPLITZ or not)
+// whether tk_jacobi_prolong's fused rows cover the level (any 4 < n_u <= 2048: rows that
+// are not full multiples of the chunk count take the guarded loads)
 bool part_full_rows(const tk_level* Lv) {
-    const int w = part_warps(Lv->n_u, 3);
-    return w > 0 && part_cluster(Lv->n_u, 3) == 1 && Lv->n_u == kChunk * 32 * w &&
-           Lv->n_z % 2 == 0;
+    return part_warps(Lv->n_u, 3) > 0 && part_cluster(Lv->n_u, 3) == 1;
 }
 
 }  // namespace tk

@@ -1125,7 +1125,10 @@ int part_dispatch_x(const tk_level* Lv, int mode, bool full, const double* b, co
         if (full) return part_launch_t<WW, 3, true, CC, true>(Lv, b, x, y, omega, chain, s, rc, opt);
         return part_launch_t<WW, 3, false, CC, true>(Lv, b, x, y, omega, chain, s, rc, opt);
     }
-    if (ec) return part_launch_t<WW, 3, true, CC, false, true>(Lv, b, x, y, omega, ec, s);
+    if (ec) {
+        if (full) return part_launch_t<WW, 3, true, CC, false, true>(Lv, b, x, y, omega, ec, s);
+        return part_launch_t<WW, 3, false, CC, false, true>(Lv, b, x, y, omega, ec, s);
+    }
     if (full) {
         if (mode == 3) return part_launch_t<WW, 3, true, CC>(Lv, b, x, y, omega, chain, s);
         if (mode == 1) return part_launch_t<WW, 1, true, CC>(Lv, b, x, y, omega, chain, s);

@@ -40,7 +40,7 @@ def test_splitting_form_matches_residual_form_and_oracle(n_u):
     assert rel(P.jacobi_apply(a, None, b, x, 2, 0.7), O.jacobi(oa, od, b, x, 2, 0.7)) < 1e-11
 
 
-@pytest.mark.parametrize("n_u", [128, 256, 512, 1024, 2048])
+@pytest.mark.parametrize("n_u", [33, 100, 128, 256, 300, 512, 1024, 1100, 2048])
 def test_fused_pre_and_post_vs_unfused(n_u):
     import torch
     from paper_2405_04808_b200 import _lib, device as dev
@@ -82,7 +82,7 @@ def test_fused_pre_and_post_vs_unfused(n_u):
         assert rel(y.cpu().numpy(), O.jacobi(oa, od, b.cpu().numpy(), xo, 1, 1.0)) < 1e-11
 
 
-@pytest.mark.parametrize("n_u,levels", [(128, 3), (256, 2)])
+@pytest.mark.parametrize("n_u,levels", [(100, 3), (128, 3), (256, 2)])
 def test_fused_cycle_vs_oracle_and_unfused(n_u, levels, monkeypatch):
     from paper_2405_04808_b200 import multigrid as M
     P, O, p, op, grid, u, v, z, rng = _case(n_u, n=32)
