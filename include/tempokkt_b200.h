@@ -234,6 +234,14 @@ int tk_residual_restrict(const tk_level* L, const double* b, const double* x, do
  * the partitioned rows (4 < n_u <= 2048); whole level, even N: check
  * tk_jacobi_prolong_ok(), else TK_ERR_UNSUPPORTED. */
 int32_t tk_jacobi_prolong_ok(const tk_level* L, double omega);
+/* One omega = 1 sweep from x_in (NULL: from zero) that also writes its
+ * restricted residual rc = R (b - A x_out) (multigrid.py:285-288 with any
+ * number of sweeps: the LAST pre-smoothing sweep).  After an omega = 1 sweep
+ * D x_out = b + (L + U) x_in, hence b - A x_out = (L + U)(x_out - x_in): only
+ * the continuity couplings of the update, which the sweep has in registers.
+ * Where tk_jacobi0_restrict_ok(L, 1) holds. */
+int tk_jacobi_restrict(const tk_level* L, const double* b, const double* x_in, double* x_out,
+                       double* rc, void* stream);
 int tk_jacobi0_restrict_um(const tk_level* L, const double* b, double* x_um, double* rc,
                            void* stream);
 int tk_jacobi_prolong(const tk_level* L, const double* b, const double* x, const double* ec,

@@ -61,6 +61,7 @@ _SIGS = {
     "tk_jacobi0_restrict_ok": (_i32, [C.POINTER(TkLevel), _d]),
     "tk_jacobi0_restrict": (C.c_int, [C.POINTER(TkLevel), _p, _d, _p, _p, _p]),
     "tk_jacobi_prolong_ok": (_i32, [C.POINTER(TkLevel), _d]),
+    "tk_jacobi_restrict": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p, _p]),
     "tk_jacobi0_restrict_um": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p]),
     "tk_jacobi_prolong": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p, _p]),
     "tk_forward_subst": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),

@@ -31,6 +31,8 @@ bool tri_jacobi0_restrict_ok(const tk_level*, double);
 int tri_jacobi0_restrict_launch(const tk_level*, const double*, double, double*, double*, cudaStream_t,
                                 int partial = 0);
 bool tri_jacobi_prolong_ok(const tk_level*, double);
+int tri_jacobi_restrict_launch(const tk_level*, const double*, const double*, double*, double*,
+                               cudaStream_t);
 int tri_jacobi_prolong_launch(const tk_level*, const double*, const double*, const double*, double*,
                               cudaStream_t);
 int dense_jacobi0_restrict(const tk_level*, const double*, double*, double*, cudaStream_t);
@@ -199,6 +201,20 @@ int tk_jacobi0_restrict_um(const tk_level* L, const double* b, double* x_um, dou
     if (L->family == TK_FAMILY_DENSE)
         return dense_split(L, b, nullptr, x_um, nullptr, rc, 1, as_stream(stream));
     return tri_jacobi0_restrict_launch(L, b, 1.0, x_um, rc, as_stream(stream), 1);
+}
+
+int tk_jacobi_restrict(const tk_level* L, const double* b, const double* x_in, double* x_out,
+                       double* rc, void* stream) {
+    TK_CHECK_ARG(b && x_out && rc && x_in != x_out, "tk_jacobi_restrict: bad vectors");
+    const int e = check_level(L);
+    if (e) return e;
+    if (!tk_jacobi0_restrict_ok(L, 1.0)) {
+        set_error("tk_jacobi_restrict: level not supported (see tk_jacobi0_restrict_ok)");
+        return TK_ERR_UNSUPPORTED;
+    }
+    if (L->family == TK_FAMILY_DENSE)
+        return dense_split(L, b, x_in, x_out, nullptr, rc, 0, as_stream(stream));
+    return tri_jacobi_restrict_launch(L, b, x_in, x_out, rc, as_stream(stream));
 }
 
 int tk_jacobi_prolong(const tk_level* L, const double* b, const double* x, const double* ec,

@@ -470,17 +470,19 @@ __global__ void __launch_bounds__(128) dense_rows_split(DView<NU, NZ> V, const d
         } else {
             store_seg<NU, NZ>(L, i, y, ys, bs0);
         }
-        if (rc) {
+        if (rc) {   // R (b - A y) = R (L + U)(y - x): couplings of the update
             if (i & 1) {
                 double* p = rc + Lc.t_mu((i + 1) / 2);
+                const double* xo = x ? x + (L.off_u(i) - bs0) : nullptr;
 #pragma unroll
-                for (int e = 0; e < NU; ++e) p[e] = 0.0 - ys.u[e];
+                for (int e = 0; e < NU; ++e) p[e] = (xo ? xo[e] : 0.0) - ys.u[e];
             } else {
                 const int c = i / 2;
                 if (i >= 2) {
                     double* p = rc + Lc.t_u(c);
+                    const double* xo = x ? x + (L.off_mu(i) - bs0) : nullptr;
 #pragma unroll
-                    for (int e = 0; e < NU; ++e) p[e] = 0.0 - ys.m[e];
+                    for (int e = 0; e < NU; ++e) p[e] = (xo ? xo[e] : 0.0) - ys.m[e];
                 }
                 if (c >= 1) {
                     double* p = rc + Lc.off_v(c);

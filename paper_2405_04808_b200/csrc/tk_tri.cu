@@ -2129,6 +2129,16 @@ int tri_jacobi0_restrict_launch(const tk_level* Lv, const double* b, double omeg
     }
     return part_launch(Lv, 0, b, nullptr, y, omega, nullptr, s, rc, nullptr, partial ? 1 : 0);
 }
+// one omega = 1 sweep from x (may be null) + its restricted residual
+int tri_jacobi_restrict_launch(const tk_level* Lv, const double* b, const double* x, double* y,
+                               double* rc, cudaStream_t s) {
+    if (!tri_jacobi0_restrict_ok(Lv, 1.0)) {
+        set_error("tk_jacobi_restrict: level not supported (TRI partitioned rows, whole level, "
+                  "even N)");
+        return TK_ERR_UNSUPPORTED;
+    }
+    return part_launch(Lv, 0, b, x, y, 1.0, nullptr, s, rc, nullptr, 0);
+}
 
 // y = D^{-1}(b + (L + U)(x + P ec)): the V-cycle's prolongation fused into
 // the omega = 1 post-smoothing sweep (tri_rows_part<..., PR>); only the u and

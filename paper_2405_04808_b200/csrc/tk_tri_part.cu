@@ -47,9 +47,9 @@ int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, 
     auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     const bool whole_even = Lv->row0 == 0 && (Lv->row1 == 0 || Lv->row1 == Lv->n_steps + 1) &&
                             (Lv->n_steps & 1) == 0;
-    if (rc && (mode != 3 || x || omega != 1.0 || !whole_even)) {
-        set_error("tri_rows_part: the fused restriction needs a zero-start sweep with omega = 1 "
-                  "on a whole level with even N");
+    if (rc && (mode != 3 || omega != 1.0 || !whole_even || (x && (opt & 1)))) {
+        set_error("tri_rows_part: the fused restriction needs a sweep with omega = 1 on a whole "
+                  "level with even N (partial output only from zero)");
         return TK_ERR_UNSUPPORTED;
     }
     const bool full = w > 0 && Lv->n_u == kChunk * 32 * w * cl && Lv->n_u % 2 == 0 && Lv->n_z % 2 == 0 &&

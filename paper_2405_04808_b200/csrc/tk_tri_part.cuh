@@ -314,10 +314,11 @@ extern "C" int tk_debug_part_prof(long long* out10) {
 // value and the first lam of the right neighbour) read the peer's shared
 // memory (distributed shared memory) after cluster barriers.
 //
-// RJ (MODE 3, x == nullptr, omega == 1, whole level, even N): the zero-start
-// sweep also writes the restricted residual rc = R (b - A y) of
-// tk_residual_restrict_jacobi0 (D y = b, so b - A y is the continuity
-// coupling): row 2c-1 writes -u_{2c} as the coarse mu_c, row 2c writes
+// RJ (MODE 3, omega == 1, whole level, even N): the sweep also writes the
+// restricted residual rc = R (b - A y).  After ANY omega = 1 sweep
+// D y = b + (L + U) x, so b - A y = (L + U)(y - x): only the continuity
+// couplings of the update y - x (x == nullptr: the zero-start sweep of
+// tk_residual_restrict_jacobi0, y itself): row 2c-1 writes -u_{2c} as the coarse mu_c, row 2c writes
 // -mu_{2c} as the coarse u_c and the zero v_c, z_{c+1}, lam_{c+1} of coarse
 // row c -- the separate restriction kernel and its re-read of y disappear.
 //
@@ -666,9 +667,11 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
 #pragma unroll
             for (int k = 0; k < NA; ++k) o[k] = xm[k] + omega * pm[k];
             st4<FULL>(y, om, j0, n, o);
-            if (RJ) {   // coarse u_{N/2} (coarse row N/2 - 1) = -mu_N
+            if (RJ) {   // coarse u_{N/2} (coarse row N/2 - 1) = -(mu_N - mu_N of x)
+                double xo[NA];
+                ld4<FULL>(x, om, j0, n, x != nullptr, xo);
 #pragma unroll
-                for (int k = 0; k < NA; ++k) o[k] = 0.0 - o[k];
+                for (int k = 0; k < NA; ++k) o[k] = xo[k] - o[k];
                 st4<FULL>(rc, Lc.t_u(i / 2), j0, n, o);
             }
             continue;
@@ -973,9 +976,11 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
 #pragma unroll
             for (int k = 0; k < NA; ++k) o[k] = oxu[k] + omega * yu[k];
             st4<FULL>(y, ou, j0, n, o);
-            if (RJ && (i & 1)) {   // row 2c-1: coarse mu_c = -u_{2c}
+            if (RJ && (i & 1)) {   // row 2c-1: coarse mu_c = -(u_{2c} - u_{2c} of x)
+                double xo[NA];
+                ld4<FULL>(x, ou, j0, n, x != nullptr, xo);
 #pragma unroll
-                for (int k = 0; k < NA; ++k) o[k] = 0.0 - o[k];
+                for (int k = 0; k < NA; ++k) o[k] = xo[k] - o[k];
                 st4<FULL>(rc, Lc.t_mu((i + 1) / 2), j0, n, o);
             }
             if (!px) {
@@ -1001,9 +1006,11 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                     o[k] = oxm[k] + omega * dm;
                 }
                 st4<FULL>(y, om, j0, n, o);
-                if (RJ && (i & 1) == 0) {   // row 2c: coarse u_c = -mu_{2c}
+                if (RJ && (i & 1) == 0) {   // row 2c: coarse u_c = -(mu_{2c} - mu_{2c} of x)
+                    double xo[NA];
+                    ld4<FULL>(x, om, j0, n, x != nullptr, xo);
 #pragma unroll
-                    for (int k = 0; k < NA; ++k) o[k] = 0.0 - o[k];
+                    for (int k = 0; k < NA; ++k) o[k] = xo[k] - o[k];
                     st4<FULL>(rc, Lc.t_u(i / 2), j0, n, o);
                 }
             }

@@ -142,7 +142,7 @@ class VCycleGraph:
         return cur
 
     def _record_level(self, l, body_stream):
-        from .multigrid import JACOBI0_RESIDUAL, fused_jacobi0_ok, fused_v11_ok
+        from .multigrid import JACOBI0_RESIDUAL, fused_jacobi0_ok, fused_v11_ok, fused_vnn_ok
         h = self.h
         L = h.n_levels
         a = h.levels[l].kkt
@@ -158,6 +158,17 @@ class VCycleGraph:
             self._record_level(l + 1, body_stream)
             dev.call("tk_jacobi_prolong", a.lref, dev.P(self.B[l]), dev.P(self.X[l]),
                      dev.P(self.E[l + 1]), dev.P(self.E[l]), s)
+            return
+        if h.sweeps > 1 and fused_vnn_ok(h, a):
+            # omega = 1, several sweeps: the last pre-smoothing sweep writes the
+            # restricted residual, the first post-smoothing sweep prolongs
+            xi = self._sweeps(a, self.B[l], None, [self.W[l], self.Y[l]], h.sweeps - 1)
+            dev.call("tk_jacobi_restrict", a.lref, dev.P(self.B[l]), dev.P(xi), dev.P(self.X[l]),
+                     dev.P(self.B[l + 1]), s)
+            self._record_level(l + 1, body_stream)
+            dev.call("tk_jacobi_prolong", a.lref, dev.P(self.B[l]), dev.P(self.X[l]),
+                     dev.P(self.E[l + 1]), dev.P(self.Y[l]), s)
+            self._sweeps(a, self.B[l], self.Y[l], [self.E[l], self.W[l]], h.sweeps - 1)
             return
         # pre-smoothing from zero: X (sweeps 1) or X/Y ping-pong ending in X
         bufs = [self.X[l]] if h.sweeps == 1 else [self.X[l], self.Y[l]]
@@ -251,11 +262,14 @@ class VCycleGraph:
         self.per_coarse_iter = sgs + zb + 1 + 1 + 1     # prec, (store z), apply, arnoldi, givens
         from .multigrid import fused_jacobi0_ok
         fixed = 0
-        from .multigrid import fused_v11_ok
+        from .multigrid import fused_v11_ok, fused_vnn_ok
         for l in range(self.start, h.n_levels - 1):     # sweeps, restrict, prolong
             fused = h.sweeps == 1 and fused_jacobi0_ok(h.levels[l].kkt, h.omega)
             if fused and fused_v11_ok(h, h.levels[l].kkt):
                 fixed += 2
+                continue
+            if h.sweeps > 1 and fused_vnn_ok(h, h.levels[l].kkt):
+                fixed += 2 * h.sweeps
                 continue
             fixed += 2 * h.sweeps + (0 if fused else 1) + 1
         fixed += 2 + 1 + 1 + 2 + (0 if zb else sgs) + 1 + 1 + 2 * 2 + 1  # begin, combine, (prec), apply, finish
@@ -297,12 +311,19 @@ def graphed_vcycle(h, b):
         h._graph = None
         g = h._graph = VCycleGraph(h)
     a = h.levels[0].kkt
-    from .multigrid import fused_v11_ok
+    from .multigrid import fused_v11_ok, fused_vnn_ok
     v11 = fused_v11_ok(h, a) and fused_jacobi0_ok(a, h.omega)
+    vnn = (not v11) and h.sweeps > 1 and fused_vnn_ok(h, a)
     if v11:
         x = dev.empty(a.dim)
         dev.call("tk_jacobi0_restrict_um", a.lref, dev.P(b), dev.P(x), dev.P(g.B[1]),
                  dev.stream())
+    elif vnn:
+        xi = jacobi_sweeps(a, b, None, h.sweeps - 1, 1.0)
+        x = dev.empty(a.dim)
+        dev.call("tk_jacobi_restrict", a.lref, dev.P(b), dev.P(xi), dev.P(x), dev.P(g.B[1]),
+                 dev.stream())
+        del xi
     elif h.sweeps == 1 and JACOBI0_RESIDUAL and fused_jacobi0_ok(a, h.omega):
         x = dev.empty(a.dim)
         dev.call("tk_jacobi0_restrict", a.lref, dev.P(b), float(h.omega), dev.P(x),
@@ -320,11 +341,11 @@ def graphed_vcycle(h, b):
     g.run()
     if dev.INSTR.counting:
         dev.INSTR.launches += g.launches
-    if v11:
+    if v11 or vnn:
         y = dev.empty(a.dim)
         dev.call("tk_jacobi_prolong", a.lref, dev.P(b), dev.P(x), dev.P(g.E[1]), dev.P(y),
                  dev.stream())
-        x = y
+        x = jacobi_sweeps(a, b, y, h.sweeps - 1, 1.0) if vnn else y
     else:
         h.transfers[0].prolong_add(g.E[1], x)
         x = jacobi_sweeps(a, b, x, h.sweeps, h.omega)

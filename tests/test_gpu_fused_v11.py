@@ -150,3 +150,80 @@ def test_dense_fused_cycle_vs_oracle_and_unfused(n_controls, monkeypatch):
     monkeypatch.setattr(M, "FUSED_PROLONG", False)
     h2 = P.build_hierarchy(vp, uv, vv, zc, grid, 4, sweeps=1)
     assert rel(P.cycle(h2, 0, b), x_eager) < 1e-12
+
+
+@pytest.mark.parametrize("n_u", [33, 128, 300, 512, 2048])
+def test_jacobi_restrict_from_nonzero_start(n_u):
+    """tk_jacobi_restrict: an omega = 1 sweep from any x that also writes
+    R (b - A y) = R (L + U)(y - x) (multigrid.py:285-288, last pre-smoothing
+    sweep) against tk_jacobi_sweep + the general tk_residual_restrict."""
+    import torch
+    from paper_2405_04808_b200 import device as dev
+    from paper_2405_04808_b200.multigrid import TransferOps
+    from paper_2405_04808_b200.smoothers import jacobi_sweeps
+    N = 8
+    P, O, p, op, grid, u, v, z, rng = _case(n_u, n=N)
+    a = P.assemble_kkt(P.build_stage_blocks(p, grid.dt, u, v, z))
+    t = TransferOps(N, N // 2, n_u, n_u)
+    b = dev.to_device(rng.standard_normal(a.dim))
+    x = dev.to_device(rng.standard_normal(a.dim))
+    y, rc = dev.empty(a.dim), dev.empty(t.coarse_dim)
+    dev.call("tk_jacobi_restrict", a.lref, dev.P(b), dev.P(x), dev.P(y), dev.P(rc), dev.stream())
+    y_ref = jacobi_sweeps(a, b, x, 1, 1.0)
+    assert torch.equal(y, y_ref)
+    rc_ref, work = dev.empty(t.coarse_dim), dev.empty(a.dim)
+    dev.call("tk_residual_restrict", a.lref, dev.P(b), dev.P(y_ref), dev.P(rc_ref), dev.P(work),
+             dev.stream())
+    # b - A y cancels to rounding where the fused form writes exact zeros
+    scale = float(torch.linalg.norm(b))
+    assert float(torch.linalg.norm(rc - rc_ref)) < 1e-12 * scale
+    # from zero (NULL): the zero-start kernel
+    y0, rc0, y1, rc1 = (dev.empty(a.dim), dev.empty(t.coarse_dim), dev.empty(a.dim),
+                        dev.empty(t.coarse_dim))
+    dev.call("tk_jacobi_restrict", a.lref, dev.P(b), dev.P(None), dev.P(y0), dev.P(rc0), dev.stream())
+    dev.call("tk_jacobi0_restrict", a.lref, dev.P(b), 1.0, dev.P(y1), dev.P(rc1), dev.stream())
+    assert torch.equal(y0, y1) and torch.equal(rc0, rc1)
+
+
+@pytest.mark.parametrize("kind,sweeps", [("v", 2), ("v", 3), ("w", 2), ("f", 1)])
+def test_multi_sweep_fused_cycle_vs_oracle(kind, sweeps, monkeypatch):
+    """sweeps > 1 and the W / F revisits with a non-zero iterate take
+    tk_jacobi_restrict + tk_jacobi_prolong (eager and graph replay) --
+    against the oracle and the unfused kernels."""
+    from paper_2405_04808_b200 import multigrid as M
+    P, O, p, op, grid, u, v, z, rng = _case(128, n=32)
+    h = P.build_hierarchy(p, u, v, z, grid, 3, sweeps=sweeps, coarse_tol=1e-2, cycle_kind=kind)
+    assert M.fused_vnn_ok(h, h.levels[0].kkt)
+    oh = O.build_hierarchy(op, u, v, z, 32, grid.dt, 3, sweeps=sweeps, coarse_tol=1e-2,
+                           cycle_kind=kind)
+    b = rng.standard_normal(h.levels[0].kkt.dim)
+    xo = O.cycle(oh, 0, b)
+    x1 = P.cycle(h, 0, b)
+    assert rel(x1, xo) < 1e-10
+    assert h.stats.iters == oh.coarse_iters
+    assert rel(P.cycle(h, 0, b), xo) < 1e-10          # V: graph replay
+    monkeypatch.setattr(M, "FUSED_PROLONG", False)
+    h2 = P.build_hierarchy(p, u, v, z, grid, 3, sweeps=sweeps, coarse_tol=1e-2, cycle_kind=kind)
+    assert rel(P.cycle(h2, 0, b), x1) < 1e-11
+
+
+def test_dense_multi_sweep_fused_cycle_vs_oracle():
+    import paper_2405_04808_b200 as P
+    from oracle import tk_oracle as O
+    from paper_2405_04808_b200 import multigrid as M
+    n = 64
+    grid = P.TimeGrid(5.0, n)
+    vp = P.build_vanderpol(P.VanDerPolConfig(n_controls=1, u_init=(1.0, 0.0)), grid,
+                           with_targets=False)
+    rng = np.random.default_rng(5)
+    zc = 0.3 * rng.standard_normal((n, 1))
+    uv = P.forward_solve(vp, zc, grid).states
+    h = P.build_hierarchy(vp, uv, uv, zc, grid, 4, sweeps=2)
+    assert M.fused_vnn_ok(h, h.levels[0].kkt)
+    oh = O.build_hierarchy(O.vanderpol(n_controls=1, u0=(1.0, 0.0)), uv, uv, zc, n, grid.dt, 4,
+                           sweeps=2)
+    b = rng.standard_normal(h.levels[0].kkt.dim)
+    xo = O.cycle(oh, 0, b)
+    assert rel(P.cycle(h, 0, b), xo) < 1e-10
+    assert h.stats.iters == oh.coarse_iters
+    assert rel(P.cycle(h, 0, b), xo) < 1e-10
