@@ -244,6 +244,22 @@ int tk_jacobi_restrict(const tk_level* L, const double* b, const double* x_in, d
                        double* rc, void* stream);
 int tk_jacobi0_restrict_um(const tk_level* L, const double* b, double* x_um, double* rc,
                            void* stream);
+/* The fused V(1,1) pair on a TIME SLAB (TRI levels; L->row0 even, L->row1 even
+ * or n_steps+1; tk_jacobi0_restrict_ok / tk_jacobi_prolong_ok say yes for such
+ * slabs too).  tk_jacobi0_restrict(_um) / tk_jacobi_restrict write the coarse
+ * entries (local coarse slice, as tk_restrict_slab) their own rows feed; the
+ * slab's first coarse mu comes from the previous slab's last row and its last
+ * coarse u from the next slab's first row: after the halo exchange of the
+ * iterate (L->halo_u / L->halo_mu, needed by the post-smoothing anyway)
+ * tk_restrict_fix_slab writes those two segments (zero-start sweeps:
+ * rc = -halo).  tk_jacobi_prolong_slab is tk_jacobi_prolong with the coarse
+ * segments outside the slab taken from chalo = [previous slab's last coarse
+ * (u, lam) | next slab's first coarse (v, mu)] (4 n_u doubles; the two halves
+ * are tk_prolong_add_slab's halo_prev_ul / halo_next_vm).
+ * Reference: multigrid.py:104-132, :285-299 on one time slab. */
+int tk_restrict_fix_slab(const tk_level* L, double* rc, void* stream);
+int tk_jacobi_prolong_slab(const tk_level* L, const double* b, const double* x, const double* ec,
+                           const double* chalo, double* x_out, void* stream);
 int tk_jacobi_prolong(const tk_level* L, const double* b, const double* x, const double* ec,
                       double* x_out, void* stream);
 

@@ -64,6 +64,8 @@ _SIGS = {
     "tk_jacobi_restrict": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p, _p]),
     "tk_jacobi0_restrict_um": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p]),
     "tk_jacobi_prolong": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p, _p]),
+    "tk_restrict_fix_slab": (C.c_int, [C.POINTER(TkLevel), _p, _p]),
+    "tk_jacobi_prolong_slab": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p, _p, _p]),
     "tk_forward_subst": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
     "tk_backward_subst": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
     "tk_sgs_back_half": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),

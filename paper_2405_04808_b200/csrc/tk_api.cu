@@ -34,7 +34,8 @@ bool tri_jacobi_prolong_ok(const tk_level*, double);
 int tri_jacobi_restrict_launch(const tk_level*, const double*, const double*, double*, double*,
                                cudaStream_t);
 int tri_jacobi_prolong_launch(const tk_level*, const double*, const double*, const double*, double*,
-                              cudaStream_t);
+                              cudaStream_t, const double* chalo = nullptr);
+int tri_restrict_fix_slab_launch(const tk_level*, double*, cudaStream_t);
 int dense_jacobi0_restrict(const tk_level*, const double*, double*, double*, cudaStream_t);
 int dense_split(const tk_level*, const double*, const double*, double*, const double*, double*, int,
                 cudaStream_t);
@@ -230,6 +231,30 @@ int tk_jacobi_prolong(const tk_level* L, const double* b, const double* x, const
         return dense_split(L, b, x, x_out, ec, nullptr, 0, as_stream(stream));
     }
     return tri_jacobi_prolong_launch(L, b, x, ec, x_out, as_stream(stream));
+}
+
+int tk_jacobi_prolong_slab(const tk_level* L, const double* b, const double* x, const double* ec,
+                           const double* chalo, double* x_out, void* stream) {
+    TK_CHECK_ARG(b && x && ec && chalo && x_out && x != x_out && b != x_out,
+                 "tk_jacobi_prolong_slab: bad vectors");
+    const int e = check_level(L);
+    if (e) return e;
+    if (L->family != TK_FAMILY_TRI) {
+        set_error("tk_jacobi_prolong_slab: TRI levels only");
+        return TK_ERR_UNSUPPORTED;
+    }
+    return tri_jacobi_prolong_launch(L, b, x, ec, x_out, as_stream(stream), chalo);
+}
+
+int tk_restrict_fix_slab(const tk_level* L, double* rc, void* stream) {
+    TK_CHECK_ARG(rc, "tk_restrict_fix_slab: null vector");
+    const int e = check_level(L);
+    if (e) return e;
+    if (L->family != TK_FAMILY_TRI) {
+        set_error("tk_restrict_fix_slab: TRI levels only");
+        return TK_ERR_UNSUPPORTED;
+    }
+    return tri_restrict_fix_slab_launch(L, rc, as_stream(stream));
 }
 
 int tk_forward_subst(const tk_level* L, const double* r, double* delta, void* stream) {

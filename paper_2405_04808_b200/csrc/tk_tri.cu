@@ -2116,9 +2116,46 @@ bool tri_jacobi0_restrict_ok(const tk_level* Lv, double omega) {
     const int n = Lv->n_u;
     const bool rec = Lv->fac != nullptr && !(Lv->flags & TK_FLAG_ONTHEFLY) &&
                      (!use_part(n) || (Lv->flags & TK_FLAG_RECROWS));
-    const bool whole = Lv->row0 == 0 && (Lv->row1 == 0 || Lv->row1 == Lv->n_steps + 1);
+    // the whole level, or a time slab cut at even rows (the coarse entries fed by
+    // the neighbouring slabs' rows: tk_restrict_fix_slab)
+    const int r1 = Lv->row1 > 0 ? Lv->row1 : Lv->n_steps + 1;
+    const bool slab = (Lv->row0 & 1) == 0 && (r1 == Lv->n_steps + 1 || (r1 & 1) == 0) &&
+                      r1 - Lv->row0 >= 2;
     return Lv->family == TK_FAMILY_TRI && omega == 1.0 && !rec && use_part(n) &&
-           part_nodes_per_lane(n) > 0 && whole && (Lv->n_steps % 2) == 0 && Lv->n_steps >= 2;
+           part_nodes_per_lane(n) > 0 && slab && (Lv->n_steps % 2) == 0 && Lv->n_steps >= 2;
+}
+
+// after tk_jacobi0_restrict(_um) on a time slab and the halo exchange of its
+// iterate y: the two coarse segments fed by the neighbouring slabs' rows --
+// the slab's first coarse mu = -(u of fine row row0 - 1) = -halo_u, its last
+// coarse u = -(mu of fine row row1) = -halo_mu
+__global__ void tri_restrict_fix_slab(Lay Lc, int64_t cb, int c0, int c1, bool has_prev,
+                                      bool has_next, const double* __restrict__ hu,
+                                      const double* __restrict__ hm, double* __restrict__ rc) {
+    const int n = Lc.nu;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < 2 * n; j += gridDim.x * blockDim.x) {
+        if (j < n) {
+            if (has_prev) rc[Lc.off_mu(c0) - cb + j] = 0.0 - hu[j];
+        } else if (has_next) {
+            rc[Lc.off_u(c1 - 1) - cb + (j - n)] = 0.0 - hm[j - n];
+        }
+    }
+}
+int tri_restrict_fix_slab_launch(const tk_level* Lv, double* rc, cudaStream_t s) {
+    const int N = Lv->n_steps, n = Lv->n_u;
+    const int r1 = Lv->row1 > 0 ? Lv->row1 : N + 1;
+    const bool has_prev = Lv->row0 > 0, has_next = r1 <= N;
+    if (!has_prev && !has_next) return TK_OK;
+    if ((N & 1) || (Lv->row0 & 1) || (has_next && (r1 & 1)) || (has_prev && !Lv->halo_u) ||
+        (has_next && !Lv->halo_mu)) {
+        set_error("tk_restrict_fix_slab: slab cut at even rows with its halos");
+        return TK_ERR_ARG;
+    }
+    const Lay Lc(N / 2, n, Lv->n_z);
+    const int c0 = Lv->row0 / 2, c1 = has_next ? r1 / 2 : N / 2 + 1;
+    tri_restrict_fix_slab<<<(2 * n + 255) / 256, 256, 0, s>>>(Lc, Lc.start(c0), c0, c1, has_prev,
+                                                            has_next, Lv->halo_u, Lv->halo_mu, rc);
+    return check_launch("tri_restrict_fix_slab");
 }
 int tri_jacobi0_restrict_launch(const tk_level* Lv, const double* b, double omega, double* y,
                                 double* rc, cudaStream_t s, int partial) {
@@ -2146,14 +2183,21 @@ int tri_jacobi_restrict_launch(const tk_level* Lv, const double* b, const double
 bool tri_jacobi_prolong_ok(const tk_level* Lv, double omega) {
     return tri_jacobi0_restrict_ok(Lv, omega) && part_full_rows(Lv);
 }
+// chalo (time slabs): [previous slab's last coarse (u, lam) | next slab's first
+// coarse (v, mu)], 4 n_u doubles
 int tri_jacobi_prolong_launch(const tk_level* Lv, const double* b, const double* x,
-                              const double* ec, double* y, cudaStream_t s) {
+                              const double* ec, double* y, cudaStream_t s, const double* chalo) {
     if (!tri_jacobi_prolong_ok(Lv, 1.0)) {
         set_error("tk_jacobi_prolong: level not supported (TRI partitioned full rows, whole "
-                  "level, even N)");
+                  "level or slab cut at even rows, even N)");
         return TK_ERR_UNSUPPORTED;
     }
-    return part_launch(Lv, 0, b, x, y, 1.0, nullptr, s, nullptr, ec, 0);
+    const bool whole = Lv->row0 == 0 && (Lv->row1 == 0 || Lv->row1 == Lv->n_steps + 1);
+    if (!whole && !chalo) {
+        set_error("tk_jacobi_prolong: a time slab needs its coarse halos (tk_jacobi_prolong_slab)");
+        return TK_ERR_ARG;
+    }
+    return part_launch(Lv, 0, b, x, y, 1.0, nullptr, s, const_cast<double*>(chalo), ec, 0);
 }
 
 int tri_launch(const tk_level* Lv, int op, const double* b, const double* x, double* y,

@@ -45,20 +45,23 @@ int part_launch(const tk_level* Lv, int mode, const double* b, const double* x, 
     // FULL: every chunk is complete and every segment 16-byte aligned
     const int w = part_warps(Lv->n_u, mode), cl = part_cluster(Lv->n_u, mode);
     auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    const bool whole_even = Lv->row0 == 0 && (Lv->row1 == 0 || Lv->row1 == Lv->n_steps + 1) &&
-                            (Lv->n_steps & 1) == 0;
-    if (rc && (mode != 3 || omega != 1.0 || !whole_even || (x && (opt & 1)))) {
-        set_error("tri_rows_part: the fused restriction needs a sweep with omega = 1 on a whole "
-                  "level with even N (partial output only from zero)");
+    // a whole level with even N, or a time slab cut at even rows
+    const int r1 = Lv->row1 > 0 ? Lv->row1 : Lv->n_steps + 1;
+    const bool slab_even = (Lv->n_steps & 1) == 0 && (Lv->row0 & 1) == 0 &&
+                           (r1 == Lv->n_steps + 1 || (r1 & 1) == 0) && r1 - Lv->row0 >= 2;
+    const bool whole = Lv->row0 == 0 && r1 == Lv->n_steps + 1;
+    if (rc && !ec && (mode != 3 || omega != 1.0 || !slab_even || (x && (opt & 1)))) {
+        set_error("tri_rows_part: the fused restriction needs a sweep with omega = 1 on a level "
+                  "(or slab cut at even rows) with even N (partial output only from zero)");
         return TK_ERR_UNSUPPORTED;
     }
     const bool full = w > 0 && Lv->n_u == kChunk * 32 * w * cl && Lv->n_u % 2 == 0 && Lv->n_z % 2 == 0 &&
                       al(b) && al(x) && al(y) && al(chain) && al(rc) && al(ec) && al(Lv->K) &&
                       al(Lv->C) && al(Lv->Qm) && al(Lv->Ql) && al(Lv->Qz) && al(Lv->halo_u) &&
                       al(Lv->halo_mu);
-    if (ec && (mode != 3 || !x || rc || !whole_even || w == 0 || cl != 1)) {
-        set_error("tri_rows_part: the fused prolongation needs omega = 1, x and a whole level with "
-                  "even N");
+    if (ec && (mode != 3 || !x || !slab_even || w == 0 || cl != 1 || (!whole && !rc))) {
+        set_error("tri_rows_part: the fused prolongation needs omega = 1, x and a level (or slab "
+                  "cut at even rows, with its coarse halos) with even N");
         return TK_ERR_UNSUPPORTED;
     }
     TK_PART_X(1, 1)

@@ -357,6 +357,9 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
     const double kap = V.kappa, k2 = kap * kap;
     const double* Qz = V.Qz;
     const bool px = RJ && (opt & 1);   // partial x: only the u and mu segments are stored
+    // PR on a time slab: the rc argument carries the coarse halos
+    // [previous slab's last coarse (u, lam) | next slab's first coarse (v, mu)]
+    const double* chalo = PR ? rc : nullptr;
     double* PX[2] = {sm, Cf::kSingle ? sm : sm + kPX * T};   // PCR ping-pong slots (or one)
     double* XB[1] = {PX[1]};               // exchange 1 (12 per thread; PX[1] is first written at step 2)
     double* SG = sm + (Cf::kSingle ? 1 : 2) * kPX * T;   // staged vector data of the next row [kSgC*4 + kSgN][T]
@@ -409,15 +412,24 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                     pf_l2(V.sl.munext(L, x, i2), n);
                     if (PR) {   // and the coarse segments this row's couplings interpolate
                         const Lay Lp(L.N / 2, n, L.nz);
+                        const int p0 = V.sl.r0 / 2,
+                                  p1 = V.sl.r1 == L.N + 1 ? L.N / 2 + 1 : V.sl.r1 / 2;
+                        const int64_t pb = Lp.start(p0);
+                        auto pu = [&](int tc) {
+                            if (tc - 1 >= p0) pf_l2(chain + (Lp.t_u(tc) - pb), n);
+                        };
+                        auto pm_ = [&](int tc) {
+                            if (tc < p1) pf_l2(chain + (Lp.t_mu(tc) - pb), n);
+                        };
                         if (i2 >= 1) {                      // u_t, t = i2
                             const int t = i2;
-                            if ((t & 1) == 0 || t == 1) pf_l2(chain + Lp.t_u(t == 1 ? 1 : t / 2), n);
-                            else { pf_l2(chain + Lp.t_u((t - 1) / 2), n); pf_l2(chain + Lp.t_u((t + 1) / 2), n); }
+                            if ((t & 1) == 0 || t == 1) pu(t == 1 ? 1 : t / 2);
+                            else { pu((t - 1) / 2); pu((t + 1) / 2); }
                         }
                         if (i2 < L.N) {                     // mu_t, t = i2 + 1
                             const int t = i2 + 1;
-                            if ((t & 1) == 0 || t == 1) pf_l2(chain + Lp.t_mu(t == 1 ? 1 : t / 2), n);
-                            else { pf_l2(chain + Lp.t_mu((t - 1) / 2), n); pf_l2(chain + Lp.t_mu((t + 1) / 2), n); }
+                            if ((t & 1) == 0 || t == 1) pm_(t == 1 ? 1 : t / 2);
+                            else { pm_((t - 1) / 2); pm_((t + 1) / 2); }
                         }
                     }
                 }
@@ -445,6 +457,10 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         const bool hx = MODE == 0 && x != nullptr;
         const bool hc = C != nullptr;
         const Lay Lc(L.N / 2, n, L.nz);
+        // coarse slice of the slab: coarse rows [c0, c1) stored from offset cb
+        // (whole level: every coarse row, cb = 0)
+        const int c0 = V.sl.r0 / 2, c1 = V.sl.r1 == L.N + 1 ? L.N / 2 + 1 : V.sl.r1 / 2;
+        const int64_t cb = Lc.start(c0);
         // PR: the couplings are those of x + P e (e = chain, the coarse
         // correction; multigrid.py:115-132): for the fine time t of the segment,
         // even t adds coarse t/2, t = 1 coarse 1, odd t >= 3 the mean of coarse
@@ -452,15 +468,24 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         const double *upa = nullptr, *upb = nullptr, *mna = nullptr, *mnb = nullptr;
         if (PR) {
             static_assert(!PR || (MODE == 3 && !kStage && !RJ), "PR: MODE 3 rows only");
+            // coarse u of time tc (coarse row tc - 1; outside the slab: the previous
+            // slab's last coarse u) and coarse mu of time tc (coarse row tc; outside:
+            // the next slab's first coarse mu); chalo = [prev (u, lam) | next (v, mu)]
+            auto cu = [&](int tc) -> const double* {
+                return tc - 1 >= c0 ? chain + (Lc.t_u(tc) - cb) : chalo;
+            };
+            auto cm = [&](int tc) -> const double* {
+                return tc < c1 ? chain + (Lc.t_mu(tc) - cb) : chalo + 3 * n;
+            };
             if (uprev) {          // u_t, t = i
                 const int t = i;
-                if ((t & 1) == 0 || t == 1) upa = chain + Lc.t_u(t == 1 ? 1 : t / 2);
-                else { upa = chain + Lc.t_u((t - 1) / 2); upb = chain + Lc.t_u((t + 1) / 2); }
+                if ((t & 1) == 0 || t == 1) upa = cu(t == 1 ? 1 : t / 2);
+                else { upa = cu((t - 1) / 2); upb = cu((t + 1) / 2); }
             }
             if (munext) {         // mu_t, t = i + 1
                 const int t = i + 1;
-                if ((t & 1) == 0 || t == 1) mna = chain + Lc.t_mu(t == 1 ? 1 : t / 2);
-                else { mna = chain + Lc.t_mu((t - 1) / 2); mnb = chain + Lc.t_mu((t + 1) / 2); }
+                if ((t & 1) == 0 || t == 1) mna = cm(t == 1 ? 1 : t / 2);
+                else { mna = cm((t - 1) / 2); mnb = cm((t + 1) / 2); }
             }
         }
         // x' = x + P e on the chunk nodes / one node of a coupling segment
@@ -655,10 +680,10 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             double zr[NA];
 #pragma unroll
             for (int k = 0; k < NA; ++k) zr[k] = 0.0;
-            if (c >= 1) st4<FULL>(rc, Lc.off_v(c), j0, n, zr);
+            if (c >= 1) st4<FULL>(rc, Lc.off_v(c) - cb, j0, n, zr);
             if (c < Lc.N) {
-                st4<FULL>(rc, Lc.off_z(c), j0, n, zr);
-                st4<FULL>(rc, Lc.off_l(c), j0, n, zr);
+                st4<FULL>(rc, Lc.off_z(c) - cb, j0, n, zr);
+                st4<FULL>(rc, Lc.off_l(c) - cb, j0, n, zr);
             }
         }
         if (!has_uzl) {   // last block (v_N, mu_N): mu = Qv v - r_v
@@ -672,7 +697,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 ld4<FULL>(x, om, j0, n, x != nullptr, xo);
 #pragma unroll
                 for (int k = 0; k < NA; ++k) o[k] = xo[k] - o[k];
-                st4<FULL>(rc, Lc.t_u(i / 2), j0, n, o);
+                st4<FULL>(rc, Lc.t_u(i / 2) - cb, j0, n, o);
             }
             continue;
         }
@@ -976,12 +1001,15 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
 #pragma unroll
             for (int k = 0; k < NA; ++k) o[k] = oxu[k] + omega * yu[k];
             st4<FULL>(y, ou, j0, n, o);
-            if (RJ && (i & 1)) {   // row 2c-1: coarse mu_c = -(u_{2c} - u_{2c} of x)
+            // (a slab's last odd row feeds the NEXT slab's first coarse mu, its first
+            // even row the PREVIOUS slab's last coarse u: tk_restrict_fix_slab
+            // writes those from the halos of y)
+            if (RJ && (i & 1) && (i + 1) / 2 < c1) {   // row 2c-1: coarse mu_c = -(u_{2c} - u_{2c} of x)
                 double xo[NA];
                 ld4<FULL>(x, ou, j0, n, x != nullptr, xo);
 #pragma unroll
                 for (int k = 0; k < NA; ++k) o[k] = xo[k] - o[k];
-                st4<FULL>(rc, Lc.t_mu((i + 1) / 2), j0, n, o);
+                st4<FULL>(rc, Lc.t_mu((i + 1) / 2) - cb, j0, n, o);
             }
             if (!px) {
 #pragma unroll
@@ -1006,12 +1034,12 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                     o[k] = oxm[k] + omega * dm;
                 }
                 st4<FULL>(y, om, j0, n, o);
-                if (RJ && (i & 1) == 0) {   // row 2c: coarse u_c = -(mu_{2c} - mu_{2c} of x)
+                if (RJ && (i & 1) == 0 && i / 2 - 1 >= c0) {   // row 2c: coarse u_c = -(mu_{2c} - mu_{2c} of x)
                     double xo[NA];
                     ld4<FULL>(x, om, j0, n, x != nullptr, xo);
 #pragma unroll
                     for (int k = 0; k < NA; ++k) o[k] = xo[k] - o[k];
-                    st4<FULL>(rc, Lc.t_u(i / 2), j0, n, o);
+                    st4<FULL>(rc, Lc.t_u(i / 2) - cb, j0, n, o);
                 }
             }
         }
@@ -1128,13 +1156,13 @@ template <int WW, int CC>
 int part_dispatch_x(const tk_level* Lv, int mode, bool full, const double* b, const double* x,
                     double* y, double omega, const double* chain, cudaStream_t s, double* rc,
                     const double* ec, int opt) {
+    if (ec) {   // rc: the coarse halos of a time slab (or null)
+        if (full) return part_launch_t<WW, 3, true, CC, false, true>(Lv, b, x, y, omega, ec, s, rc);
+        return part_launch_t<WW, 3, false, CC, false, true>(Lv, b, x, y, omega, ec, s, rc);
+    }
     if (rc) {
         if (full) return part_launch_t<WW, 3, true, CC, true>(Lv, b, x, y, omega, chain, s, rc, opt);
         return part_launch_t<WW, 3, false, CC, true>(Lv, b, x, y, omega, chain, s, rc, opt);
-    }
-    if (ec) {
-        if (full) return part_launch_t<WW, 3, true, CC, false, true>(Lv, b, x, y, omega, ec, s);
-        return part_launch_t<WW, 3, false, CC, false, true>(Lv, b, x, y, omega, ec, s);
     }
     if (full) {
         if (mode == 3) return part_launch_t<WW, 3, true, CC>(Lv, b, x, y, omega, chain, s);

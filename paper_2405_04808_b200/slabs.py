@@ -351,6 +351,31 @@ class CudaBackend:
                       a.row1 if a.row1 <= a.n_steps else a.n_steps + 1, self.dev.P(ec),
                       self.dev.P(hprev), self.dev.P(hnext), self.dev.P(x), self.dev.stream())
 
+    # the fused V(1,1) pair on a slab (TRI levels, omega = 1, one sweep) ---------
+    def fused_pair_ok(self, a) -> bool:
+        from . import _lib, multigrid
+        if not (multigrid.FUSED_PROLONG and multigrid.FUSED_JACOBI0 and multigrid.JACOBI0_RESIDUAL):
+            return False
+        from .kkt import FAMILY_TRI
+        return a.family == FAMILY_TRI and bool(_lib.load().tk_jacobi_prolong_ok(a.lref, 1.0))
+
+    def jacobi0_restrict_um(self, a, b, coarse_len):
+        """Zero-start sweep (u / mu segments of x only) + the coarse entries its
+        own rows feed; restrict_fix completes rc after the halo exchange of x."""
+        x, rc = self.dev.empty(a.dim), self.dev.empty(coarse_len)
+        self.dev.call("tk_jacobi0_restrict_um", a.lref, self.dev.P(b), self.dev.P(x),
+                      self.dev.P(rc), self.dev.stream())
+        return x, rc
+
+    def restrict_fix(self, a, rc):
+        self.dev.call("tk_restrict_fix_slab", a.lref, self.dev.P(rc), self.dev.stream())
+
+    def jacobi_prolong(self, a, b, x, ec, chalo):
+        y = self.dev.empty(a.dim)
+        self.dev.call("tk_jacobi_prolong_slab", a.lref, self.dev.P(b), self.dev.P(x),
+                      self.dev.P(ec), self.dev.P(chalo), self.dev.P(y), self.dev.stream())
+        return y
+
     def coarse_solve(self, h, r):
         from .multigrid import coarse_solve
         return coarse_solve(h, r)
@@ -471,8 +496,9 @@ class SlabHierarchy:
         c, nu, nz = self.comm, self.nu, self.nz
         nc = self.plan.n_at(lvl + 1)
         c0, c1 = self._coarse_rows(lvl, c.rank)
-        hprev = self.be.zeros(2 * nu)
-        hnext = self.be.zeros(2 * nu)
+        both = self.be.zeros(4 * nu)      # one buffer: tk_jacobi_prolong_slab's chalo
+        hprev, hnext = both[:2 * nu], both[2 * nu:]
+        self._chalo = both
         send_prev = send_next = None
         if c.rank > 0:
             ov = seg_offset(nc, nu, nz, c0, "v", c0)
@@ -496,24 +522,38 @@ class SlabHierarchy:
 
     def _cycle(self, lvl, b):
         a = self.levels[lvl]
-        x = self._smooth(lvl, b, None, self.sweeps)
-        self.exchange_x(lvl, x)
         c0, c1 = self._coarse_rows(lvl, self.comm.rank)
         nc = self.plan.n_at(lvl + 1)
         clen = slab_span(nc, self.nu, self.nz, c0, c1)[1]
         from . import multigrid
+        fp = getattr(self.be, "fused_pair_ok", None)
+        if self.sweeps == 1 and float(self.omega) == 1.0 and fp is not None and fp(a):
+            # V(1,1), omega = 1: pre-smoothing + restriction and prolongation +
+            # post-smoothing as the two fused kernels (multigrid._cycle's v11 path);
+            # the one exchange of x serves the coarse boundary entries and the
+            # post-smoothing couplings
+            x, rc = self.be.jacobi0_restrict_um(a, b, clen)
+            self.exchange_x(lvl, x)
+            self.be.restrict_fix(a, rc)
+            ec = self._coarse_correction(lvl, rc)
+            self.exchange_coarse(lvl, ec)
+            return self.be.jacobi_prolong(a, b, x, ec, self._chalo)
+        x = self._smooth(lvl, b, None, self.sweeps)
+        self.exchange_x(lvl, x)
         j0 = self.omega if (self.sweeps == 1 and multigrid.JACOBI0_RESIDUAL and
                             getattr(self.be, "jacobi0", True)) else None
         rc = self.be.residual_restrict(a, b, x, clen, j0)
-        if lvl + 1 == len(self.levels):
-            full = self.comm.gather(rc, self.coarse_sizes)
-            ef = self.be.coarse_solve(self.coarse, full) if self.comm.rank == 0 else None
-            ec = self.comm.scatter(ef, self.coarse_sizes, rc)
-        else:
-            ec = self._cycle(lvl + 1, rc)
+        ec = self._coarse_correction(lvl, rc)
         hprev, hnext = self.exchange_coarse(lvl, ec)
         self.be.prolong_add(a, ec, hprev, hnext, x)
         return self._smooth(lvl, b, x, self.sweeps)
+
+    def _coarse_correction(self, lvl, rc):
+        if lvl + 1 == len(self.levels):
+            full = self.comm.gather(rc, self.coarse_sizes)
+            ef = self.be.coarse_solve(self.coarse, full) if self.comm.rank == 0 else None
+            return self.comm.scatter(ef, self.coarse_sizes, rc)
+        return self._cycle(lvl + 1, rc)
 
     def vcycle(self, b_local):
         return self._cycle(0, b_local)
