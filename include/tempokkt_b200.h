@@ -244,7 +244,7 @@ int tk_jacobi_restrict(const tk_level* L, const double* b, const double* x_in, d
                        double* rc, void* stream);
 int tk_jacobi0_restrict_um(const tk_level* L, const double* b, double* x_um, double* rc,
                            void* stream);
-/* The fused V(1,1) pair on a TIME SLAB (TRI levels; L->row0 even, L->row1 even
+/* The fused V(1,1) pair on a TIME SLAB (both families; L->row0 even, L->row1 even
  * or n_steps+1; tk_jacobi0_restrict_ok / tk_jacobi_prolong_ok say yes for such
  * slabs too).  tk_jacobi0_restrict(_um) / tk_jacobi_restrict write the coarse
  * entries (local coarse slice, as tk_restrict_slab) their own rows feed; the

@@ -38,7 +38,7 @@ int tri_jacobi_prolong_launch(const tk_level*, const double*, const double*, con
 int tri_restrict_fix_slab_launch(const tk_level*, double*, cudaStream_t);
 int dense_jacobi0_restrict(const tk_level*, const double*, double*, double*, cudaStream_t);
 int dense_split(const tk_level*, const double*, const double*, double*, const double*, double*, int,
-                cudaStream_t);
+                cudaStream_t, const double* chalo = nullptr);
 int64_t tri_fac_len(const tk_level*);
 int64_t tri_scratch_len(const tk_level*);
 int64_t dense_fac_len(const tk_level*);
@@ -163,6 +163,17 @@ static bool dense_jacobi0_restrict_ok(const tk_level* L, double omega) {
            L->n_z <= TK_MAX_DENSE;
 }
 
+// the u/mu-only pre-smoothing + folded prolongation (dense_rows_split) also run on
+// a time slab cut at even rows
+static bool dense_pair_ok(const tk_level* L, double omega) {
+    const int r1 = L->row1 > 0 ? L->row1 : L->n_steps + 1;
+    const bool slab = (L->row0 & 1) == 0 && (r1 == L->n_steps + 1 || (r1 & 1) == 0) &&
+                      r1 - L->row0 >= 2;
+    return L->family == TK_FAMILY_DENSE && omega == 1.0 && slab && (L->n_steps % 2) == 0 &&
+           L->n_steps >= 2 && L->n_u >= 1 && L->n_u <= TK_MAX_DENSE && L->n_z >= 1 &&
+           L->n_z <= TK_MAX_DENSE;
+}
+
 int32_t tk_jacobi0_restrict_ok(const tk_level* L, double omega) {
     if (check_level(L)) return 0;
     if (L->family == TK_FAMILY_DENSE) return dense_jacobi0_restrict_ok(L, omega) ? 1 : 0;
@@ -186,7 +197,7 @@ int tk_jacobi0_restrict(const tk_level* L, const double* b, double omega, double
 
 int32_t tk_jacobi_prolong_ok(const tk_level* L, double omega) {
     if (check_level(L)) return 0;
-    if (L->family == TK_FAMILY_DENSE) return dense_jacobi0_restrict_ok(L, omega) ? 1 : 0;
+    if (L->family == TK_FAMILY_DENSE) return dense_pair_ok(L, omega) ? 1 : 0;
     return tri_jacobi_prolong_ok(L, omega) ? 1 : 0;
 }
 
@@ -239,9 +250,12 @@ int tk_jacobi_prolong_slab(const tk_level* L, const double* b, const double* x, 
                  "tk_jacobi_prolong_slab: bad vectors");
     const int e = check_level(L);
     if (e) return e;
-    if (L->family != TK_FAMILY_TRI) {
-        set_error("tk_jacobi_prolong_slab: TRI levels only");
-        return TK_ERR_UNSUPPORTED;
+    if (L->family == TK_FAMILY_DENSE) {
+        if (!dense_pair_ok(L, 1.0)) {
+            set_error("tk_jacobi_prolong_slab: level not supported (slab cut at even rows, even N)");
+            return TK_ERR_UNSUPPORTED;
+        }
+        return dense_split(L, b, x, x_out, ec, nullptr, 0, as_stream(stream), chalo);
     }
     return tri_jacobi_prolong_launch(L, b, x, ec, x_out, as_stream(stream), chalo);
 }
@@ -250,10 +264,6 @@ int tk_restrict_fix_slab(const tk_level* L, double* rc, void* stream) {
     TK_CHECK_ARG(rc, "tk_restrict_fix_slab: null vector");
     const int e = check_level(L);
     if (e) return e;
-    if (L->family != TK_FAMILY_TRI) {
-        set_error("tk_restrict_fix_slab: TRI levels only");
-        return TK_ERR_UNSUPPORTED;
-    }
     return tri_restrict_fix_slab_launch(L, rc, as_stream(stream));
 }
 

@@ -407,11 +407,23 @@ __global__ void __launch_bounds__(128) dense_rows_split(DView<NU, NZ> V, const d
                                                         const double* __restrict__ x,
                                                         double* __restrict__ y, double omega,
                                                         const double* __restrict__ ec,
-                                                        double* __restrict__ rc, int partial) {
+                                                        double* __restrict__ rc, int partial,
+                                                        const double* __restrict__ chalo) {
     const Lay& L = V.lay;
     const Slab& S = V.sl;
     const int64_t bs0 = S.base;
     const Lay Lc(L.N / 2, NU, NZ);
+    // time slab: coarse rows [c0, c1) stored from offset cb; coarse segments
+    // outside the slab come from chalo = [prev (u, lam) | next (v, mu)], the two
+    // coarse entries fed by the neighbours' rows from tk_restrict_fix_slab
+    const int c0 = S.r0 / 2, c1 = S.r1 == L.N + 1 ? L.N / 2 + 1 : S.r1 / 2;
+    const int64_t cb = Lc.start(c0);
+    auto cu = [&](int tc) -> const double* {
+        return tc - 1 >= c0 ? ec + (Lc.t_u(tc) - cb) : chalo;
+    };
+    auto cm = [&](int tc) -> const double* {
+        return tc < c1 ? ec + (Lc.t_mu(tc) - cb) : chalo + 3 * NU;
+    };
     for (int i = S.r0 + blockIdx.x * blockDim.x + threadIdx.x; i < S.r1;
          i += gridDim.x * blockDim.x) {
         Seg<NU, NZ> bs, ys;
@@ -421,30 +433,30 @@ __global__ void __launch_bounds__(128) dense_rows_split(DView<NU, NZ> V, const d
         if (uprev) {          // u_t, t = i
             const int t = i;
             const double* ca = nullptr;
-            const double* cb = nullptr;
+            const double* cb2 = nullptr;
             if (ec) {
-                if ((t & 1) == 0 || t == 1) ca = ec + Lc.t_u(t == 1 ? 1 : t / 2);
-                else { ca = ec + Lc.t_u((t - 1) / 2); cb = ec + Lc.t_u((t + 1) / 2); }
+                if ((t & 1) == 0 || t == 1) ca = cu(t == 1 ? 1 : t / 2);
+                else { ca = cu((t - 1) / 2); cb2 = cu((t + 1) / 2); }
             }
 #pragma unroll
             for (int e = 0; e < NU; ++e) {
                 double up = uprev[e];
-                if (ca) up = cb ? up + 0.5 * (ca[e] + cb[e]) : up + ca[e];
+                if (ca) up = cb2 ? up + 0.5 * (ca[e] + cb2[e]) : up + ca[e];
                 bs.m[e] -= up;
             }
         }
         if (munext) {         // mu_t, t = i + 1
             const int t = i + 1;
             const double* ca = nullptr;
-            const double* cb = nullptr;
+            const double* cb2 = nullptr;
             if (ec) {
-                if ((t & 1) == 0 || t == 1) ca = ec + Lc.t_mu(t == 1 ? 1 : t / 2);
-                else { ca = ec + Lc.t_mu((t - 1) / 2); cb = ec + Lc.t_mu((t + 1) / 2); }
+                if ((t & 1) == 0 || t == 1) ca = cm(t == 1 ? 1 : t / 2);
+                else { ca = cm((t - 1) / 2); cb2 = cm((t + 1) / 2); }
             }
 #pragma unroll
             for (int e = 0; e < NU; ++e) {
                 double mn = munext[e];
-                if (ca) mn = cb ? mn + 0.5 * (ca[e] + cb[e]) : mn + ca[e];
+                if (ca) mn = cb2 ? mn + 0.5 * (ca[e] + cb2[e]) : mn + ca[e];
                 bs.u[e] -= mn;
             }
         }
@@ -472,26 +484,28 @@ __global__ void __launch_bounds__(128) dense_rows_split(DView<NU, NZ> V, const d
         }
         if (rc) {   // R (b - A y) = R (L + U)(y - x): couplings of the update
             if (i & 1) {
-                double* p = rc + Lc.t_mu((i + 1) / 2);
-                const double* xo = x ? x + (L.off_u(i) - bs0) : nullptr;
+                if ((i + 1) / 2 < c1) {
+                    double* p = rc + (Lc.t_mu((i + 1) / 2) - cb);
+                    const double* xo = x ? x + (L.off_u(i) - bs0) : nullptr;
 #pragma unroll
-                for (int e = 0; e < NU; ++e) p[e] = (xo ? xo[e] : 0.0) - ys.u[e];
+                    for (int e = 0; e < NU; ++e) p[e] = (xo ? xo[e] : 0.0) - ys.u[e];
+                }
             } else {
                 const int c = i / 2;
-                if (i >= 2) {
-                    double* p = rc + Lc.t_u(c);
+                if (i >= 2 && c - 1 >= c0) {
+                    double* p = rc + (Lc.t_u(c) - cb);
                     const double* xo = x ? x + (L.off_mu(i) - bs0) : nullptr;
 #pragma unroll
                     for (int e = 0; e < NU; ++e) p[e] = (xo ? xo[e] : 0.0) - ys.m[e];
                 }
                 if (c >= 1) {
-                    double* p = rc + Lc.off_v(c);
+                    double* p = rc + (Lc.off_v(c) - cb);
 #pragma unroll
                     for (int e = 0; e < NU; ++e) p[e] = 0.0;
                 }
                 if (c < Lc.N) {
-                    double* pz = rc + Lc.off_z(c);
-                    double* pl = rc + Lc.off_l(c);
+                    double* pz = rc + (Lc.off_z(c) - cb);
+                    double* pl = rc + (Lc.off_l(c) - cb);
 #pragma unroll
                     for (int e = 0; e < NZ; ++e) pz[e] = 0.0;
 #pragma unroll
@@ -504,11 +518,12 @@ __global__ void __launch_bounds__(128) dense_rows_split(DView<NU, NZ> V, const d
 
 template <int NU, int NZ>
 static int dense_split_t(const tk_level* Lv, const double* b, const double* x, double* y,
-                         double omega, const double* ec, double* rc, int partial, cudaStream_t s) {
+                         double omega, const double* ec, double* rc, int partial, cudaStream_t s,
+                         const double* chalo) {
     DView<NU, NZ> V(Lv);
     const int rows = V.sl.r1 - V.sl.r0;
     dense_rows_split<NU, NZ><<<grid_for(rows, 128, 1 << 20), 128, 0, s>>>(V, b, x, y, omega, ec, rc,
-                                                                           partial);
+                                                                           partial, chalo);
     return check_launch("dense_rows_split");
 }
 
@@ -746,7 +761,7 @@ static int dense_launch_t(const tk_level* Lv, int op, const double* b, const dou
             // omega = 1 or from zero: x enters through the two couplings only
             // (TK_JACOBI_RESIDUAL_FORM=1 keeps x + omega D^{-1}(b - A x))
             if ((x == nullptr || omega == 1.0) && !dense_resid_form())
-                return dense_split_t<NU, NZ>(Lv, b, x, y, omega, nullptr, nullptr, 0, s);
+                return dense_split_t<NU, NZ>(Lv, b, x, y, omega, nullptr, nullptr, 0, s, nullptr);
             dense_rows<NU, NZ, D_JACOBI><<<grid, th, 0, s>>>(V, b, x, y, omega);
             break;
         case 10:
@@ -800,9 +815,9 @@ int dense_jacobi0_restrict(const tk_level* Lv, const double* b, double* y, doubl
 
 // tk_jacobi0_restrict_um (x == nullptr, rc, partial) / tk_jacobi_prolong (x, ec) on DENSE levels
 int dense_split(const tk_level* Lv, const double* b, const double* x, double* y, const double* ec,
-                double* rc, int partial, cudaStream_t s) {
+                double* rc, int partial, cudaStream_t s, const double* chalo) {
 #define TK_DSP(NU, NZ) \
-    if (Lv->n_u == NU && Lv->n_z == NZ) return dense_split_t<NU, NZ>(Lv, b, x, y, 1.0, ec, rc, partial, s);
+    if (Lv->n_u == NU && Lv->n_z == NZ) return dense_split_t<NU, NZ>(Lv, b, x, y, 1.0, ec, rc, partial, s, chalo);
     TK_DSP(1, 1) TK_DSP(1, 2) TK_DSP(1, 3) TK_DSP(1, 4)
     TK_DSP(2, 1) TK_DSP(2, 2) TK_DSP(2, 3) TK_DSP(2, 4)
     TK_DSP(3, 1) TK_DSP(3, 2) TK_DSP(3, 3) TK_DSP(3, 4)

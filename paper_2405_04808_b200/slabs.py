@@ -351,13 +351,12 @@ class CudaBackend:
                       a.row1 if a.row1 <= a.n_steps else a.n_steps + 1, self.dev.P(ec),
                       self.dev.P(hprev), self.dev.P(hnext), self.dev.P(x), self.dev.stream())
 
-    # the fused V(1,1) pair on a slab (TRI levels, omega = 1, one sweep) ---------
+    # the fused V(1,1) pair on a slab (omega = 1, one sweep) ------------------
     def fused_pair_ok(self, a) -> bool:
         from . import _lib, multigrid
         if not (multigrid.FUSED_PROLONG and multigrid.FUSED_JACOBI0 and multigrid.JACOBI0_RESIDUAL):
             return False
-        from .kkt import FAMILY_TRI
-        return a.family == FAMILY_TRI and bool(_lib.load().tk_jacobi_prolong_ok(a.lref, 1.0))
+        return bool(_lib.load().tk_jacobi_prolong_ok(a.lref, 1.0))
 
     def jacobi0_restrict_um(self, a, b, coarse_len):
         """Zero-start sweep (u / mu segments of x only) + the coarse entries its

@@ -185,3 +185,40 @@ def test_fused_pair_on_slabs_bitwise(n_u, R):
     assert all(used) and len(used) == R
     got = np.concatenate([r[1] for r in sorted(res, key=lambda t: t[0])])
     assert np.array_equal(got, ref), np.abs(got - ref).max()
+
+
+@pytest.mark.parametrize("n_controls,R", [(1, 2), (2, 4)])
+def test_dense_fused_pair_on_slabs_bitwise(n_controls, R):
+    """van der Pol (DENSE family): the slab cycle through dense_rows_split with
+    the coarse halos, bitwise against the single-GPU fused cycle."""
+    import torch
+
+    import paper_2405_04808_b200 as P
+    from paper_2405_04808_b200 import slabs
+    n, levels = 64, 3
+    grid = P.TimeGrid(5.0, n)
+    vp = P.build_vanderpol(P.VanDerPolConfig(n_controls=n_controls, u_init=(1.0, 0.0)), grid,
+                           with_targets=False)
+    rng = np.random.default_rng(11)
+    zc = 0.3 * rng.standard_normal((n, n_controls))
+    uv = P.forward_solve(vp, zc, grid).states
+    vv = uv + 0.01 * rng.standard_normal(uv.shape)
+    h = P.build_hierarchy(vp, uv, vv, zc, grid, levels, sweeps=1)
+    b = rng.standard_normal(h.levels[0].kkt.dim)
+    ref = P.cycle(h, 0, b)
+    comms = slabs.ThreadComm.group(R)
+    used = []
+
+    def body(c):
+        sh = slabs.SlabHierarchy(vp, uv, vv, zc, grid, levels, c, sweeps=1)
+        used.append(all(sh.be.fused_pair_ok(a) for a in sh.levels))
+        off, ln = sh.local_span()
+        bl = torch.from_numpy(np.ascontiguousarray(b[off:off + ln])).cuda()
+        out = sh.vcycle(bl)
+        torch.cuda.synchronize()
+        return off, out.cpu().numpy()
+
+    res = slabs.run_threads(comms, body)
+    assert all(used) and len(used) == R
+    got = np.concatenate([r[1] for r in sorted(res, key=lambda t: t[0])])
+    assert np.array_equal(got, ref), np.abs(got - ref).max()
