@@ -678,7 +678,34 @@ __device__ long long g_tk_prof[16];
         if (threadIdx.x == 0 && blockIdx.x == 0) g_tk_prof[slot] += (v); \
     } while (0)
 #define TKCLK() clock64()
+// kernel-wide span of the grouped carry: [0] min CTA start, [1] max CTA end,
+// [2] max start, [3] CTA 0 end - start (globaltimer ns)
+__device__ unsigned long long g_tk_span[8] = {~0ull, 0ull, 0ull, 0ull, ~0ull, 0ull, 0ull, 0ull};
+__device__ __forceinline__ unsigned long long tk_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TKSPAN_BEGIN(o)                                                  \
+    unsigned long long tk_t0 = 0;                                        \
+    if (threadIdx.x == 0) {                                              \
+        tk_t0 = tk_gtime();                                              \
+        atomicMin(&g_tk_span[(o) + 0], tk_t0);                           \
+        atomicMax(&g_tk_span[(o) + 2], tk_t0);                           \
+    }
+#define TKSPAN_END(o)                                                    \
+    if (threadIdx.x == 0) {                                              \
+        const unsigned long long t1 = tk_gtime();                        \
+        atomicMax(&g_tk_span[(o) + 1], t1);                              \
+        if (blockIdx.x == 0) g_tk_span[(o) + 3] = t1 - tk_t0;            \
+    }
 #else
+#define TKSPAN_BEGIN(o) \
+    do {                \
+    } while (0)
+#define TKSPAN_END(o) \
+    do {              \
+    } while (0)
 #define TKA(slot, v) \
     do {             \
     } while (0)
@@ -1074,6 +1101,31 @@ __device__ __forceinline__ void st_async_f64(unsigned raddr, double v, unsigned 
                  : "memory");
 }
 
+// Register-row variant of the carry matvec (staged == 2: n % 64 == 0, n <= 512
+// and exactly one row per warp): the lane's 16 entries of its row of the NEXT
+// propagator are loaded into registers right after the current ones have been
+// consumed, so they fly while the new U is pushed and awaited; shared memory
+// then carries only U (the TMA-staged row block doubled its traffic: 256 KB
+// per step and CTA at 128 B/clk was the step's largest part).  Same order of
+// the products and sums as the staged loop.
+static constexpr int kCarryNI = 16;
+__device__ __forceinline__ void carry_loadrow(const double* __restrict__ row, int n, int lane,
+                                              double (&m)[kCarryNI]) {
+#pragma unroll
+    for (int i = 0; i < kCarryNI; ++i) m[i] = (32 * i < n) ? __ldcg(row + lane + 32 * i) : 0.0;
+}
+__device__ __forceinline__ double carry_dotrow(const double (&m)[kCarryNI],
+                                               const double* __restrict__ cur, int n, int lane) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < kCarryNI; i += 2)
+        if (32 * i < n) {
+            a0 = fma(m[i], cur[lane + 32 * i], a0);
+            a1 = fma(m[i + 1], cur[lane + 32 * i + 32], a1);
+        }
+    return a0 + a1;
+}
+
 // Serial carry over the chunk ends (one thread-block cluster):
 //   U = ends[first];  for each next chunk c in chain order:
 //     starts[c] = U;  U = ends[c] + M_c U
@@ -1084,7 +1136,7 @@ __device__ __forceinline__ void st_async_f64(unsigned raddr, double v, unsigned 
 // per chunk is that transaction count (no cluster-wide barrier).  staged:
 // the CTA's row block of the next M_c is TMA bulk-copied into shared memory
 // as soon as the current one has been consumed.
-template <bool FWD>
+template <bool FWD, bool RG = false>
 __global__ void __launch_bounds__(1024, 1)
     tri_chain_carry(int n, int nc, const double* __restrict__ M, const double* __restrict__ ends,
                     double* __restrict__ starts, int staged) {
@@ -1099,9 +1151,15 @@ __global__ void __launch_bounds__(1024, 1)
     const int r0 = min(n, rank * rpc), r1 = min(n, r0 + rpc);
     double* blk = sm + 2 * n;
     const unsigned bytes = (unsigned)((size_t)(r1 - r0) * n * sizeof(double));
-    const bool stg = staged && bytes > 0;
+    constexpr bool rg = RG;                      // register rows (one per warp)
+    const bool stg = !RG && staged == 1 && bytes > 0;
     const unsigned ubytes = (unsigned)(n * sizeof(double));
     auto chunk_at = [&](int t) { return FWD ? t : nc - 1 - t; };
+    double m[kCarryNI];
+    auto rowp = [&](int t) { return M + (size_t)chunk_at(t) * n * n + (size_t)(r0 + warp) * n; };
+    auto pf = [&](int t) {   // this CTA's row block of step t -> L2
+        if (t < nc - 1) l2_prefetch_bulk(M + (size_t)chunk_at(t) * n * n + (size_t)r0 * n, bytes);
+    };
     auto issue = [&](int t) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_expect_tx(&tbar, bytes);
@@ -1120,6 +1178,10 @@ __global__ void __launch_bounds__(1024, 1)
     }
     __syncthreads();
     if (stg && tid == 0 && nc > 2) issue(1);
+    if (rg && nc > 2) {
+        if (tid == 0) { pf(2); pf(3); }
+        carry_loadrow(rowp(1), n, lane, m);
+    }
     const int first = FWD ? 0 : nc - 1;
     for (int j = tid; j < n; j += blockDim.x) sm[j] = ends[(size_t)first * n + j];
     cl.sync();   // every CTA's barriers are initialised before any st.async
@@ -1142,6 +1204,21 @@ __global__ void __launch_bounds__(1024, 1)
         const double* ec = ends + (size_t)c * n;
         const unsigned nxt = smem_u32(sm + (t & 1) * n);
         const unsigned bar = smem_u32(&ubar[t & 1]);
+        if (rg) {
+            const int r = r0 + warp;
+            const double e = ec[r];
+            double acc = carry_dotrow(m, cur, n, lane);
+            if (t + 1 < nc - 1) carry_loadrow(rowp(t + 1), n, lane, m);
+            if (tid == 0) pf(t + 3);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            const double v = e + acc;
+            for (int d = lane; d < CS; d += 32)
+                st_async_f64(mapa_u32(nxt + 8u * r, d), v, mapa_u32(bar, d));
+            TKA(10, TKCLK() - c1);
+            __syncthreads();   // the warps stay within one step of each other
+            continue;
+        }
         for (int r = r0 + warp; r < r1; r += nw) {
             const double* row = src + (size_t)(r - r0) * n;
             const double e = ec[r];
@@ -1181,7 +1258,7 @@ __global__ void __launch_bounds__(1024, 1)
 //     transitions from GS[g], writing the exact chunk starts.
 // The group last in chain order also writes the start of the final chunk.
 // Serial depth: 2G + nc/G matvecs instead of nc.
-template <bool FWD>
+template <bool FWD, bool RG = false>
 __global__ void __launch_bounds__(1024, 1)
     tri_chain_carry_seg(int n, int nc, int G, int mode, const double* __restrict__ M,
                         const double* __restrict__ ends, double* __restrict__ starts,
@@ -1189,6 +1266,8 @@ __global__ void __launch_bounds__(1024, 1)
     extern __shared__ __align__(16) double sm[];   // U ping-pong [2][n], row block
     __shared__ __align__(8) uint64_t tbar;
     __shared__ __align__(8) uint64_t ubar[2];
+    TKSPAN_BEGIN(mode == 2 ? 4 : 0);
+    long long cp = TKCLK();
     cg::cluster_group cl = cg::this_cluster();
     const int CS = (int)cl.num_blocks();
     const int rank = (int)cl.block_rank();
@@ -1205,8 +1284,14 @@ __global__ void __launch_bounds__(1024, 1)
     const int r0 = min(n, rank * rpc), r1 = min(n, r0 + rpc);
     double* blk = sm + 2 * n;
     const unsigned bytes = (unsigned)((size_t)(r1 - r0) * n * sizeof(double));
-    const bool stg = staged && bytes > 0;
+    constexpr bool rg = RG;                      // register rows (one per warp)
+    const bool stg = !RG && staged == 1 && bytes > 0;
     const unsigned ubytes = (unsigned)(n * sizeof(double));
+    double m[kCarryNI];
+    auto rowp = [&](int t) { return M + (size_t)chunk_of(t) * n * n + (size_t)(r0 + warp) * n; };
+    auto pf = [&](int t) {   // this CTA's row block of transition t -> L2
+        if (t < L) l2_prefetch_bulk(M + (size_t)chunk_of(t) * n * n + (size_t)r0 * n, bytes);
+    };
     auto issue = [&](int t) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_expect_tx(&tbar, bytes);
@@ -1223,24 +1308,53 @@ __global__ void __launch_bounds__(1024, 1)
     }
     __syncthreads();
     if (stg && tid == 0 && L > 0) issue(0);
+    if (rg && L > 0) {
+        if (tid == 0) { pf(1); pf(2); }
+        carry_loadrow(rowp(0), n, lane, m);
+    }
     const double* init = mode == 2 ? GS + (size_t)gi * n
                                    : (first ? ends + (size_t)(FWD ? 0 : nc - 1) * n : nullptr);
     for (int j = tid; j < n; j += blockDim.x) sm[j] = init ? init[j] : 0.0;
     cl.sync();   // every CTA's barriers are initialised before any st.async
     const bool wstart = mode == 2 || first;
     unsigned tphase = 0;
+    TKA(0, TKCLK() - cp);
     for (int t = 0; t < L; ++t) {   // transition t: U_{t+1} = E_c + M_c U_t
         const int c = chunk_of(t);
+        long long c0 = TKCLK();
         if (t >= 1) mbar_wait(&ubar[t & 1], (unsigned)(((t - 1) >> 1) & 1));
+        long long c1 = TKCLK();
+        TKA(12, c1 - c0);
         const double* cur = sm + (t & 1) * n;
         if (wstart)
             for (int j = r0 + tid; j < r1; j += blockDim.x) starts[(size_t)c * n + j] = cur[j];
         if (tid == 0) mbar_expect_tx(&ubar[(t + 1) & 1], ubytes);   // arm the copy of U_{t+1}
+        c0 = TKCLK();
+        TKA(1, c0 - c1);
         if (stg) { mbar_wait(&tbar, tphase); tphase ^= 1u; }
+        c1 = TKCLK();
+        TKA(13, c1 - c0);
         const double* src = stg ? blk : M + (size_t)c * n * n + (size_t)r0 * n;
         const double* ec = ends + (size_t)c * n;
         const unsigned nxt = smem_u32(sm + ((t + 1) & 1) * n);
         const unsigned bar = smem_u32(&ubar[(t + 1) & 1]);
+        if (rg) {
+            const int r = r0 + warp;
+            const double e = ec[r];
+            double acc = carry_dotrow(m, cur, n, lane);
+            if (t + 1 < L) carry_loadrow(rowp(t + 1), n, lane, m);
+            if (tid == 0) pf(t + 3);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            const double v = e + acc;
+            for (int d = lane; d < CS; d += 32)
+                st_async_f64(mapa_u32(nxt + 8u * r, d), v, mapa_u32(bar, d));
+            c0 = TKCLK();
+            TKA(14, c0 - c1);
+            __syncthreads();   // the warps stay within one step of each other
+            TKA(2, TKCLK() - c0);
+            continue;
+        }
         for (int r = r0 + warp; r < r1; r += nw) {
             const double* row = src + (size_t)(r - r0) * n;
             const double e = ec[r];
@@ -1258,11 +1372,15 @@ __global__ void __launch_bounds__(1024, 1)
             for (int d = lane; d < CS; d += 32)
                 st_async_f64(mapa_u32(nxt + 8u * r, d), v, mapa_u32(bar, d));
         }
+        c0 = TKCLK();
+        TKA(14, c0 - c1);
         if (stg) {
             __syncthreads();   // row block consumed: refill with the next transition's
             if (tid == 0 && t + 1 < L) issue(t + 1);
         }
+        TKA(2, TKCLK() - c0);
     }
+    cp = TKCLK();
     if (L > 0) mbar_wait(&ubar[L & 1], (unsigned)(((L - 1) >> 1) & 1));
     const double* fin = sm + (L & 1) * n;
     if (mode == 1)
@@ -1272,6 +1390,8 @@ __global__ void __launch_bounds__(1024, 1)
         for (int j = r0 + tid; j < r1; j += blockDim.x) starts[(size_t)cf * n + j] = fin[j];
     }
     cl.sync();   // no CTA leaves while peers may still write into it
+    TKA(3, TKCLK() - cp);
+    TKSPAN_END(mode == 2 ? 4 : 0);
 }
 
 // Grid-wide variant of the carry (one CTA per SM, cooperative launch): CTA g
@@ -1610,6 +1730,20 @@ __global__ void __launch_bounds__(256, 3) tri_rows_cpl(TView V, const double* __
 extern "C" int tk_debug_prof(long long* out16) {
     return cudaMemcpyFromSymbol(out16, g_tk_prof, sizeof(long long) * 16) == cudaSuccess ? 0 : 2;
 }
+// span of the grouped-carry launches since the last call (ns): kernel-wide
+// last end - first start, last start - first start, CTA 0's own duration, for
+// phase A (mode 1) and phase C (mode 2)
+extern "C" int tk_debug_span(long long* out6) {
+    unsigned long long v[8];
+    if (cudaMemcpyFromSymbol(v, g_tk_span, sizeof(v)) != cudaSuccess) return 2;
+    for (int m = 0; m < 2; ++m) {
+        out6[3 * m + 0] = (long long)(v[4 * m + 1] - v[4 * m + 0]);
+        out6[3 * m + 1] = (long long)(v[4 * m + 2] - v[4 * m + 0]);
+        out6[3 * m + 2] = (long long)v[4 * m + 3];
+    }
+    const unsigned long long r[8] = {~0ull, 0ull, 0ull, 0ull, ~0ull, 0ull, 0ull, 0ull};
+    return cudaMemcpyToSymbol(g_tk_span, r, sizeof(r)) == cudaSuccess ? 0 : 2;
+}
 #endif
 
 int64_t tri_fac_len(const tk_level* Lv) {
@@ -1740,7 +1874,10 @@ static int carry_launch(bool fwd, int n, int nc, const double* M, const double* 
     const int64_t lim = 227 * 1024 - 1024;
     if (!cs_ok) {
         for (void* f : {(void*)tri_chain_carry<true>, (void*)tri_chain_carry<false>,
-                        (void*)tri_chain_carry_seg<true>, (void*)tri_chain_carry_seg<false>}) {
+                        (void*)tri_chain_carry_seg<true>, (void*)tri_chain_carry_seg<false>,
+                        (void*)tri_chain_carry<true, true>, (void*)tri_chain_carry<false, true>,
+                        (void*)tri_chain_carry_seg<true, true>,
+                        (void*)tri_chain_carry_seg<false, true>}) {
             cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
         }
@@ -1766,8 +1903,15 @@ static int carry_launch(bool fwd, int n, int nc, const double* M, const double* 
     }
     if (forced == 8 || forced == 16) cs = forced < cs_ok ? forced : cs_ok;
     int64_t smem = smem_for(cs);
-    const int staged = (n % 2 == 0) && smem <= lim && (smem - base_for(cs)) < (1 << 20);
-    if (!staged) smem = base_for(cs);
+    int staged = (n % 2 == 0) && smem <= lim && (smem - base_for(cs)) < (1 << 20);
+    // register rows (see carry_loadrow): one row per warp; TK_CARRY_REGS=0 keeps the
+    // TMA-staged row blocks
+    static const bool regs_ok = [] {
+        const char* e = getenv("TK_CARRY_REGS");
+        return !(e && e[0] == '0');
+    }();
+    if (regs_ok && n % 64 == 0 && n <= 32 * kCarryNI && n == cs * 32) staged = 2;
+    if (staged != 1) smem = base_for(cs);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1782,12 +1926,14 @@ static int carry_launch(bool fwd, int n, int nc, const double* M, const double* 
     cfg.stream = s; cfg.attrs = at; cfg.numAttrs = 1;
     cudaError_t e;
     if (seg_mode) {
-        if (fwd) e = cudaLaunchKernelEx(&cfg, tri_chain_carry_seg<true>, n, nc, G, seg_mode, M, E, S, GE, GS, staged);
-        else e = cudaLaunchKernelEx(&cfg, tri_chain_carry_seg<false>, n, nc, G, seg_mode, M, E, S, GE, GS, staged);
+        auto k = staged == 2 ? (fwd ? tri_chain_carry_seg<true, true> : tri_chain_carry_seg<false, true>)
+                             : (fwd ? tri_chain_carry_seg<true> : tri_chain_carry_seg<false>);
+        e = cudaLaunchKernelEx(&cfg, k, n, nc, G, seg_mode, M, E, S, GE, GS, staged);
         return cuda_status(e, "tri_chain_carry_seg");
     }
-    if (fwd) e = cudaLaunchKernelEx(&cfg, tri_chain_carry<true>, n, nc, M, E, S, staged);
-    else e = cudaLaunchKernelEx(&cfg, tri_chain_carry<false>, n, nc, M, E, S, staged);
+    auto k = staged == 2 ? (fwd ? tri_chain_carry<true, true> : tri_chain_carry<false, true>)
+                         : (fwd ? tri_chain_carry<true> : tri_chain_carry<false>);
+    e = cudaLaunchKernelEx(&cfg, k, n, nc, M, E, S, staged);
     return cuda_status(e, "tri_chain_carry");
 }
 
