@@ -1109,6 +1109,10 @@ __device__ __forceinline__ void st_async_f64(unsigned raddr, double v, unsigned 
 // per step and CTA at 128 B/clk was the step's largest part).  Same order of
 // the products and sums as the staged loop.
 static constexpr int kCarryNI = 16;
+#ifndef TK_CARRY_AHEAD
+#define TK_CARRY_AHEAD 2
+#endif
+static constexpr int kCarryAhead = TK_CARRY_AHEAD;   // row blocks prefetched into L2 ahead of the step
 __device__ __forceinline__ void carry_loadrow(const double* __restrict__ row, int n, int lane,
                                               double (&m)[kCarryNI]) {
 #pragma unroll
@@ -1179,7 +1183,10 @@ __global__ void __launch_bounds__(1024, 1)
     __syncthreads();
     if (stg && tid == 0 && nc > 2) issue(1);
     if (rg && nc > 2) {
-        if (tid == 0) { pf(2); pf(3); }
+        // the row blocks of the next kCarryAhead steps -> L2 (2 measured best: 4 and 8
+        // ahead slow the forward substitution by 25-35 us)
+        if (tid == 0)
+            for (int a = 2; a < 2 + kCarryAhead; ++a) pf(a);
         carry_loadrow(rowp(1), n, lane, m);
     }
     const int first = FWD ? 0 : nc - 1;
@@ -1209,7 +1216,7 @@ __global__ void __launch_bounds__(1024, 1)
             const double e = ec[r];
             double acc = carry_dotrow(m, cur, n, lane);
             if (t + 1 < nc - 1) carry_loadrow(rowp(t + 1), n, lane, m);
-            if (tid == 0) pf(t + 3);
+            if (tid == 0) pf(t + 1 + kCarryAhead);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             const double v = e + acc;
@@ -1309,7 +1316,8 @@ __global__ void __launch_bounds__(1024, 1)
     __syncthreads();
     if (stg && tid == 0 && L > 0) issue(0);
     if (rg && L > 0) {
-        if (tid == 0) { pf(1); pf(2); }
+        if (tid == 0)
+            for (int a = 1; a < 1 + kCarryAhead; ++a) pf(a);
         carry_loadrow(rowp(0), n, lane, m);
     }
     const double* init = mode == 2 ? GS + (size_t)gi * n
@@ -1343,7 +1351,7 @@ __global__ void __launch_bounds__(1024, 1)
             const double e = ec[r];
             double acc = carry_dotrow(m, cur, n, lane);
             if (t + 1 < L) carry_loadrow(rowp(t + 1), n, lane, m);
-            if (tid == 0) pf(t + 3);
+            if (tid == 0) pf(t + 1 + kCarryAhead);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             const double v = e + acc;

@@ -325,7 +325,7 @@ extern "C" int tk_debug_part_prof(long long* out10) {
 // TOE (TK_FLAG_TOEPLITZ_W): the weights Qm, Ql, Qz have constant diagonals
 // (uniform P1 mass matrices), so each diagonal is one scalar per row instead
 // of per-node loads -- same values, same arithmetic, fewer loads/registers.
-template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE, bool PR, int MB>
+template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE, bool PR, int MB, bool SLAB>
 __global__ void __launch_bounds__(32 * W, PartCta<W>::min_blocks(MODE, MB))
 tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ x,
               double* __restrict__ y, double omega, const double* __restrict__ chain,
@@ -412,14 +412,15 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                     pf_l2(V.sl.munext(L, x, i2), n);
                     if (PR) {   // and the coarse segments this row's couplings interpolate
                         const Lay Lp(L.N / 2, n, L.nz);
-                        const int p0 = V.sl.r0 / 2,
-                                  p1 = V.sl.r1 == L.N + 1 ? L.N / 2 + 1 : V.sl.r1 / 2;
-                        const int64_t pb = Lp.start(p0);
+                        const int p0 = SLAB ? V.sl.r0 / 2 : 0;
+                        const int p1 = SLAB ? (V.sl.r1 == L.N + 1 ? L.N / 2 + 1 : V.sl.r1 / 2)
+                                            : L.N / 2 + 1;
+                        const int64_t pb = SLAB ? Lp.start(p0) : 0;
                         auto pu = [&](int tc) {
-                            if (tc - 1 >= p0) pf_l2(chain + (Lp.t_u(tc) - pb), n);
+                            if (!SLAB || tc - 1 >= p0) pf_l2(chain + (Lp.t_u(tc) - pb), n);
                         };
                         auto pm_ = [&](int tc) {
-                            if (tc < p1) pf_l2(chain + (Lp.t_mu(tc) - pb), n);
+                            if (!SLAB || tc < p1) pf_l2(chain + (Lp.t_mu(tc) - pb), n);
                         };
                         if (i2 >= 1) {                      // u_t, t = i2
                             const int t = i2;
@@ -459,8 +460,10 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
         const Lay Lc(L.N / 2, n, L.nz);
         // coarse slice of the slab: coarse rows [c0, c1) stored from offset cb
         // (whole level: every coarse row, cb = 0)
-        const int c0 = V.sl.r0 / 2, c1 = V.sl.r1 == L.N + 1 ? L.N / 2 + 1 : V.sl.r1 / 2;
-        const int64_t cb = Lc.start(c0);
+        // (SLAB == false: compile-time constants, the whole-level kernels pay nothing)
+        const int c0 = SLAB ? V.sl.r0 / 2 : 0;
+        const int c1 = SLAB ? (V.sl.r1 == L.N + 1 ? L.N / 2 + 1 : V.sl.r1 / 2) : L.N / 2 + 1;
+        const int64_t cb = SLAB ? Lc.start(c0) : 0;
         // PR: the couplings are those of x + P e (e = chain, the coarse
         // correction; multigrid.py:115-132): for the fine time t of the segment,
         // even t adds coarse t/2, t = 1 coarse 1, odd t >= 3 the mean of coarse
@@ -472,10 +475,10 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             // slab's last coarse u) and coarse mu of time tc (coarse row tc; outside:
             // the next slab's first coarse mu); chalo = [prev (u, lam) | next (v, mu)]
             auto cu = [&](int tc) -> const double* {
-                return tc - 1 >= c0 ? chain + (Lc.t_u(tc) - cb) : chalo;
+                return (!SLAB || tc - 1 >= c0) ? chain + (Lc.t_u(tc) - cb) : chalo;
             };
             auto cm = [&](int tc) -> const double* {
-                return tc < c1 ? chain + (Lc.t_mu(tc) - cb) : chalo + 3 * n;
+                return (!SLAB || tc < c1) ? chain + (Lc.t_mu(tc) - cb) : chalo + 3 * n;
             };
             if (uprev) {          // u_t, t = i
                 const int t = i;
@@ -1004,7 +1007,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             // (a slab's last odd row feeds the NEXT slab's first coarse mu, its first
             // even row the PREVIOUS slab's last coarse u: tk_restrict_fix_slab
             // writes those from the halos of y)
-            if (RJ && (i & 1) && (i + 1) / 2 < c1) {   // row 2c-1: coarse mu_c = -(u_{2c} - u_{2c} of x)
+            if (RJ && (i & 1) && (!SLAB || (i + 1) / 2 < c1)) {   // row 2c-1: coarse mu_c = -(u_{2c} - u_{2c} of x)
                 double xo[NA];
                 ld4<FULL>(x, ou, j0, n, x != nullptr, xo);
 #pragma unroll
@@ -1034,7 +1037,7 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                     o[k] = oxm[k] + omega * dm;
                 }
                 st4<FULL>(y, om, j0, n, o);
-                if (RJ && (i & 1) == 0 && i / 2 - 1 >= c0) {   // row 2c: coarse u_c = -(mu_{2c} - mu_{2c} of x)
+                if (RJ && (i & 1) == 0 && (!SLAB || i / 2 - 1 >= c0)) {   // row 2c: coarse u_c = -(mu_{2c} - mu_{2c} of x)
                     double xo[NA];
                     ld4<FULL>(x, om, j0, n, x != nullptr, xo);
 #pragma unroll
@@ -1069,14 +1072,14 @@ static int part_cluster(int n, int mode) { return n > kChunk * 32 * part_wmax(mo
 int part_nodes_per_lane(int n) { return part_warps(n, 0) ? kChunk : 0; }
 #endif
 
-template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE, bool PR, int MB = 0>
+template <int W, int MODE, bool FULL, int CL, bool RJ, bool TOE, bool PR, int MB = 0, bool SLAB = false>
 static int part_launch_tt(const tk_level* Lv, const double* b, const double* x, double* y,
                           double omega, const double* chain, cudaStream_t s, double* rc, int opt) {
     using Cf = PartCta<W>;
     static int per_sm = 0;
     static int nsm = 0;
     const int64_t smem = Cf::smem_bytes();
-    auto kern = tri_rows_part<W, MODE, FULL, CL, RJ, TOE, PR, MB>;
+    auto kern = tri_rows_part<W, MODE, FULL, CL, RJ, TOE, PR, MB, SLAB>;
     if (!per_sm) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // shared memory only as large as the resident CTAs need: the rest of the
@@ -1121,6 +1124,10 @@ static int part_launch_tt(const tk_level* Lv, const double* b, const double* x, 
                        "tri_rows_part (cluster)");
 }
 
+static inline bool level_whole(const tk_level* Lv) {
+    return Lv->row0 == 0 && (Lv->row1 == 0 || Lv->row1 == Lv->n_steps + 1);
+}
+
 // TOE only for FULL rows (every chunk inside the level, so the masked
 // boundary entries of the stored diagonals are never needed)
 template <int W, int MODE, bool FULL, int CL, bool RJ = false, bool PR = false>
@@ -1143,8 +1150,14 @@ static int part_launch_t(const tk_level* Lv, const double* b, const double* x, d
                 return part_launch_tt<W, MODE, FULL, CL, RJ, FULL, PR, (W == 4 && MODE != 0 && !RJ && !PR) ? 4 : 0>(
                     Lv, b, x, y, omega, chain, s, rc, opt);
         }
+        if ((RJ || PR) && !level_whole(Lv))   // time slab: the coarse slice / coarse halos
+            return part_launch_tt<W, MODE, FULL, CL, RJ, FULL, PR, 0, RJ || PR>(Lv, b, x, y, omega, chain,
+                                                                                s, rc, opt);
         return part_launch_tt<W, MODE, FULL, CL, RJ, FULL, PR>(Lv, b, x, y, omega, chain, s, rc, opt);
     }
+    if ((RJ || PR) && !level_whole(Lv))
+        return part_launch_tt<W, MODE, FULL, CL, RJ, false, PR, 0, RJ || PR>(Lv, b, x, y, omega, chain, s,
+                                                                             rc, opt);
     return part_launch_tt<W, MODE, FULL, CL, RJ, false, PR>(Lv, b, x, y, omega, chain, s, rc, opt);
 }
 
