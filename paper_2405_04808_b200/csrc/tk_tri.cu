@@ -1269,11 +1269,12 @@ template <bool FWD, bool RG = false>
 __global__ void __launch_bounds__(1024, 1)
     tri_chain_carry_seg(int n, int nc, int G, int mode, const double* __restrict__ M,
                         const double* __restrict__ ends, double* __restrict__ starts,
-                        double* __restrict__ GE, const double* __restrict__ GS, int staged) {
+                        double* __restrict__ GE, const double* __restrict__ GS, int staged,
+                        const double* __restrict__ Phi) {
     extern __shared__ __align__(16) double sm[];   // U ping-pong [2][n], row block
     __shared__ __align__(8) uint64_t tbar;
     __shared__ __align__(8) uint64_t ubar[2];
-    TKSPAN_BEGIN(mode == 2 ? 4 : 0);
+    TKSPAN_BEGIN(mode >= 2 ? 4 : 0);
     long long cp = TKCLK();
     cg::cluster_group cl = cg::this_cluster();
     const int CS = (int)cl.num_blocks();
@@ -1281,7 +1282,7 @@ __global__ void __launch_bounds__(1024, 1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     const int ng = (nc - 2 + G - 1) / G;
     const int q = blockIdx.x / CS;
-    const int gi = (mode == 2 && FWD) ? q + 1 : q;
+    const int gi = (mode >= 2 && FWD) ? q + 1 : q;
     const bool first = FWD ? gi == 0 : gi == ng - 1;
     const bool last = FWD ? gi == ng - 1 : gi == 0;
     const int lo = 1 + gi * G, hi = min(nc - 2, (gi + 1) * G);
@@ -1294,18 +1295,31 @@ __global__ void __launch_bounds__(1024, 1)
     constexpr bool rg = RG;                      // register rows (one per warp)
     const bool stg = !RG && staged == 1 && bytes > 0;
     const unsigned ubytes = (unsigned)(n * sizeof(double));
+    // mode 3: P prelude steps of the group-start recurrence (phase B's
+    // GS[g'] = GE[g] + Phi_g GS[g], from the exact GE of the group first in
+    // chain order) run by every cluster up to its own group, then the L
+    // transitions of mode 2 -- same mat-vecs in the same order as phase B
+    const int P = mode == 3 ? (FWD ? gi - 1 : ng - 2 - gi) : 0;
+    const int LT = P + L;
+    auto mat_of = [&](int t) -> const double* {   // n x n propagator of step t
+        if (t < P) return Phi + (size_t)(FWD ? 1 + t : ng - 2 - t) * n * n;
+        return M + (size_t)chunk_of(t - P) * n * n;
+    };
+    auto end_of = [&](int t) -> const double* {
+        if (t < P) return GE + (size_t)(FWD ? 1 + t : ng - 2 - t) * n;
+        return ends + (size_t)chunk_of(t - P) * n;
+    };
     double m[kCarryNI];
-    auto rowp = [&](int t) { return M + (size_t)chunk_of(t) * n * n + (size_t)(r0 + warp) * n; };
-    auto pf = [&](int t) {   // this CTA's row block of transition t -> L2
-        if (t < L) l2_prefetch_bulk(M + (size_t)chunk_of(t) * n * n + (size_t)r0 * n, bytes);
+    auto rowp = [&](int t) { return mat_of(t) + (size_t)(r0 + warp) * n; };
+    auto pf = [&](int t) {   // this CTA's row block of step t -> L2
+        if (t < LT) l2_prefetch_bulk(mat_of(t) + (size_t)r0 * n, bytes);
     };
     auto issue = [&](int t) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_expect_tx(&tbar, bytes);
-        tma_g2s(blk, M + (size_t)chunk_of(t) * n * n + (size_t)r0 * n, bytes, &tbar);
+        tma_g2s(blk, mat_of(t) + (size_t)r0 * n, bytes, &tbar);
         for (int a = 1; a <= 2; ++a)   // the next two row blocks -> L2 (see tri_chain_carry)
-            if (t + a < L)
-                l2_prefetch_bulk(M + (size_t)chunk_of(t + a) * n * n + (size_t)r0 * n, bytes);
+            if (t + a < LT) l2_prefetch_bulk(mat_of(t + a) + (size_t)r0 * n, bytes);
     };
     if (tid == 0) {
         mbar_init(&tbar, 1);
@@ -1314,27 +1328,28 @@ __global__ void __launch_bounds__(1024, 1)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    if (stg && tid == 0 && L > 0) issue(0);
-    if (rg && L > 0) {
+    if (stg && tid == 0 && LT > 0) issue(0);
+    if (rg && LT > 0) {
         if (tid == 0)
             for (int a = 1; a < 1 + kCarryAhead; ++a) pf(a);
         carry_loadrow(rowp(0), n, lane, m);
     }
-    const double* init = mode == 2 ? GS + (size_t)gi * n
-                                   : (first ? ends + (size_t)(FWD ? 0 : nc - 1) * n : nullptr);
+    const double* init = mode == 3 ? GE + (size_t)(FWD ? 0 : ng - 1) * n
+                         : mode == 2 ? GS + (size_t)gi * n
+                                     : (first ? ends + (size_t)(FWD ? 0 : nc - 1) * n : nullptr);
     for (int j = tid; j < n; j += blockDim.x) sm[j] = init ? init[j] : 0.0;
     cl.sync();   // every CTA's barriers are initialised before any st.async
-    const bool wstart = mode == 2 || first;
+    const bool wstart = mode >= 2 || first;
     unsigned tphase = 0;
     TKA(0, TKCLK() - cp);
-    for (int t = 0; t < L; ++t) {   // transition t: U_{t+1} = E_c + M_c U_t
-        const int c = chunk_of(t);
+    for (int t = 0; t < LT; ++t) {   // step t: U_{t+1} = E_c + M_c U_t
+        const int c = chunk_of(t >= P ? t - P : 0);
         long long c0 = TKCLK();
         if (t >= 1) mbar_wait(&ubar[t & 1], (unsigned)(((t - 1) >> 1) & 1));
         long long c1 = TKCLK();
         TKA(12, c1 - c0);
         const double* cur = sm + (t & 1) * n;
-        if (wstart)
+        if (wstart && t >= P)
             for (int j = r0 + tid; j < r1; j += blockDim.x) starts[(size_t)c * n + j] = cur[j];
         if (tid == 0) mbar_expect_tx(&ubar[(t + 1) & 1], ubytes);   // arm the copy of U_{t+1}
         c0 = TKCLK();
@@ -1342,15 +1357,15 @@ __global__ void __launch_bounds__(1024, 1)
         if (stg) { mbar_wait(&tbar, tphase); tphase ^= 1u; }
         c1 = TKCLK();
         TKA(13, c1 - c0);
-        const double* src = stg ? blk : M + (size_t)c * n * n + (size_t)r0 * n;
-        const double* ec = ends + (size_t)c * n;
+        const double* src = stg ? blk : mat_of(t) + (size_t)r0 * n;
+        const double* ec = end_of(t);
         const unsigned nxt = smem_u32(sm + ((t + 1) & 1) * n);
         const unsigned bar = smem_u32(&ubar[(t + 1) & 1]);
         if (rg) {
             const int r = r0 + warp;
             const double e = ec[r];
             double acc = carry_dotrow(m, cur, n, lane);
-            if (t + 1 < L) carry_loadrow(rowp(t + 1), n, lane, m);
+            if (t + 1 < LT) carry_loadrow(rowp(t + 1), n, lane, m);
             if (tid == 0) pf(t + 1 + kCarryAhead);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -1384,22 +1399,22 @@ __global__ void __launch_bounds__(1024, 1)
         TKA(14, c0 - c1);
         if (stg) {
             __syncthreads();   // row block consumed: refill with the next transition's
-            if (tid == 0 && t + 1 < L) issue(t + 1);
+            if (tid == 0 && t + 1 < LT) issue(t + 1);
         }
         TKA(2, TKCLK() - c0);
     }
     cp = TKCLK();
-    if (L > 0) mbar_wait(&ubar[L & 1], (unsigned)(((L - 1) >> 1) & 1));
-    const double* fin = sm + (L & 1) * n;
+    if (LT > 0) mbar_wait(&ubar[LT & 1], (unsigned)(((LT - 1) >> 1) & 1));
+    const double* fin = sm + (LT & 1) * n;
     if (mode == 1)
         for (int j = r0 + tid; j < r1; j += blockDim.x) GE[(size_t)gi * n + j] = fin[j];
-    if (last && (mode == 2 || first)) {
+    if (last && (mode >= 2 || first)) {
         const int cf = FWD ? nc - 1 : 0;
         for (int j = r0 + tid; j < r1; j += blockDim.x) starts[(size_t)cf * n + j] = fin[j];
     }
     cl.sync();   // no CTA leaves while peers may still write into it
     TKA(3, TKCLK() - cp);
-    TKSPAN_END(mode == 2 ? 4 : 0);
+    TKSPAN_END(mode >= 2 ? 4 : 0);
 }
 
 // Grid-wide variant of the carry (one CTA per SM, cooperative launch): CTA g
@@ -1872,7 +1887,7 @@ static int tri_chain_threads(int n) {
 // seg_mode 1/2: the grouped carry's phase A / C (clusters = groups).
 static int carry_launch(bool fwd, int n, int nc, const double* M, const double* E, double* S,
                         cudaStream_t s, int seg_mode = 0, int G = 0, double* GE = nullptr,
-                        const double* GS = nullptr) {
+                        const double* GS = nullptr, const double* Phi = nullptr) {
     static int cs_ok = 0;   // cluster size verified for this process
     auto base_for = [&](int) -> int64_t { return (int64_t)2 * n * 8; };   // U ping-pong
     auto smem_for = [&](int cs) -> int64_t {
@@ -1936,7 +1951,7 @@ static int carry_launch(bool fwd, int n, int nc, const double* M, const double* 
     if (seg_mode) {
         auto k = staged == 2 ? (fwd ? tri_chain_carry_seg<true, true> : tri_chain_carry_seg<false, true>)
                              : (fwd ? tri_chain_carry_seg<true> : tri_chain_carry_seg<false>);
-        e = cudaLaunchKernelEx(&cfg, k, n, nc, G, seg_mode, M, E, S, GE, GS, staged);
+        e = cudaLaunchKernelEx(&cfg, k, n, nc, G, seg_mode, M, E, S, GE, GS, staged, Phi);
         return cuda_status(e, "tri_chain_carry_seg");
     }
     auto k = staged == 2 ? (fwd ? tri_chain_carry<true, true> : tri_chain_carry<false, true>)
@@ -2168,8 +2183,22 @@ static int tri_launch_t(const tk_level* Lv, int op, const double* b, const doubl
                     double* GE = PhiT + (size_t)ng * n * n;
                     double* GS = GE + (size_t)ng * n;
                     rc = carry_launch(fwd, n, nc, fwd ? P : PT, E, S, s, 1, G, GE, GS);
-                    if (!rc && ng >= 2) rc = carry_launch(fwd, n, ng, fwd ? PhiF : PhiT, GE, GS, s);
-                    if (!rc && ng >= 2) rc = carry_launch(fwd, n, nc, fwd ? P : PT, E, S, s, 2, G, GE, GS);
+                    // phases B + C in one launch (seg mode 3: every cluster runs the
+                    // group-start recurrence up to its own group, then its transitions);
+                    // TK_CARRY_FUSEB=0: the separate phase-B launch
+                    static const bool fuse_b = [] {
+                        const char* e = getenv("TK_CARRY_FUSEB");
+                        return !(e && e[0] == '0');
+                    }();
+                    if (fuse_b) {
+                        if (!rc && ng >= 2)
+                            rc = carry_launch(fwd, n, nc, fwd ? P : PT, E, S, s, 3, G, GE, GS,
+                                              fwd ? PhiF : PhiT);
+                    } else {
+                        if (!rc && ng >= 2) rc = carry_launch(fwd, n, ng, fwd ? PhiF : PhiT, GE, GS, s);
+                        if (!rc && ng >= 2)
+                            rc = carry_launch(fwd, n, nc, fwd ? P : PT, E, S, s, 2, G, GE, GS);
+                    }
                 } else {
                     rc = carry_mode(n) == 1
                              ? carry_launch(fwd, n, nc, fwd ? P : PT, E, S, s)

@@ -491,6 +491,21 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
                 else { mna = cm((t - 1) / 2); mnb = cm((t + 1) / 2); }
             }
         }
+#ifdef TK_PART_PFL1
+        // (experiment) the thread's 32 bytes of every segment of the row -> L1 at
+        // the row's start, so that the staggered loads below are L1 hits
+        if (MODE == 3 && !kStage && FULL) {
+            auto p1 = [&](const double* p, int64_t off) {
+                if (p) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + off + j0));
+            };
+            if (has_vm) { p1(b, ov); p1(b, om); }
+            if (has_uzl) { p1(b, ou); p1(b, oz); p1(b, ol); }
+            p1(uprev, 0); p1(munext, 0);
+            p1(upa, 0); p1(upb, 0); p1(mna, 0); p1(mnb, 0);
+            if (K) { p1(K, 0); p1(K, n); p1(K, 2 * n); }
+            if (C) { p1(C, 0); p1(C, n); p1(C, 2 * n); }
+        }
+#endif
         // x' = x + P e on the chunk nodes / one node of a coupling segment
         auto pr4 = [&](const double* ca, const double* cb, double (&r)[NA]) {
             if (!PR || !ca) return;
