@@ -84,13 +84,12 @@ _NCU_NAMES = {"tk_jacobi_sweep": ("tri_rows_part<W, 3, ., CL, 0, .>", "dense_row
               "tk_kkt_apply": ("tri_apply<0>", "dense_rows<NU, NZ, 0>"),
               "tk_residual_restrict_jacobi0": ("restrict_jacobi0_rows", "restrict_jacobi0_small")}
 _NCU_KERNELS = {
-    "tk_forward_subst": ("tri_rows_part<4, 3, 1, 1, 0, 1, 0, 4>", "tri_chainw_kernel<1", "tri_chainw_kernel<1",
-                         "tri_chain_carry_seg<1", "tri_chain_carry_seg<1", "tri_chain_carry<1",
-                         "tri_rows_part<4, 1,"),
+    "tk_forward_subst": ("tri_rows_part<4, 3, 1, 1, 0, 1, 0, 4", "tri_chainw_kernel<1", "tri_chainw_kernel<1",
+                         "tri_chain_carry_seg<1", "tri_chain_carry_seg<1", "tri_rows_part<4, 1,"),
     "tk_backward_subst": ("tri_chainw_kernel<0", "tri_chainw_kernel<0", "tri_chain_carry_seg<0",
-                          "tri_chain_carry_seg<0", "tri_chain_carry<0", "tri_rows_part<4, 2,"),
+                          "tri_chain_carry_seg<0", "tri_rows_part<4, 2,"),
     "tk_sgs_back_half": ("tri_chainw_kernel<0", "tri_chainw_kernel<0", "tri_chain_carry_seg<0",
-                         "tri_chain_carry_seg<0", "tri_chain_carry<0", "tri_rows_part<4, 4,"),
+                         "tri_chain_carry_seg<0", "tri_rows_part<4, 4,"),
 }
 
 
