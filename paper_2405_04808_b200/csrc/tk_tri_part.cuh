@@ -693,6 +693,24 @@ tri_rows_part(TView V, const double* __restrict__ b, const double* __restrict__ 
             }
         }
         TKPP(1);
+#ifdef TK_PART_PFL1N
+        // (experiment) the NEXT row's segments -> L1 once this row's loads are in
+        // registers: with one CTA per SM (n_u = 2048) nothing else overlaps a row's
+        // load phase
+        if (MODE == 3 && !kStage && FULL && i + ncl < V.sl.r1) {
+            const int i2 = i + ncl;
+            auto p1 = [&](const double* p, int64_t off) {
+                if (p) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + off + j0));
+            };
+            if (i2 >= 1) { p1(b, L.off_v(i2) - bs); p1(b, L.off_mu(i2) - bs); }
+            if (i2 < L.N) {
+                p1(b, L.off_u(i2) - bs); p1(b, L.off_z(i2) - bs); p1(b, L.off_l(i2) - bs);
+                p1(V.Ki(i2, n), 0); p1(V.Ki(i2, n), n); p1(V.Ki(i2, n), 2 * n);
+                if (i2 >= 1) { p1(V.Ci(i2, n), 0); p1(V.Ci(i2, n), n); p1(V.Ci(i2, n), 2 * n); }
+            }
+            if (x) { p1(V.sl.uprev(L, x, i2), 0); p1(V.sl.munext(L, x, i2), 0); }
+        }
+#endif
         if (RJ && (i & 1) == 0) {   // zeros of coarse row c = i/2: v_c, z_{c+1}, lam_{c+1}
             const int c = i / 2;
             double zr[NA];

@@ -34,6 +34,10 @@ def test_null_args_rejected_without_gpu():
     assert lib.tk_kkt_apply(None, None, None, None) == _lib.TK_ERR_ARG
     assert lib.tk_restrict(3, 2, 1, None, None, None) == _lib.TK_ERR_ARG
     assert b"n_fine" in lib.tk_last_error() or lib.tk_last_error()
+    # the fused sweeps and their time-slab versions reject null vectors before any launch
+    assert lib.tk_jacobi_restrict(None, None, None, None, None, None) == _lib.TK_ERR_ARG
+    assert lib.tk_jacobi_prolong_slab(None, None, None, None, None, None, None) == _lib.TK_ERR_ARG
+    assert lib.tk_restrict_fix_slab(None, None, None) == _lib.TK_ERR_ARG
 
 
 @pytest.mark.parametrize("name", CASES)

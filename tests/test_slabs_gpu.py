@@ -222,3 +222,36 @@ def test_dense_fused_pair_on_slabs_bitwise(n_controls, R):
     assert all(used) and len(used) == R
     got = np.concatenate([r[1] for r in sorted(res, key=lambda t: t[0])])
     assert np.array_equal(got, ref), np.abs(got - ref).max()
+
+
+def test_slab_pair_error_paths():
+    """A slab level asks for its coarse halos (tk_jacobi_prolong -> TK_ERR_ARG
+    without them); tk_restrict_fix_slab is a no-op on a whole level."""
+    import torch
+
+    import paper_2405_04808_b200 as P
+    from paper_2405_04808_b200 import _lib, device as dev, slabs
+    nt, n_u = 16, 128
+    grid = P.TimeGrid(1.0, nt)
+    p = P.build_burgers(P.BurgersConfig(n_elems=n_u + 1, theta=0.5, u0_kind="sinstep"), grid)
+    u = P.forward_solve(p, np.zeros((nt, n_u)), grid).states
+    z = np.zeros((nt, n_u))
+    comms = slabs.ThreadComm.group(2)
+
+    def body(c):
+        sh = slabs.SlabHierarchy(p, u, u, z, grid, 2, c, sweeps=1)
+        a = sh.levels[0]
+        b = torch.randn(a.dim, dtype=torch.float64, device="cuda")
+        x, y = dev.empty(a.dim), dev.empty(a.dim)
+        ec = dev.zeros(sh.coarse_sizes[c.rank])
+        rc = _lib.load().tk_jacobi_prolong(a.lref, dev.P(b), dev.P(x), dev.P(ec), dev.P(y),
+                                           dev.stream())
+        return rc
+
+    assert all(rc == _lib.TK_ERR_ARG for rc in slabs.run_threads(comms, body))
+    h = P.build_hierarchy(p, u, u, z, grid, 2, sweeps=1)
+    a = h.levels[0].kkt
+    rc = torch.full((h.transfers[0].coarse_dim,), 3.0, dtype=torch.float64, device="cuda")
+    dev.call("tk_restrict_fix_slab", a.lref, dev.P(rc), dev.stream())
+    torch.cuda.synchronize()
+    assert bool((rc == 3.0).all())
