@@ -247,3 +247,29 @@ def test_large_n_substitutions_identities(n_u):
     t = d(s) - up(s)
     t = P.DiagonalSolver(a).solve_all(t)
     assert float(torch.linalg.norm(d(t) - low(t) - r)) < 1e-8 * nr
+
+
+def test_grouped_carry_register_rows_identities():
+    """n_u = 512 with a long level (256 intervals: 32 chunks, grouped two-level
+    carry): the carry runs with one propagator row per warp in registers and
+    phases B + C in one launch (tri_chain_carry_seg<FWD, RG>, mode 3) -- the
+    configs[2] coarse-level path.  Checked through the substitutions' defining
+    identities (reference smoothers.py:79-152), as test_large_n_substitutions_identities."""
+    import torch
+    from paper_2405_04808_b200.smoothers import backward_subst, forward_subst, sgs_zero
+    P, O, p, op, grid, u, v, z, rng = _case(512, n=256)
+    a = P.assemble_kkt(P.build_stage_blocks(p, grid.dt, u, v, z))
+    a.ensure_subst()
+    lc = a.level.chain_chunk
+    assert lc > 0 and (255 + lc - 1) // lc - 2 > 12      # enough chunks for the grouped carry
+    d, low, up = P.split_parts(a)
+    r = torch.from_numpy(rng.standard_normal(a.dim)).cuda()
+    nr = float(torch.linalg.norm(r))
+    f = forward_subst(a, r)
+    assert float(torch.linalg.norm(d(f) - low(f) - r)) < 1e-9 * nr
+    bk = backward_subst(a, r)
+    assert float(torch.linalg.norm(d(bk) - up(bk) - r)) < 1e-9 * nr
+    s = sgs_zero(a, r)
+    t = d(s) - up(s)
+    t = P.DiagonalSolver(a).solve_all(t)
+    assert float(torch.linalg.norm(d(t) - low(t) - r)) < 1e-8 * nr
