@@ -258,6 +258,11 @@ int tk_jacobi0_restrict_um(const tk_level* L, const double* b, double* x_um, dou
  * are tk_prolong_add_slab's halo_prev_ul / halo_next_vm).
  * Reference: multigrid.py:104-132, :285-299 on one time slab. */
 int tk_restrict_fix_slab(const tk_level* L, double* rc, void* stream);
+/* The same two segments after tk_jacobi_restrict from a NON-zero iterate x
+ * (several sweeps): they are (x - y) of the neighbours' rows, so phase 1
+ * (halos = those of x, i.e. before the exchange of y) stores +halo and phase 2
+ * (halos = those of y) subtracts the halo. */
+int tk_restrict_fix_slab_x(const tk_level* L, double* rc, int32_t phase, void* stream);
 int tk_jacobi_prolong_slab(const tk_level* L, const double* b, const double* x, const double* ec,
                            const double* chalo, double* x_out, void* stream);
 int tk_jacobi_prolong(const tk_level* L, const double* b, const double* x, const double* ec,

@@ -65,6 +65,7 @@ _SIGS = {
     "tk_jacobi0_restrict_um": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p]),
     "tk_jacobi_prolong": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p, _p]),
     "tk_restrict_fix_slab": (C.c_int, [C.POINTER(TkLevel), _p, _p]),
+    "tk_restrict_fix_slab_x": (C.c_int, [C.POINTER(TkLevel), _p, _i32, _p]),
     "tk_jacobi_prolong_slab": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p, _p, _p, _p]),
     "tk_forward_subst": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),
     "tk_backward_subst": (C.c_int, [C.POINTER(TkLevel), _p, _p, _p]),

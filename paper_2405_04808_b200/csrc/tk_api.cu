@@ -35,7 +35,7 @@ int tri_jacobi_restrict_launch(const tk_level*, const double*, const double*, do
                                cudaStream_t);
 int tri_jacobi_prolong_launch(const tk_level*, const double*, const double*, const double*, double*,
                               cudaStream_t, const double* chalo = nullptr);
-int tri_restrict_fix_slab_launch(const tk_level*, double*, cudaStream_t);
+int tri_restrict_fix_slab_launch(const tk_level*, double*, cudaStream_t, int phase = 0);
 int dense_jacobi0_restrict(const tk_level*, const double*, double*, double*, cudaStream_t);
 int dense_split(const tk_level*, const double*, const double*, double*, const double*, double*, int,
                 cudaStream_t, const double* chalo = nullptr);
@@ -220,7 +220,7 @@ int tk_jacobi_restrict(const tk_level* L, const double* b, const double* x_in, d
     TK_CHECK_ARG(b && x_out && rc && x_in != x_out, "tk_jacobi_restrict: bad vectors");
     const int e = check_level(L);
     if (e) return e;
-    if (!tk_jacobi0_restrict_ok(L, 1.0)) {
+    if (!(L->family == TK_FAMILY_DENSE ? dense_pair_ok(L, 1.0) : tk_jacobi0_restrict_ok(L, 1.0) != 0)) {
         set_error("tk_jacobi_restrict: level not supported (see tk_jacobi0_restrict_ok)");
         return TK_ERR_UNSUPPORTED;
     }
@@ -265,6 +265,13 @@ int tk_restrict_fix_slab(const tk_level* L, double* rc, void* stream) {
     const int e = check_level(L);
     if (e) return e;
     return tri_restrict_fix_slab_launch(L, rc, as_stream(stream));
+}
+
+int tk_restrict_fix_slab_x(const tk_level* L, double* rc, int32_t phase, void* stream) {
+    TK_CHECK_ARG(rc && (phase == 1 || phase == 2), "tk_restrict_fix_slab_x: bad arguments");
+    const int e = check_level(L);
+    if (e) return e;
+    return tri_restrict_fix_slab_launch(L, rc, as_stream(stream), phase);
 }
 
 int tk_forward_subst(const tk_level* L, const double* r, double* delta, void* stream) {

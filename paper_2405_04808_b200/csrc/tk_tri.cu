@@ -2312,19 +2312,26 @@ bool tri_jacobi0_restrict_ok(const tk_level* Lv, double omega) {
 // iterate y: the two coarse segments fed by the neighbouring slabs' rows --
 // the slab's first coarse mu = -(u of fine row row0 - 1) = -halo_u, its last
 // coarse u = -(mu of fine row row1) = -halo_mu
+// phase 0: rc = 0 - halo (zero-start sweep); 1: rc = halo (the halos of the sweep's
+// INPUT x, before the exchange of its output y); 2: rc = rc - halo (after it):
+// phases 1 + 2 give (x - y) at the two segments, as the rows write it in-slab
 __global__ void tri_restrict_fix_slab(Lay Lc, int64_t cb, int c0, int c1, bool has_prev,
                                       bool has_next, const double* __restrict__ hu,
-                                      const double* __restrict__ hm, double* __restrict__ rc) {
+                                      const double* __restrict__ hm, double* __restrict__ rc,
+                                      int phase) {
     const int n = Lc.nu;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < 2 * n; j += gridDim.x * blockDim.x) {
+        double* p = nullptr;
+        double h = 0.0;
         if (j < n) {
-            if (has_prev) rc[Lc.off_mu(c0) - cb + j] = 0.0 - hu[j];
+            if (has_prev) { p = rc + (Lc.off_mu(c0) - cb + j); h = hu[j]; }
         } else if (has_next) {
-            rc[Lc.off_u(c1 - 1) - cb + (j - n)] = 0.0 - hm[j - n];
+            p = rc + (Lc.off_u(c1 - 1) - cb + (j - n)); h = hm[j - n];
         }
+        if (p) *p = phase == 1 ? h : (phase == 2 ? *p - h : 0.0 - h);
     }
 }
-int tri_restrict_fix_slab_launch(const tk_level* Lv, double* rc, cudaStream_t s) {
+int tri_restrict_fix_slab_launch(const tk_level* Lv, double* rc, cudaStream_t s, int phase) {
     const int N = Lv->n_steps, n = Lv->n_u;
     const int r1 = Lv->row1 > 0 ? Lv->row1 : N + 1;
     const bool has_prev = Lv->row0 > 0, has_next = r1 <= N;
@@ -2337,7 +2344,8 @@ int tri_restrict_fix_slab_launch(const tk_level* Lv, double* rc, cudaStream_t s)
     const Lay Lc(N / 2, n, Lv->n_z);
     const int c0 = Lv->row0 / 2, c1 = has_next ? r1 / 2 : N / 2 + 1;
     tri_restrict_fix_slab<<<(2 * n + 255) / 256, 256, 0, s>>>(Lc, Lc.start(c0), c0, c1, has_prev,
-                                                            has_next, Lv->halo_u, Lv->halo_mu, rc);
+                                                            has_next, Lv->halo_u, Lv->halo_mu, rc,
+                                                            phase);
     return check_launch("tri_restrict_fix_slab");
 }
 int tri_jacobi0_restrict_launch(const tk_level* Lv, const double* b, double omega, double* y,

@@ -369,6 +369,19 @@ class CudaBackend:
     def restrict_fix(self, a, rc):
         self.dev.call("tk_restrict_fix_slab", a.lref, self.dev.P(rc), self.dev.stream())
 
+    def jacobi_restrict(self, a, b, x_in, coarse_len):
+        """An omega = 1 sweep from x_in (its halos exchanged) + the coarse entries
+        its own rows feed; restrict_fix_x(…, 1) before and (…, 2) after the halo
+        exchange of the result complete rc."""
+        x, rc = self.dev.empty(a.dim), self.dev.empty(coarse_len)
+        self.dev.call("tk_jacobi_restrict", a.lref, self.dev.P(b), self.dev.P(x_in),
+                      self.dev.P(x), self.dev.P(rc), self.dev.stream())
+        return x, rc
+
+    def restrict_fix_x(self, a, rc, phase):
+        self.dev.call("tk_restrict_fix_slab_x", a.lref, self.dev.P(rc), int(phase),
+                      self.dev.stream())
+
     def jacobi_prolong(self, a, b, x, ec, chalo):
         y = self.dev.empty(a.dim)
         self.dev.call("tk_jacobi_prolong_slab", a.lref, self.dev.P(b), self.dev.P(x),
@@ -537,6 +550,22 @@ class SlabHierarchy:
             ec = self._coarse_correction(lvl, rc)
             self.exchange_coarse(lvl, ec)
             return self.be.jacobi_prolong(a, b, x, ec, self._chalo)
+        if self.sweeps > 1 and float(self.omega) == 1.0 and fp is not None and fp(a):
+            # several sweeps (multigrid._cycle's vnn path): the LAST pre-smoothing
+            # sweep writes the restricted residual (x_in - x at the couplings; the two
+            # boundary segments from the halos of x_in, then of x), the FIRST
+            # post-smoothing sweep takes the prolongation
+            x_in = self._smooth(lvl, b, None, self.sweeps - 1)
+            self.exchange_x(lvl, x_in)
+            x, rc = self.be.jacobi_restrict(a, b, x_in, clen)
+            self.be.restrict_fix_x(a, rc, 1)
+            self.exchange_x(lvl, x)
+            self.be.restrict_fix_x(a, rc, 2)
+            del x_in
+            ec = self._coarse_correction(lvl, rc)
+            self.exchange_coarse(lvl, ec)
+            y = self.be.jacobi_prolong(a, b, x, ec, self._chalo)
+            return self._smooth(lvl, b, y, self.sweeps - 1)
         x = self._smooth(lvl, b, None, self.sweeps)
         self.exchange_x(lvl, x)
         j0 = self.omega if (self.sweeps == 1 and multigrid.JACOBI0_RESIDUAL and
